@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Headline benchmark: progressive path tracing of C2 (Cornell box 1024x1024, depth 8) in paths/s.
+
+    python bench.py [--gpus N --steps K --warmup W]            # our B200 path (torchrun for N > 1)
+    python bench.py --impl reference [--steps K --warmup W]     # the CPU path on the host cores
+
+A step is one progressive pass of `--pass-iterations` (default 16) QMC iterations per GPU over all
+1024x1024 pixels (weak scaling: every rank renders its own disjoint iteration block of the global
+pass), followed by the per-pass int64 framebuffer sum-reduction (NCCL all_reduce when N > 1).
+`value` is whole-job paths/s (device-timed, max over ranks); `e2e` is the same metric through the
+public Python API with the scene uploaded from host buffers and the resolved image read back every
+step.  The reference package has no renderer, so the CPU path is the oracle's C
+restatement of the render (oracle/lw_oracle.c, OpenMP over all host threads): "kind": "port".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "paths/sec (samples/sec) on C2 Cornell 1024x1024 depth 8"
+UNIT = "paths/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pass-iterations", type=int, default=16)
+    ap.add_argument("--engine", default="wavefront", choices=["wavefront", "megakernel"])
+    ap.add_argument("--pool-log2", type=int, default=20)
+    ap.add_argument("--regen-fraction", type=float, default=0.5)
+    ap.add_argument("--megakernel-tail", type=int, default=0)
+    ap.add_argument("--width", type=int, default=1024)
+    ap.add_argument("--height", type=int, default=1024)
+    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the bounded CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(a):
+    return (f"C2 Cornell box (procedural quads, one area light, diffuse) {a.width}x{a.height}, depth {a.depth}, "
+            f"{a.pass_iterations} spp per GPU per step")
+
+
+# ---- clocks ---------------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        os.unlink(self.path)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---- CPU path (oracle restatement) ----------------------------------------------------------
+
+def cpu_render_sample(a, budget_s, threads=0):
+    """Bounded sample of the same workload on the host cores: full-width pixel rows x 1 iteration."""
+    from oracle import oracle as O
+    from paper_1705_01263_b200 import scenes
+    from paper_1705_01263_b200.render import RenderParams
+    from paper_1705_01263_b200.scene import pack_scene
+
+    packed = pack_scene(scenes.cornell())
+    osc = O.OracleScene(packed)
+    params = RenderParams(a.width, a.height, a.depth)
+    threads = threads or os.cpu_count()
+    rows = 16
+    t0 = time.perf_counter()
+    osc.render(params, 3, 4, 0, rows * a.width, nthreads=threads)
+    dt = time.perf_counter() - t0
+    rows = int(max(16, min(a.height, rows * budget_s / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    _, st = osc.render(params, 3, 4, 0, rows * a.width, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": st["paths"] / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{rows} rows x {a.width} px x 1 iteration (iteration 3) of the workload, "
+                      f"{st['paths']} paths in {dt:.2f} s, oracle/lw_oracle.c OpenMP",
+            "mrays_per_s": (st["rays_extension"] + st["rays_shadow"]) / dt / 1e6}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    vals = []
+    for step in range(a.warmup + a.steps):
+        r = cpu_render_sample(a, max(a.cpu_seconds / max(a.steps, 1), 1.0))
+        if step >= a.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    base = vals[0]
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (procedural Cornell box)", "impl": "reference",
+            "config": {"workload": workload(a), "parallelism": "host threads (OpenMP)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "port",
+                             "sample": base["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- our path -----------------------------------------------------------------------------
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def load_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "trace_ext_traffic.json")))
+    except OSError:
+        return None
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1705_01263_b200 import scenes
+    from paper_1705_01263_b200.distributed import partition_iterations
+    from paper_1705_01263_b200.render import Renderer
+    from paper_1705_01263_b200.scene import pack_scene
+
+    rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    packed = pack_scene(scenes.cornell())
+    W, H, P = a.width, a.height, a.width * a.height
+    its = a.pass_iterations
+    r = Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
+                 regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail)
+    r.set_stream(stream.cuda_stream)
+    glob = torch.zeros((P, 3), dtype=torch.int64, device="cuda")
+    tmp = torch.empty_like(glob)
+
+    def step(s):
+        # global pass s covers iterations [s*world*its, (s+1)*world*its); this rank takes its block
+        lo, hi = partition_iterations(s * world * its, (s + 1) * world * its, rank, world)
+        r.render_pass(lo, hi)
+        r.copy_framebuffer_to(tmp.data_ptr())
+        if world > 1:
+            dist.all_reduce(tmp)
+        glob.add_(tmp)
+        r.clear()
+
+    # untimed instrumented pass: traversal work per ray (node fetches, triangle tests)
+    r.set_instrumentation(count_work=True)
+    step(10_000)
+    work = r.kernel_profile()
+    r.set_instrumentation(time_kernels=True)
+    for s in range(a.warmup):
+        step(s)
+    glob.zero_()
+    clocks = ClockSampler(local)
+    rays_ext = rays_sh = launches = 0
+    prof_ms = 0.0
+    prof_launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(a.warmup, a.warmup + a.steps):
+        step(s)
+        kp = r.kernel_profile()
+        rays_ext += kp["ext_rays"]
+        rays_sh += kp["shadow_rays"]
+        launches += kp["kernel_launches"]
+        prof_ms += kp["trace_ext_ms"]
+        prof_launches += kp["trace_ext_launches"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms, rays_ext, rays_sh], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t[1:].clone()
+        dist.all_reduce(sm)
+        t = torch.cat([mx, sm])
+    ms_max, rays_ext_all, rays_sh_all = float(t[0]), float(t[1]), float(t[2])
+    paths = a.steps * world * its * P
+    value = paths / (ms_max / 1e3)
+
+    # e2e through the public API with host buffers: scene upload (H2D) + pass + resolved image (D2H)
+    e2e = None
+    if not a.no_e2e:
+        h2d = sum(getattr(packed.arrays[k], "nbytes", 0) for k in packed.arrays if packed.arrays[k] is not None)
+        img_bytes = P * 3 * 4
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(a.steps):
+            r2 = Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
+                          regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail) if s == 0 else r2
+            if s > 0:
+                r2.lib.lw_scene_upload(r2.ctx, __import__("ctypes").byref(packed.desc))
+            lo, hi = partition_iterations(s * world * its, (s + 1) * world * its, rank, world)
+            r2.clear()
+            r2.render_pass(lo, hi)
+            if world > 1:
+                r2.set_stream(stream.cuda_stream)
+                r2.copy_framebuffer_to(tmp.data_ptr())
+                dist.all_reduce(tmp)
+                r2.load_framebuffer_from(tmp.data_ptr())
+            img = r2.image(hi - lo)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        r2.close()
+        e2e = {"value": paths / float(tt[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(img_bytes), "note": "per step: scene upload + GPU BVH build + pass + resolved float32 image readback"}
+        del img
+
+    peaks = load_peaks()
+    nodes_per_ray = work["ext_nodes"] / max(work["ext_rays"], 1)
+    tris_per_ray = work["ext_tris"] / max(work["ext_rays"], 1)
+    bytes_per_ray = 128.0 * nodes_per_ray + 80.0 * tris_per_ray + 80.0
+    ext_rays_rank = rays_ext  # this rank's timed extension rays
+    achieved = (bytes_per_ray * ext_rays_rank / max(prof_launches, 1)) / (prof_ms / max(prof_launches, 1) / 1e3) / 1e9
+    traffic = load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (procedural Cornell box, QMC samples)",
+        "config": {"workload": workload(a), "engine": a.engine, "pool_slots": 1 << a.pool_log2,
+                   "regen_fraction": a.regen_fraction, "parallelism": f"sample-space dp{world}",
+                   "l2": "wavefront state pool (~300 MB) + framebuffers (50 MB) exceed the 126 MB L2; the 5 KB scene "
+                         "BVH is shared-memory resident by design"},
+        "mrays_per_s": (rays_ext_all + rays_sh_all) / (ms_max / 1e3) / 1e6,
+        "gsegments_per_s": rays_ext_all / (ms_max / 1e3) / 1e9,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                     "frac": achieved / peaks.get("hbm_gbs", 6650.0), "kernel": "k_trace_ext (closest-hit traversal)",
+                     "bytes_per_ray": bytes_per_ray, "nodes_per_ray": nodes_per_ray, "tris_per_ray": tris_per_ray,
+                     "avg_launch_ms": prof_ms / max(prof_launches, 1), "launches": prof_launches,
+                     "trace_share_of_step": prof_ms / ms_max,
+                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = {k: v for k, v in cpu_render_sample(a, a.cpu_seconds).items() if k != "mrays_per_s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

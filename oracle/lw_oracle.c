@@ -1,0 +1,1426 @@
+/*
+ * lw_oracle.c -- CPU restatement oracle (TEST INFRASTRUCTURE ONLY; see lw_oracle.h).
+ *
+ * Compile with -ffp-contract=off: every expression below is evaluated as written
+ * in IEEE binary64 with round-to-nearest, like the reference's Cython output
+ * (which contains no FMA) and like the device code (built with -fmad=false).
+ * libm `log` is called directly in the pixel filter exactly as the reference does.
+ */
+#include "lw_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ========================================================================== */
+/* QMC: scrambled radical inverse, _kernels.py:160-208                        */
+/* ========================================================================== */
+
+/* radical_inverse_scrambled, _kernels.py:160-178 (cdivision=False; index > 0 loop) */
+static double ri_scrambled(int64_t base, const int64_t* perm, int64_t perm_off, int64_t index) {
+  double rev = 0.0, scale = 1.0, b = (double)base;
+  while (index > 0) {
+    int64_t digit = index % base;
+    index = index / base;
+    rev = rev * b + (double)perm[perm_off + digit];
+    scale = scale * b;
+  }
+  return rev / scale;
+}
+
+/* radical_inverse_base2, _kernels.py:181-192 */
+static double ri_base2(int64_t index) {
+  double rev = 0.0, scale = 1.0;
+  while (index > 0) {
+    rev = rev * 2.0 + (double)(index & 1);
+    scale = scale * 2.0;
+    index = index >> 1;
+  }
+  return rev / scale;
+}
+
+/* halton_dim, _kernels.py:195-208 */
+double lwo_halton_dim(const int64_t* bases, const int64_t* perm_flat, const int64_t* perm_offset, int64_t dim,
+                      int64_t index) {
+  int64_t b = bases[dim];
+  if (b == 2) return ri_base2(index);
+  return ri_scrambled(b, perm_flat, perm_offset[dim], index);
+}
+
+/* halton_batch, _kernels.py:211-222 */
+void lwo_halton_batch(const int64_t* bases, const int64_t* perm_flat, const int64_t* perm_offset, int64_t dim,
+                      const int64_t* indices, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; i++) out[i] = lwo_halton_dim(bases, perm_flat, perm_offset, dim, indices[i]);
+}
+
+/* ========================================================================== */
+/* Pixel filter, _kernels.py:82-134                                           */
+/* ========================================================================== */
+
+/* Acklam inverse normal CDF, _kernels.py:87-109 (libm log + sqrt in the tails) */
+static double norm_inv_cdf(double p) {
+  double q, r;
+  if (p <= 0.0) return -38.0;
+  if (p >= 1.0) return 38.0;
+  if (p < 0.02425) {
+    q = sqrt(-2.0 * log(p));
+    return (((((-7.784894002430293e-03 * q - 3.223964580411365e-01) * q - 2.400758277161838e00) * q -
+              2.549732539343734e00) * q + 4.374664141464968e00) * q + 2.938163982698783e00) /
+           ((((7.784695709041462e-03 * q + 3.224671290700398e-01) * q + 2.445134137142996e00) * q +
+             3.754408661907416e00) * q + 1.0);
+  }
+  if (p > 1.0 - 0.02425) {
+    q = sqrt(-2.0 * log(1.0 - p));
+    return -(((((-7.784894002430293e-03 * q - 3.223964580411365e-01) * q - 2.400758277161838e00) * q -
+               2.549732539343734e00) * q + 4.374664141464968e00) * q + 2.938163982698783e00) /
+           ((((7.784695709041462e-03 * q + 3.224671290700398e-01) * q + 2.445134137142996e00) * q +
+             3.754408661907416e00) * q + 1.0);
+  }
+  q = p - 0.5;
+  r = q * q;
+  return (((((-3.969683028665376e01 * r + 2.209460984245205e02) * r - 2.759285104469687e02) * r +
+            1.383577518672690e02) * r - 3.066479806614716e01) * r + 2.506628277459239e00) * q /
+         (((((-5.447609879822406e01 * r + 1.615858368580409e02) * r - 1.556989798598866e02) * r +
+            6.680131188771972e01) * r - 1.328068155288572e01) * r + 1.0);
+}
+
+#define PHI_NEG3 0.0013498980316300933 /* _kernels.py:114 */
+#define PHI_POS3 0.9986501019683699    /* _kernels.py:115 */
+
+/* gauss_filter_offset, _kernels.py:121-129 */
+double lwo_gauss_filter_offset(double u) {
+  double p = PHI_NEG3 + u * (PHI_POS3 - PHI_NEG3);
+  double x = norm_inv_cdf(p);
+  if (x < -3.0) x = -3.0;
+  if (x > 3.0) x = 3.0;
+  return 0.5 * x;
+}
+
+void lwo_pixel_offset_batch(const double* u, int64_t n, double* out) {
+  for (int64_t i = 0; i < 2 * n; i++) out[i] = lwo_gauss_filter_offset(u[i]);
+}
+
+/* ========================================================================== */
+/* Octahedral compression, _kernels.py:233-342                                */
+/* ========================================================================== */
+
+int64_t lwo_oct_encode(double x, double y, double z) {
+  double ax = fabs(x), ay = fabs(y), az = fabs(z);
+  double norm = ax + ay + az;
+  if (norm <= 0.0) return 0;
+  double u = x / norm, v = y / norm;
+  if (z < 0.0) {
+    double fu = (1.0 - fabs(v)) * (u >= 0.0 ? 1.0 : -1.0);
+    double fv = (1.0 - fabs(u)) * (v >= 0.0 ? 1.0 : -1.0);
+    u = fu;
+    v = fv;
+  }
+  int64_t eu = (int64_t)floor((u + 1.0) * 0.5 * 65535.0 + 0.5);
+  int64_t ev = (int64_t)floor((v + 1.0) * 0.5 * 65535.0 + 0.5);
+  if (eu < 0) eu = 0;
+  if (eu > 65535) eu = 65535;
+  if (ev < 0) ev = 0;
+  if (ev > 65535) ev = 65535;
+  return (eu << 16) | ev;
+}
+
+void lwo_oct_decode(int64_t packed, double* o) {
+  int64_t eu = (packed >> 16) & 0xFFFF, ev = packed & 0xFFFF;
+  double u = (double)eu / 65535.0 * 2.0 - 1.0;
+  double v = (double)ev / 65535.0 * 2.0 - 1.0;
+  double z = 1.0 - fabs(u) - fabs(v);
+  double x = u, y = v;
+  if (z < 0.0) {
+    x = (1.0 - fabs(v)) * (u >= 0.0 ? 1.0 : -1.0);
+    y = (1.0 - fabs(u)) * (v >= 0.0 ? 1.0 : -1.0);
+  }
+  o[0] = x;
+  o[1] = y;
+  o[2] = z;
+}
+
+/* oct_roundtrip_batch, _kernels.py:321-342 (rows with zero length are left untouched) */
+void lwo_oct_roundtrip_batch(const double* vecs, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; i++) {
+    double d[3];
+    lwo_oct_decode(lwo_oct_encode(vecs[3 * i], vecs[3 * i + 1], vecs[3 * i + 2]), d);
+    double ln = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (ln > 0.0) {
+      out[3 * i] = d[0] / ln;
+      out[3 * i + 1] = d[1] / ln;
+      out[3 * i + 2] = d[2] / ln;
+    }
+  }
+}
+
+/* ========================================================================== */
+/* Watertight triangle test and BVH traversal, _kernels.py:345-585            */
+/* ========================================================================== */
+
+typedef struct {
+  double t, bu, bv;
+  int64_t tri;
+} hitrec;
+
+typedef struct {
+  int kx, ky, kz;
+  double sx, sy, sz;
+  double o[3];  /* original origin */
+  double op[3]; /* origin passed to the triangle test: unpermuted (D1) or permuted */
+} shear;
+
+/* _kernels.py:439-477 */
+static void shear_setup(const double* o, const double* d, int compat, shear* s) {
+  double adx = fabs(d[0]), ady = fabs(d[1]), adz = fabs(d[2]);
+  int kz = 0;
+  if (ady > adx) {
+    kz = 1;
+    if (adz > ady) kz = 2;
+  } else if (adz > adx) {
+    kz = 2;
+  }
+  int kx = kz + 1;
+  if (kx == 3) kx = 0;
+  int ky = kx + 1;
+  if (ky == 3) ky = 0;
+  if (d[kz] < 0.0) {
+    int t = kx;
+    kx = ky;
+    ky = t;
+  }
+  s->kx = kx;
+  s->ky = ky;
+  s->kz = kz;
+  s->sz = 1.0 / d[kz];
+  s->sx = d[kx] * s->sz;
+  s->sy = d[ky] * s->sz;
+  for (int a = 0; a < 3; a++) s->o[a] = o[a];
+  if (compat) { /* D1: _tri_hit receives (ox, oy, oz) and subtracts them from permuted components */
+    s->op[0] = o[0];
+    s->op[1] = o[1];
+    s->op[2] = o[2];
+  } else {
+    s->op[0] = o[kx];
+    s->op[1] = o[ky];
+    s->op[2] = o[kz];
+  }
+}
+
+/* _tri_hit, _kernels.py:368-416.  accept_tie: closest-hit tie rule; returns 1 on update. */
+static int tri_test(const double* v, int64_t tri, const shear* s, double tmin, hitrec* r) {
+  double ax = v[0 + s->kx] - s->op[0], ay = v[0 + s->ky] - s->op[1], az = v[0 + s->kz] - s->op[2];
+  double bx = v[3 + s->kx] - s->op[0], by = v[3 + s->ky] - s->op[1], bz = v[3 + s->kz] - s->op[2];
+  double cx = v[6 + s->kx] - s->op[0], cy = v[6 + s->ky] - s->op[1], cz = v[6 + s->kz] - s->op[2];
+  double sax = ax - s->sx * az, say = ay - s->sy * az;
+  double sbx = bx - s->sx * bz, sby = by - s->sy * bz;
+  double scx = cx - s->sx * cz, scy = cy - s->sy * cz;
+  double u = scx * sby - scy * sbx;
+  double vv = sax * scy - say * scx;
+  double w = sbx * say - sby * sax;
+  if ((u < 0.0 || vv < 0.0 || w < 0.0) && (u > 0.0 || vv > 0.0 || w > 0.0)) return 0;
+  double det = u + vv + w;
+  if (det == 0.0) return 0;
+  double t_scaled = u * (s->sz * az) + vv * (s->sz * bz) + w * (s->sz * cz);
+  double t = t_scaled / det;
+  if (t <= tmin) return 0;
+  if (t > r->t) return 0;
+  if (t == r->t && r->tri >= 0 && tri >= r->tri) return 0;
+  r->t = t;
+  r->tri = tri;
+  r->bu = vv / det;
+  r->bv = w / det;
+  return 1;
+}
+
+/* any-hit variant: strict tmin < t < tmax */
+static int tri_occludes(const double* v, const shear* s, double tmax) {
+  double ax = v[0 + s->kx] - s->op[0], ay = v[0 + s->ky] - s->op[1], az = v[0 + s->kz] - s->op[2];
+  double bx = v[3 + s->kx] - s->op[0], by = v[3 + s->ky] - s->op[1], bz = v[3 + s->kz] - s->op[2];
+  double cx = v[6 + s->kx] - s->op[0], cy = v[6 + s->ky] - s->op[1], cz = v[6 + s->kz] - s->op[2];
+  double sax = ax - s->sx * az, say = ay - s->sy * az;
+  double sbx = bx - s->sx * bz, sby = by - s->sy * bz;
+  double scx = cx - s->sx * cz, scy = cy - s->sy * cz;
+  double u = scx * sby - scy * sbx;
+  double vv = sax * scy - say * scx;
+  double w = sbx * say - sby * sax;
+  if ((u < 0.0 || vv < 0.0 || w < 0.0) && (u > 0.0 || vv > 0.0 || w > 0.0)) return 0;
+  double det = u + vv + w;
+  if (det == 0.0) return 0;
+  double t_scaled = u * (s->sz * az) + vv * (s->sz * bz) + w * (s->sz * cz);
+  double t = t_scaled / det;
+  return t > 0.0 && t < tmax;
+}
+
+/* _safe_inv, _kernels.py:357-362 */
+static double safe_inv(double d) {
+  if (d > 1e-200 || d < -1e-200) return 1.0 / d;
+  if (d >= 0.0) return 1e200;
+  return -1e200;
+}
+
+/* _traverse_closest, _kernels.py:422-545 (compat = pristine; otherwise D1/D2 corrected) */
+static void traverse_ref(int compat, const double* bounds, const int64_t* children, const int64_t* order,
+                         const double* verts, int64_t ntris, const double* o, const double* d, double tmin,
+                         double tmax, hitrec* r, int64_t* stack) {
+  r->t = tmax;
+  r->tri = -1;
+  r->bu = 0.0;
+  r->bv = 0.0;
+  if (ntris == 0) return;
+  shear s;
+  shear_setup(o, d, compat, &s);
+  double inv[3] = {safe_inv(d[0]), safe_inv(d[1]), safe_inv(d[2])};
+  int zero[3];
+  for (int a = 0; a < 3; a++) zero[a] = !compat && (inv[a] == 1e200 || inv[a] == -1e200);
+  int64_t sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    int64_t node = stack[--sp];
+    const double* b = bounds + 6 * node;
+    double tn = -INFINITY, tf = INFINITY;
+    int culled = 0;
+    for (int a = 0; a < 3; a++) {
+      if (zero[a]) { /* D2 fix: a ray parallel to the slab is inside it or misses */
+        if (o[a] < b[a] || o[a] > b[3 + a]) culled = 1;
+        continue;
+      }
+      double t0 = (b[a] - o[a]) * inv[a];
+      double t1 = (b[3 + a] - o[a]) * inv[a];
+      if (compat && a == 0) { /* _kernels.py:500-507 */
+        if (t0 > t1) {
+          tn = t1;
+          tf = t0;
+        } else {
+          tn = t0;
+          tf = t1;
+        }
+        continue;
+      }
+      if (t0 > t1) { /* _kernels.py:510-531 */
+        if (t0 < tf) tf = t0;
+        if (t1 > tn) tn = t1;
+      } else {
+        if (t1 < tf) tf = t1;
+        if (t0 > tn) tn = t0;
+      }
+    }
+    if (culled) continue;
+    if (tn > tf || tn > r->t || tf < tmin) continue; /* _kernels.py:532 */
+    int64_t c0 = children[2 * node], c1 = children[2 * node + 1];
+    if (c0 < 0) {
+      int64_t start = -(c0 + 1);
+      for (int64_t i = 0; i < c1; i++) {
+        int64_t tri = order[start + i];
+        tri_test(verts + 9 * tri, tri, &s, tmin, r);
+      }
+    } else {
+      stack[sp++] = c0;
+      stack[sp++] = c1;
+    }
+  }
+}
+
+void lwo_intersect_batch(int mode, const double* bounds, const int64_t* children, const int64_t* order,
+                         const double* verts, int64_t ntris, const double* origins, const double* dirs,
+                         const double* tmaxs, int64_t n, double* out_t, int64_t* out_tri, double* out_bary) {
+  int64_t stack[256];
+  for (int64_t i = 0; i < n; i++) {
+    hitrec r;
+    const double* o = origins + 3 * i;
+    const double* d = dirs + 3 * i;
+    if (mode == LW_TRAVERSE_BRUTE) {
+      r.t = tmaxs[i];
+      r.tri = -1;
+      r.bu = r.bv = 0.0;
+      shear s;
+      shear_setup(o, d, 0, &s);
+      for (int64_t k = 0; k < ntris; k++) tri_test(verts + 9 * k, k, &s, 0.0, &r);
+    } else {
+      traverse_ref(mode == LW_TRAVERSE_COMPAT, bounds, children, order, verts, ntris, o, d, 0.0, tmaxs[i], &r,
+                   stack);
+    }
+    if (r.tri >= 0) { /* _kernels.py:576-585 */
+      out_t[i] = r.t;
+      out_tri[i] = r.tri;
+      out_bary[2 * i] = r.bu;
+      out_bary[2 * i + 1] = r.bv;
+    } else {
+      out_t[i] = 1e308;
+      out_tri[i] = -1;
+      out_bary[2 * i] = 0.0;
+      out_bary[2 * i + 1] = 0.0;
+    }
+  }
+}
+
+/* ========================================================================== */
+/* BVH build, geometry.py:100-148                                             */
+/* ========================================================================== */
+
+typedef struct {
+  const double* tri_min;
+  const double* tri_max;
+  const double* centroid;
+  double* bounds;
+  int64_t* children;
+  int64_t* order;
+  int64_t nnodes;
+  int64_t norder;
+} bvh_build_ctx;
+
+static const double* g_sort_keys; /* centroid column for the comparator (oracle is single-threaded here) */
+static int g_sort_axis;
+
+/* np.lexsort((idx, centroid[idx, axis])): primary centroid, secondary triangle index */
+static int cmp_centroid(const void* pa, const void* pb) {
+  int64_t a = *(const int64_t*)pa, b = *(const int64_t*)pb;
+  double ka = g_sort_keys[3 * a + g_sort_axis], kb = g_sort_keys[3 * b + g_sort_axis];
+  if (ka < kb) return -1;
+  if (ka > kb) return 1;
+  return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+/* emit(), geometry.py:116-134 */
+static int64_t bvh_emit(bvh_build_ctx* c, int64_t* idx, int64_t n) {
+  int64_t node = c->nnodes++;
+  double bmin[3], bmax[3];
+  for (int a = 0; a < 3; a++) {
+    bmin[a] = c->tri_min[3 * idx[0] + a];
+    bmax[a] = c->tri_max[3 * idx[0] + a];
+  }
+  for (int64_t i = 1; i < n; i++)
+    for (int a = 0; a < 3; a++) {
+      double lo = c->tri_min[3 * idx[i] + a], hi = c->tri_max[3 * idx[i] + a];
+      if (lo < bmin[a]) bmin[a] = lo;
+      if (hi > bmax[a]) bmax[a] = hi;
+    }
+  for (int a = 0; a < 3; a++) {
+    c->bounds[6 * node + a] = bmin[a];
+    c->bounds[6 * node + 3 + a] = bmax[a];
+  }
+  if (n <= 4) { /* LEAF_SIZE, geometry.py:20, 122-125 */
+    c->children[2 * node] = -(c->norder + 1);
+    c->children[2 * node + 1] = n;
+    for (int64_t i = 0; i < n; i++) c->order[c->norder++] = idx[i];
+    return node;
+  }
+  int axis = 0; /* np.argmax: first maximum */
+  double ext0 = bmax[0] - bmin[0], ext1 = bmax[1] - bmin[1], ext2 = bmax[2] - bmin[2];
+  if (ext1 > ext0) axis = 1;
+  if (ext2 > (axis == 1 ? ext1 : ext0)) axis = 2;
+  g_sort_keys = c->centroid;
+  g_sort_axis = axis;
+  qsort(idx, (size_t)n, sizeof(int64_t), cmp_centroid);
+  int64_t half = n / 2;
+  int64_t left = bvh_emit(c, idx, half);
+  int64_t right = bvh_emit(c, idx + half, n - half);
+  c->children[2 * node] = left;
+  c->children[2 * node + 1] = right;
+  return node;
+}
+
+int64_t lwo_build_bvh(const double* verts, int64_t n, double* bounds, int64_t* children, int64_t* order) {
+  if (n == 0) { /* geometry.py:103-106 */
+    for (int a = 0; a < 6; a++) bounds[a] = 0.0;
+    children[0] = -1;
+    children[1] = 0;
+    return 1;
+  }
+  double* tmin = (double*)malloc(sizeof(double) * 3 * n);
+  double* tmax = (double*)malloc(sizeof(double) * 3 * n);
+  double* cen = (double*)malloc(sizeof(double) * 3 * n);
+  int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * n);
+  for (int64_t i = 0; i < n; i++) {
+    const double* v = verts + 9 * i;
+    for (int a = 0; a < 3; a++) {
+      double lo = v[a], hi = v[a];
+      if (v[3 + a] < lo) lo = v[3 + a];
+      if (v[6 + a] < lo) lo = v[6 + a];
+      if (v[3 + a] > hi) hi = v[3 + a];
+      if (v[6 + a] > hi) hi = v[6 + a];
+      tmin[3 * i + a] = lo;
+      tmax[3 * i + a] = hi;
+      cen[3 * i + a] = 0.5 * (lo + hi);
+    }
+    idx[i] = i;
+  }
+  bvh_build_ctx c = {tmin, tmax, cen, bounds, children, order, 0, 0};
+  bvh_emit(&c, idx, n);
+  free(tmin);
+  free(tmax);
+  free(cen);
+  free(idx);
+  return c.nnodes;
+}
+
+/* ========================================================================== */
+/* Deterministic math (basic IEEE ops only; restated in lw_detmath.cuh)       */
+/* ========================================================================== */
+
+#define LW_PI 3.141592653589793
+#define LW_TWO_PI 6.283185307179586
+#define LW_HALF_PI 1.5707963267948966
+#define LW_QUARTER_PI 0.7853981633974483
+#define LW_INV_PI 0.3183098861837907
+#define LW_INV_FOUR_PI 0.07957747154594767
+#define LW_TWO_PI_SQ 19.739208802178716
+
+/* sin(2*pi*u), cos(2*pi*u): quadrant reduction, Taylor series on [-pi/4, pi/4] */
+void lwo_sincos2pi(double u, double* s, double* c) {
+  double k = floor(u * 4.0 + 0.5);
+  double r = u - k * 0.25;
+  double x = r * LW_TWO_PI;
+  double x2 = x * x;
+  double sp = x * (1.0 + x2 * (-1.6666666666666666e-01 + x2 * (8.3333333333333332e-03 + x2 * (-1.9841269841269841e-04 +
+             x2 * (2.7557319223985893e-06 + x2 * (-2.5052108385441720e-08 + x2 * (1.6059043836821613e-10 +
+             x2 * (-7.6471637318198164e-13 + x2 * 2.8114572543455206e-15))))))));
+  double cp = 1.0 + x2 * (-0.5 + x2 * (4.1666666666666664e-02 + x2 * (-1.3888888888888889e-03 + x2 * (2.4801587301587302e-05 +
+             x2 * (-2.7557319223985888e-07 + x2 * (2.0876756987868100e-09 + x2 * (-1.1470745597729725e-11 +
+             x2 * 4.7794773323873853e-14)))))));
+  int q = ((int)k) & 3;
+  if (q == 0) {
+    *s = sp;
+    *c = cp;
+  } else if (q == 1) {
+    *s = cp;
+    *c = -sp;
+  } else if (q == 2) {
+    *s = -sp;
+    *c = -cp;
+  } else {
+    *s = -cp;
+    *c = sp;
+  }
+}
+
+/* atan for t in [0, 1]: two argument halvings (tan(a/4) <= tan(pi/16)), then the odd Taylor series */
+static const double ATAN_C[12] = {1.0, -1.0 / 3.0, 1.0 / 5.0, -1.0 / 7.0, 1.0 / 9.0, -1.0 / 11.0,
+                                  1.0 / 13.0, -1.0 / 15.0, 1.0 / 17.0, -1.0 / 19.0, 1.0 / 21.0, -1.0 / 23.0};
+static double det_atan01(double t) {
+  double h = t / (1.0 + sqrt(1.0 + t * t));
+  h = h / (1.0 + sqrt(1.0 + h * h));
+  double h2 = h * h;
+  double p = ATAN_C[11];
+  for (int k = 10; k >= 0; k--) p = p * h2 + ATAN_C[k];
+  return 4.0 * (h * p);
+}
+
+double lwo_atan2(double y, double x) {
+  double ax = fabs(x), ay = fabs(y);
+  int swap = ay > ax;
+  double num = swap ? ax : ay, den = swap ? ay : ax;
+  double t = den == 0.0 ? 0.0 : num / den;
+  double r = det_atan01(t);
+  if (swap) r = LW_HALF_PI - r;
+  if (x < 0.0) r = LW_PI - r;
+  if (y < 0.0) r = -r;
+  return r;
+}
+
+/* ========================================================================== */
+/* Alias tables (Vose)                                        */
+/* ========================================================================== */
+
+int lwo_alias_build(const double* w, int64_t n, double* prob, int32_t* alias, double* pdf) {
+  if (n <= 0) return 1;
+  double total = 0.0;
+  for (int64_t i = 0; i < n; i++) {
+    if (!(w[i] >= 0.0) || w[i] == INFINITY) return 1;
+    total += w[i];
+  }
+  if (!(total > 0.0)) return 1;
+  double* scaled = (double*)malloc(sizeof(double) * n);
+  int64_t* small = (int64_t*)malloc(sizeof(int64_t) * n);
+  int64_t* large = (int64_t*)malloc(sizeof(int64_t) * n);
+  int64_t ns = 0, nl = 0;
+  double dn = (double)n;
+  for (int64_t i = 0; i < n; i++) {
+    pdf[i] = w[i] / total;
+    scaled[i] = pdf[i] * dn;
+    if (scaled[i] < 1.0)
+      small[ns++] = i;
+    else
+      large[nl++] = i;
+  }
+  while (ns > 0 && nl > 0) {
+    int64_t s = small[--ns];
+    int64_t l = large[--nl];
+    prob[s] = scaled[s];
+    alias[s] = (int32_t)l;
+    scaled[l] = (scaled[l] + scaled[s]) - 1.0;
+    if (scaled[l] < 1.0)
+      small[ns++] = l;
+    else
+      large[nl++] = l;
+  }
+  while (nl > 0) {
+    int64_t l = large[--nl];
+    prob[l] = 1.0;
+    alias[l] = (int32_t)l;
+  }
+  while (ns > 0) {
+    int64_t s = small[--ns];
+    prob[s] = 1.0;
+    alias[s] = (int32_t)s;
+  }
+  free(scaled);
+  free(small);
+  free(large);
+  return 0;
+}
+
+/* sample: returns the entry and remaps u to a fresh uniform in [0,1) */
+static int64_t alias_sample(const double* prob, const int32_t* alias, int64_t n, double u, double* u_out) {
+  double x = u * (double)n;
+  double fi = floor(x);
+  int64_t i = (int64_t)fi;
+  if (i >= n) i = n - 1;
+  double f = x - (double)i;
+  double pr = prob[i];
+  if (f < pr) {
+    *u_out = f / pr;
+    return i;
+  }
+  *u_out = (f - pr) / (1.0 - pr);
+  if (*u_out >= 1.0) *u_out = 0.9999999999999999;
+  return alias[i];
+}
+
+/* ========================================================================== */
+/* Render scene: render BVH (child-box layout), lights, materials             */
+/* ========================================================================== */
+
+typedef struct {
+  double box[2][6]; /* lo xyz, hi xyz of child 0 / child 1 */
+  int32_t ref[2];   /* >= 0 internal node index; < 0 leaf: -(1 + (start << 3 | count)) */
+} rnode;
+
+struct lwo_scene {
+  lw_scene_desc d;
+  int64_t ntris;
+  double* verts;  /* [ntris*9] original order */
+  double* normals;
+  int32_t* material;
+  lw_material* materials;
+  /* reference-layout BVH */
+  int64_t nnodes;
+  double* bounds;
+  int64_t* children;
+  int64_t* order;
+  /* render BVH */
+  int64_t nrnodes;
+  rnode* rnodes;
+  int32_t root_ref;
+  double root_box[6];
+  double* lverts; /* leaf-ordered verts [ntris*9] */
+  int64_t* ltri;  /* leaf slot -> original triangle id */
+  /* emitters */
+  int64_t nemit;
+  int64_t* emit_of_tri; /* [ntris] emitter index or -1 */
+  int64_t* emit_tri;
+  double* emit_rad;
+  int32_t* emit_two;
+  double* emit_area;
+  double* emit_prob;
+  int32_t* emit_alias;
+  double* emit_pdf;
+  /* environment */
+  int env_kind;
+  int env_w, env_h;
+  float* env_img;
+  double* env_prob;
+  int32_t* env_alias;
+  double* env_pdf;
+  double p_env, p_tri;
+};
+
+static int32_t leaf_ref(int64_t start, int64_t count) { return (int32_t)(-(1 + ((start << 3) | count))); }
+
+static void build_render_bvh(lwo_scene* s) {
+  int64_t nn = s->nnodes;
+  int64_t* map = (int64_t*)malloc(sizeof(int64_t) * nn);
+  int64_t ni = 0;
+  for (int64_t k = 0; k < nn; k++) map[k] = s->children[2 * k] >= 0 ? ni++ : -1;
+  s->nrnodes = ni;
+  s->rnodes = (rnode*)calloc(ni > 0 ? ni : 1, sizeof(rnode));
+  for (int64_t k = 0; k < nn; k++) {
+    if (map[k] < 0) continue;
+    rnode* r = s->rnodes + map[k];
+    for (int c = 0; c < 2; c++) {
+      int64_t ch = s->children[2 * k + c];
+      memcpy(r->box[c], s->bounds + 6 * ch, sizeof(double) * 6);
+      if (s->children[2 * ch] >= 0)
+        r->ref[c] = (int32_t)map[ch];
+      else
+        r->ref[c] = leaf_ref(-(s->children[2 * ch] + 1), s->children[2 * ch + 1]);
+    }
+  }
+  memcpy(s->root_box, s->bounds, sizeof(double) * 6);
+  s->root_ref = s->children[0] >= 0 ? 0 : leaf_ref(-(s->children[0] + 1), s->children[1]);
+  s->lverts = (double*)malloc(sizeof(double) * 9 * (s->ntris > 0 ? s->ntris : 1));
+  s->ltri = (int64_t*)malloc(sizeof(int64_t) * (s->ntris > 0 ? s->ntris : 1));
+  for (int64_t k = 0; k < s->ntris; k++) {
+    memcpy(s->lverts + 9 * k, s->verts + 9 * s->order[k], sizeof(double) * 9);
+    s->ltri[k] = s->order[k];
+  }
+  free(map);
+}
+
+static double* dup_d(const double* p, int64_t n) {
+  double* q = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+  if (n > 0) memcpy(q, p, sizeof(double) * n);
+  return q;
+}
+
+lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
+  lwo_scene* s = (lwo_scene*)calloc(1, sizeof(lwo_scene));
+  s->d = *d;
+  s->ntris = d->ntris;
+  s->verts = dup_d(d->verts, 9 * d->ntris);
+  s->normals = dup_d(d->normals, 9 * d->ntris);
+  s->material = (int32_t*)malloc(sizeof(int32_t) * (d->ntris > 0 ? d->ntris : 1));
+  if (d->ntris) memcpy(s->material, d->material, sizeof(int32_t) * d->ntris);
+  s->materials = (lw_material*)malloc(sizeof(lw_material) * (d->nmaterials > 0 ? d->nmaterials : 1));
+  if (d->nmaterials) memcpy(s->materials, d->materials, sizeof(lw_material) * d->nmaterials);
+  int64_t cap = d->ntris > 0 ? 2 * d->ntris : 1;
+  s->bounds = (double*)malloc(sizeof(double) * 6 * cap);
+  s->children = (int64_t*)malloc(sizeof(int64_t) * 2 * cap);
+  s->order = (int64_t*)malloc(sizeof(int64_t) * (d->ntris > 0 ? d->ntris : 1));
+  s->nnodes = lwo_build_bvh(s->verts, s->ntris, s->bounds, s->children, s->order);
+  build_render_bvh(s);
+  /* emitters */
+  s->nemit = d->nemit;
+  s->emit_of_tri = (int64_t*)malloc(sizeof(int64_t) * (s->ntris > 0 ? s->ntris : 1));
+  for (int64_t k = 0; k < s->ntris; k++) s->emit_of_tri[k] = -1;
+  if (s->nemit > 0) {
+    s->emit_tri = (int64_t*)malloc(sizeof(int64_t) * s->nemit);
+    memcpy(s->emit_tri, d->emit_tri, sizeof(int64_t) * s->nemit);
+    s->emit_rad = dup_d(d->emit_radiance, 3 * s->nemit);
+    s->emit_two = (int32_t*)malloc(sizeof(int32_t) * s->nemit);
+    memcpy(s->emit_two, d->emit_twosided, sizeof(int32_t) * s->nemit);
+    s->emit_area = (double*)malloc(sizeof(double) * s->nemit);
+    s->emit_prob = (double*)malloc(sizeof(double) * s->nemit);
+    s->emit_alias = (int32_t*)malloc(sizeof(int32_t) * s->nemit);
+    s->emit_pdf = (double*)malloc(sizeof(double) * s->nemit);
+    for (int64_t e = 0; e < s->nemit; e++) {
+      const double* v = s->verts + 9 * s->emit_tri[e];
+      double e1[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]};
+      double e2[3] = {v[6] - v[0], v[7] - v[1], v[8] - v[2]};
+      double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2],
+             cz = e1[0] * e2[1] - e1[1] * e2[0];
+      s->emit_area[e] = 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+      s->emit_of_tri[s->emit_tri[e]] = e;
+    }
+    if (lwo_alias_build(d->emit_weight, s->nemit, s->emit_prob, s->emit_alias, s->emit_pdf)) s->nemit = 0;
+  }
+  s->env_kind = d->env_kind;
+  s->env_w = d->env_width;
+  s->env_h = d->env_height;
+  if (s->env_kind == LW_ENV_IMAGE) {
+    int64_t nt = (int64_t)s->env_w * s->env_h;
+    s->env_img = (float*)malloc(sizeof(float) * 3 * nt);
+    memcpy(s->env_img, d->env_image, sizeof(float) * 3 * nt);
+    s->env_prob = (double*)malloc(sizeof(double) * nt);
+    s->env_alias = (int32_t*)malloc(sizeof(int32_t) * nt);
+    s->env_pdf = (double*)malloc(sizeof(double) * nt);
+    if (lwo_alias_build(d->env_weight, nt, s->env_prob, s->env_alias, s->env_pdf)) s->env_kind = LW_ENV_NONE;
+  }
+  int has_env = s->env_kind != LW_ENV_NONE;
+  int has_tri = s->nemit > 0;
+  s->p_env = has_env ? (has_tri ? d->p_env : 1.0) : 0.0;
+  s->p_tri = has_tri ? (has_env ? 1.0 - d->p_env : 1.0) : 0.0;
+  return s;
+}
+
+void lwo_scene_destroy(lwo_scene* s) {
+  if (!s) return;
+  free(s->verts);
+  free(s->normals);
+  free(s->material);
+  free(s->materials);
+  free(s->bounds);
+  free(s->children);
+  free(s->order);
+  free(s->rnodes);
+  free(s->lverts);
+  free(s->ltri);
+  free(s->emit_of_tri);
+  free(s->emit_tri);
+  free(s->emit_rad);
+  free(s->emit_two);
+  free(s->emit_area);
+  free(s->emit_prob);
+  free(s->emit_alias);
+  free(s->emit_pdf);
+  free(s->env_img);
+  free(s->env_prob);
+  free(s->env_alias);
+  free(s->env_pdf);
+  free(s);
+}
+
+/* ---- render traversal: near-first over child boxes, conservative cull ----- */
+
+#define CULL_M 9.094947017729282e-13 /* 2^-40 relative slack on every slab comparison */
+
+typedef struct {
+  double o[3], inv[3];
+  int zero[3];
+  shear sh;
+} rray;
+
+static void rray_setup(rray* r, const double* o, const double* d) {
+  for (int a = 0; a < 3; a++) {
+    r->o[a] = o[a];
+    r->zero[a] = !(d[a] > 1e-200 || d[a] < -1e-200);
+    r->inv[a] = r->zero[a] ? 0.0 : 1.0 / d[a];
+  }
+  shear_setup(o, d, 0, &r->sh);
+}
+
+/* returns 1 if the box may contain a hit in [0, best]; *tn_out = raw entry distance */
+static int box_hit(const rray* r, const double* box, double best, double* tn_out) {
+  double tn = -INFINITY, tf = INFINITY;
+  for (int a = 0; a < 3; a++) {
+    if (r->zero[a]) {
+      if (r->o[a] < box[a] || r->o[a] > box[3 + a]) return 0;
+      continue;
+    }
+    double t0 = (box[a] - r->o[a]) * r->inv[a];
+    double t1 = (box[3 + a] - r->o[a]) * r->inv[a];
+    if (t0 > t1) {
+      double t = t0;
+      t0 = t1;
+      t1 = t;
+    }
+    if (t0 > tn) tn = t0;
+    if (t1 < tf) tf = t1;
+  }
+  double tn_lo = tn - CULL_M * fabs(tn);
+  double tf_hi = tf + CULL_M * fabs(tf);
+  double best_hi = best + CULL_M * fabs(best);
+  *tn_out = tn;
+  return tn_lo <= tf_hi && tn_lo <= best_hi && tf_hi >= 0.0;
+}
+
+static int pop_keep(double tn, double best) { return tn - CULL_M * fabs(tn) <= best + CULL_M * fabs(best); }
+
+static void leaf_decode(int32_t ref, int64_t* start, int64_t* count) {
+  int64_t v = -(int64_t)ref - 1;
+  *start = v >> 3;
+  *count = v & 7;
+}
+
+/* closest hit; tie -> lower original triangle id */
+static void trace_closest(const lwo_scene* s, const double* o, const double* d, double tmax, hitrec* h) {
+  h->t = tmax;
+  h->tri = -1;
+  h->bu = h->bv = 0.0;
+  if (s->ntris == 0) return;
+  rray r;
+  rray_setup(&r, o, d);
+  double tn;
+  if (!box_hit(&r, s->root_box, h->t, &tn)) return;
+  int32_t stack_ref[64];
+  double stack_tn[64];
+  int sp = 0;
+  int32_t ref = s->root_ref;
+  for (;;) {
+    while (ref >= 0) {
+      const rnode* nd = s->rnodes + ref;
+      double tn0, tn1;
+      int h0 = box_hit(&r, nd->box[0], h->t, &tn0);
+      int h1 = box_hit(&r, nd->box[1], h->t, &tn1);
+      if (h0 && h1) {
+        if (tn1 < tn0) {
+          stack_ref[sp] = nd->ref[0];
+          stack_tn[sp++] = tn0;
+          ref = nd->ref[1];
+        } else {
+          stack_ref[sp] = nd->ref[1];
+          stack_tn[sp++] = tn1;
+          ref = nd->ref[0];
+        }
+      } else if (h0) {
+        ref = nd->ref[0];
+      } else if (h1) {
+        ref = nd->ref[1];
+      } else {
+        ref = 0x7fffffff; /* nothing to descend into */
+        break;
+      }
+    }
+    if (ref != 0x7fffffff) {
+      int64_t start, count;
+      leaf_decode(ref, &start, &count);
+      for (int64_t k = start; k < start + count; k++) tri_test(s->lverts + 9 * k, s->ltri[k], &r.sh, 0.0, h);
+    }
+    ref = 0x7fffffff;
+    while (sp > 0) {
+      sp--;
+      if (pop_keep(stack_tn[sp], h->t)) {
+        ref = stack_ref[sp];
+        break;
+      }
+    }
+    if (ref == 0x7fffffff) return;
+  }
+}
+
+/* any hit with 0 < t < tmax */
+static int trace_any(const lwo_scene* s, const double* o, const double* d, double tmax) {
+  if (s->ntris == 0) return 0;
+  rray r;
+  rray_setup(&r, o, d);
+  double tn;
+  if (!box_hit(&r, s->root_box, tmax, &tn)) return 0;
+  int32_t stack_ref[64];
+  int sp = 0;
+  int32_t ref = s->root_ref;
+  for (;;) {
+    while (ref >= 0) {
+      const rnode* nd = s->rnodes + ref;
+      double tn0, tn1;
+      int h0 = box_hit(&r, nd->box[0], tmax, &tn0);
+      int h1 = box_hit(&r, nd->box[1], tmax, &tn1);
+      if (h0 && h1) {
+        stack_ref[sp++] = nd->ref[1];
+        ref = nd->ref[0];
+      } else if (h0) {
+        ref = nd->ref[0];
+      } else if (h1) {
+        ref = nd->ref[1];
+      } else {
+        ref = 0x7fffffff;
+        break;
+      }
+    }
+    if (ref != 0x7fffffff) {
+      int64_t start, count;
+      leaf_decode(ref, &start, &count);
+      for (int64_t k = start; k < start + count; k++)
+        if (tri_occludes(s->lverts + 9 * k, &r.sh, tmax)) return 1;
+    }
+    if (sp == 0) return 0;
+    ref = stack_ref[--sp];
+  }
+}
+
+void lwo_trace_closest_batch(const lwo_scene* s, const double* origins, const double* dirs, const double* tmaxs,
+                             int64_t n, double* out_t, int64_t* out_tri, double* out_bary) {
+  for (int64_t i = 0; i < n; i++) {
+    hitrec h;
+    trace_closest(s, origins + 3 * i, dirs + 3 * i, tmaxs[i], &h);
+    if (h.tri >= 0) {
+      out_t[i] = h.t;
+      out_tri[i] = h.tri;
+      out_bary[2 * i] = h.bu;
+      out_bary[2 * i + 1] = h.bv;
+    } else {
+      out_t[i] = 1e308;
+      out_tri[i] = -1;
+      out_bary[2 * i] = out_bary[2 * i + 1] = 0.0;
+    }
+  }
+}
+
+void lwo_trace_any_batch(const lwo_scene* s, const double* origins, const double* dirs, const double* tmaxs,
+                         int64_t n, int32_t* out) {
+  for (int64_t i = 0; i < n; i++) out[i] = trace_any(s, origins + 3 * i, dirs + 3 * i, tmaxs[i]);
+}
+
+/* ========================================================================== */
+/* Integrator                                 */
+/* ========================================================================== */
+
+typedef struct {
+  double x, y, z;
+} v3;
+
+static v3 mk(double x, double y, double z) {
+  v3 r = {x, y, z};
+  return r;
+}
+static v3 add(v3 a, v3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
+static v3 sub(v3 a, v3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+static v3 scl(v3 a, double s) { return mk(a.x * s, a.y * s, a.z * s); }
+static v3 neg(v3 a) { return mk(-a.x, -a.y, -a.z); }
+static double dot(v3 a, v3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+static v3 cross(v3 a, v3 b) { return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x); }
+static v3 normalize(v3 a) {
+  double l = sqrt(dot(a, a));
+  return mk(a.x / l, a.y / l, a.z / l);
+}
+static v3 ld3(const double* p) { return mk(p[0], p[1], p[2]); }
+static v3 bary3(v3 a, v3 b, v3 c, double w, double bu, double bv) {
+  return mk((w * a.x + bu * b.x) + bv * c.x, (w * a.y + bu * b.y) + bv * c.y, (w * a.z + bu * b.z) + bv * c.z);
+}
+
+typedef struct {
+  const lwo_scene* s;
+  const lw_render_params* p;
+} rctx;
+
+static double qmc(const rctx* c, int64_t dim, int64_t index) {
+  return lwo_halton_dim(c->p->bases, c->p->perm_flat, c->p->perm_offset, dim, index);
+}
+
+/* camera ray */
+static void camera_ray(const rctx* c, int64_t index, v3* o, v3* d) {
+  const lw_scene_desc* sd = &c->s->d;
+  int64_t W = c->p->width, H = c->p->height, P = W * H;
+  int64_t pix = index % P;
+  int64_t x = pix % W, y = pix / W;
+  double dx = lwo_gauss_filter_offset(qmc(c, 0, index));
+  double dy = lwo_gauss_filter_offset(qmc(c, 1, index));
+  double fx = (((double)x + 0.5) + dx) / (double)W;
+  double fy = (((double)y + 0.5) + dy) / (double)H;
+  double sx = fx * 2.0 - 1.0;
+  double sy = 1.0 - fy * 2.0;
+  double aspect = (double)W / (double)H;
+  double ax = sx * (sd->tan_half_fov * aspect);
+  double ay = sy * sd->tan_half_fov;
+  v3 f = ld3(sd->cam_fwd), r = ld3(sd->cam_right), u = ld3(sd->cam_up);
+  v3 dd = mk((f.x + ax * r.x) + ay * u.x, (f.y + ax * r.y) + ay * u.y, (f.z + ax * r.z) + ay * u.z);
+  *d = normalize(dd);
+  *o = ld3(sd->cam_pos);
+}
+
+void lwo_camera_rays(const lwo_scene* s, const lw_render_params* p, const int64_t* idx, int64_t n, double* oo,
+                     double* od) {
+  rctx c = {s, p};
+  for (int64_t i = 0; i < n; i++) {
+    v3 o, d;
+    camera_ray(&c, idx[i], &o, &d);
+    oo[3 * i] = o.x;
+    oo[3 * i + 1] = o.y;
+    oo[3 * i + 2] = o.z;
+    od[3 * i] = d.x;
+    od[3 * i + 1] = d.y;
+    od[3 * i + 2] = d.z;
+  }
+}
+
+static v3 offset_origin(v3 p, v3 n, v3 dir) {
+  double m = fabs(p.x);
+  if (fabs(p.y) > m) m = fabs(p.y);
+  if (fabs(p.z) > m) m = fabs(p.z);
+  if (m < 1.0) m = 1.0;
+  double eps = 1e-9 * m;
+  double sgn = dot(n, dir) >= 0.0 ? eps : -eps;
+  return mk(p.x + n.x * sgn, p.y + n.y * sgn, p.z + n.z * sgn);
+}
+
+/* environment lookup: lat-long, y up, row 0 at +y */
+static v3 env_eval(const lwo_scene* s, v3 d, double* pdf) {
+  if (s->env_kind == LW_ENV_CONSTANT) {
+    *pdf = s->p_env * LW_INV_FOUR_PI;
+    return scl(ld3(s->d.env_constant), s->d.env_scale);
+  }
+  if (s->env_kind == LW_ENV_IMAGE) {
+    double phi = lwo_atan2(d.z, d.x);
+    if (phi < 0.0) phi = phi + LW_TWO_PI;
+    double sin_t = sqrt(d.x * d.x + d.z * d.z);
+    double theta = lwo_atan2(sin_t, d.y);
+    int64_t W = s->env_w, H = s->env_h;
+    int64_t col = (int64_t)(phi / LW_TWO_PI * (double)W);
+    int64_t row = (int64_t)(theta / LW_PI * (double)H);
+    if (col >= W) col = W - 1;
+    if (row >= H) row = H - 1;
+    if (col < 0) col = 0;
+    if (row < 0) row = 0;
+    int64_t j = row * W + col;
+    *pdf = sin_t > 0.0 ? s->p_env * s->env_pdf[j] * (double)(W * H) / (LW_TWO_PI_SQ * sin_t) : 0.0;
+    const float* px = s->env_img + 3 * j;
+    return mk((double)px[0] * s->d.env_scale, (double)px[1] * s->d.env_scale, (double)px[2] * s->d.env_scale);
+  }
+  *pdf = 0.0;
+  return mk(0, 0, 0);
+}
+
+/* ---- BSDF ------------------------------------------------- */
+
+typedef struct {
+  v3 t, b, n;
+} frame;
+
+static frame make_frame(v3 n) { /* Duff et al. 2017 */
+  frame f;
+  double sgn = n.z >= 0.0 ? 1.0 : -1.0;
+  double a = -1.0 / (sgn + n.z);
+  double b = n.x * n.y * a;
+  f.t = mk(1.0 + sgn * n.x * n.x * a, sgn * b, -sgn * n.x);
+  f.b = mk(b, sgn + n.y * n.y * a, -n.y);
+  f.n = n;
+  return f;
+}
+static v3 to_local(const frame* f, v3 v) { return mk(dot(v, f->t), dot(v, f->b), dot(v, f->n)); }
+static v3 to_world(const frame* f, v3 v) {
+  return mk((v.x * f->t.x + v.y * f->b.x) + v.z * f->n.x, (v.x * f->t.y + v.y * f->b.y) + v.z * f->n.y,
+            (v.x * f->t.z + v.y * f->b.z) + v.z * f->n.z);
+}
+
+typedef struct {
+  double a[LW_MAX_LAYERS]; /* layer mixture weights */
+  double sum_a;
+  int nonspec; /* any non-delta layer with a > 0 */
+} layerw;
+
+static double schlick(double cosv, double ior) {
+  double r0 = (ior - 1.0) / (ior + 1.0);
+  double f0 = r0 * r0;
+  double m = 1.0 - cosv;
+  double m2 = m * m;
+  return f0 + (1.0 - f0) * (m2 * m2 * m);
+}
+
+static void layer_weights(const lw_material* m, double cos_o, layerw* lw) {
+  double r = 1.0;
+  lw->sum_a = 0.0;
+  lw->nonspec = 0;
+  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+    lw->a[l] = 0.0;
+    if (l >= m->nlayers) continue;
+    const lw_layer* L = m->layers + l;
+    double a = L->coat ? r * (L->weight * schlick(cos_o, m->ior)) : r * L->weight;
+    lw->a[l] = a;
+    r = r - a;
+    lw->sum_a = lw->sum_a + a;
+    if (a > 0.0 && (L->kind == LW_BSDF_DIFFUSE || L->kind == LW_BSDF_GLOSSY)) lw->nonspec = 1;
+  }
+}
+
+static double ggx_d(double alpha, double cos_h) {
+  double a2 = alpha * alpha;
+  double t = cos_h * cos_h * (a2 - 1.0) + 1.0;
+  return a2 / (LW_PI * (t * t));
+}
+static double ggx_g1(double alpha, double cos_v) {
+  double a2 = alpha * alpha;
+  return 2.0 * cos_v / (cos_v + sqrt(a2 + (1.0 - a2) * (cos_v * cos_v)));
+}
+static double alpha_of(const lw_layer* L) {
+  double a = L->roughness;
+  if (a < 1e-4) a = 1e-4;
+  if (a > 1.0) a = 1.0;
+  return a;
+}
+
+/* non-delta part of the layered BSDF: f (rgb) and mixture pdf (solid angle) */
+static v3 bsdf_eval(const lw_material* m, const layerw* lw, v3 wo, v3 wi, double* pdf) {
+  v3 f = mk(0, 0, 0);
+  *pdf = 0.0;
+  if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw->sum_a > 0.0)) return f;
+  for (int l = 0; l < m->nlayers; l++) {
+    const lw_layer* L = m->layers + l;
+    double a = lw->a[l];
+    if (!(a > 0.0)) continue;
+    double sel = a / lw->sum_a;
+    if (L->kind == LW_BSDF_DIFFUSE) {
+      double k = a * LW_INV_PI;
+      f = add(f, mk(L->tint[0] * k, L->tint[1] * k, L->tint[2] * k));
+      *pdf = *pdf + sel * (wi.z * LW_INV_PI);
+    } else if (L->kind == LW_BSDF_GLOSSY) {
+      double al = alpha_of(L);
+      v3 h = normalize(add(wo, wi));
+      double D = ggx_d(al, h.z);
+      double G = ggx_g1(al, wo.z) * ggx_g1(al, wi.z);
+      double k = a * (D * G / (4.0 * wo.z * wi.z));
+      f = add(f, mk(L->tint[0] * k, L->tint[1] * k, L->tint[2] * k));
+      double oh = dot(wo, h);
+      if (oh > 0.0) *pdf = *pdf + sel * (D * h.z / (4.0 * oh));
+    }
+  }
+  return f;
+}
+
+static double fresnel_dielectric(double cos_i, double eta) { /* eta = eta_i / eta_t */
+  double sin2t = eta * eta * (1.0 - cos_i * cos_i);
+  if (sin2t >= 1.0) return 1.0;
+  double cos_t = sqrt(1.0 - sin2t);
+  double rs = (eta * cos_i - cos_t) / (eta * cos_i + cos_t);
+  double rp = (cos_i - eta * cos_t) / (cos_i + eta * cos_t);
+  return 0.5 * (rs * rs + rp * rp);
+}
+
+typedef struct {
+  v3 wi;       /* local */
+  v3 weight;   /* f * cos / pdf */
+  double pdf;  /* mixture pdf (non-delta) */
+  int delta;
+  int transmit;
+} bsample;
+
+/* returns 0 if no valid sample */
+static int bsdf_sample(const lw_material* m, const layerw* lw, v3 wo, int front, double u, double v, bsample* bs) {
+  if (!(lw->sum_a > 0.0) || wo.z <= 0.0) return 0;
+  double x = u * lw->sum_a;
+  int pick = -1;
+  double cum = 0.0, prev = 0.0;
+  for (int l = 0; l < m->nlayers; l++) {
+    if (!(lw->a[l] > 0.0)) continue;
+    prev = cum;
+    cum = cum + lw->a[l];
+    pick = l;
+    if (x < cum) break;
+  }
+  if (pick < 0) return 0;
+  double ur = (x - prev) / lw->a[pick];
+  if (ur < 0.0) ur = 0.0;
+  if (ur >= 1.0) ur = 0.9999999999999999;
+  const lw_layer* L = m->layers + pick;
+  bs->delta = 0;
+  bs->transmit = 0;
+  if (L->kind == LW_BSDF_DIFFUSE) {
+    double r = sqrt(ur), sp, cp;
+    lwo_sincos2pi(v, &sp, &cp);
+    double z = 1.0 - ur;
+    bs->wi = mk(r * cp, r * sp, sqrt(z > 0.0 ? z : 0.0));
+  } else if (L->kind == LW_BSDF_GLOSSY) {
+    double al = alpha_of(L);
+    double tan2 = al * al * ur / (1.0 - ur);
+    double ch = 1.0 / sqrt(1.0 + tan2);
+    double sh2 = 1.0 - ch * ch;
+    double sh = sqrt(sh2 > 0.0 ? sh2 : 0.0);
+    double sp, cp;
+    lwo_sincos2pi(v, &sp, &cp);
+    v3 h = mk(sh * cp, sh * sp, ch);
+    double oh = dot(wo, h);
+    bs->wi = sub(scl(h, 2.0 * oh), wo);
+  } else if (L->kind == LW_BSDF_SPECULAR_REFLECT) {
+    bs->wi = mk(-wo.x, -wo.y, wo.z);
+    bs->delta = 1;
+    bs->weight = mk(lw->sum_a * L->tint[0], lw->sum_a * L->tint[1], lw->sum_a * L->tint[2]);
+    bs->pdf = 0.0;
+    return 1;
+  } else { /* specular transmit: dielectric, choose reflect/refract by Fresnel */
+    double eta = front ? 1.0 / m->ior : m->ior;
+    double F = fresnel_dielectric(wo.z, eta);
+    bs->delta = 1;
+    bs->pdf = 0.0;
+    if (ur < F) {
+      bs->wi = mk(-wo.x, -wo.y, wo.z);
+      bs->weight = mk(lw->sum_a * L->tint[0], lw->sum_a * L->tint[1], lw->sum_a * L->tint[2]);
+    } else {
+      double sin2t = eta * eta * (1.0 - wo.z * wo.z);
+      double cos_t = sqrt(1.0 - sin2t);
+      bs->wi = mk(-eta * wo.x, -eta * wo.y, -cos_t);
+      bs->transmit = 1;
+      double k = lw->sum_a * (eta * eta);
+      bs->weight = mk(k * L->tint[0], k * L->tint[1], k * L->tint[2]);
+    }
+    return 1;
+  }
+  if (bs->wi.z <= 0.0) return 0;
+  double pdf;
+  v3 f = bsdf_eval(m, lw, wo, bs->wi, &pdf);
+  if (!(pdf > 0.0)) return 0;
+  double k = bs->wi.z / pdf;
+  bs->weight = mk(f.x * k, f.y * k, f.z * k);
+  bs->pdf = pdf;
+  return 1;
+}
+
+static int has_light(const lwo_scene* s) { return s->nemit > 0 || s->env_kind != LW_ENV_NONE; }
+
+static void accumulate(int64_t* fb, int64_t pix, v3 L, lw_render_stats* st) {
+  double c[3] = {L.x, L.y, L.z};
+  for (int k = 0; k < 3; k++) {
+    double v = c[k];
+    if (!(v == v) || v == INFINITY || v == -INFINITY) {
+      if (st) st->nonfinite++;
+      v = 0.0;
+    }
+    if (v < 0.0) v = 0.0;
+    if (v > LW_FB_SAMPLE_CLAMP) v = LW_FB_SAMPLE_CLAMP;
+    fb[3 * pix + k] += (int64_t)llrint(v * 1048576.0);
+  }
+}
+
+/* one path, DESIGN.md §4 (SPEC.md:385-402 trace_eye_path / next_event) */
+static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
+  const lwo_scene* s = c->s;
+  int depth = c->p->max_depth;
+  v3 o, d;
+  camera_ray(c, index, &o, &d);
+  v3 beta = mk(1, 1, 1), L = mk(0, 0, 0);
+  int spec_prev = 1;
+  double pdf_prev = 0.0;
+  for (int b = 0; b < depth; b++) {
+    hitrec h;
+    trace_closest(s, &o.x, &d.x, INFINITY, &h);
+    if (st) st->rays_extension++;
+    if (h.tri < 0) {
+      if (s->env_kind != LW_ENV_NONE) {
+        double pe;
+        v3 Le = env_eval(s, d, &pe);
+        double w = spec_prev ? 1.0 : pdf_prev / (pdf_prev + pe);
+        L = add(L, mk(beta.x * Le.x * w, beta.y * Le.y * w, beta.z * Le.z * w));
+      }
+      break;
+    }
+    const double* vv = s->verts + 9 * h.tri;
+    v3 v0 = ld3(vv), v1 = ld3(vv + 3), v2 = ld3(vv + 6);
+    double w = (1.0 - h.bu) - h.bv;
+    v3 p = bary3(v0, v1, v2, w, h.bu, h.bv);
+    v3 e1 = sub(v1, v0), e2 = sub(v2, v0);
+    v3 ng = normalize(cross(e1, e2));
+    int front = dot(ng, d) < 0.0;
+    /* emission with MIS against the light-sampling strategy */
+    int64_t e = s->emit_of_tri[h.tri];
+    if (e >= 0 && s->nemit > 0 && (front || s->emit_two[e])) {
+      v3 Le = ld3(s->emit_rad + 3 * e);
+      double wm = 1.0;
+      if (!spec_prev) {
+        double cos_l = fabs(dot(ng, d));
+        double pdf_area = s->p_tri * s->emit_pdf[e] / s->emit_area[e];
+        double pl = pdf_area * (h.t * h.t) / cos_l;
+        wm = pdf_prev / (pdf_prev + pl);
+      }
+      L = add(L, mk(beta.x * Le.x * wm, beta.y * Le.y * wm, beta.z * Le.z * wm));
+    }
+    if (b == depth - 1) break;
+    /* shading frame */
+    const double* nn = s->normals + 9 * h.tri;
+    v3 ns = bary3(ld3(nn), ld3(nn + 3), ld3(nn + 6), w, h.bu, h.bv);
+    double nl = dot(ns, ns);
+    ns = nl > 0.0 ? scl(ns, 1.0 / sqrt(nl)) : ng;
+    v3 wo = neg(d);
+    v3 ngf = front ? ng : neg(ng);
+    if (dot(ns, ngf) < 0.0) ns = neg(ns);
+    if (dot(ns, wo) <= 0.0) ns = ngf;
+    frame fr = make_frame(ns);
+    v3 wol = to_local(&fr, wo);
+    const lw_material* m = s->materials + s->material[h.tri];
+    layerw lw;
+    layer_weights(m, wol.z, &lw);
+    int64_t bd = 4 + 8 * (int64_t)b;
+    /* next-event estimation */
+    if (lw.nonspec && has_light(s)) {
+      double ul = qmc(c, bd + 2, index), vl = qmc(c, bd + 3, index);
+      v3 wi, Le = mk(0, 0, 0);
+      double pl = 0.0, tmax_sh = INFINITY;
+      int ok = 0;
+      if (s->env_kind != LW_ENV_NONE && ul < s->p_env) {
+        double ue = s->nemit > 0 ? ul / s->p_env : ul;
+        if (s->env_kind == LW_ENV_CONSTANT) {
+          double z = 1.0 - 2.0 * ue;
+          double r2 = 1.0 - z * z;
+          double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
+          lwo_sincos2pi(vl, &sp, &cp);
+          wi = mk(r * cp, z, r * sp);
+          pl = s->p_env * LW_INV_FOUR_PI;
+          Le = scl(ld3(s->d.env_constant), s->d.env_scale);
+          ok = 1;
+        } else {
+          double ur;
+          int64_t j = alias_sample(s->env_prob, s->env_alias, (int64_t)s->env_w * s->env_h, ue, &ur);
+          int64_t row = j / s->env_w, col = j % s->env_w;
+          double uu = ((double)col + ur) / (double)s->env_w;
+          double vv2 = ((double)row + vl) / (double)s->env_h;
+          double st_, ct, sp, cp;
+          lwo_sincos2pi(vv2 * 0.5, &st_, &ct);
+          lwo_sincos2pi(uu, &sp, &cp);
+          wi = mk(st_ * cp, ct, st_ * sp);
+          if (st_ > 0.0) {
+            pl = s->p_env * s->env_pdf[j] * (double)((int64_t)s->env_w * s->env_h) / (LW_TWO_PI_SQ * st_);
+            const float* px = s->env_img + 3 * j;
+            Le = mk((double)px[0] * s->d.env_scale, (double)px[1] * s->d.env_scale, (double)px[2] * s->d.env_scale);
+            ok = 1;
+          }
+        }
+      } else if (s->nemit > 0) {
+        double ut = s->env_kind != LW_ENV_NONE ? (ul - s->p_env) / (1.0 - s->p_env) : ul;
+        double ur;
+        int64_t le = alias_sample(s->emit_prob, s->emit_alias, s->nemit, ut, &ur);
+        const double* lv = s->verts + 9 * s->emit_tri[le];
+        v3 l0 = ld3(lv), l1 = ld3(lv + 3), l2 = ld3(lv + 6);
+        double su = sqrt(ur);
+        double b0 = 1.0 - su, b1 = vl * su;
+        double b2 = (1.0 - b0) - b1;
+        v3 q = bary3(l0, l1, l2, b0, b1, b2);
+        v3 dl = sub(q, p);
+        double dist2 = dot(dl, dl);
+        double dist = sqrt(dist2);
+        wi = mk(dl.x / dist, dl.y / dist, dl.z / dist);
+        v3 ngl = normalize(cross(sub(l1, l0), sub(l2, l0)));
+        double cos_l = -dot(ngl, wi);
+        if (s->emit_two[le]) cos_l = fabs(cos_l);
+        if (cos_l > 0.0 && dist > 0.0) {
+          pl = (s->p_tri * s->emit_pdf[le] / s->emit_area[le]) * dist2 / cos_l;
+          Le = ld3(s->emit_rad + 3 * le);
+          tmax_sh = dist * (1.0 - 1e-7);
+          ok = 1;
+        }
+      }
+      if (ok && pl > 0.0 && dot(ngf, wi) > 0.0) {
+        v3 wil = to_local(&fr, wi);
+        double pb;
+        v3 f = bsdf_eval(m, &lw, wol, wil, &pb);
+        if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
+          double wm = pl / (pl + pb);
+          double k = (wil.z * wm) / pl;
+          v3 contrib = mk(beta.x * f.x * Le.x * k, beta.y * f.y * Le.y * k, beta.z * f.z * Le.z * k);
+          v3 so = offset_origin(p, ngf, wi);
+          if (st) st->rays_shadow++;
+          if (!trace_any(s, &so.x, &wi.x, tmax_sh)) L = add(L, contrib);
+        }
+      }
+    }
+    /* BSDF sampling */
+    bsample bs;
+    double ub = qmc(c, bd + 0, index), vb = qmc(c, bd + 1, index);
+    if (!bsdf_sample(m, &lw, wol, front, ub, vb, &bs)) break;
+    v3 wi = to_world(&fr, bs.wi);
+    double gside = dot(ngf, wi);
+    if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) break;
+    beta = mk(beta.x * bs.weight.x, beta.y * bs.weight.y, beta.z * bs.weight.z);
+    spec_prev = bs.delta;
+    pdf_prev = bs.pdf;
+    if (b >= c->p->rr_start) {
+      double q = beta.x;
+      if (beta.y > q) q = beta.y;
+      if (beta.z > q) q = beta.z;
+      if (q > 1.0) q = 1.0;
+      double ur = qmc(c, bd + 4, index);
+      if (!(ur < q)) break;
+      beta = mk(beta.x / q, beta.y / q, beta.z / q);
+    }
+    o = offset_origin(p, ngf, wi);
+    d = wi;
+  }
+  return L;
+}
+
+void lwo_render(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin, int64_t pix_end, int64_t it_begin,
+                int64_t it_end, int64_t* fb, int nthreads, lw_render_stats* stats) {
+  rctx c = {s, p};
+  int64_t P = (int64_t)p->width * p->height;
+  int64_t ext = 0, shd = 0, nonf = 0;
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads) reduction(+ : ext, shd, nonf)
+#endif
+  for (int64_t pix = pix_begin; pix < pix_end; pix++) {
+    lw_render_stats st;
+    memset(&st, 0, sizeof(st));
+    for (int64_t it = it_begin; it < it_end; it++) {
+      v3 L = trace_path(&c, it * P + pix, &st);
+      accumulate(fb, pix, L, &st);
+    }
+    ext += st.rays_extension;
+    shd += st.rays_shadow;
+    nonf += st.nonfinite;
+  }
+  (void)nthreads;
+  if (stats) {
+    stats->paths += (pix_end - pix_begin) * (it_end - it_begin);
+    stats->rays_extension += ext;
+    stats->rays_shadow += shd;
+    stats->nonfinite += nonf;
+  }
+}
+

@@ -1,0 +1,70 @@
+/*
+ * lw_oracle.h -- CPU restatement oracle for the lumenwave light-transport hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product (paper_1705_01263_b200/,
+ * include/, liblw_b200.so) links, imports or calls this code.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * use it, and only as the checker or the CPU baseline.
+ *
+ * Pinning: QMC, pixel filter, octahedral and traversal functions are checked
+ * bit-exactly against the reference's own Cython kernels compiled from
+ * /root/reference by oracle/Makefile (oracle/_ref/) and against golden
+ * vectors generated from the reference (tests/golden/, tests/gen_golden.py).
+ * The render path (lwo_render) restates SPEC.md (the reference has no
+ * renderer): it is "parity unpinned" beyond the SPEC known answers.
+ */
+#pragma once
+#include <stdint.h>
+#include "../include/lw_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* _kernels.py:160-222 */
+double lwo_halton_dim(const int64_t* bases, const int64_t* perm_flat, const int64_t* perm_offset,
+                      int64_t dim, int64_t index);
+void lwo_halton_batch(const int64_t* bases, const int64_t* perm_flat, const int64_t* perm_offset,
+                      int64_t dim, const int64_t* indices, int64_t n, double* out);
+
+/* _kernels.py:87-134 */
+double lwo_gauss_filter_offset(double u);
+void lwo_pixel_offset_batch(const double* u, int64_t n, double* out);
+
+/* _kernels.py:233-342 */
+int64_t lwo_oct_encode(double x, double y, double z);
+void lwo_oct_decode(int64_t packed, double* out3);
+void lwo_oct_roundtrip_batch(const double* vecs, int64_t n, double* out);
+
+/* _kernels.py:357-585.  mode: LW_TRAVERSE_COMPAT | LW_TRAVERSE_CORRECTED | LW_TRAVERSE_BRUTE */
+void lwo_intersect_batch(int mode, const double* bounds, const int64_t* children, const int64_t* order,
+                         const double* verts, int64_t ntris, const double* origins, const double* dirs,
+                         const double* tmaxs, int64_t n, double* out_t, int64_t* out_tri, double* out_bary);
+
+/* geometry.py:100-148.  Returns node count; arrays must hold 2*ntris-1 (>=1) nodes. */
+int64_t lwo_build_bvh(const double* verts, int64_t ntris, double* bounds, int64_t* children, int64_t* order);
+
+/* Vose alias table. prob/alias/pdf have n entries. Returns 0 on success. */
+int lwo_alias_build(const double* weights, int64_t n, double* prob, int32_t* alias, double* pdf);
+
+/* Closest hit / any hit in the render traversal order (near-first, conservative cull). */
+typedef struct lwo_scene lwo_scene;
+lwo_scene* lwo_scene_create(const lw_scene_desc* desc);
+void lwo_scene_destroy(lwo_scene* s);
+void lwo_trace_closest_batch(const lwo_scene* s, const double* origins, const double* dirs, const double* tmaxs,
+                             int64_t n, double* out_t, int64_t* out_tri, double* out_bary);
+void lwo_trace_any_batch(const lwo_scene* s, const double* origins, const double* dirs, const double* tmaxs,
+                         int64_t n, int32_t* out_occluded);
+void lwo_camera_rays(const lwo_scene* s, const lw_render_params* p, const int64_t* sample_index, int64_t n,
+                     double* out_o, double* out_d);
+/* Progressive render of pixels [pix_begin, pix_end) x iterations [it_begin, it_end) into fb (int64 W*H*3). */
+void lwo_render(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin, int64_t pix_end,
+                int64_t it_begin, int64_t it_end, int64_t* fb, int nthreads, lw_render_stats* stats);
+
+/* Deterministic math shared by oracle and device (restated independently in lw_detmath.cuh). */
+void lwo_sincos2pi(double u, double* s, double* c);
+double lwo_atan2(double y, double x);
+
+#ifdef __cplusplus
+}
+#endif

@@ -1,0 +1,397 @@
+// lw_capi.cu -- library plumbing and the stateless kernel entry points of include/lw_b200.h.
+//
+// Each entry replaces one function of the reference's Cython kernel module
+// (lumenwave/core/_kernels.py), keeping its argument meaning: caller-owned
+// C-contiguous buffers, misses encoded as data, no exceptions.  The host-buffer
+// variants copy in, launch one sm_100a kernel, and copy out on cudaStreamPerThread.
+#include <stdarg.h>
+#include <string.h>
+
+#include <vector>
+
+#include "lw_common.cuh"
+#include "lw_detmath.cuh"
+#include "lw_host.h"
+#include "lw_qmc.cuh"
+#include "lw_traverse.cuh"
+
+namespace lw {
+
+static thread_local std::string g_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_error = buf;
+}
+
+// qmc.py:153-164 construction, for `bits`-wide operands
+static void fast_divisor(uint64_t d, int bits, uint64_t& magic, int& shift, int& add) {
+  if ((d & (d - 1)) == 0) {
+    magic = 0;
+    shift = 63 - __builtin_clzll(d);
+    add = 0;
+    return;
+  }
+  int ell = 64 - __builtin_clzll(d - 1);
+  unsigned __int128 num = ((unsigned __int128)1) << (bits + ell);
+  unsigned __int128 m = (num + d - 1) / d;
+  unsigned __int128 lim = ((unsigned __int128)1) << bits;
+  if (m < lim) {
+    magic = (uint64_t)m;
+    shift = ell;
+    add = 0;
+  } else {
+    magic = (uint64_t)(m - lim);
+    shift = ell - 1;
+    add = 1;
+  }
+}
+
+int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_flat, int64_t perm_len,
+                    const int64_t* perm_offset, std::vector<QmcDim>& dims, std::vector<uint16_t>& perm) {
+  LW_CHECK_ARG(ndims > 0 && bases && perm_offset, "qmc tables: empty dimension table");
+  dims.resize(ndims);
+  perm.resize(perm_len > 0 ? perm_len : 1);
+  for (int64_t i = 0; i < perm_len; i++) {
+    LW_CHECK_ARG(perm_flat[i] >= 0 && perm_flat[i] < 65536, "qmc tables: permutation digit out of range");
+    perm[i] = (uint16_t)perm_flat[i];
+  }
+  for (int64_t k = 0; k < ndims; k++) {
+    int64_t b = bases[k];
+    LW_CHECK_ARG(b >= 2 && b < (1LL << 31), "qmc tables: base must be in [2, 2^31)");
+    LW_CHECK_ARG(b == 2 || (perm_offset[k] >= 0 && perm_offset[k] + b <= perm_len),
+                 "qmc tables: permutation slice out of range");
+    QmcDim& q = dims[k];
+    memset(&q, 0, sizeof(q));
+    q.base = (uint32_t)b;
+    q.perm_off = (uint32_t)(b == 2 ? 0 : perm_offset[k]);
+    uint64_t m;
+    int s, a;
+    fast_divisor((uint64_t)b, 32, m, s, a);
+    q.magic32 = (uint32_t)m;
+    q.shift32 = (uint8_t)s;
+    q.add32 = (uint8_t)a;
+    fast_divisor((uint64_t)b, 64, m, s, a);
+    q.magic64 = m;
+    q.shift64 = (uint8_t)s;
+    q.add64 = (uint8_t)a;
+    q.exact_limit = ((1ULL << 53) - 1) / (uint64_t)b;
+  }
+  return LW_OK;
+}
+
+// Vose alias table, identical in operation order to oracle lwo_alias_build
+int alias_build(const double* w, int64_t n, double* prob, int32_t* alias, double* pdf) {
+  LW_CHECK_ARG(n > 0, "alias table: no entries");
+  double total = 0.0;
+  for (int64_t i = 0; i < n; i++) {
+    LW_CHECK_ARG(w[i] >= 0.0 && w[i] != INFINITY, "alias table: weights must be finite and >= 0");
+    total += w[i];
+  }
+  LW_CHECK_ARG(total > 0.0, "alias table: all weights are zero");
+  std::vector<double> scaled(n);
+  std::vector<int64_t> small(n), large(n);
+  int64_t ns = 0, nl = 0;
+  double dn = (double)n;
+  for (int64_t i = 0; i < n; i++) {
+    pdf[i] = w[i] / total;
+    scaled[i] = pdf[i] * dn;
+    if (scaled[i] < 1.0)
+      small[ns++] = i;
+    else
+      large[nl++] = i;
+  }
+  while (ns > 0 && nl > 0) {
+    int64_t s = small[--ns];
+    int64_t l = large[--nl];
+    prob[s] = scaled[s];
+    alias[s] = (int32_t)l;
+    scaled[l] = (scaled[l] + scaled[s]) - 1.0;
+    if (scaled[l] < 1.0)
+      small[ns++] = l;
+    else
+      large[nl++] = l;
+  }
+  while (nl > 0) {
+    int64_t l = large[--nl];
+    prob[l] = 1.0;
+    alias[l] = (int32_t)l;
+  }
+  while (ns > 0) {
+    int64_t s = small[--ns];
+    prob[s] = 1.0;
+    alias[s] = (int32_t)s;
+  }
+  return LW_OK;
+}
+
+}  // namespace lw
+
+using namespace lw;
+
+// ---- kernels ------------------------------------------------------------------------------
+
+__global__ void k_halton(const QmcDim* __restrict__ dims, const uint16_t* __restrict__ perm, int dim,
+                         const long long* __restrict__ idx, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = lw_halton(dims, perm, dim, idx[i]);
+}
+
+__global__ void k_pixel_offset(const double* __restrict__ u, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = lw_gauss_filter_offset(u[i]);
+}
+
+// oct_roundtrip_batch (_kernels.py:321-342): rows whose decoded length is 0 are untouched
+__global__ void k_oct_roundtrip(const double* __restrict__ v, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    v3 d = lw_oct_decode(lw_oct_encode(v[3 * i], v[3 * i + 1], v[3 * i + 2]));
+    double ln = sqrt(d.x * d.x + d.y * d.y + d.z * d.z);
+    if (ln > 0.0) {
+      out[3 * i] = d.x / ln;
+      out[3 * i + 1] = d.y / ln;
+      out[3 * i + 2] = d.z / ln;
+    }
+  }
+}
+
+__global__ void k_oct_encode(const double* __restrict__ v, long long n, long long* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = lw_oct_encode(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+}
+
+__global__ void k_oct_decode(const long long* __restrict__ p, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    v3 d = lw_oct_decode(p[i]);
+    out[3 * i] = d.x;
+    out[3 * i + 1] = d.y;
+    out[3 * i + 2] = d.z;
+  }
+}
+
+__global__ void k_intersect_ref(int compat, const double* __restrict__ bounds, const long long* __restrict__ children,
+                                const long long* __restrict__ order, const double* __restrict__ verts, long long ntris,
+                                const double* __restrict__ origins, const double* __restrict__ dirs,
+                                const double* __restrict__ tmaxs, long long n, double* __restrict__ out_t,
+                                long long* __restrict__ out_tri, double* __restrict__ out_bary) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double o[3] = {origins[3 * i], origins[3 * i + 1], origins[3 * i + 2]};
+  double d[3] = {dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]};
+  LwHit h;
+  lw_traverse_ref(compat != 0, bounds, children, order, verts, ntris, o, d, tmaxs[i], h);
+  if (h.tri >= 0) {
+    out_t[i] = h.t;
+    out_tri[i] = h.tri;
+    out_bary[2 * i] = h.bu;
+    out_bary[2 * i + 1] = h.bv;
+  } else {
+    out_t[i] = 1e308;
+    out_tri[i] = -1;
+    out_bary[2 * i] = 0.0;
+    out_bary[2 * i + 1] = 0.0;
+  }
+}
+
+__global__ void k_intersect_brute(const double* __restrict__ verts, long long ntris, const double* __restrict__ origins,
+                                  const double* __restrict__ dirs, const double* __restrict__ tmaxs, long long n,
+                                  double* __restrict__ out_t, long long* __restrict__ out_tri,
+                                  double* __restrict__ out_bary) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double o[3] = {origins[3 * i], origins[3 * i + 1], origins[3 * i + 2]};
+  double d[3] = {dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]};
+  LwShear s;
+  lw_shear_setup(o, d, false, s);
+  LwHit h;
+  h.t = tmaxs[i];
+  h.tri = -1;
+  h.bu = h.bv = 0.0;
+  for (long long k = 0; k < ntris; k++) lw_tri_test(verts + 9 * k, k, s, 0.0, h);
+  if (h.tri >= 0) {
+    out_t[i] = h.t;
+    out_tri[i] = h.tri;
+    out_bary[2 * i] = h.bu;
+    out_bary[2 * i + 1] = h.bv;
+  } else {
+    out_t[i] = 1e308;
+    out_tri[i] = -1;
+    out_bary[2 * i] = 0.0;
+    out_bary[2 * i + 1] = 0.0;
+  }
+}
+
+// ---- C ABI --------------------------------------------------------------------------------
+
+#define S_ cudaStreamPerThread
+
+template <class T>
+static int upload(DevBuf& b, const T* host, int64_t count) {
+  LW_CUDA_TRY(b.alloc(sizeof(T) * (count > 0 ? count : 1)));
+  if (count > 0) LW_CUDA_TRY(cudaMemcpyAsync(b.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, S_));
+  return LW_OK;
+}
+
+extern "C" {
+
+const char* lw_last_error(void) { return g_error.c_str(); }
+int lw_abi_version(void) { return LW_ABI_VERSION; }
+
+int lw_device_count(int* count) {
+  LW_CHECK_ARG(count, "null count");
+  LW_CUDA_TRY(cudaGetDeviceCount(count));
+  return LW_OK;
+}
+
+int lw_set_device(int device) {
+  LW_CUDA_TRY(cudaSetDevice(device));
+  return LW_OK;
+}
+
+int lw_alias_build(const double* weights, int64_t n, double* prob, int32_t* alias, double* pdf) {
+  LW_CHECK_ARG(weights && prob && alias && pdf, "null pointer");
+  return alias_build(weights, n, prob, alias, pdf);
+}
+
+static int halton_impl(const int64_t* bases, int64_t ndims, const int64_t* perm_flat, int64_t perm_len,
+                       const int64_t* perm_offset, int64_t dim, const long long* d_idx, int64_t n, double* d_out) {
+  LW_CHECK_ARG(dim >= 0 && dim < ndims, "dim out of range");
+  std::vector<QmcDim> dims;
+  std::vector<uint16_t> perm;
+  LW_STATUS_TRY(pack_qmc_tables(bases, ndims, perm_flat, perm_len, perm_offset, dims, perm));
+  DevBuf b_dims, b_perm;
+  LW_STATUS_TRY(upload(b_dims, dims.data(), (int64_t)dims.size()));
+  LW_STATUS_TRY(upload(b_perm, perm.data(), (int64_t)perm.size()));
+  if (n > 0) k_halton<<<grid_for(n, 256), 256, 0, S_>>>(b_dims.as<QmcDim>(), b_perm.as<uint16_t>(), (int)dim, d_idx, n, d_out);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
+  return LW_OK;
+}
+
+int lw_halton_batch(const int64_t* bases, int64_t ndims, const int64_t* perm_flat, int64_t perm_len,
+                    const int64_t* perm_offset, int64_t dim, const int64_t* indices, int64_t n, double* out) {
+  LW_CHECK_ARG(n >= 0 && (n == 0 || (indices && out)), "bad batch");
+  DevBuf b_idx, b_out;
+  LW_STATUS_TRY(upload(b_idx, indices, n));
+  LW_CUDA_TRY(b_out.alloc(sizeof(double) * (n > 0 ? n : 1)));
+  LW_STATUS_TRY(halton_impl(bases, ndims, perm_flat, perm_len, perm_offset, dim, b_idx.as<long long>(), n, b_out.as<double>()));
+  if (n > 0) LW_CUDA_TRY(cudaMemcpy(out, b_out.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return LW_OK;
+}
+
+int lw_halton_batch_device(const int64_t* bases, int64_t ndims, const int64_t* perm_flat, int64_t perm_len,
+                           const int64_t* perm_offset, int64_t dim, const int64_t* indices_device, int64_t n,
+                           double* out_device) {
+  return halton_impl(bases, ndims, perm_flat, perm_len, perm_offset, dim, (const long long*)indices_device, n, out_device);
+}
+
+int lw_pixel_offset_batch(const double* u, int64_t n, double* out) {
+  LW_CHECK_ARG(n >= 0 && (n == 0 || (u && out)), "bad batch");
+  if (n == 0) return LW_OK;
+  DevBuf b_u, b_o;
+  LW_STATUS_TRY(upload(b_u, u, 2 * n));
+  LW_CUDA_TRY(b_o.alloc(sizeof(double) * 2 * n));
+  k_pixel_offset<<<grid_for(2 * n, 256), 256, 0, S_>>>(b_u.as<double>(), 2 * n, b_o.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
+  return LW_OK;
+}
+
+int lw_oct_roundtrip_batch(const double* vecs, int64_t n, double* out) {
+  LW_CHECK_ARG(n >= 0 && (n == 0 || (vecs && out)), "bad batch");
+  if (n == 0) return LW_OK;
+  DevBuf b_v, b_o;
+  LW_STATUS_TRY(upload(b_v, vecs, 3 * n));
+  LW_STATUS_TRY(upload(b_o, out, 3 * n));  // untouched rows keep the caller's values
+  k_oct_roundtrip<<<grid_for(n, 256), 256, 0, S_>>>(b_v.as<double>(), n, b_o.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
+  return LW_OK;
+}
+
+int lw_oct_encode_batch(const double* vecs, int64_t n, int64_t* out) {
+  LW_CHECK_ARG(n >= 0 && (n == 0 || (vecs && out)), "bad batch");
+  if (n == 0) return LW_OK;
+  DevBuf b_v, b_o;
+  LW_STATUS_TRY(upload(b_v, vecs, 3 * n));
+  LW_CUDA_TRY(b_o.alloc(sizeof(long long) * n));
+  k_oct_encode<<<grid_for(n, 256), 256, 0, S_>>>(b_v.as<double>(), n, b_o.as<long long>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
+  return LW_OK;
+}
+
+int lw_oct_decode_batch(const int64_t* packed, int64_t n, double* out) {
+  LW_CHECK_ARG(n >= 0 && (n == 0 || (packed && out)), "bad batch");
+  if (n == 0) return LW_OK;
+  DevBuf b_p, b_o;
+  LW_STATUS_TRY(upload(b_p, packed, n));
+  LW_CUDA_TRY(b_o.alloc(sizeof(double) * 3 * n));
+  k_oct_decode<<<grid_for(n, 256), 256, 0, S_>>>(b_p.as<long long>(), n, b_o.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
+  return LW_OK;
+}
+
+static int intersect_launch(int mode, const double* bounds, const int64_t* children, const int64_t* order,
+                            const double* verts, int64_t ntris, const double* origins, const double* dirs,
+                            const double* tmaxs, int64_t n, double* out_t, int64_t* out_tri, double* out_bary) {
+  LW_CHECK_ARG(mode == LW_TRAVERSE_COMPAT || mode == LW_TRAVERSE_CORRECTED || mode == LW_TRAVERSE_BRUTE,
+               "unknown traversal mode");
+  if (n == 0) return LW_OK;
+  if (mode == LW_TRAVERSE_BRUTE)
+    k_intersect_brute<<<(int)((n + 127) / 128), 128, 0, S_>>>(verts, ntris, origins, dirs, tmaxs, n, out_t,
+                                                               (long long*)out_tri, out_bary);
+  else
+    k_intersect_ref<<<(int)((n + 127) / 128), 128, 0, S_>>>(mode == LW_TRAVERSE_COMPAT, bounds,
+                                                             (const long long*)children, (const long long*)order, verts,
+                                                             ntris, origins, dirs, tmaxs, n, out_t,
+                                                             (long long*)out_tri, out_bary);
+  LW_CUDA_TRY(cudaGetLastError());
+  return LW_OK;
+}
+
+int lw_intersect_batch(int mode, const double* bounds, const int64_t* children, int64_t nnodes, const int64_t* order,
+                       const double* verts, int64_t ntris, const double* origins, const double* dirs,
+                       const double* tmaxs, int64_t n, double* out_t, int64_t* out_tri, double* out_bary) {
+  LW_CHECK_ARG(n >= 0 && ntris >= 0 && nnodes >= 1, "bad sizes");
+  LW_CHECK_ARG(n == 0 || (origins && dirs && tmaxs && out_t && out_tri && out_bary), "null ray buffers");
+  if (n == 0) return LW_OK;
+  DevBuf b_bounds, b_children, b_order, b_verts, b_o, b_d, b_tm, b_t, b_tri, b_bary;
+  LW_STATUS_TRY(upload(b_bounds, bounds, 6 * nnodes));
+  LW_STATUS_TRY(upload(b_children, children, 2 * nnodes));
+  LW_STATUS_TRY(upload(b_order, order, ntris));
+  LW_STATUS_TRY(upload(b_verts, verts, 9 * ntris));
+  LW_STATUS_TRY(upload(b_o, origins, 3 * n));
+  LW_STATUS_TRY(upload(b_d, dirs, 3 * n));
+  LW_STATUS_TRY(upload(b_tm, tmaxs, n));
+  LW_CUDA_TRY(b_t.alloc(sizeof(double) * n));
+  LW_CUDA_TRY(b_tri.alloc(sizeof(int64_t) * n));
+  LW_CUDA_TRY(b_bary.alloc(sizeof(double) * 2 * n));
+  LW_STATUS_TRY(intersect_launch(mode, b_bounds.as<double>(), b_children.as<int64_t>(), b_order.as<int64_t>(),
+                                 b_verts.as<double>(), ntris, b_o.as<double>(), b_d.as<double>(), b_tm.as<double>(), n,
+                                 b_t.as<double>(), b_tri.as<int64_t>(), b_bary.as<double>()));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_t, b_t.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_tri, b_tri.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_bary, b_bary.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
+  return LW_OK;
+}
+
+int lw_intersect_batch_device(int mode, const double* bounds, const int64_t* children, int64_t nnodes,
+                              const int64_t* order, const double* verts, int64_t ntris, const double* origins,
+                              const double* dirs, const double* tmaxs, int64_t n, double* out_t, int64_t* out_tri,
+                              double* out_bary) {
+  LW_CHECK_ARG(n >= 0 && ntris >= 0 && nnodes >= 1, "bad sizes");
+  return intersect_launch(mode, bounds, children, order, verts, ntris, origins, dirs, tmaxs, n, out_t, out_tri, out_bary);
+}
+
+}  // extern "C"

@@ -1,0 +1,500 @@
+// lw_integrator.cuh -- path-tracing stages shared by the wavefront engine and the megakernel.
+//
+// Implements the SPEC-only render path (SPEC.md:366-506 integrator, 309-317/351-355
+// materials, 195-230 light/env selection) as defined in DESIGN.md §4, split into the
+// wavefront stage functions of SPEC.md:508-567 (generate -> trace -> material/NEE ->
+// shadow trace -> accumulate).  Every arithmetic step matches oracle/lw_oracle.c
+// (trace_path) in operation order, so a (pixel, iteration) sample produces the same
+// bits on the CPU oracle, in the megakernel, and in the wavefront engine.
+#pragma once
+#include "lw_common.cuh"
+#include "lw_detmath.cuh"
+#include "lw_qmc.cuh"
+#include "lw_traverse.cuh"
+
+struct DevScene {
+  RenderBVH bvh;
+  const double* verts;    // [ntris*9] original triangle order
+  const double* normals;  // [ntris*9]
+  const int* material;    // [ntris]
+  const lw_material* materials;
+  const int* emit_of_tri;  // [ntris] emitter index or -1
+  long long nemit;
+  const long long* emit_tri;
+  const double* emit_rad;  // [nemit*3]
+  const int* emit_two;
+  const double* emit_area;
+  const double* emit_prob;
+  const double* emit_pdf;
+  const int* emit_alias;
+  int env_kind;
+  int env_w, env_h;
+  const float* env_img;
+  const double* env_prob;
+  const double* env_pdf;
+  const int* env_alias;
+  double env_const[3];
+  double env_scale;
+  double p_env, p_tri;
+  double cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3];
+  double tan_half;
+  int W, H, max_depth, rr_start;
+  const QmcDim* qdims;
+  const uint16_t* qperm;
+};
+
+struct PathState {
+  v3 o, d;
+  v3 beta, L;
+  double pdf_prev;
+  long long index;
+  int bounce;
+  int spec_prev;
+};
+
+struct ShadowRay {
+  v3 o, d;
+  double tmax;
+  v3 contrib;
+  int valid;
+};
+
+__device__ __forceinline__ double lw_qmc_s(const DevScene& S, int dim, long long index) {
+  return lw_halton(S.qdims, S.qperm, dim, index);
+}
+
+__device__ __forceinline__ v3 lw_ld3(const double* p) { return mk3(p[0], p[1], p[2]); }
+
+// DESIGN.md §4.1 (oracle camera_ray)
+__device__ __forceinline__ void lw_camera_ray(const DevScene& S, long long index, v3& o, v3& d) {
+  long long W = S.W, H = S.H, P = W * H;
+  long long pix = index % P;
+  long long x = pix % W, y = pix / W;
+  double dx = lw_gauss_filter_offset(lw_qmc_s(S, 0, index));
+  double dy = lw_gauss_filter_offset(lw_qmc_s(S, 1, index));
+  double fx = (((double)x + 0.5) + dx) / (double)W;
+  double fy = (((double)y + 0.5) + dy) / (double)H;
+  double sx = fx * 2.0 - 1.0;
+  double sy = 1.0 - fy * 2.0;
+  double aspect = (double)W / (double)H;
+  double ax = sx * (S.tan_half * aspect);
+  double ay = sy * S.tan_half;
+  v3 f = lw_ld3(S.cam_fwd), r = lw_ld3(S.cam_right), u = lw_ld3(S.cam_up);
+  v3 dd = mk3((f.x + ax * r.x) + ay * u.x, (f.y + ax * r.y) + ay * u.y, (f.z + ax * r.z) + ay * u.z);
+  d = normalize3(dd);
+  o = lw_ld3(S.cam_pos);
+}
+
+__device__ __forceinline__ v3 lw_offset_origin(v3 p, v3 n, v3 dir) {
+  double m = fabs(p.x);
+  if (fabs(p.y) > m) m = fabs(p.y);
+  if (fabs(p.z) > m) m = fabs(p.z);
+  if (m < 1.0) m = 1.0;
+  double eps = 1e-9 * m;
+  double sgn = dot3(n, dir) >= 0.0 ? eps : -eps;
+  return mk3(p.x + n.x * sgn, p.y + n.y * sgn, p.z + n.z * sgn);
+}
+
+__device__ __forceinline__ v3 lw_env_eval(const DevScene& S, v3 d, double& pdf) {
+  if (S.env_kind == LW_ENV_CONSTANT) {
+    pdf = S.p_env * LW_INV_FOUR_PI;
+    return mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
+  }
+  if (S.env_kind == LW_ENV_IMAGE) {
+    double phi = lw_atan2(d.z, d.x);
+    if (phi < 0.0) phi = phi + LW_TWO_PI;
+    double sin_t = sqrt(d.x * d.x + d.z * d.z);
+    double theta = lw_atan2(sin_t, d.y);
+    long long W = S.env_w, H = S.env_h;
+    long long col = (long long)(phi / LW_TWO_PI * (double)W);
+    long long row = (long long)(theta / LW_PI * (double)H);
+    if (col >= W) col = W - 1;
+    if (row >= H) row = H - 1;
+    if (col < 0) col = 0;
+    if (row < 0) row = 0;
+    long long j = row * W + col;
+    pdf = sin_t > 0.0 ? S.p_env * __ldg(S.env_pdf + j) * (double)(W * H) / (LW_TWO_PI_SQ * sin_t) : 0.0;
+    const float* px = S.env_img + 3 * j;
+    return mk3((double)__ldg(px) * S.env_scale, (double)__ldg(px + 1) * S.env_scale, (double)__ldg(px + 2) * S.env_scale);
+  }
+  pdf = 0.0;
+  return mk3(0.0, 0.0, 0.0);
+}
+
+// ---- BSDF (oracle: make_frame .. bsdf_sample) --------------------------------------------
+
+struct LwFrame {
+  v3 t, b, n;
+};
+
+__device__ __forceinline__ LwFrame lw_make_frame(v3 n) {
+  LwFrame f;
+  double sgn = n.z >= 0.0 ? 1.0 : -1.0;
+  double a = -1.0 / (sgn + n.z);
+  double b = n.x * n.y * a;
+  f.t = mk3(1.0 + sgn * n.x * n.x * a, sgn * b, -sgn * n.x);
+  f.b = mk3(b, sgn + n.y * n.y * a, -n.y);
+  f.n = n;
+  return f;
+}
+__device__ __forceinline__ v3 lw_to_local(const LwFrame& f, v3 v) { return mk3(dot3(v, f.t), dot3(v, f.b), dot3(v, f.n)); }
+__device__ __forceinline__ v3 lw_to_world(const LwFrame& f, v3 v) {
+  return mk3((v.x * f.t.x + v.y * f.b.x) + v.z * f.n.x, (v.x * f.t.y + v.y * f.b.y) + v.z * f.n.y,
+             (v.x * f.t.z + v.y * f.b.z) + v.z * f.n.z);
+}
+
+struct LayerW {
+  double a[LW_MAX_LAYERS];
+  double sum_a;
+  int nonspec;
+};
+
+__device__ __forceinline__ double lw_schlick(double cosv, double ior) {
+  double r0 = (ior - 1.0) / (ior + 1.0);
+  double f0 = r0 * r0;
+  double m = 1.0 - cosv;
+  double m2 = m * m;
+  return f0 + (1.0 - f0) * (m2 * m2 * m);
+}
+
+__device__ __forceinline__ void lw_layer_weights(const lw_material& m, double cos_o, LayerW& lw) {
+  double r = 1.0;
+  lw.sum_a = 0.0;
+  lw.nonspec = 0;
+#pragma unroll
+  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+    lw.a[l] = 0.0;
+    if (l >= m.nlayers) continue;
+    const lw_layer& L = m.layers[l];
+    double a = L.coat ? r * (L.weight * lw_schlick(cos_o, m.ior)) : r * L.weight;
+    lw.a[l] = a;
+    r = r - a;
+    lw.sum_a = lw.sum_a + a;
+    if (a > 0.0 && (L.kind == LW_BSDF_DIFFUSE || L.kind == LW_BSDF_GLOSSY)) lw.nonspec = 1;
+  }
+}
+
+__device__ __forceinline__ double lw_ggx_d(double alpha, double cos_h) {
+  double a2 = alpha * alpha;
+  double t = cos_h * cos_h * (a2 - 1.0) + 1.0;
+  return a2 / (LW_PI * (t * t));
+}
+__device__ __forceinline__ double lw_ggx_g1(double alpha, double cos_v) {
+  double a2 = alpha * alpha;
+  return 2.0 * cos_v / (cos_v + sqrt(a2 + (1.0 - a2) * (cos_v * cos_v)));
+}
+__device__ __forceinline__ double lw_alpha_of(const lw_layer& L) {
+  double a = L.roughness;
+  if (a < 1e-4) a = 1e-4;
+  if (a > 1.0) a = 1.0;
+  return a;
+}
+
+__device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& lw, v3 wo, v3 wi, double& pdf) {
+  v3 f = mk3(0.0, 0.0, 0.0);
+  pdf = 0.0;
+  if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return f;
+  for (int l = 0; l < m.nlayers; l++) {
+    const lw_layer& L = m.layers[l];
+    double a = lw.a[l];
+    if (!(a > 0.0)) continue;
+    double sel = a / lw.sum_a;
+    if (L.kind == LW_BSDF_DIFFUSE) {
+      double k = a * LW_INV_PI;
+      f = f + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
+      pdf = pdf + sel * (wi.z * LW_INV_PI);
+    } else if (L.kind == LW_BSDF_GLOSSY) {
+      double al = lw_alpha_of(L);
+      v3 h = normalize3(wo + wi);
+      double D = lw_ggx_d(al, h.z);
+      double G = lw_ggx_g1(al, wo.z) * lw_ggx_g1(al, wi.z);
+      double k = a * (D * G / (4.0 * wo.z * wi.z));
+      f = f + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
+      double oh = dot3(wo, h);
+      if (oh > 0.0) pdf = pdf + sel * (D * h.z / (4.0 * oh));
+    }
+  }
+  return f;
+}
+
+__device__ __forceinline__ double lw_fresnel_dielectric(double cos_i, double eta) {
+  double sin2t = eta * eta * (1.0 - cos_i * cos_i);
+  if (sin2t >= 1.0) return 1.0;
+  double cos_t = sqrt(1.0 - sin2t);
+  double rs = (eta * cos_i - cos_t) / (eta * cos_i + cos_t);
+  double rp = (cos_i - eta * cos_t) / (cos_i + eta * cos_t);
+  return 0.5 * (rs * rs + rp * rp);
+}
+
+struct BSample {
+  v3 wi, weight;
+  double pdf;
+  int delta, transmit;
+};
+
+__device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const LayerW& lw, v3 wo, bool front, double u,
+                                               double v, BSample& bs) {
+  if (!(lw.sum_a > 0.0) || wo.z <= 0.0) return false;
+  double x = u * lw.sum_a;
+  int pick = -1;
+  double cum = 0.0, prev = 0.0;
+  for (int l = 0; l < m.nlayers; l++) {
+    if (!(lw.a[l] > 0.0)) continue;
+    prev = cum;
+    cum = cum + lw.a[l];
+    pick = l;
+    if (x < cum) break;
+  }
+  if (pick < 0) return false;
+  double ur = (x - prev) / lw.a[pick];
+  if (ur < 0.0) ur = 0.0;
+  if (ur >= 1.0) ur = 0.9999999999999999;
+  const lw_layer& L = m.layers[pick];
+  bs.delta = 0;
+  bs.transmit = 0;
+  if (L.kind == LW_BSDF_DIFFUSE) {
+    double r = sqrt(ur), sp, cp;
+    lw_sincos2pi(v, &sp, &cp);
+    double z = 1.0 - ur;
+    bs.wi = mk3(r * cp, r * sp, sqrt(z > 0.0 ? z : 0.0));
+  } else if (L.kind == LW_BSDF_GLOSSY) {
+    double al = lw_alpha_of(L);
+    double tan2 = al * al * ur / (1.0 - ur);
+    double ch = 1.0 / sqrt(1.0 + tan2);
+    double sh2 = 1.0 - ch * ch;
+    double sh = sqrt(sh2 > 0.0 ? sh2 : 0.0);
+    double sp, cp;
+    lw_sincos2pi(v, &sp, &cp);
+    v3 h = mk3(sh * cp, sh * sp, ch);
+    double oh = dot3(wo, h);
+    bs.wi = h * (2.0 * oh) - wo;
+  } else if (L.kind == LW_BSDF_SPECULAR_REFLECT) {
+    bs.wi = mk3(-wo.x, -wo.y, wo.z);
+    bs.delta = 1;
+    bs.weight = mk3(lw.sum_a * L.tint[0], lw.sum_a * L.tint[1], lw.sum_a * L.tint[2]);
+    bs.pdf = 0.0;
+    return true;
+  } else {
+    double eta = front ? 1.0 / m.ior : m.ior;
+    double F = lw_fresnel_dielectric(wo.z, eta);
+    bs.delta = 1;
+    bs.pdf = 0.0;
+    if (ur < F) {
+      bs.wi = mk3(-wo.x, -wo.y, wo.z);
+      bs.weight = mk3(lw.sum_a * L.tint[0], lw.sum_a * L.tint[1], lw.sum_a * L.tint[2]);
+    } else {
+      double sin2t = eta * eta * (1.0 - wo.z * wo.z);
+      double cos_t = sqrt(1.0 - sin2t);
+      bs.wi = mk3(-eta * wo.x, -eta * wo.y, -cos_t);
+      bs.transmit = 1;
+      double k = lw.sum_a * (eta * eta);
+      bs.weight = mk3(k * L.tint[0], k * L.tint[1], k * L.tint[2]);
+    }
+    return true;
+  }
+  if (bs.wi.z <= 0.0) return false;
+  double pdf;
+  v3 f = lw_bsdf_eval(m, lw, wo, bs.wi, pdf);
+  if (!(pdf > 0.0)) return false;
+  double k = bs.wi.z / pdf;
+  bs.weight = mk3(f.x * k, f.y * k, f.z * k);
+  bs.pdf = pdf;
+  return true;
+}
+
+__device__ __forceinline__ long long lw_alias_sample(const double* __restrict__ prob, const int* __restrict__ alias,
+                                                     long long n, double u, double& u_out) {
+  double x = u * (double)n;
+  double fi = floor(x);
+  long long i = (long long)fi;
+  if (i >= n) i = n - 1;
+  double f = x - (double)i;
+  double pr = __ldg(prob + i);
+  if (f < pr) {
+    u_out = f / pr;
+    return i;
+  }
+  u_out = (f - pr) / (1.0 - pr);
+  if (u_out >= 1.0) u_out = 0.9999999999999999;
+  return __ldg(alias + i);
+}
+
+// ---- stages ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void lw_path_init(const DevScene& S, long long index, PathState& ps) {
+  lw_camera_ray(S, index, ps.o, ps.d);
+  ps.beta = mk3(1.0, 1.0, 1.0);
+  ps.L = mk3(0.0, 0.0, 0.0);
+  ps.pdf_prev = 0.0;
+  ps.index = index;
+  ps.bounce = 0;
+  ps.spec_prev = 1;
+}
+
+// Material / NEE stage for the hit of the current segment (oracle trace_path loop body).
+// Returns true if the path continues (ps holds the next ray).  sh.valid marks a shadow ray
+// whose contribution must be added to ps.L if unoccluded, before the path is flushed.
+__device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, const LwHit& h, ShadowRay& sh) {
+  sh.valid = 0;
+  const int b = ps.bounce;
+  v3 d = ps.d;
+  if (h.tri < 0) {
+    if (S.env_kind != LW_ENV_NONE) {
+      double pe;
+      v3 Le = lw_env_eval(S, d, pe);
+      double w = ps.spec_prev ? 1.0 : ps.pdf_prev / (ps.pdf_prev + pe);
+      ps.L = ps.L + mk3(ps.beta.x * Le.x * w, ps.beta.y * Le.y * w, ps.beta.z * Le.z * w);
+    }
+    return false;
+  }
+  const double* vv = S.verts + 9 * h.tri;
+  v3 v0 = lw_ld3(vv), v1 = lw_ld3(vv + 3), v2 = lw_ld3(vv + 6);
+  double w = (1.0 - h.bu) - h.bv;
+  v3 p = bary3(v0, v1, v2, w, h.bu, h.bv);
+  v3 e1 = v1 - v0, e2 = v2 - v0;
+  v3 ng = normalize3(cross3(e1, e2));
+  bool front = dot3(ng, d) < 0.0;
+  int e = S.emit_of_tri[h.tri];
+  if (e >= 0 && S.nemit > 0 && (front || S.emit_two[e])) {
+    v3 Le = lw_ld3(S.emit_rad + 3 * e);
+    double wm = 1.0;
+    if (!ps.spec_prev) {
+      double cos_l = fabs(dot3(ng, d));
+      double pdf_area = S.p_tri * S.emit_pdf[e] / S.emit_area[e];
+      double pl = pdf_area * (h.t * h.t) / cos_l;
+      wm = ps.pdf_prev / (ps.pdf_prev + pl);
+    }
+    ps.L = ps.L + mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
+  }
+  if (b == S.max_depth - 1) return false;
+  const double* nn = S.normals + 9 * h.tri;
+  v3 ns = bary3(lw_ld3(nn), lw_ld3(nn + 3), lw_ld3(nn + 6), w, h.bu, h.bv);
+  double nl = dot3(ns, ns);
+  ns = nl > 0.0 ? ns * (1.0 / sqrt(nl)) : ng;
+  v3 wo = neg3(d);
+  v3 ngf = front ? ng : neg3(ng);
+  if (dot3(ns, ngf) < 0.0) ns = neg3(ns);
+  if (dot3(ns, wo) <= 0.0) ns = ngf;
+  LwFrame fr = lw_make_frame(ns);
+  v3 wol = lw_to_local(fr, wo);
+  const lw_material m = S.materials[S.material[h.tri]];
+  LayerW lw;
+  lw_layer_weights(m, wol.z, lw);
+  const int bd = 4 + 8 * b;
+  const long long index = ps.index;
+  if (lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE)) {
+    double ul = lw_qmc_s(S, bd + 2, index), vl = lw_qmc_s(S, bd + 3, index);
+    v3 wi = mk3(0.0, 0.0, 0.0), Le = mk3(0.0, 0.0, 0.0);
+    double pl = 0.0, tmax_sh = INFINITY;
+    bool ok = false;
+    if (S.env_kind != LW_ENV_NONE && ul < S.p_env) {
+      double ue = S.nemit > 0 ? ul / S.p_env : ul;
+      if (S.env_kind == LW_ENV_CONSTANT) {
+        double z = 1.0 - 2.0 * ue;
+        double r2 = 1.0 - z * z;
+        double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
+        lw_sincos2pi(vl, &sp, &cp);
+        wi = mk3(r * cp, z, r * sp);
+        pl = S.p_env * LW_INV_FOUR_PI;
+        Le = mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
+        ok = true;
+      } else {
+        double ur;
+        long long nt = (long long)S.env_w * S.env_h;
+        long long j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
+        long long row = j / S.env_w, col = j % S.env_w;
+        double uu = ((double)col + ur) / (double)S.env_w;
+        double vv2 = ((double)row + vl) / (double)S.env_h;
+        double st, ct, sp, cp;
+        lw_sincos2pi(vv2 * 0.5, &st, &ct);
+        lw_sincos2pi(uu, &sp, &cp);
+        wi = mk3(st * cp, ct, st * sp);
+        if (st > 0.0) {
+          pl = S.p_env * __ldg(S.env_pdf + j) * (double)nt / (LW_TWO_PI_SQ * st);
+          const float* px = S.env_img + 3 * j;
+          Le = mk3((double)__ldg(px) * S.env_scale, (double)__ldg(px + 1) * S.env_scale,
+                   (double)__ldg(px + 2) * S.env_scale);
+          ok = true;
+        }
+      }
+    } else if (S.nemit > 0) {
+      double ut = S.env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
+      double ur;
+      long long le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
+      const double* lv = S.verts + 9 * S.emit_tri[le];
+      v3 l0 = lw_ld3(lv), l1 = lw_ld3(lv + 3), l2 = lw_ld3(lv + 6);
+      double su = sqrt(ur);
+      double b0 = 1.0 - su, b1 = vl * su;
+      double b2 = (1.0 - b0) - b1;
+      v3 q = bary3(l0, l1, l2, b0, b1, b2);
+      v3 dl = q - p;
+      double dist2 = dot3(dl, dl);
+      double dist = sqrt(dist2);
+      wi = mk3(dl.x / dist, dl.y / dist, dl.z / dist);
+      v3 ngl = normalize3(cross3(l1 - l0, l2 - l0));
+      double cos_l = -dot3(ngl, wi);
+      if (S.emit_two[le]) cos_l = fabs(cos_l);
+      if (cos_l > 0.0 && dist > 0.0) {
+        pl = (S.p_tri * S.emit_pdf[le] / S.emit_area[le]) * dist2 / cos_l;
+        Le = lw_ld3(S.emit_rad + 3 * le);
+        tmax_sh = dist * (1.0 - 1e-7);
+        ok = true;
+      }
+    }
+    if (ok && pl > 0.0 && dot3(ngf, wi) > 0.0) {
+      v3 wil = lw_to_local(fr, wi);
+      double pb;
+      v3 f = lw_bsdf_eval(m, lw, wol, wil, pb);
+      if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
+        double wm = pl / (pl + pb);
+        double k = (wil.z * wm) / pl;
+        sh.contrib = mk3(ps.beta.x * f.x * Le.x * k, ps.beta.y * f.y * Le.y * k, ps.beta.z * f.z * Le.z * k);
+        sh.o = lw_offset_origin(p, ngf, wi);
+        sh.d = wi;
+        sh.tmax = tmax_sh;
+        sh.valid = 1;
+      }
+    }
+  }
+  BSample bs;
+  double ub = lw_qmc_s(S, bd + 0, index), vb = lw_qmc_s(S, bd + 1, index);
+  if (!lw_bsdf_sample(m, lw, wol, front, ub, vb, bs)) return false;
+  v3 wi = lw_to_world(fr, bs.wi);
+  double gside = dot3(ngf, wi);
+  if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) return false;
+  ps.beta = mk3(ps.beta.x * bs.weight.x, ps.beta.y * bs.weight.y, ps.beta.z * bs.weight.z);
+  ps.spec_prev = bs.delta;
+  ps.pdf_prev = bs.pdf;
+  if (b >= S.rr_start) {
+    double q = ps.beta.x;
+    if (ps.beta.y > q) q = ps.beta.y;
+    if (ps.beta.z > q) q = ps.beta.z;
+    if (q > 1.0) q = 1.0;
+    double ur = lw_qmc_s(S, bd + 4, index);
+    if (!(ur < q)) return false;
+    ps.beta = mk3(ps.beta.x / q, ps.beta.y / q, ps.beta.z / q);
+  }
+  ps.o = lw_offset_origin(p, ngf, wi);
+  ps.d = wi;
+  ps.bounce = b + 1;
+  return true;
+}
+
+// fixed-point accumulation (oracle accumulate); returns 1 if a channel was non-finite
+__device__ __forceinline__ int lw_accumulate(unsigned long long* fb, long long pix, v3 L) {
+  double c[3] = {L.x, L.y, L.z};
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    double v = c[k];
+    if (!(v == v) || v == INFINITY || v == -INFINITY) {
+      bad = 1;
+      v = 0.0;
+    }
+    if (v < 0.0) v = 0.0;
+    if (v > LW_FB_SAMPLE_CLAMP) v = LW_FB_SAMPLE_CLAMP;
+    long long q = __double2ll_rn(v * 1048576.0);
+    if (q) atomicAdd(fb + 3 * pix + k, (unsigned long long)q);
+  }
+  return bad;
+}

@@ -1,0 +1,90 @@
+// lw_qmc.cuh -- scrambled Halton sampler on the device (_kernels.py:160-208, qmc.py:112-135).
+//
+// Per dimension the host packs {base, perm offset, 32- and 64-bit magic dividers}
+// (qmc.py:153-164 construction).  Digits come from strength-reduced division
+// (__umulhi / __umul64hi) instead of hardware division.  Two evaluation regimes give
+// results bit-identical to the reference kernel:
+//   * base*index < 2^53: every intermediate of the reference's double accumulation is an
+//     exact integer, so the digit reversal is accumulated in uint64 and rounded once by
+//     the final IEEE division (the reference's single rounding);
+//   * otherwise: the reference's double operations are replayed one by one.
+#pragma once
+#include "lw_common.cuh"
+
+struct QmcDim {
+  uint32_t base;
+  uint32_t perm_off;
+  uint32_t magic32;
+  uint8_t shift32, add32, shift64, add64;
+  uint64_t magic64;
+  uint64_t exact_limit;  // largest index with base*index < 2^53
+};
+
+__device__ __forceinline__ uint32_t lw_div32(uint32_t n, const QmcDim& d) {
+  uint32_t q = __umulhi(n, d.magic32);
+  if (d.add32) return (((n - q) >> 1) + q) >> d.shift32;
+  return q >> d.shift32;
+}
+
+__device__ __forceinline__ uint64_t lw_div64(uint64_t n, const QmcDim& d) {
+  uint64_t q = __umul64hi(n, d.magic64);
+  if (d.add64) return (((n - q) >> 1) + q) >> d.shift64;
+  return q >> d.shift64;
+}
+
+// radical_inverse_base2, _kernels.py:181-192
+__device__ __forceinline__ double lw_ri_base2(long long index) {
+  if (index <= 0) return 0.0;
+  uint64_t n = (uint64_t)index;
+  int nbits = 64 - __clzll((long long)n);
+  if (n < (1ULL << 53)) {
+    uint64_t rev = __brevll(n) >> (64 - nbits);
+    return (double)rev / (double)(1ULL << nbits);
+  }
+  double rev = 0.0, scale = 1.0;
+  while (n > 0) {
+    rev = rev * 2.0 + (double)(n & 1);
+    scale = scale * 2.0;
+    n >>= 1;
+  }
+  return rev / scale;
+}
+
+// halton_dim, _kernels.py:195-208
+__device__ __forceinline__ double lw_halton(const QmcDim* __restrict__ dims, const uint16_t* __restrict__ perm,
+                                            int dim, long long index) {
+  QmcDim d = dims[dim];
+  if (d.base == 2) return lw_ri_base2(index);
+  if (index <= 0) return 0.0;
+  uint64_t n = (uint64_t)index;
+  const uint16_t* p = perm + d.perm_off;
+  const uint32_t b = d.base;
+  if (n <= d.exact_limit) {
+    uint64_t rev = 0, scale = 1;
+    while (n >> 32) {
+      uint64_t q = lw_div64(n, d);
+      uint32_t digit = (uint32_t)(n - q * b);
+      rev = rev * b + __ldg(p + digit);
+      scale *= b;
+      n = q;
+    }
+    uint32_t m = (uint32_t)n;
+    while (m) {
+      uint32_t q = lw_div32(m, d);
+      uint32_t digit = m - q * b;
+      rev = rev * b + __ldg(p + digit);
+      scale *= b;
+      m = q;
+    }
+    return (double)rev / (double)scale;
+  }
+  double rev = 0.0, scale = 1.0, bd = (double)b;
+  while (n > 0) {
+    uint64_t q = lw_div64(n, d);
+    uint32_t digit = (uint32_t)(n - q * b);
+    rev = rev * bd + (double)__ldg(p + digit);
+    scale = scale * bd;
+    n = q;
+  }
+  return rev / scale;
+}

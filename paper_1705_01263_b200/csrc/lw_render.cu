@@ -1,0 +1,1115 @@
+// lw_render.cu -- render context, scene upload and the two execution engines.
+//
+// SPEC.md:508-588 (wavefront) and PAPER.md:599-699:
+//  * sample states live in a fixed-size SoA pool (one array per field, coalesced);
+//  * each wave runs the stage kernels generate/regenerate -> trace -> material+NEE ->
+//    shadow trace over compact queues rebuilt every stage with warp ballots
+//    (__ballot_sync + __popc, one atomic per warp);
+//  * terminated slots are regenerated with new (iteration, pixel) work once more than
+//    `regen_fraction` of the pool is free (paper: one half);
+//  * the tail of a pass can switch to the megakernel.
+// Radiance is accumulated per path into an int64 fixed-point framebuffer, so the image is
+// independent of execution strategy, pool size, switch threshold and GPU count.
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "lw_common.cuh"
+#include "lw_host.h"
+#include "lw_integrator.cuh"
+
+using namespace lw;
+
+namespace {
+
+struct Counters {
+  unsigned long long work_next;  // next work item (iteration-major over the pixel range)
+  int n_ext, n_ext_next, n_shadow, n_free;
+  int regen_now, nfree_snap;  // decision of the current wave's regeneration step
+  unsigned long long rays_ext, rays_shadow, paths, nonfinite, regens, waves;
+  unsigned long long ext_nodes, ext_tris, sh_nodes, sh_tris;
+};
+
+struct Pool {
+  int size = 0;
+  double *ox, *oy, *oz, *dx, *dy, *dz;
+  double *bx, *by, *bz, *lx, *ly, *lz;
+  double* pdf_prev;
+  long long* index;
+  int* pix;
+  int* flags;  // bounce | spec_prev << 8 | live << 9 | pending flush << 10
+  double *ht, *hbu, *hbv;
+  int* htri;
+  double *sox, *soy, *soz, *sdx, *sdy, *sdz, *stmax, *scx, *scy, *scz;
+  int *q_ext, *q_ext_next, *q_shadow, *q_free;
+  void* block = nullptr;
+};
+
+}  // namespace
+
+struct lw_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool has_scene = false, configured = false;
+  DevScene S;
+  std::vector<void*> scene_allocs;
+  DeviceBVH ref_bvh;
+  int64_t ntris = 0;
+  lw_render_params params;
+  QmcDim* d_qdims = nullptr;
+  uint16_t* d_qperm = nullptr;
+  unsigned long long* d_fb = nullptr;
+  int64_t fb_pixels = 0;
+  Pool pool;
+  Counters* d_cnt = nullptr;
+  Counters* h_cnt = nullptr;  // pinned mirror
+  lw_render_stats stats;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_total_ms = 0.0, last_trace_ms = 0.0;
+  int64_t last_launches = 0;
+  size_t smem_bytes = 0;  // scene bytes staged in shared memory (0 = use global/L1)
+  cudaStream_t own_stream = nullptr;
+  int instr = 0;
+  std::vector<cudaEvent_t> evpool;  // pairs bracketing trace launches
+  lw_kernel_profile prof;
+};
+
+namespace {
+
+template <class T>
+int dev_upload(lw_ctx* c, T*& dst, const T* src, int64_t count) {
+  LW_CUDA_TRY(cudaMalloc(&dst, sizeof(T) * (count > 0 ? count : 1)));
+  c->scene_allocs.push_back(dst);
+  if (count > 0) LW_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, c->stream));
+  return LW_OK;
+}
+
+template <class T>
+int dev_alloc(lw_ctx* c, T*& dst, int64_t count) {
+  LW_CUDA_TRY(cudaMalloc(&dst, sizeof(T) * (count > 0 ? count : 1)));
+  c->scene_allocs.push_back(dst);
+  return LW_OK;
+}
+
+void free_scene(lw_ctx* c) {
+  for (void* p : c->scene_allocs) cudaFree(p);
+  c->scene_allocs.clear();
+  cudaFree(c->ref_bvh.bounds);
+  cudaFree(c->ref_bvh.children);
+  cudaFree(c->ref_bvh.order);
+  c->ref_bvh = DeviceBVH();
+  c->has_scene = false;
+}
+
+void free_pool(lw_ctx* c) {
+  if (c->pool.block) cudaFree(c->pool.block);
+  c->pool = Pool();
+}
+
+// ---- warp-aggregated queue append ---------------------------------------------------------
+// all 32 lanes of the warp must call it (kernels keep grid-stride loops warp-uniform)
+__device__ __forceinline__ int warp_push(int* count, bool pred) {
+  unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (m == 0) return -1;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!pred) return -1;
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long long v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, v);
+}
+
+// stage the render BVH in shared memory when it fits (small scenes: Cornell box)
+__device__ __forceinline__ RenderBVH stage_bvh(const RenderBVH& g, int nnodes, unsigned char* smem, bool use_smem) {
+  if (!use_smem) return g;
+  RNode* sn = reinterpret_cast<RNode*>(smem);
+  LTri* st = reinterpret_cast<LTri*>(smem + sizeof(RNode) * nnodes);
+  const int4* src = reinterpret_cast<const int4*>(g.nodes);
+  int4* dst = reinterpret_cast<int4*>(sn);
+  int nn4 = nnodes * (int)(sizeof(RNode) / 16);
+  for (int k = threadIdx.x; k < nn4; k += blockDim.x) dst[k] = src[k];
+  src = reinterpret_cast<const int4*>(g.tris);
+  dst = reinterpret_cast<int4*>(st);
+  int nt4 = (int)g.ntris * (int)(sizeof(LTri) / 16);
+  for (int k = threadIdx.x; k < nt4; k += blockDim.x) dst[k] = src[k];
+  __syncthreads();
+  RenderBVH b = g;
+  b.nodes = sn;
+  b.tris = st;
+  return b;
+}
+
+// ---- scene preparation kernels ------------------------------------------------------------
+
+__global__ void k_internal_flags(const long long* __restrict__ children, long long nnodes, int* __restrict__ flag) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k < nnodes) flag[k] = children[2 * k] >= 0 ? 1 : 0;
+}
+
+__device__ __forceinline__ int leaf_ref(long long start, long long count) { return (int)(-(1 + ((start << 3) | count))); }
+
+__global__ void k_build_rnodes(const double* __restrict__ bounds, const long long* __restrict__ children,
+                               long long nnodes, const int* __restrict__ imap, RNode* __restrict__ out) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= nnodes) return;
+  if (children[2 * k] < 0) return;
+  RNode r;
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    long long ch = children[2 * k + c];
+#pragma unroll
+    for (int a = 0; a < 6; a++) r.box[6 * c + a] = bounds[6 * ch + a];
+    long long c0 = children[2 * ch], c1 = children[2 * ch + 1];
+    r.ref[c] = c0 >= 0 ? imap[ch] : leaf_ref(-(c0 + 1), c1);
+  }
+#pragma unroll
+  for (int p = 0; p < 6; p++) r.pad[p] = 0;
+  out[imap[k]] = r;
+}
+
+__global__ void k_build_ltris(const double* __restrict__ verts, const long long* __restrict__ order, long long n,
+                              LTri* __restrict__ out) {
+  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  long long t = order[j];
+  LTri r;
+#pragma unroll
+  for (int k = 0; k < 9; k++) r.v[k] = verts[9 * t + k];
+  r.id = t;
+  out[j] = r;
+}
+
+__global__ void k_emitters(const double* __restrict__ verts, const long long* __restrict__ emit_tri, long long nemit,
+                           double* __restrict__ area, int* __restrict__ emit_of_tri) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= nemit) return;
+  const double* v = verts + 9 * emit_tri[e];
+  double e1x = v[3] - v[0], e1y = v[4] - v[1], e1z = v[5] - v[2];
+  double e2x = v[6] - v[0], e2y = v[7] - v[1], e2z = v[8] - v[2];
+  double cx = e1y * e2z - e1z * e2y, cy = e1z * e2x - e1x * e2z, cz = e1x * e2y - e1y * e2x;
+  area[e] = 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+  emit_of_tri[emit_tri[e]] = (int)e;
+}
+
+// ---- megakernel ----------------------------------------------------------------------------
+
+struct WorkRange {
+  long long it_begin, nits, pix_begin, npix;
+};
+
+__device__ __forceinline__ long long work_index(const DevScene& S, const WorkRange& w, long long item, int& pix) {
+  long long it = w.it_begin + item / w.npix;
+  long long p = w.pix_begin + item % w.npix;
+  pix = (int)p;
+  return it * ((long long)S.W * S.H) + p;
+}
+
+__device__ __forceinline__ void run_to_completion(const DevScene& S, const RenderBVH& bvh, PathState& ps,
+                                                  unsigned long long& next, unsigned long long& nsh) {
+  for (;;) {
+    double o[3] = {ps.o.x, ps.o.y, ps.o.z}, d[3] = {ps.d.x, ps.d.y, ps.d.z};
+    LwHit h;
+    lw_trace_closest(bvh, o, d, INFINITY, h);
+    next++;
+    ShadowRay sh;
+    bool alive = lw_path_shade(S, ps, h, sh);
+    if (sh.valid) {
+      double so[3] = {sh.o.x, sh.o.y, sh.o.z}, sd[3] = {sh.d.x, sh.d.y, sh.d.z};
+      nsh++;
+      if (!lw_trace_any(bvh, so, sd, sh.tmax)) ps.L = ps.L + sh.contrib;
+    }
+    if (!alive) break;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, unsigned long long* __restrict__ fb,
+                                                    Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
+  long long total = w.nits * w.npix;
+  unsigned long long next = 0, nsh = 0, bad = 0, paths = 0;
+  for (long long base = blockIdx.x * (long long)blockDim.x; base < total; base += (long long)gridDim.x * blockDim.x) {
+    long long item = base + threadIdx.x;
+    if (item < total) {
+      int pix;
+      long long index = work_index(S, w, item, pix);
+      PathState ps;
+      lw_path_init(S, index, ps);
+      run_to_completion(S, bvh, ps, next, nsh);
+      bad += lw_accumulate(fb, pix, ps.L);
+      paths++;
+    }
+  }
+  warp_add(&cnt->rays_ext, next);
+  warp_add(&cnt->rays_shadow, nsh);
+  warp_add(&cnt->nonfinite, bad);
+  warp_add(&cnt->paths, paths);
+}
+
+// ---- wavefront stages -----------------------------------------------------------------------
+
+#define F_BOUNCE 0xff
+#define F_SPEC (1 << 8)
+#define F_PENDING (1 << 10)
+
+__device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) {
+  ps.o = mk3(P.ox[s], P.oy[s], P.oz[s]);
+  ps.d = mk3(P.dx[s], P.dy[s], P.dz[s]);
+  ps.beta = mk3(P.bx[s], P.by[s], P.bz[s]);
+  ps.L = mk3(P.lx[s], P.ly[s], P.lz[s]);
+  ps.pdf_prev = P.pdf_prev[s];
+  ps.index = P.index[s];
+  int f = P.flags[s];
+  ps.bounce = f & F_BOUNCE;
+  ps.spec_prev = (f & F_SPEC) ? 1 : 0;
+}
+
+__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps, int extra_flags) {
+  P.ox[s] = ps.o.x;
+  P.oy[s] = ps.o.y;
+  P.oz[s] = ps.o.z;
+  P.dx[s] = ps.d.x;
+  P.dy[s] = ps.d.y;
+  P.dz[s] = ps.d.z;
+  P.bx[s] = ps.beta.x;
+  P.by[s] = ps.beta.y;
+  P.bz[s] = ps.beta.z;
+  P.lx[s] = ps.L.x;
+  P.ly[s] = ps.L.y;
+  P.lz[s] = ps.L.z;
+  P.pdf_prev[s] = ps.pdf_prev;
+  P.index[s] = ps.index;
+  P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0) | extra_flags;
+}
+
+// paper §3.1.3: regenerate only once more than regen_fraction of the pool has terminated
+// (or nothing is in flight).  One thread decides and takes the free queue, so every block of
+// k_regenerate sees the same snapshot and the material stage can refill the queue from 0.
+__global__ void k_regen_decide(Counters* cnt, int pool, double regen_fraction, int force) {
+  int nfree = cnt->n_free;
+  bool regen = force || nfree > (int)(regen_fraction * (double)pool) || cnt->n_ext == 0;
+  cnt->regen_now = regen ? 1 : 0;
+  cnt->nfree_snap = regen ? nfree : 0;
+  if (regen) {
+    cnt->n_free = 0;
+    cnt->regens += 1;
+  }
+}
+
+// flush finished paths from the free queue, then refill their slots with new samples
+__global__ void __launch_bounds__(256) k_regenerate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
+                                                    Counters* __restrict__ cnt) {
+  if (!cnt->regen_now) return;
+  int nfree = cnt->nfree_snap;
+  long long total = w.nits * w.npix;
+  unsigned long long bad = 0, paths = 0;
+  for (int base = blockIdx.x * blockDim.x; base < nfree; base += gridDim.x * blockDim.x) {
+    int k = base + threadIdx.x;
+    bool valid = k < nfree;
+    int s = valid ? P.q_free[k] : 0;
+    if (valid && (P.flags[s] & F_PENDING)) {
+      bad += lw_accumulate(fb, P.pix[s], mk3(P.lx[s], P.ly[s], P.lz[s]));
+      paths++;
+      P.flags[s] = 0;
+    }
+    // claim work items, one atomic per warp (lane 0 is always valid inside the loop)
+    unsigned m = __ballot_sync(0xffffffffu, valid);
+    int lane = threadIdx.x & 31;
+    unsigned long long wb = 0;
+    if (lane == 0) wb = atomicAdd(&cnt->work_next, (unsigned long long)__popc(m));
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    long long item = (long long)wb + __popc(m & ((1u << lane) - 1u));
+    bool got = valid && item < total;
+    if (got) {
+      int pix;
+      long long index = work_index(S, w, item, pix);
+      PathState ps;
+      lw_path_init(S, index, ps);
+      store_state(P, s, ps, 0);
+      P.pix[s] = pix;
+    }
+    int q = warp_push(&cnt->n_ext, got);
+    if (q >= 0) P.q_ext[q] = s;
+  }
+  warp_add(&cnt->nonfinite, bad);
+  warp_add(&cnt->paths, paths);
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(128) k_trace_ext(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
+  int n = cnt->n_ext;
+  LwTraceCount tc;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    int k = base + threadIdx.x;
+    if (k < n) {
+      int s = P.q_ext[k];
+      double o[3] = {P.ox[s], P.oy[s], P.oz[s]}, d[3] = {P.dx[s], P.dy[s], P.dz[s]};
+      LwHit h;
+      lw_trace_closest<COUNT>(bvh, o, d, INFINITY, h, &tc);
+      P.ht[s] = h.t;
+      P.hbu[s] = h.bu;
+      P.hbv[s] = h.bv;
+      P.htri[s] = (int)h.tri;
+    }
+  }
+  if (COUNT) {
+    warp_add(&cnt->ext_nodes, tc.nodes);
+    warp_add(&cnt->ext_tris, tc.tris);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    cnt->rays_ext += (unsigned long long)n;
+    cnt->waves += 1;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt) {
+  int n = cnt->n_ext;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    int k = base + threadIdx.x;
+    bool valid = k < n;
+    int s = 0;
+    bool alive = false, shadow = false;
+    if (valid) {
+      s = P.q_ext[k];
+      PathState ps;
+      load_state(P, s, ps);
+      LwHit h;
+      h.t = P.ht[s];
+      h.bu = P.hbu[s];
+      h.bv = P.hbv[s];
+      h.tri = P.htri[s];
+      ShadowRay sh;
+      alive = lw_path_shade(S, ps, h, sh);
+      shadow = sh.valid != 0;
+      store_state(P, s, ps, alive ? 0 : F_PENDING);
+      if (shadow) {
+        P.sox[s] = sh.o.x;
+        P.soy[s] = sh.o.y;
+        P.soz[s] = sh.o.z;
+        P.sdx[s] = sh.d.x;
+        P.sdy[s] = sh.d.y;
+        P.sdz[s] = sh.d.z;
+        P.stmax[s] = sh.tmax;
+        P.scx[s] = sh.contrib.x;
+        P.scy[s] = sh.contrib.y;
+        P.scz[s] = sh.contrib.z;
+      }
+    }
+    int q = warp_push(&cnt->n_shadow, valid && shadow);
+    if (q >= 0) P.q_shadow[q] = s;
+    q = warp_push(&cnt->n_ext_next, valid && alive);
+    if (q >= 0) P.q_ext_next[q] = s;
+    q = warp_push(&cnt->n_free, valid && !alive);
+    if (q >= 0) P.q_free[q] = s;
+  }
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(128) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
+  int n = cnt->n_shadow;
+  LwTraceCount tc;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    int k = base + threadIdx.x;
+    if (k < n) {
+      int s = P.q_shadow[k];
+      double o[3] = {P.sox[s], P.soy[s], P.soz[s]}, d[3] = {P.sdx[s], P.sdy[s], P.sdz[s]};
+      if (!lw_trace_any<COUNT>(bvh, o, d, P.stmax[s], &tc)) {
+        P.lx[s] = P.lx[s] + P.scx[s];
+        P.ly[s] = P.ly[s] + P.scy[s];
+        P.lz[s] = P.lz[s] + P.scz[s];
+      }
+    }
+  }
+  if (COUNT) {
+    warp_add(&cnt->sh_nodes, tc.nodes);
+    warp_add(&cnt->sh_tris, tc.tris);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt->rays_shadow += (unsigned long long)n;
+}
+
+// end of wave: next-extension queue becomes current; shadow queue consumed
+__global__ void k_swap_queues(Counters* cnt) {
+  cnt->n_ext = cnt->n_ext_next;
+  cnt->n_ext_next = 0;
+  cnt->n_shadow = 0;
+}
+
+// megakernel tail over the slots still in flight (state is "ready to trace")
+__global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned long long* __restrict__ fb,
+                                                   Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
+  int n = cnt->n_ext;
+  unsigned long long next = 0, nsh = 0, bad = 0, paths = 0;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    int k = base + threadIdx.x;
+    if (k < n) {
+      int s = P.q_ext[k];
+      PathState ps;
+      load_state(P, s, ps);
+      run_to_completion(S, bvh, ps, next, nsh);
+      bad += lw_accumulate(fb, P.pix[s], ps.L);
+      paths++;
+      P.flags[s] = 0;
+    }
+  }
+  warp_add(&cnt->rays_ext, next);
+  warp_add(&cnt->rays_shadow, nsh);
+  warp_add(&cnt->nonfinite, bad);
+  warp_add(&cnt->paths, paths);
+}
+
+__global__ void k_tail_done(Counters* cnt) { cnt->n_ext = 0; }
+
+// ---- debug / parity kernels -------------------------------------------------------------
+
+__global__ void k_trace_closest_dbg(DevScene S, const double* o, const double* d, const double* tm, long long n,
+                                    double* ot, long long* otri, double* ob) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]}, dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  LwHit h;
+  lw_trace_closest(S.bvh, oo, dd, tm[i], h);
+  bool hit = h.tri >= 0;
+  ot[i] = hit ? h.t : 1e308;
+  otri[i] = hit ? h.tri : -1;
+  ob[2 * i] = hit ? h.bu : 0.0;
+  ob[2 * i + 1] = hit ? h.bv : 0.0;
+}
+
+__global__ void k_trace_any_dbg(DevScene S, const double* o, const double* d, const double* tm, long long n, int* occ) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]}, dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  occ[i] = lw_trace_any(S.bvh, oo, dd, tm[i]) ? 1 : 0;
+}
+
+__global__ void k_camera_dbg(DevScene S, const long long* idx, long long n, double* oo, double* od) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  v3 o, d;
+  lw_camera_ray(S, idx[i], o, d);
+  oo[3 * i] = o.x;
+  oo[3 * i + 1] = o.y;
+  oo[3 * i + 2] = o.z;
+  od[3 * i] = d.x;
+  od[3 * i + 1] = d.y;
+  od[3 * i + 2] = d.z;
+}
+
+__global__ void k_resolve(const unsigned long long* fb, long long n, double scale, float* out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (float)((double)(long long)fb[i] * scale);
+}
+
+int nrnodes_of(const lw_ctx* c) { return c->ref_bvh.nnodes > 1 ? (int)((c->ref_bvh.nnodes - 1) / 2) : 0; }
+
+int alloc_pool(lw_ctx* c, int size) {
+  if (c->pool.size == size) return LW_OK;
+  free_pool(c);
+  Pool& P = c->pool;
+  size_t nd = 33, ni = 3 + 4;  // doubles and ints per slot (+ index as long long)
+  size_t bytes = (size_t)size * (nd * 8 + 8 + ni * 4) + 4096;
+  LW_CUDA_TRY(cudaMalloc(&P.block, bytes));
+  char* p = (char*)P.block;
+  auto dd = [&](double*& x) {
+    x = (double*)p;
+    p += sizeof(double) * size;
+  };
+  auto ii = [&](int*& x) {
+    x = (int*)p;
+    p += sizeof(int) * size;
+  };
+  dd(P.ox); dd(P.oy); dd(P.oz); dd(P.dx); dd(P.dy); dd(P.dz);
+  dd(P.bx); dd(P.by); dd(P.bz); dd(P.lx); dd(P.ly); dd(P.lz);
+  dd(P.pdf_prev);
+  P.index = (long long*)p;
+  p += sizeof(long long) * size;
+  dd(P.ht); dd(P.hbu); dd(P.hbv);
+  dd(P.sox); dd(P.soy); dd(P.soz); dd(P.sdx); dd(P.sdy); dd(P.sdz); dd(P.stmax); dd(P.scx); dd(P.scy); dd(P.scz);
+  ii(P.pix); ii(P.flags); ii(P.htri);
+  ii(P.q_ext); ii(P.q_ext_next); ii(P.q_shadow); ii(P.q_free);
+  P.size = size;
+  LW_CUDA_TRY(cudaMemsetAsync(P.flags, 0, sizeof(int) * size, c->stream));
+  return LW_OK;
+}
+
+int run_pass(lw_ctx* c, const WorkRange& w) {
+  LW_CHECK_ARG(c->has_scene, "render: no scene uploaded");
+  LW_CHECK_ARG(c->configured, "render: lw_render_configure not called");
+  cudaStream_t st = c->stream;
+  const lw_render_params& p = c->params;
+  int nr = nrnodes_of(c);
+  int use_smem = c->smem_bytes > 0 ? 1 : 0;
+  size_t smem = c->smem_bytes;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  Counters zero;
+  memset(&zero, 0, sizeof(zero));
+  LW_CUDA_TRY(cudaMemcpyAsync(c->d_cnt, &zero, sizeof(Counters), cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaEventRecord(c->ev0, st));
+  int64_t launches = 0;
+  long long total = w.nits * w.npix;
+  std::vector<std::pair<size_t, int>> marks;
+  if (p.engine == LW_ENGINE_MEGAKERNEL) {
+    int grid = nsm * 8;
+    long long need = (total + 127) / 128;
+    if (need < grid) grid = (int)std::max<long long>(1, need);
+    k_megakernel<<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem);
+    LW_CUDA_TRY(cudaGetLastError());
+    launches = 1;
+  } else {
+    int pool = 1 << p.pool_log2;
+    if ((long long)pool > total) {
+      long long r = 1;
+      while (r < total) r <<= 1;
+      pool = (int)std::max<long long>(r, 1024);
+    }
+    LW_STATUS_TRY(alloc_pool(c, pool));
+    // every slot starts on the free queue
+    {
+      // initial free queue: identity
+      static thread_local std::vector<int> ident;
+      if ((int)ident.size() < pool) {
+        ident.resize(pool);
+        for (int k = 0; k < pool; k++) ident[k] = k;
+      }
+      LW_CUDA_TRY(cudaMemcpyAsync(c->pool.q_free, ident.data(), sizeof(int) * pool, cudaMemcpyHostToDevice, st));
+      LW_CUDA_TRY(cudaMemsetAsync(c->pool.flags, 0, sizeof(int) * pool, st));
+      Counters init = zero;
+      init.n_free = pool;
+      LW_CUDA_TRY(cudaMemcpyAsync(c->d_cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
+    }
+    const int gT = nsm * 8, gS = nsm * 8, gR = nsm * 4;
+    long long waves = 0;
+    const int check_every = 8;
+    const bool count = (c->instr & LW_INSTR_COUNT) != 0, timed = (c->instr & LW_INSTR_TIME) != 0;
+    size_t ev = 0;
+    auto event = [&](void) -> cudaEvent_t {
+      if (ev >= c->evpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->evpool.push_back(e);
+      }
+      return c->evpool[ev++];
+    };
+    marks.clear();  // (event index of the start, 0 = ext / 1 = shadow)
+    for (;;) {
+      for (int k = 0; k < check_every; k++) {
+        k_regen_decide<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0);
+        k_regenerate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
+        if (timed) {
+          marks.push_back({ev, 0});
+          cudaEventRecord(event(), st);
+        }
+        if (count)
+          k_trace_ext<true><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        else
+          k_trace_ext<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        if (timed) cudaEventRecord(event(), st);
+        k_shade<<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
+        if (timed) {
+          marks.push_back({ev, 1});
+          cudaEventRecord(event(), st);
+        }
+        if (count)
+          k_trace_shadow<true><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        else
+          k_trace_shadow<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        if (timed) cudaEventRecord(event(), st);
+        k_swap_queues<<<1, 1, 0, st>>>(c->d_cnt);
+        launches += 6;
+        waves++;
+      }
+      LW_CUDA_TRY(cudaGetLastError());
+      LW_CUDA_TRY(cudaMemcpyAsync(c->h_cnt, c->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+      LW_CUDA_TRY(cudaStreamSynchronize(st));
+      const Counters& h = *c->h_cnt;
+      bool work_left = h.work_next < (unsigned long long)total;
+      if (!work_left && h.n_ext == 0) break;
+      if (!work_left && p.megakernel_tail > 0 && h.n_ext < p.megakernel_tail) {
+        k_mega_tail<<<std::max(1, std::min(nsm * 8, (h.n_ext + 127) / 128)), 128, smem, st>>>(c->S, c->pool, c->d_fb,
+                                                                                               c->d_cnt, nr, use_smem);
+        k_tail_done<<<1, 1, 0, st>>>(c->d_cnt);
+        launches += 2;
+        break;
+      }
+      if (waves > 100000) {
+        set_error("wavefront did not terminate");
+        return LW_ERR_STATE;
+      }
+    }
+    // flush the remaining finished paths
+    k_regen_decide<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1);
+    k_regenerate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
+    launches += 2;
+  }
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaEventRecord(c->ev1, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(c->h_cnt, c->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  c->last_total_ms = ms;
+  c->last_launches = launches;
+  const Counters& h = *c->h_cnt;
+  memset(&c->prof, 0, sizeof(c->prof));
+  c->prof.total_ms = ms;
+  c->prof.kernel_launches = launches;
+  for (auto& m : marks) {
+    float e = 0.f;
+    cudaEventElapsedTime(&e, c->evpool[m.first], c->evpool[m.first + 1]);
+    if (m.second == 0) {
+      c->prof.trace_ext_ms += e;
+      c->prof.trace_ext_launches++;
+    } else {
+      c->prof.trace_shadow_ms += e;
+      c->prof.trace_shadow_launches++;
+    }
+  }
+  c->last_trace_ms = c->prof.trace_ext_ms + c->prof.trace_shadow_ms;
+  c->prof.ext_rays = (int64_t)h.rays_ext;
+  c->prof.shadow_rays = (int64_t)h.rays_shadow;
+  c->prof.ext_nodes = (int64_t)h.ext_nodes;
+  c->prof.ext_tris = (int64_t)h.ext_tris;
+  c->prof.shadow_nodes = (int64_t)h.sh_nodes;
+  c->prof.shadow_tris = (int64_t)h.sh_tris;
+  c->stats.paths += (int64_t)h.paths;
+  c->stats.rays_extension += (int64_t)h.rays_ext;
+  c->stats.rays_shadow += (int64_t)h.rays_shadow;
+  c->stats.nonfinite += (int64_t)h.nonfinite;
+  c->stats.waves += (int64_t)h.waves;
+  c->stats.regenerations += (int64_t)h.regens;
+  return LW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lw_ctx_create(int device, lw_ctx** out) {
+  LW_CHECK_ARG(out, "null out");
+  LW_CUDA_TRY(cudaSetDevice(device));
+  lw_ctx* c = new lw_ctx();
+  c->device = device;
+  memset(&c->S, 0, sizeof(c->S));
+  memset(&c->stats, 0, sizeof(c->stats));
+  memset(&c->params, 0, sizeof(c->params));
+  memset(&c->prof, 0, sizeof(c->prof));
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  c->stream = c->own_stream;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_cnt, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_cnt, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e != cudaSuccess) {
+    set_error("context creation failed: %s", cudaGetErrorString(e));
+    delete c;
+    return LW_ERR_CUDA;
+  }
+  *out = c;
+  return LW_OK;
+}
+
+int lw_ctx_set_stream(lw_ctx* c, void* stream) {
+  LW_CHECK_ARG(c, "null ctx");
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  return LW_OK;
+}
+
+int lw_ctx_set_instrumentation(lw_ctx* c, int flags) {
+  LW_CHECK_ARG(c, "null ctx");
+  c->instr = flags;
+  return LW_OK;
+}
+
+int lw_ctx_kernel_profile(lw_ctx* c, lw_kernel_profile* out) {
+  LW_CHECK_ARG(c && out, "null argument");
+  *out = c->prof;
+  return LW_OK;
+}
+
+int lw_ctx_destroy(lw_ctx* c) {
+  if (!c) return LW_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+  free_scene(c);
+  free_pool(c);
+  cudaFree(c->d_fb);
+  cudaFree(c->d_qdims);
+  cudaFree(c->d_qperm);
+  cudaFree(c->d_cnt);
+  cudaFreeHost(c->h_cnt);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  cudaStreamDestroy(c->own_stream);
+  delete c;
+  return LW_OK;
+}
+
+int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
+  LW_CHECK_ARG(c && d, "null argument");
+  LW_CHECK_ARG(d->ntris >= 0 && (d->ntris == 0 || (d->verts && d->normals && d->material)), "bad geometry");
+  LW_CHECK_ARG(d->nmaterials > 0 && d->materials, "scene needs at least one material");
+  LW_CHECK_ARG(d->nemit >= 0 && (d->nemit == 0 || (d->emit_tri && d->emit_radiance && d->emit_twosided && d->emit_weight)),
+               "bad emitter arrays");
+  cudaSetDevice(c->device);
+  free_scene(c);
+  cudaStream_t st = c->stream;
+  DevScene& S = c->S;
+  int64_t n = d->ntris;
+  c->ntris = n;
+  for (int64_t k = 0; k < n; k++)
+    LW_CHECK_ARG(d->material[k] >= 0 && d->material[k] < d->nmaterials, "material index out of range");
+  for (int64_t e = 0; e < d->nemit; e++) LW_CHECK_ARG(d->emit_tri[e] >= 0 && d->emit_tri[e] < n, "emitter triangle out of range");
+  double* dv;
+  LW_STATUS_TRY(dev_upload(c, dv, d->verts, 9 * n));
+  double* dn;
+  LW_STATUS_TRY(dev_upload(c, dn, d->normals, 9 * n));
+  int* dm;
+  LW_STATUS_TRY(dev_upload(c, dm, (const int*)d->material, n));
+  lw_material* dmat;
+  LW_STATUS_TRY(dev_upload(c, dmat, d->materials, d->nmaterials));
+  S.verts = dv;
+  S.normals = dn;
+  S.material = dm;
+  S.materials = dmat;
+  // BVH on the device (reference layout), then the render layout
+  LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
+  int64_t nn = c->ref_bvh.nnodes;
+  int nr = nrnodes_of(c);
+  RNode* rn;
+  LTri* lt;
+  LW_STATUS_TRY(dev_alloc(c, rn, nr > 0 ? nr : 1));
+  LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
+  if (n > 0) {
+    int* flag;
+    int* imap;
+    LW_STATUS_TRY(dev_alloc(c, flag, nn));
+    LW_STATUS_TRY(dev_alloc(c, imap, nn));
+    k_internal_flags<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.children, nn, flag);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, imap, (int)nn, st);
+    void* tmp;
+    LW_CUDA_TRY(cudaMalloc(&tmp, tb > 0 ? tb : 16));
+    LW_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, imap, (int)nn, st));
+    k_build_rnodes<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.bounds, c->ref_bvh.children, nn, imap, rn);
+    k_build_ltris<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, c->ref_bvh.order, n, lt);
+    LW_CUDA_TRY(cudaGetLastError());
+    LW_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+  }
+  double rb[6] = {0, 0, 0, 0, 0, 0};
+  long long rc[2] = {-1, 0};
+  LW_CUDA_TRY(cudaMemcpyAsync(rb, c->ref_bvh.bounds, sizeof(rb), cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(rc, c->ref_bvh.children, sizeof(rc), cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  S.bvh.nodes = rn;
+  S.bvh.tris = lt;
+  S.bvh.ntris = n;
+  for (int a = 0; a < 6; a++) S.bvh.root_box[a] = rb[a];
+  S.bvh.root_ref = rc[0] >= 0 ? 0 : (int)(-(1 + ((-(rc[0] + 1)) << 3 | rc[1])));
+  // stage in shared memory when the whole render BVH fits comfortably
+  size_t bytes = sizeof(RNode) * (size_t)nr + sizeof(LTri) * (size_t)n;
+  c->smem_bytes = (n > 0 && bytes <= 48 * 1024) ? bytes : 0;
+  // emitters
+  int* eot;
+  LW_STATUS_TRY(dev_alloc(c, eot, n > 0 ? n : 1));
+  LW_CUDA_TRY(cudaMemsetAsync(eot, 0xff, sizeof(int) * (n > 0 ? n : 1), st));
+  S.emit_of_tri = eot;
+  S.nemit = d->nemit;
+  if (d->nemit > 0) {
+    std::vector<double> prob(d->nemit), pdf(d->nemit);
+    std::vector<int32_t> alias(d->nemit);
+    if (alias_build(d->emit_weight, d->nemit, prob.data(), alias.data(), pdf.data()) != LW_OK) {
+      S.nemit = 0;  // no light carries energy (oracle: same rule)
+    }
+    long long* et;
+    double *er, *ea, *ep, *epdf;
+    int *e2, *eal;
+    LW_STATUS_TRY(dev_upload(c, et, (const long long*)d->emit_tri, d->nemit));
+    LW_STATUS_TRY(dev_upload(c, er, d->emit_radiance, 3 * d->nemit));
+    LW_STATUS_TRY(dev_upload(c, e2, (const int*)d->emit_twosided, d->nemit));
+    LW_STATUS_TRY(dev_alloc(c, ea, d->nemit));
+    LW_STATUS_TRY(dev_upload(c, ep, prob.data(), d->nemit));
+    LW_STATUS_TRY(dev_upload(c, epdf, pdf.data(), d->nemit));
+    LW_STATUS_TRY(dev_upload(c, eal, (const int*)alias.data(), d->nemit));
+    k_emitters<<<grid_for(d->nemit, 256, 1 << 30), 256, 0, st>>>(dv, et, d->nemit, ea, eot);
+    LW_CUDA_TRY(cudaGetLastError());
+    S.emit_tri = et;
+    S.emit_rad = er;
+    S.emit_two = e2;
+    S.emit_area = ea;
+    S.emit_prob = ep;
+    S.emit_pdf = epdf;
+    S.emit_alias = eal;
+    LW_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  // environment
+  S.env_kind = d->env_kind;
+  S.env_w = d->env_width;
+  S.env_h = d->env_height;
+  for (int k = 0; k < 3; k++) S.env_const[k] = d->env_constant[k];
+  S.env_scale = d->env_scale;
+  if (d->env_kind == LW_ENV_IMAGE) {
+    LW_CHECK_ARG(d->env_width > 0 && d->env_height > 0 && d->env_image && d->env_weight, "bad environment image");
+    int64_t nt = (int64_t)d->env_width * d->env_height;
+    std::vector<double> prob(nt), pdf(nt);
+    std::vector<int32_t> alias(nt);
+    if (alias_build(d->env_weight, nt, prob.data(), alias.data(), pdf.data()) != LW_OK) {
+      S.env_kind = LW_ENV_NONE;
+    } else {
+      float* img;
+      double *pp, *pd;
+      int* pa;
+      LW_STATUS_TRY(dev_upload(c, img, d->env_image, 3 * nt));
+      LW_STATUS_TRY(dev_upload(c, pp, prob.data(), nt));
+      LW_STATUS_TRY(dev_upload(c, pd, pdf.data(), nt));
+      LW_STATUS_TRY(dev_upload(c, pa, (const int*)alias.data(), nt));
+      S.env_img = img;
+      S.env_prob = pp;
+      S.env_pdf = pd;
+      S.env_alias = pa;
+    }
+  } else if (d->env_kind != LW_ENV_CONSTANT) {
+    S.env_kind = LW_ENV_NONE;
+  }
+  bool has_env = S.env_kind != LW_ENV_NONE, has_tri = S.nemit > 0;
+  S.p_env = has_env ? (has_tri ? d->p_env : 1.0) : 0.0;
+  S.p_tri = has_tri ? (has_env ? 1.0 - d->p_env : 1.0) : 0.0;
+  for (int k = 0; k < 3; k++) {
+    S.cam_pos[k] = d->cam_pos[k];
+    S.cam_fwd[k] = d->cam_fwd[k];
+    S.cam_right[k] = d->cam_right[k];
+    S.cam_up[k] = d->cam_up[k];
+  }
+  S.tan_half = d->tan_half_fov;
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  c->has_scene = true;
+  return LW_OK;
+}
+
+int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
+  LW_CHECK_ARG(c && p, "null argument");
+  LW_CHECK_ARG(p->width > 0 && p->height > 0, "resolution must be positive");
+  LW_CHECK_ARG((int64_t)p->width * p->height < (1LL << 31), "resolution too large");
+  LW_CHECK_ARG(p->max_depth >= 1 && p->max_depth <= 255, "max_depth must be in [1, 255]");
+  LW_CHECK_ARG(p->engine == LW_ENGINE_WAVEFRONT || p->engine == LW_ENGINE_MEGAKERNEL, "unknown engine");
+  LW_CHECK_ARG(p->pool_log2 >= 10 && p->pool_log2 <= 26, "pool_log2 must be in [10, 26]");
+  LW_CHECK_ARG(p->ndims >= 4 + 8 * (int64_t)p->max_depth, "dimension table too small for max_depth");
+  cudaSetDevice(c->device);
+  std::vector<QmcDim> dims;
+  std::vector<uint16_t> perm;
+  LW_STATUS_TRY(pack_qmc_tables(p->bases, p->ndims, p->perm_flat, p->perm_len, p->perm_offset, dims, perm));
+  cudaFree(c->d_qdims);
+  cudaFree(c->d_qperm);
+  c->d_qdims = nullptr;
+  c->d_qperm = nullptr;
+  LW_CUDA_TRY(cudaMalloc(&c->d_qdims, sizeof(QmcDim) * dims.size()));
+  LW_CUDA_TRY(cudaMalloc(&c->d_qperm, sizeof(uint16_t) * perm.size()));
+  LW_CUDA_TRY(cudaMemcpy(c->d_qdims, dims.data(), sizeof(QmcDim) * dims.size(), cudaMemcpyHostToDevice));
+  LW_CUDA_TRY(cudaMemcpy(c->d_qperm, perm.data(), sizeof(uint16_t) * perm.size(), cudaMemcpyHostToDevice));
+  c->params = *p;
+  c->params.bases = nullptr;
+  c->params.perm_flat = nullptr;
+  c->params.perm_offset = nullptr;
+  c->S.qdims = c->d_qdims;
+  c->S.qperm = c->d_qperm;
+  c->S.W = p->width;
+  c->S.H = p->height;
+  c->S.max_depth = p->max_depth;
+  c->S.rr_start = p->rr_start;
+  int64_t px = (int64_t)p->width * p->height;
+  if (px != c->fb_pixels) {
+    cudaFree(c->d_fb);
+    c->d_fb = nullptr;
+    LW_CUDA_TRY(cudaMalloc(&c->d_fb, sizeof(unsigned long long) * 3 * px));
+    c->fb_pixels = px;
+    LW_CUDA_TRY(cudaMemset(c->d_fb, 0, sizeof(unsigned long long) * 3 * px));
+  }
+  c->configured = true;
+  return LW_OK;
+}
+
+int lw_framebuffer_clear(lw_ctx* c) {
+  LW_CHECK_ARG(c && c->configured, "not configured");
+  LW_CUDA_TRY(cudaMemsetAsync(c->d_fb, 0, sizeof(unsigned long long) * 3 * c->fb_pixels, c->stream));
+  memset(&c->stats, 0, sizeof(c->stats));
+  return LW_OK;
+}
+
+int lw_render_pass(lw_ctx* c, int64_t it_begin, int64_t it_end) {
+  LW_CHECK_ARG(c && c->configured, "not configured");
+  return lw_render_pass_pixels(c, it_begin, it_end, 0, c->fb_pixels);
+}
+
+int lw_render_pass_pixels(lw_ctx* c, int64_t it_begin, int64_t it_end, int64_t pix_begin, int64_t pix_end) {
+  LW_CHECK_ARG(c && c->configured, "not configured");
+  LW_CHECK_ARG(it_begin >= 0 && it_end >= it_begin, "bad iteration range");
+  LW_CHECK_ARG(pix_begin >= 0 && pix_end <= c->fb_pixels && pix_end >= pix_begin, "bad pixel range");
+  if (it_end == it_begin || pix_end == pix_begin) return LW_OK;
+  // qmc.py:194-195: the global sample index must fit in 64 bits (here: in a signed int64)
+  unsigned __int128 maxidx = (unsigned __int128)(it_end - 1) * (unsigned __int128)c->fb_pixels + (unsigned __int128)pix_end;
+  if (maxidx >> 63) {
+    set_error("sample index exceeds 64 bits");
+    return LW_ERR_OVERFLOW;
+  }
+  cudaSetDevice(c->device);
+  WorkRange w{it_begin, it_end - it_begin, pix_begin, pix_end - pix_begin};
+  return run_pass(c, w);
+}
+
+int lw_ctx_synchronize(lw_ctx* c) {
+  LW_CHECK_ARG(c, "null ctx");
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_framebuffer_download(lw_ctx* c, int64_t* host_fb) {
+  LW_CHECK_ARG(c && c->configured && host_fb, "bad arguments");
+  LW_CUDA_TRY(cudaMemcpyAsync(host_fb, c->d_fb, sizeof(int64_t) * 3 * c->fb_pixels, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_framebuffer_resolve(lw_ctx* c, double inv_samples, float* host_rgb) {
+  LW_CHECK_ARG(c && c->configured && host_rgb, "bad arguments");
+  long long n = 3 * c->fb_pixels;
+  float* d_out;
+  LW_CUDA_TRY(cudaMallocAsync((void**)&d_out, sizeof(float) * n, c->stream));
+  double scale = inv_samples / 1048576.0;
+  k_resolve<<<grid_for(n, 256, 1 << 30), 256, 0, c->stream>>>(c->d_fb, n, scale, d_out);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(host_rgb, d_out, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaFreeAsync(d_out, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_framebuffer_copy_device(lw_ctx* c, void* dst) {
+  LW_CHECK_ARG(c && c->configured && dst, "bad arguments");
+  LW_CUDA_TRY(cudaMemcpyAsync(dst, c->d_fb, sizeof(int64_t) * 3 * c->fb_pixels, cudaMemcpyDeviceToDevice, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_framebuffer_load_device(lw_ctx* c, const void* src) {
+  LW_CHECK_ARG(c && c->configured && src, "bad arguments");
+  LW_CUDA_TRY(cudaMemcpyAsync(c->d_fb, src, sizeof(int64_t) * 3 * c->fb_pixels, cudaMemcpyDeviceToDevice, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_get_stats(lw_ctx* c, lw_render_stats* s) {
+  LW_CHECK_ARG(c && s, "null argument");
+  *s = c->stats;
+  return LW_OK;
+}
+
+int lw_ctx_last_pass_timing(lw_ctx* c, double* trace_ms, double* total_ms, int64_t* launches) {
+  LW_CHECK_ARG(c, "null ctx");
+  if (trace_ms) *trace_ms = c->last_trace_ms;
+  if (total_ms) *total_ms = c->last_total_ms;
+  if (launches) *launches = c->last_launches;
+  return LW_OK;
+}
+
+static int dbg_rays(lw_ctx* c, const double* o, const double* d, const double* tm, int64_t n, DevBuf& bo, DevBuf& bd,
+                    DevBuf& bt) {
+  LW_CUDA_TRY(bo.alloc(sizeof(double) * 3 * n));
+  LW_CUDA_TRY(bd.alloc(sizeof(double) * 3 * n));
+  LW_CUDA_TRY(bt.alloc(sizeof(double) * n));
+  LW_CUDA_TRY(cudaMemcpyAsync(bo.p, o, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(bd.p, d, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(bt.p, tm, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_trace_closest(lw_ctx* c, const double* o, const double* d, const double* tm, int64_t n, double* out_t,
+                         int64_t* out_tri, double* out_bary) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  if (n <= 0) return LW_OK;
+  cudaSetDevice(c->device);
+  DevBuf bo, bd, bt, rt, rtri, rb;
+  LW_STATUS_TRY(dbg_rays(c, o, d, tm, n, bo, bd, bt));
+  LW_CUDA_TRY(rt.alloc(sizeof(double) * n));
+  LW_CUDA_TRY(rtri.alloc(sizeof(long long) * n));
+  LW_CUDA_TRY(rb.alloc(sizeof(double) * 2 * n));
+  k_trace_closest_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, c->stream>>>(c->S, bo.as<double>(), bd.as<double>(),
+                                                                         bt.as<double>(), n, rt.as<double>(),
+                                                                         rtri.as<long long>(), rb.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_t, rt.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_tri, rtri.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_bary, rb.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_trace_any(lw_ctx* c, const double* o, const double* d, const double* tm, int64_t n, int32_t* occ) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  if (n <= 0) return LW_OK;
+  cudaSetDevice(c->device);
+  DevBuf bo, bd, bt, ro;
+  LW_STATUS_TRY(dbg_rays(c, o, d, tm, n, bo, bd, bt));
+  LW_CUDA_TRY(ro.alloc(sizeof(int) * n));
+  k_trace_any_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, c->stream>>>(c->S, bo.as<double>(), bd.as<double>(),
+                                                                     bt.as<double>(), n, ro.as<int>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(occ, ro.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_camera_rays(lw_ctx* c, const int64_t* idx, int64_t n, double* out_o, double* out_d) {
+  LW_CHECK_ARG(c && c->has_scene && c->configured, "scene and configuration required");
+  if (n <= 0) return LW_OK;
+  cudaSetDevice(c->device);
+  DevBuf bi, bo, bd;
+  LW_CUDA_TRY(bi.alloc(sizeof(long long) * n));
+  LW_CUDA_TRY(bo.alloc(sizeof(double) * 3 * n));
+  LW_CUDA_TRY(bd.alloc(sizeof(double) * 3 * n));
+  LW_CUDA_TRY(cudaMemcpyAsync(bi.p, idx, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+  k_camera_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, c->stream>>>(c->S, bi.as<long long>(), n, bo.as<double>(),
+                                                                  bd.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_o, bo.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_d, bd.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_bvh_info(lw_ctx* c, int64_t* nnodes) {
+  LW_CHECK_ARG(c && c->has_scene && nnodes, "no scene");
+  *nnodes = c->ref_bvh.nnodes;
+  return LW_OK;
+}
+
+int lw_ctx_bvh_download(lw_ctx* c, double* bounds, int64_t* children, int64_t* order) {
+  LW_CHECK_ARG(c && c->has_scene && bounds && children, "no scene");
+  int64_t nn = c->ref_bvh.nnodes;
+  LW_CUDA_TRY(cudaMemcpyAsync(bounds, c->ref_bvh.bounds, sizeof(double) * 6 * nn, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(children, c->ref_bvh.children, sizeof(long long) * 2 * nn, cudaMemcpyDeviceToHost, c->stream));
+  if (c->ntris > 0 && order)
+    LW_CUDA_TRY(cudaMemcpyAsync(order, c->ref_bvh.order, sizeof(long long) * c->ntris, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+"""Render entry points: scene in, progressive framebuffer out.
+
+Implements the call stack the reference declares but does not ship
+(`lumenwave.cli:main` -> `cmd_render`, SPEC.md:765-773 -> scheduler -> wavefront
+-> integrator).  One `Renderer` owns one GPU context (liblw_b200.so `lw_ctx`);
+multi-GPU rendering partitions QMC sample space (distributed.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from paper_1705_01263_b200 import _abi
+from paper_1705_01263_b200._abi import LwRenderParams, LwRenderStats, check, ptr
+from paper_1705_01263_b200.qmc import DimensionTable
+from paper_1705_01263_b200.scene import pack_scene
+
+ENGINES = {"wavefront": _abi.LW_ENGINE_WAVEFRONT, "megakernel": _abi.LW_ENGINE_MEGAKERNEL}
+FB_SCALE = float(1 << _abi.LW_FB_FRAC_BITS)
+
+
+class RenderParams:
+    """Resolution, depth, QMC dimension table and engine knobs (LwRenderParams + owned arrays)."""
+
+    def __init__(self, width, height, max_depth=8, rr_start=4, engine="wavefront", pool_log2=20,
+                 regen_fraction=0.5, megakernel_tail=0):
+        if engine not in ENGINES:
+            raise ValueError(f"unknown engine '{engine}'")
+        self.width, self.height, self.max_depth = int(width), int(height), int(max_depth)
+        self.table = DimensionTable(max(self.max_depth, 1))
+        self.bases = np.ascontiguousarray(self.table.bases, dtype=np.int64)
+        self.perm_flat = np.ascontiguousarray(self.table.perm_flat, dtype=np.int64)
+        self.perm_offset = np.ascontiguousarray(self.table.perm_offset, dtype=np.int64)
+        s = LwRenderParams()
+        s.width, s.height, s.max_depth, s.rr_start = self.width, self.height, self.max_depth, int(rr_start)
+        s.ndims = len(self.bases)
+        s.bases = ptr(self.bases, C.c_int64)
+        s.perm_flat = ptr(self.perm_flat, C.c_int64)
+        s.perm_len = len(self.perm_flat)
+        s.perm_offset = ptr(self.perm_offset, C.c_int64)
+        s.engine = ENGINES[engine]
+        s.pool_log2 = int(pool_log2)
+        s.regen_fraction = float(regen_fraction)
+        s.megakernel_tail = int(megakernel_tail)
+        self.struct = s
+        self.engine = engine
+
+    @property
+    def pixels(self):
+        return self.width * self.height
+
+
+class Renderer:
+    """Progressive renderer on one GPU."""
+
+    def __init__(self, scene, width, height, max_depth=8, device=0, engine="wavefront", p_env=0.5, rr_start=4,
+                 pool_log2=20, regen_fraction=0.5, megakernel_tail=0, packed=None):
+        self.lib = _abi.lib()
+        self.packed = packed if packed is not None else pack_scene(scene, p_env=p_env)
+        self.params = RenderParams(width, height, max_depth, rr_start, engine, pool_log2, regen_fraction,
+                                   megakernel_tail)
+        self.device = int(device)
+        h = C.c_void_p()
+        check(self.lib.lw_ctx_create(self.device, C.byref(h)))
+        self.ctx = h
+        try:
+            check(self.lib.lw_scene_upload(self.ctx, C.byref(self.packed.desc)))
+            check(self.lib.lw_render_configure(self.ctx, C.byref(self.params.struct)))
+        except Exception:
+            self.close()
+            raise
+        self.iterations = 0
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.lw_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- rendering
+    def clear(self):
+        check(self.lib.lw_framebuffer_clear(self.ctx))
+        self.iterations = 0
+
+    def render_pass(self, it_begin, it_end, pix_begin=0, pix_end=None):
+        """Accumulate iterations [it_begin, it_end) (optionally a pixel range) into the framebuffer."""
+        if pix_end is None:
+            pix_end = self.params.pixels
+        check(self.lib.lw_render_pass_pixels(self.ctx, int(it_begin), int(it_end), int(pix_begin), int(pix_end)))
+        self.iterations += int(it_end) - int(it_begin)
+
+    def synchronize(self):
+        check(self.lib.lw_ctx_synchronize(self.ctx))
+
+    def framebuffer(self) -> np.ndarray:
+        """Raw int64 fixed-point framebuffer, (H*W, 3) in units of 2^-20 radiance."""
+        fb = np.empty((self.params.pixels, 3), dtype=np.int64)
+        check(self.lib.lw_framebuffer_download(self.ctx, ptr(fb, C.c_int64)))
+        return fb
+
+    def image(self, samples=None) -> np.ndarray:
+        """Resolved (H, W, 3) float32 radiance = framebuffer / samples per pixel (GPU resolve)."""
+        samples = self.iterations if samples is None else samples
+        out = np.empty((self.params.height, self.params.width, 3), dtype=np.float32)
+        check(self.lib.lw_framebuffer_resolve(self.ctx, 1.0 / max(samples, 1), ptr(out, C.c_float)))
+        return out
+
+    def copy_framebuffer_to(self, device_ptr: int):
+        check(self.lib.lw_framebuffer_copy_device(self.ctx, C.c_void_p(device_ptr)))
+
+    def load_framebuffer_from(self, device_ptr: int):
+        check(self.lib.lw_framebuffer_load_device(self.ctx, C.c_void_p(device_ptr)))
+
+    def set_stream(self, stream_handle: int | None):
+        """Run this context's work on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        check(self.lib.lw_ctx_set_stream(self.ctx, C.c_void_p(stream_handle or None)))
+
+    def set_instrumentation(self, time_kernels=False, count_work=False):
+        flags = (_abi.LW_INSTR_TIME if time_kernels else 0) | (_abi.LW_INSTR_COUNT if count_work else 0)
+        check(self.lib.lw_ctx_set_instrumentation(self.ctx, flags))
+
+    def kernel_profile(self) -> dict:
+        p = _abi.LwKernelProfile()
+        check(self.lib.lw_ctx_kernel_profile(self.ctx, C.byref(p)))
+        return p.as_dict()
+
+    def stats(self) -> dict:
+        s = LwRenderStats()
+        check(self.lib.lw_get_stats(self.ctx, C.byref(s)))
+        return s.as_dict()
+
+    def last_pass_timing(self) -> dict:
+        tr = C.c_double()
+        tot = C.c_double()
+        ln = C.c_int64()
+        check(self.lib.lw_ctx_last_pass_timing(self.ctx, C.byref(tr), C.byref(tot), C.byref(ln)))
+        return {"trace_ms": tr.value, "total_ms": tot.value, "launches": ln.value}
+
+    # -- parity surface
+    def trace_closest(self, origins, dirs, tmaxs=None):
+        o = np.ascontiguousarray(origins, np.float64)
+        d = np.ascontiguousarray(dirs, np.float64)
+        n = len(o)
+        tm = np.full(n, np.inf) if tmaxs is None else np.ascontiguousarray(tmaxs, np.float64)
+        t = np.empty(n)
+        tri = np.empty(n, np.int64)
+        b = np.empty((n, 2))
+        check(self.lib.lw_ctx_trace_closest(self.ctx, ptr(o, C.c_double), ptr(d, C.c_double), ptr(tm, C.c_double), n,
+                                            ptr(t, C.c_double), ptr(tri, C.c_int64), ptr(b, C.c_double)))
+        return t, tri, b
+
+    def trace_any(self, origins, dirs, tmaxs):
+        o = np.ascontiguousarray(origins, np.float64)
+        d = np.ascontiguousarray(dirs, np.float64)
+        tm = np.ascontiguousarray(tmaxs, np.float64)
+        occ = np.empty(len(o), np.int32)
+        check(self.lib.lw_ctx_trace_any(self.ctx, ptr(o, C.c_double), ptr(d, C.c_double), ptr(tm, C.c_double), len(o),
+                                        ptr(occ, C.c_int32)))
+        return occ
+
+    def camera_rays(self, sample_index):
+        idx = np.ascontiguousarray(sample_index, np.int64)
+        o = np.empty((len(idx), 3))
+        d = np.empty((len(idx), 3))
+        check(self.lib.lw_ctx_camera_rays(self.ctx, ptr(idx, C.c_int64), len(idx), ptr(o, C.c_double),
+                                          ptr(d, C.c_double)))
+        return o, d
+
+    def bvh(self):
+        nn = C.c_int64()
+        check(self.lib.lw_ctx_bvh_info(self.ctx, C.byref(nn)))
+        k = nn.value
+        bounds = np.empty((k, 6))
+        children = np.empty((k, 2), np.int64)
+        order = np.empty(max(self.packed.ntris, 1), np.int64)
+        check(self.lib.lw_ctx_bvh_download(self.ctx, ptr(bounds, C.c_double), ptr(children, C.c_int64),
+                                           ptr(order, C.c_int64)))
+        return bounds, children, order[: self.packed.ntris]
+
+
+def render(scene, width, height, spp, max_depth=8, device=0, pass_iterations=16, engine="wavefront", **kw):
+    """Progressive render generator: yields (iterations_done, float32 (H, W, 3) image) after every pass."""
+    with Renderer(scene, width, height, max_depth, device=device, engine=engine, **kw) as r:
+        done = 0
+        while done < spp:
+            step = min(pass_iterations, spp - done)
+            r.render_pass(done, done + step)
+            done += step
+            yield done, r.image(done)

@@ -1,0 +1,191 @@
+"""Render path on the GPU vs the CPU oracle (SPEC-only path).
+
+Bars:
+  * camera rays, render-traversal hit ids / t / barycentrics, any-hit: bit-exact;
+  * framebuffers (int64 fixed point): bit-exact vs the oracle on the same (pixel, iteration) set;
+  * execution-strategy invariance: megakernel == wavefront == any pool size, bit for bit;
+  * SPEC known answers: constant-env camera rays give L exactly, furnace within 1%.
+"""
+
+import numpy as np
+import pytest
+
+from paper_1705_01263_b200 import scenes
+from paper_1705_01263_b200.scene import Environment, Instance, Scene, layered_material, make_camera, pack_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+@pytest.fixture(scope="module")
+def cornell_packed(gpu):
+    return pack_scene(scenes.cornell())
+
+
+def _renderer(packed, w, h, depth, **kw):
+    from paper_1705_01263_b200.render import Renderer
+
+    return Renderer(None, w, h, depth, packed=packed, **kw)
+
+
+def test_scene_bvh_matches_oracle(cornell_packed, oracle):
+    with _renderer(cornell_packed, 64, 64, 4) as r:
+        b, c, o = r.bvh()
+    b2, c2, o2 = oracle.build_bvh(cornell_packed.verts)
+    assert np.array_equal(b, b2) and np.array_equal(c, c2) and np.array_equal(o, o2)
+
+
+def test_camera_rays_bit_exact(cornell_packed, oracle):
+    from paper_1705_01263_b200.render import RenderParams
+
+    w, h = 97, 61
+    rng = np.random.default_rng(1)
+    idx = np.concatenate([np.arange(w * h), rng.integers(0, w * h * 4096, 20000)]).astype(np.int64)
+    with _renderer(cornell_packed, w, h, 4) as r:
+        o, d = r.camera_rays(idx)
+    os_ = oracle.OracleScene(cornell_packed)
+    o2, d2 = os_.camera_rays(RenderParams(w, h, 4), idx)
+    assert np.array_equal(_bits(o), _bits(o2)) and np.array_equal(_bits(d), _bits(d2))
+
+
+def _random_rays(n, lo, hi, seed):
+    rng = np.random.default_rng(seed)
+    o = lo + rng.random((n, 3)) * (hi - lo)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d[:200, 1] = 0.0
+    d[200:300, :2] = 0.0
+    d[200:300, 2] = 1.0
+    return o, d
+
+
+@pytest.mark.parametrize("which", ["cornell", "soup"])
+def test_render_traversal_bit_exact(gpu, oracle, which):
+    if which == "cornell":
+        packed = pack_scene(scenes.cornell())
+        o, d = _random_rays(50000, np.array([0.0, 0.0, -0.5]), np.array([1.0, 1.0, 3.0]), 3)
+    else:
+        packed = pack_scene(scenes.soup(1 << 16, n_materials=8))
+        o, d = _random_rays(50000, np.zeros(3), np.full(3, 20.0), 4)
+    tm = np.where(np.arange(len(o)) % 5 == 0, 3.0, np.inf)
+    with _renderer(packed, 64, 64, 4) as r:
+        t, tri, b = r.trace_closest(o, d, tm)
+        occ = r.trace_any(o, d, np.where(np.isinf(tm), 2.0, tm))
+    os_ = oracle.OracleScene(packed)
+    t2, tri2, b2 = os_.trace_closest(o, d, tm)
+    occ2 = os_.trace_any(o, d, np.where(np.isinf(tm), 2.0, tm))
+    assert np.array_equal(tri, tri2)
+    assert np.array_equal(_bits(t), _bits(t2)) and np.array_equal(_bits(b), _bits(b2))
+    assert np.array_equal(occ, occ2)
+    # near-first + conservative cull == exhaustive search (brute force) on these rays
+    if which == "cornell":
+        v = packed.verts
+        t3, tri3, _ = oracle.intersect_batch(2, np.zeros((1, 6)), np.zeros((1, 2), np.int64), np.zeros(0, np.int64), v, o, d, tm)
+        assert np.array_equal(tri, tri3)
+
+
+@pytest.mark.parametrize("engine", ["megakernel", "wavefront"])
+def test_c1_framebuffer_bit_exact_vs_oracle(cornell_packed, oracle, engine):
+    """C1 (Cornell 64x64, 16 spp, depth 4): the whole accumulated framebuffer, bit for bit."""
+    from paper_1705_01263_b200.render import RenderParams
+
+    with _renderer(cornell_packed, 64, 64, 4, engine=engine, pool_log2=12) as r:
+        r.render_pass(0, 16)
+        fb = r.framebuffer()
+        st = r.stats()
+    fb2, st2 = oracle.OracleScene(cornell_packed).render(RenderParams(64, 64, 4), 0, 16)
+    assert np.array_equal(fb, fb2)
+    assert st["paths"] == 64 * 64 * 16
+    assert st["rays_extension"] == st2["rays_extension"] and st["rays_shadow"] == st2["rays_shadow"]
+
+
+def test_c2_subset_bit_exact(cornell_packed, oracle):
+    """C2 (1024^2, depth 8): a pixel band x 4 iterations bit-exact vs the oracle."""
+    from paper_1705_01263_b200.render import RenderParams
+
+    W = H = 1024
+    pb, pe = 400 * W, 420 * W
+    with _renderer(cornell_packed, W, H, 8) as r:
+        r.render_pass(5, 9, pb, pe)
+        fb = r.framebuffer()
+    fb2, _ = oracle.OracleScene(cornell_packed).render(RenderParams(W, H, 8), 5, 9, pb, pe)
+    assert np.array_equal(fb, fb2)
+
+
+def test_execution_strategy_invariance(cornell_packed):
+    """megakernel, wavefront at several pool sizes / regen thresholds / tail switch: identical."""
+    outs = []
+    cfgs = [dict(engine="megakernel"), dict(engine="wavefront", pool_log2=10), dict(engine="wavefront", pool_log2=14),
+            dict(engine="wavefront", pool_log2=16, regen_fraction=0.0),
+            dict(engine="wavefront", pool_log2=12, megakernel_tail=3000)]
+    for cfg in cfgs:
+        with _renderer(cornell_packed, 128, 96, 8, **cfg) as r:
+            r.render_pass(0, 8)
+            r.render_pass(8, 11)
+            outs.append(r.framebuffer())
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_other_configs_subset_bit_exact(gpu, oracle, cfg):
+    from paper_1705_01263_b200.render import RenderParams
+
+    c = scenes.CONFIGS[cfg]
+    if cfg == "C3":
+        sc = scenes.soup(1 << 16, n_materials=16)
+    elif cfg == "C4":
+        sc = scenes.envmap_scene(512, 256, sphere_subdiv=3)
+    else:
+        sc = scenes.many_lights(2000)
+    packed = pack_scene(sc)
+    W, H = 192, 108
+    with _renderer(packed, W, H, c.max_depth) as r:
+        r.render_pass(0, 3)
+        fb = r.framebuffer()
+    fb2, _ = oracle.OracleScene(packed).render(RenderParams(W, H, c.max_depth), 0, 3)
+    assert np.array_equal(fb, fb2)
+    assert fb.sum() > 0
+
+
+def test_constant_env_camera_rays_return_L(gpu):
+    """camera ray straight to a constant environment L returns L (every pixel, exactly)."""
+    sc = Scene(camera=make_camera((0, 0, 5), (0, 0, 0)), meshes=[], instances=[],
+               materials=[layered_material("m", [{"bsdf": "diffuse", "tint": 0.5}])], emitters=[],
+               environment=Environment(constant=(0.25, 0.5, 1.0)))
+    packed = pack_scene(sc)
+    with _renderer(packed, 32, 32, 4) as r:
+        r.render_pass(0, 4)
+        img = r.image()
+    assert np.all(img == np.array([0.25, 0.5, 1.0], dtype=np.float32))
+
+
+def test_white_furnace(gpu):
+    """unit-albedo diffuse sphere in a constant env converges to the env (1%)."""
+    from paper_1705_01263_b200 import meshgen
+    from paper_1705_01263_b200.scene import Mesh
+
+    pos, nrm, uvw, tris = meshgen.icosphere((0, 0, 0), 1.0, 3)
+    sc = Scene(camera=make_camera((0, 0, 4), (0, 0, 0), fov_y=30.0), meshes=[Mesh("s", pos, nrm, uvw, tris)],
+               instances=[Instance("s", 0, 0)], materials=[layered_material("w", [{"bsdf": "diffuse", "tint": 1.0}])],
+               emitters=[], environment=Environment(constant=(1.0, 1.0, 1.0)))
+    packed = pack_scene(sc)
+    with _renderer(packed, 32, 32, 8, rr_start=8) as r:
+        r.render_pass(0, 256)
+        img = r.image()
+    assert abs(float(img.mean()) - 1.0) < 0.01
+
+
+def test_nee_and_bsdf_agree_single_light(gpu):
+    """Cornell image is stable between two disjoint sample sets (estimator sanity, 3 sigma)."""
+    packed = pack_scene(scenes.cornell())
+    with _renderer(packed, 32, 32, 4) as r:
+        r.render_pass(0, 64)
+        a = r.image().astype(np.float64)
+        r.clear()
+        r.render_pass(64, 128)
+        b = r.image().astype(np.float64)
+    assert abs(a.mean() - b.mean()) / a.mean() < 0.03
