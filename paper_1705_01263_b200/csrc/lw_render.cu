@@ -632,6 +632,8 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           k_trace_shadow<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         if (timed) cudaEventRecord(event(), st);
         k_swap_queues<<<1, 1, 0, st>>>(c->d_cnt);
+        // the next-extension array becomes the current one (kernels take the Pool by value)
+        std::swap(c->pool.q_ext, c->pool.q_ext_next);
         launches += 6;
         waves++;
       }
