@@ -273,9 +273,19 @@ def run_ours(a):
     peaks = load_peaks()
     nodes_per_ray = work["ext_nodes"] / max(work["ext_rays"], 1)
     tris_per_ray = work["ext_tris"] / max(work["ext_rays"], 1)
+    # algorithmic bytes per extension ray: one 128-byte node per node visit, one 80-byte
+    # triangle record per test, plus the SoA ray read (48 B), queue index (4 B) and hit write (28 B)
     bytes_per_ray = 128.0 * nodes_per_ray + 80.0 * tris_per_ray + 80.0
-    ext_rays_rank = rays_ext  # this rank's timed extension rays
-    achieved = (bytes_per_ray * ext_rays_rank / max(prof_launches, 1)) / (prof_ms / max(prof_launches, 1) / 1e3) / 1e9
+    if prof_launches > 0:  # wavefront: the extension-ray trace kernel, timed per launch with CUDA events
+        kernel = "k_trace_ext (closest-hit traversal, wavefront stage)"
+        avg_ms = prof_ms / prof_launches
+        achieved = bytes_per_ray * rays_ext / prof_ms / 1e6  # GB/s
+    else:  # megakernel: the whole pass is one launch; count extension + shadow traversal bytes
+        kernel = "k_megakernel (trace + shade + shadow)"
+        sh_bytes = (128.0 * work["shadow_nodes"] + 80.0 * work["shadow_tris"]) / max(work["shadow_rays"], 1)
+        avg_ms = ms_max / a.steps
+        achieved = (bytes_per_ray * rays_ext + sh_bytes * rays_sh) / ms_max / 1e6
+        prof_ms, prof_launches = ms_max, a.steps
     traffic = load_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -290,9 +300,9 @@ def run_ours(a):
         "gpu_launches": int(launches),
         "clocks": clk,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                     "frac": achieved / peaks.get("hbm_gbs", 6650.0), "kernel": "k_trace_ext (closest-hit traversal)",
+                     "frac": achieved / peaks.get("hbm_gbs", 6650.0), "kernel": kernel,
                      "bytes_per_ray": bytes_per_ray, "nodes_per_ray": nodes_per_ray, "tris_per_ray": tris_per_ray,
-                     "avg_launch_ms": prof_ms / max(prof_launches, 1), "launches": prof_launches,
+                     "avg_launch_ms": avg_ms, "launches": prof_launches,
                      "trace_share_of_step": prof_ms / ms_max,
                      "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},

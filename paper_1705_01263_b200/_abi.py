@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "build", "liblw_b200.so")
+LIB_PATH = os.environ.get("LW_B200_LIB") or os.path.join(_HERE, "csrc", "build", "liblw_b200.so")
 
 LW_OK = 0
 LW_ERR_INVALID = 1

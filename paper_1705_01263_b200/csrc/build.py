@@ -37,8 +37,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(os.path.join(HERE, d)) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile liblw_b200.so (or an experiment variant with extra -D defines into `out`)."""
+    lib = out or LIB
+    if not force and not defines and not _stale():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
@@ -47,18 +49,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     env.pop("CC", None)
     env.pop("CXX", None)
     for src in SOURCES:
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(HERE, src), "-o", obj]
+        tag = "_".join(d.replace("=", "") for d in defines)
+        obj = os.path.join(BUILD, src.replace(".cu", f"{tag}.o"))
+        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(HERE, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         subprocess.run(cmd, check=True, env=env)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
                     "-cudart", "static"], check=True, env=env)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

@@ -80,6 +80,10 @@ int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_fla
     q.shift64 = (uint8_t)s;
     q.add64 = (uint8_t)a;
     q.exact_limit = ((1ULL << 53) - 1) / (uint64_t)b;
+    // digit count of 2^32-1; padding with zero digits needs sigma(0) == 0 (Faure tables have it)
+    uint32_t nd = 0;
+    for (uint64_t v = 0xffffffffULL; v; v /= (uint64_t)b) nd++;
+    q.digits32 = (b != 2 && perm_flat[perm_offset[k]] == 0) ? nd : 0;
   }
   return LW_OK;
 }

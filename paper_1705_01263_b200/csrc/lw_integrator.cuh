@@ -194,7 +194,9 @@ __device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& l
   v3 f = mk3(0.0, 0.0, 0.0);
   pdf = 0.0;
   if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return f;
-  for (int l = 0; l < m.nlayers; l++) {
+#pragma unroll
+  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+    if (l >= m.nlayers) break;
     const lw_layer& L = m.layers[l];
     double a = lw.a[l];
     if (!(a > 0.0)) continue;
@@ -237,16 +239,19 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
   if (!(lw.sum_a > 0.0) || wo.z <= 0.0) return false;
   double x = u * lw.sum_a;
   int pick = -1;
-  double cum = 0.0, prev = 0.0;
-  for (int l = 0; l < m.nlayers; l++) {
-    if (!(lw.a[l] > 0.0)) continue;
+  double cum = 0.0, prev = 0.0, a_pick = 0.0;
+  bool done = false;
+#pragma unroll
+  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+    if (done || l >= m.nlayers || !(lw.a[l] > 0.0)) continue;
     prev = cum;
     cum = cum + lw.a[l];
     pick = l;
-    if (x < cum) break;
+    a_pick = lw.a[l];
+    if (x < cum) done = true;
   }
   if (pick < 0) return false;
-  double ur = (x - prev) / lw.a[pick];
+  double ur = (x - prev) / a_pick;
   if (ur < 0.0) ur = 0.0;
   if (ur >= 1.0) ur = 0.9999999999999999;
   const lw_layer& L = m.layers[pick];
@@ -377,7 +382,7 @@ __device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, 
   if (dot3(ns, wo) <= 0.0) ns = ngf;
   LwFrame fr = lw_make_frame(ns);
   v3 wol = lw_to_local(fr, wo);
-  const lw_material m = S.materials[S.material[h.tri]];
+  const lw_material& m = S.materials[S.material[h.tri]];  // read in place (no local-memory copy)
   LayerW lw;
   lw_layer_weights(m, wol.z, lw);
   const int bd = 4 + 8 * b;

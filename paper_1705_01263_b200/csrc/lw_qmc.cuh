@@ -18,6 +18,8 @@ struct QmcDim {
   uint8_t shift32, add32, shift64, add64;
   uint64_t magic64;
   uint64_t exact_limit;  // largest index with base*index < 2^53
+  uint32_t digits32;     // digits of 2^32-1 in this base if perm[0] == 0, else 0 (no padding)
+  uint32_t pad_;
 };
 
 __device__ __forceinline__ uint32_t lw_div32(uint32_t n, const QmcDim& d) {
@@ -69,6 +71,20 @@ __device__ __forceinline__ double lw_halton(const QmcDim* __restrict__ dims, con
       n = q;
     }
     uint32_t m = (uint32_t)n;
+    if (d.digits32 && scale == 1) {
+      // fixed digit count: sigma(0) == 0, so zero digits above the top one scale rev and scale
+      // alike and the exact ratio (hence its correctly rounded quotient) is unchanged; with no
+      // data-dependent exit the table loads of all digits are independent and overlap
+#pragma unroll 4
+      for (uint32_t k = 0; k < d.digits32; k++) {
+        uint32_t q = lw_div32(m, d);
+        uint32_t digit = m - q * b;
+        rev = rev * b + __ldg(p + digit);
+        scale *= b;
+        m = q;
+      }
+      return (double)rev / (double)scale;
+    }
     while (m) {
       uint32_t q = lw_div32(m, d);
       uint32_t digit = m - q * b;

@@ -23,12 +23,21 @@
 
 using namespace lw;
 
+// occupancy knobs (min resident blocks of 128 threads per SM) for the FP64-heavy stage kernels
+#ifndef LW_TRACE_MINB
+#define LW_TRACE_MINB 8
+#endif
+#ifndef LW_SHADE_MINB
+#define LW_SHADE_MINB 1
+#endif
+
 namespace {
 
 struct Counters {
   unsigned long long work_next;  // next work item (iteration-major over the pixel range)
-  int n_ext, n_ext_next, n_shadow, n_free;
-  int regen_now, nfree_snap;  // decision of the current wave's regeneration step
+  int n_ext, n_shadow, n_alive;
+  int regen_now;  // decision of the current wave's regeneration step
+  unsigned long long n_alive_ull;
   unsigned long long rays_ext, rays_shadow, paths, nonfinite, regens, waves;
   unsigned long long ext_nodes, ext_tris, sh_nodes, sh_tris;
 };
@@ -40,11 +49,12 @@ struct Pool {
   double* pdf_prev;
   long long* index;
   int* pix;
-  int* flags;  // bounce | spec_prev << 8 | live << 9 | pending flush << 10
+  int* flags;  // bounce | spec_prev << 8
+  unsigned char* stage;  // LW_STAGE_GENERATE / TRACE / TERMINATED
   double *ht, *hbu, *hbv;
   int* htri;
   double *sox, *soy, *soz, *sdx, *sdy, *sdz, *stmax, *scx, *scy, *scz;
-  int *q_ext, *q_ext_next, *q_shadow, *q_free;
+  int *q_ext, *q_shadow;
   void* block = nullptr;
 };
 
@@ -257,10 +267,16 @@ __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, uns
 }
 
 // ---- wavefront stages -----------------------------------------------------------------------
+//
+// Every slot carries a stage tag (the reference's STAGE_* contract, _kernels.py:42-48):
+// GENERATE = free, TRACE = extension ray ready, TERMINATED = finished path awaiting its
+// framebuffer flush.  Each wave: k_wave_begin (decision) -> k_generate (pool order: flush,
+// regenerate, ascending extension queue) -> k_trace_ext -> k_shade (material + NEE) ->
+// k_trace_shadow.  Queues are rebuilt from the pool every wave in ascending slot order
+// (SPEC.md:375), so SoA loads stay coalesced however the population fragments.
 
 #define F_BOUNCE 0xff
 #define F_SPEC (1 << 8)
-#define F_PENDING (1 << 10)
 
 __device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) {
   ps.o = mk3(P.ox[s], P.oy[s], P.oz[s]);
@@ -274,7 +290,7 @@ __device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) 
   ps.spec_prev = (f & F_SPEC) ? 1 : 0;
 }
 
-__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps, int extra_flags) {
+__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps) {
   P.ox[s] = ps.o.x;
   P.oy[s] = ps.o.y;
   P.oz[s] = ps.o.z;
@@ -289,64 +305,84 @@ __device__ __forceinline__ void store_state(const Pool& P, int s, const PathStat
   P.lz[s] = ps.L.z;
   P.pdf_prev[s] = ps.pdf_prev;
   P.index[s] = ps.index;
-  P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0) | extra_flags;
+  P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0);
 }
 
-// paper §3.1.3: regenerate only once more than regen_fraction of the pool has terminated
-// (or nothing is in flight).  One thread decides and takes the free queue, so every block of
-// k_regenerate sees the same snapshot and the material stage can refill the queue from 0.
-__global__ void k_regen_decide(Counters* cnt, int pool, double regen_fraction, int force) {
-  int nfree = cnt->n_free;
-  bool regen = force || nfree > (int)(regen_fraction * (double)pool) || cnt->n_ext == 0;
+// paper §3.1.3: regenerate only once more than regen_fraction of the pool is free (or nothing
+// is in flight); one thread decides so every block of k_generate sees the same choice
+__global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int force) {
+  int alive = cnt->n_alive;
+  bool regen = force || (pool - alive) > (int)(regen_fraction * (double)pool) || alive == 0;
   cnt->regen_now = regen ? 1 : 0;
-  cnt->nfree_snap = regen ? nfree : 0;
-  if (regen) {
-    cnt->n_free = 0;
-    cnt->regens += 1;
-  }
+  if (regen) cnt->regens += 1;
+  cnt->n_ext = 0;
+  cnt->n_shadow = 0;
+  cnt->n_alive = 0;
 }
 
-// flush finished paths from the free queue, then refill their slots with new samples
-__global__ void __launch_bounds__(256) k_regenerate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
-                                                    Counters* __restrict__ cnt) {
-  if (!cnt->regen_now) return;
-  int nfree = cnt->nfree_snap;
-  long long total = w.nits * w.npix;
+// pool order: flush TERMINATED slots, refill free slots with new (iteration, pixel) samples
+// (one work-claim atomic per warp), and compact TRACE slots into the extension queue as
+// ascending runs (warp ballots + block prefix, one queue atomic per 256 slots)
+__global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
+                                                  Counters* __restrict__ cnt) {
+  __shared__ int warp_off[8];
+  __shared__ int block_base;
+  const bool regen = cnt->regen_now != 0;
+  const long long total = w.nits * w.npix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   unsigned long long bad = 0, paths = 0;
-  for (int base = blockIdx.x * blockDim.x; base < nfree; base += gridDim.x * blockDim.x) {
-    int k = base + threadIdx.x;
-    bool valid = k < nfree;
-    int s = valid ? P.q_free[k] : 0;
-    if (valid && (P.flags[s] & F_PENDING)) {
+  for (int base = blockIdx.x * 256; base < P.size; base += gridDim.x * 256) {
+    int s = base + threadIdx.x;
+    bool valid = s < P.size;
+    int stage = valid ? P.stage[s] : LW_STAGE_GENERATE;
+    if (regen && valid && stage == LW_STAGE_TERMINATED) {
       bad += lw_accumulate(fb, P.pix[s], mk3(P.lx[s], P.ly[s], P.lz[s]));
       paths++;
-      P.flags[s] = 0;
+      stage = LW_STAGE_GENERATE;
+      P.stage[s] = LW_STAGE_GENERATE;
     }
-    // claim work items, one atomic per warp (lane 0 is always valid inside the loop)
-    unsigned m = __ballot_sync(0xffffffffu, valid);
-    int lane = threadIdx.x & 31;
-    unsigned long long wb = 0;
-    if (lane == 0) wb = atomicAdd(&cnt->work_next, (unsigned long long)__popc(m));
-    wb = __shfl_sync(0xffffffffu, wb, 0);
-    long long item = (long long)wb + __popc(m & ((1u << lane) - 1u));
-    bool got = valid && item < total;
-    if (got) {
-      int pix;
-      long long index = work_index(S, w, item, pix);
-      PathState ps;
-      lw_path_init(S, index, ps);
-      store_state(P, s, ps, 0);
-      P.pix[s] = pix;
+    bool want = regen && valid && stage == LW_STAGE_GENERATE;
+    unsigned m = __ballot_sync(0xffffffffu, want);
+    if (m) {
+      unsigned long long wb = 0;
+      if (lane == 0) wb = atomicAdd(&cnt->work_next, (unsigned long long)__popc(m));
+      wb = __shfl_sync(0xffffffffu, wb, 0);
+      long long item = (long long)wb + __popc(m & lt);
+      if (want && item < total) {
+        int pix;
+        long long index = work_index(S, w, item, pix);
+        PathState ps;
+        lw_path_init(S, index, ps);
+        store_state(P, s, ps);
+        P.pix[s] = pix;
+        stage = LW_STAGE_TRACE;
+        P.stage[s] = LW_STAGE_TRACE;
+      }
     }
-    int q = warp_push(&cnt->n_ext, got);
-    if (q >= 0) P.q_ext[q] = s;
+    bool ext = valid && stage == LW_STAGE_TRACE;
+    unsigned me = __ballot_sync(0xffffffffu, ext);
+    if (lane == 0) warp_off[warp] = __popc(me);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int k = 0; k < 8; k++) {
+        int c = warp_off[k];
+        warp_off[k] = t;
+        t += c;
+      }
+      block_base = t ? atomicAdd(&cnt->n_ext, t) : 0;
+    }
+    __syncthreads();
+    if (ext) P.q_ext[block_base + warp_off[warp] + __popc(me & lt)] = s;
+    __syncthreads();
   }
   warp_add(&cnt->nonfinite, bad);
   warp_add(&cnt->paths, paths);
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(128) k_trace_ext(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+__global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   int n = cnt->n_ext;
@@ -374,13 +410,14 @@ __global__ void __launch_bounds__(128) k_trace_ext(DevScene S, Pool P, Counters*
   }
 }
 
-__global__ void __launch_bounds__(128) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt) {
+__global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt) {
   int n = cnt->n_ext;
+  unsigned long long alive_count = 0;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
     bool valid = k < n;
     int s = 0;
-    bool alive = false, shadow = false;
+    bool shadow = false;
     if (valid) {
       s = P.q_ext[k];
       PathState ps;
@@ -391,9 +428,11 @@ __global__ void __launch_bounds__(128) k_shade(DevScene S, Pool P, Counters* __r
       h.bv = P.hbv[s];
       h.tri = P.htri[s];
       ShadowRay sh;
-      alive = lw_path_shade(S, ps, h, sh);
+      bool alive = lw_path_shade(S, ps, h, sh);
       shadow = sh.valid != 0;
-      store_state(P, s, ps, alive ? 0 : F_PENDING);
+      store_state(P, s, ps);
+      P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
+      alive_count += alive ? 1 : 0;
       if (shadow) {
         P.sox[s] = sh.o.x;
         P.soy[s] = sh.o.y;
@@ -409,15 +448,12 @@ __global__ void __launch_bounds__(128) k_shade(DevScene S, Pool P, Counters* __r
     }
     int q = warp_push(&cnt->n_shadow, valid && shadow);
     if (q >= 0) P.q_shadow[q] = s;
-    q = warp_push(&cnt->n_ext_next, valid && alive);
-    if (q >= 0) P.q_ext_next[q] = s;
-    q = warp_push(&cnt->n_free, valid && !alive);
-    if (q >= 0) P.q_free[q] = s;
   }
+  warp_add(&cnt->n_alive_ull, alive_count);
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(128) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+__global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   int n = cnt->n_shadow;
@@ -441,30 +477,27 @@ __global__ void __launch_bounds__(128) k_trace_shadow(DevScene S, Pool P, Counte
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->rays_shadow += (unsigned long long)n;
 }
 
-// end of wave: next-extension queue becomes current; shadow queue consumed
-__global__ void k_swap_queues(Counters* cnt) {
-  cnt->n_ext = cnt->n_ext_next;
-  cnt->n_ext_next = 0;
-  cnt->n_shadow = 0;
+// n_alive is accumulated as 64-bit by k_shade; fold it into the 32-bit field the decision reads
+__global__ void k_wave_end(Counters* cnt) {
+  cnt->n_alive = (int)cnt->n_alive_ull;
+  cnt->n_alive_ull = 0;
 }
 
-// megakernel tail over the slots still in flight (state is "ready to trace")
+// megakernel tail: run every in-flight path to completion, in pool order
 __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned long long* __restrict__ fb,
                                                    Counters* __restrict__ cnt, int nrnodes, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
-  int n = cnt->n_ext;
   unsigned long long next = 0, nsh = 0, bad = 0, paths = 0;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    int k = base + threadIdx.x;
-    if (k < n) {
-      int s = P.q_ext[k];
+  for (int base = blockIdx.x * blockDim.x; base < P.size; base += gridDim.x * blockDim.x) {
+    int s = base + threadIdx.x;
+    if (s < P.size && P.stage[s] == LW_STAGE_TRACE) {
       PathState ps;
       load_state(P, s, ps);
       run_to_completion(S, bvh, ps, next, nsh);
       bad += lw_accumulate(fb, P.pix[s], ps.L);
       paths++;
-      P.flags[s] = 0;
+      P.stage[s] = LW_STAGE_GENERATE;
     }
   }
   warp_add(&cnt->rays_ext, next);
@@ -473,7 +506,7 @@ __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned 
   warp_add(&cnt->paths, paths);
 }
 
-__global__ void k_tail_done(Counters* cnt) { cnt->n_ext = 0; }
+__global__ void k_tail_done(Counters* cnt) { cnt->n_alive = 0; }
 
 // ---- debug / parity kernels -------------------------------------------------------------
 
@@ -522,8 +555,8 @@ int alloc_pool(lw_ctx* c, int size) {
   if (c->pool.size == size) return LW_OK;
   free_pool(c);
   Pool& P = c->pool;
-  size_t nd = 33, ni = 3 + 4;  // doubles and ints per slot (+ index as long long)
-  size_t bytes = (size_t)size * (nd * 8 + 8 + ni * 4) + 4096;
+  size_t nd = 26, ni = 5;  // doubles and ints per slot (+ index as long long, + stage byte)
+  size_t bytes = (size_t)size * (nd * 8 + 8 + ni * 4 + 1) + 4096;
   LW_CUDA_TRY(cudaMalloc(&P.block, bytes));
   char* p = (char*)P.block;
   auto dd = [&](double*& x) {
@@ -542,9 +575,10 @@ int alloc_pool(lw_ctx* c, int size) {
   dd(P.ht); dd(P.hbu); dd(P.hbv);
   dd(P.sox); dd(P.soy); dd(P.soz); dd(P.sdx); dd(P.sdy); dd(P.sdz); dd(P.stmax); dd(P.scx); dd(P.scy); dd(P.scz);
   ii(P.pix); ii(P.flags); ii(P.htri);
-  ii(P.q_ext); ii(P.q_ext_next); ii(P.q_shadow); ii(P.q_free);
+  ii(P.q_ext); ii(P.q_shadow);
+  P.stage = (unsigned char*)p;
   P.size = size;
-  LW_CUDA_TRY(cudaMemsetAsync(P.flags, 0, sizeof(int) * size, c->stream));
+  LW_CUDA_TRY(cudaMemsetAsync(P.stage, LW_STAGE_GENERATE, size, c->stream));
   return LW_OK;
 }
 
@@ -580,20 +614,8 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       pool = (int)std::max<long long>(r, 1024);
     }
     LW_STATUS_TRY(alloc_pool(c, pool));
-    // every slot starts on the free queue
-    {
-      // initial free queue: identity
-      static thread_local std::vector<int> ident;
-      if ((int)ident.size() < pool) {
-        ident.resize(pool);
-        for (int k = 0; k < pool; k++) ident[k] = k;
-      }
-      LW_CUDA_TRY(cudaMemcpyAsync(c->pool.q_free, ident.data(), sizeof(int) * pool, cudaMemcpyHostToDevice, st));
-      LW_CUDA_TRY(cudaMemsetAsync(c->pool.flags, 0, sizeof(int) * pool, st));
-      Counters init = zero;
-      init.n_free = pool;
-      LW_CUDA_TRY(cudaMemcpyAsync(c->d_cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
-    }
+    // every slot starts free
+    LW_CUDA_TRY(cudaMemsetAsync(c->pool.stage, LW_STAGE_GENERATE, pool, st));
     const int gT = nsm * 8, gS = nsm * 8, gR = nsm * 4;
     long long waves = 0;
     const int check_every = 8;
@@ -610,8 +632,8 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     marks.clear();  // (event index of the start, 0 = ext / 1 = shadow)
     for (;;) {
       for (int k = 0; k < check_every; k++) {
-        k_regen_decide<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0);
-        k_regenerate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
+        k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0);
+        k_generate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
         if (timed) {
           marks.push_back({ev, 0});
           cudaEventRecord(event(), st);
@@ -631,9 +653,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
         else
           k_trace_shadow<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         if (timed) cudaEventRecord(event(), st);
-        k_swap_queues<<<1, 1, 0, st>>>(c->d_cnt);
-        // the next-extension array becomes the current one (kernels take the Pool by value)
-        std::swap(c->pool.q_ext, c->pool.q_ext_next);
+        k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 6;
         waves++;
       }
@@ -642,10 +662,9 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       LW_CUDA_TRY(cudaStreamSynchronize(st));
       const Counters& h = *c->h_cnt;
       bool work_left = h.work_next < (unsigned long long)total;
-      if (!work_left && h.n_ext == 0) break;
-      if (!work_left && p.megakernel_tail > 0 && h.n_ext < p.megakernel_tail) {
-        k_mega_tail<<<std::max(1, std::min(nsm * 8, (h.n_ext + 127) / 128)), 128, smem, st>>>(c->S, c->pool, c->d_fb,
-                                                                                               c->d_cnt, nr, use_smem);
+      if (!work_left && h.n_alive == 0) break;
+      if (!work_left && p.megakernel_tail > 0 && h.n_alive < p.megakernel_tail) {
+        k_mega_tail<<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem);
         k_tail_done<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 2;
         break;
@@ -656,8 +675,8 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       }
     }
     // flush the remaining finished paths
-    k_regen_decide<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1);
-    k_regenerate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
+    k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1);
+    k_generate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
     launches += 2;
   }
   LW_CUDA_TRY(cudaGetLastError());

@@ -64,14 +64,14 @@ struct LwHit {
   long long tri;
 };
 
-__device__ __forceinline__ double lw_pick(const double* v, int k) { return k == 0 ? v[0] : (k == 1 ? v[1] : v[2]); }
-
-// shear-space edge functions of one triangle; returns false if rejected, else t and (v, w)/det
+// shear-space edge functions of one triangle; returns false if rejected, else t and (v, w)/det.
+// `v` points at the 9 vertex doubles in memory (global or shared): the per-ray axis permutation
+// is applied through the load addresses, not with register selects.
 __device__ __forceinline__ bool lw_tri_eval(const double* __restrict__ v, const LwShear& s, double& t, double& bu,
                                             double& bv) {
-  double ax = lw_pick(v, s.kx) - s.op[0], ay = lw_pick(v, s.ky) - s.op[1], az = lw_pick(v, s.kz) - s.op[2];
-  double bx = lw_pick(v + 3, s.kx) - s.op[0], by = lw_pick(v + 3, s.ky) - s.op[1], bz = lw_pick(v + 3, s.kz) - s.op[2];
-  double cx = lw_pick(v + 6, s.kx) - s.op[0], cy = lw_pick(v + 6, s.ky) - s.op[1], cz = lw_pick(v + 6, s.kz) - s.op[2];
+  double ax = v[s.kx] - s.op[0], ay = v[s.ky] - s.op[1], az = v[s.kz] - s.op[2];
+  double bx = v[3 + s.kx] - s.op[0], by = v[3 + s.ky] - s.op[1], bz = v[3 + s.kz] - s.op[2];
+  double cx = v[6 + s.kx] - s.op[0], cy = v[6 + s.ky] - s.op[1], cz = v[6 + s.kz] - s.op[2];
   double sax = ax - s.sx * az, say = ay - s.sy * az;
   double sbx = bx - s.sx * bz, sby = by - s.sy * bz;
   double scx = cx - s.sx * cz, scy = cy - s.sy * cz;
@@ -175,10 +175,7 @@ __device__ __forceinline__ void lw_traverse_ref(bool compat, const double* __res
       long long start = -(c0 + 1);
       for (long long i = 0; i < c1; i++) {
         long long tri = __ldg(order + start + i);
-        double v[9];
-#pragma unroll
-        for (int k = 0; k < 9; k++) v[k] = __ldg(verts + 9 * tri + k);
-        lw_tri_test(v, tri, s, 0.0, h);
+        lw_tri_test(verts + 9 * tri, tri, s, 0.0, h);
       }
     } else if (sp < 126) {
       stack[sp++] = (int)c0;
@@ -335,11 +332,15 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
       int v = -ref - 1;
       int start = v >> 3, count = v & 7;
       for (int k = start; k < start + count; k++) {
-        double tv[9];
-        long long id;
-        lw_load_tri(bvh.tris + k, tv, id);
         if (COUNT) cnt->tris++;
-        lw_tri_test(tv, id, r.sh, 0.0, h);
+        double t, bu, bv;
+        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv) || t <= 0.0 || t > h.t) continue;
+        long long id = bvh.tris[k].id;
+        if (t == h.t && h.tri >= 0 && id >= h.tri) continue;
+        h.t = t;
+        h.tri = id;
+        h.bu = bu;
+        h.bv = bv;
       }
     }
     ref = LW_REF_NONE;
@@ -390,11 +391,8 @@ __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double 
       int v = -ref - 1;
       int start = v >> 3, count = v & 7;
       for (int k = start; k < start + count; k++) {
-        double tv[9];
-        long long id;
-        lw_load_tri(bvh.tris + k, tv, id);
         if (COUNT) cnt->tris++;
-        if (lw_tri_occludes(tv, r.sh, tmax)) return true;
+        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) return true;
       }
     }
     if (sp == 0) return false;
