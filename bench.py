@@ -28,8 +28,17 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "paths/sec (samples/sec) on C2 Cornell 1024x1024 depth 8"
 UNIT = "paths/s"
+
+
+def metric_name(a):
+    return f"paths/sec (samples/sec) on {a.config} {a.width}x{a.height} depth {a.depth}"
+
+
+def build_scene(a):
+    from paper_1705_01263_b200 import scenes
+
+    return scenes.CONFIGS[a.config].builder()
 
 
 def parse():
@@ -38,22 +47,33 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pass-iterations", type=int, default=16)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--pass-iterations", type=int, default=0, help="QMC iterations per GPU per step (0: ~16M paths)")
     ap.add_argument("--engine", default="wavefront", choices=["wavefront", "megakernel"])
     ap.add_argument("--pool-log2", type=int, default=20)
     ap.add_argument("--regen-fraction", type=float, default=0.5)
     ap.add_argument("--megakernel-tail", type=int, default=0)
-    ap.add_argument("--width", type=int, default=1024)
-    ap.add_argument("--height", type=int, default=1024)
-    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--width", type=int, default=0)
+    ap.add_argument("--height", type=int, default=0)
+    ap.add_argument("--depth", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    from paper_1705_01263_b200 import scenes
+
+    c = scenes.CONFIGS[a.config]
+    a.width = a.width or c.width
+    a.height = a.height or c.height
+    a.depth = a.depth or c.max_depth
+    a.pass_iterations = a.pass_iterations or max(1, (1 << 24) // (a.width * a.height))
+    return a
 
 
 def workload(a):
-    return (f"C2 Cornell box (procedural quads, one area light, diffuse) {a.width}x{a.height}, depth {a.depth}, "
+    from paper_1705_01263_b200 import scenes
+
+    return (f"{a.config}: {scenes.CONFIGS[a.config].description}; {a.width}x{a.height}, depth {a.depth}, "
             f"{a.pass_iterations} spp per GPU per step")
 
 
@@ -103,11 +123,10 @@ class ClockSampler:
 def cpu_render_sample(a, budget_s, threads=0):
     """Bounded sample of the same workload on the host cores: full-width pixel rows x 1 iteration."""
     from oracle import oracle as O
-    from paper_1705_01263_b200 import scenes
     from paper_1705_01263_b200.render import RenderParams
     from paper_1705_01263_b200.scene import pack_scene
 
-    packed = pack_scene(scenes.cornell())
+    packed = pack_scene(build_scene(a))
     osc = O.OracleScene(packed)
     params = RenderParams(a.width, a.height, a.depth)
     threads = threads or os.cpu_count()
@@ -136,9 +155,9 @@ def run_reference(a):
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
     base = vals[0]
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+    line = {"metric": metric_name(a), "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (procedural Cornell box)", "impl": "reference",
+            "data": "synthetic procedural scene (seeded)", "impl": "reference",
             "config": {"workload": workload(a), "parallelism": "host threads (OpenMP)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "port",
                              "sample": base["sample"]},
@@ -166,7 +185,6 @@ def run_ours(a):
     import torch
     import torch.distributed as dist
 
-    from paper_1705_01263_b200 import scenes
     from paper_1705_01263_b200.distributed import partition_iterations
     from paper_1705_01263_b200.render import Renderer
     from paper_1705_01263_b200.scene import pack_scene
@@ -176,7 +194,7 @@ def run_ours(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    packed = pack_scene(scenes.cornell())
+    packed = pack_scene(build_scene(a))
     W, H, P = a.width, a.height, a.width * a.height
     its = a.pass_iterations
     r = Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
@@ -288,9 +306,9 @@ def run_ours(a):
         prof_ms, prof_launches = ms_max, a.steps
     traffic = load_traffic()
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "metric": metric_name(a), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (procedural Cornell box, QMC samples)",
+        "dtype": "f64", "data": "synthetic procedural scene (seeded), QMC samples",
         "config": {"workload": workload(a), "engine": a.engine, "pool_slots": 1 << a.pool_log2,
                    "regen_fraction": a.regen_fraction, "parallelism": f"sample-space dp{world}",
                    "l2": "wavefront state pool (~300 MB) + framebuffers (50 MB) exceed the 126 MB L2; the 5 KB scene "

@@ -951,8 +951,8 @@ static v3 neg(v3 a) { return mk(-a.x, -a.y, -a.z); }
 static double dot(v3 a, v3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
 static v3 cross(v3 a, v3 b) { return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x); }
 static v3 normalize(v3 a) {
-  double l = sqrt(dot(a, a));
-  return mk(a.x / l, a.y / l, a.z / l);
+  double inv = 1.0 / sqrt(dot(a, a));
+  return mk(a.x * inv, a.y * inv, a.z * inv);
 }
 static v3 ld3(const double* p) { return mk(p[0], p[1], p[2]); }
 static v3 bary3(v3 a, v3 b, v3 c, double w, double bu, double bv) {
@@ -1065,7 +1065,7 @@ static v3 to_world(const frame* f, v3 v) {
 
 typedef struct {
   double a[LW_MAX_LAYERS]; /* layer mixture weights */
-  double sum_a;
+  double sum_a, inv_sum;
   int nonspec; /* any non-delta layer with a > 0 */
 } layerw;
 
@@ -1091,6 +1091,7 @@ static void layer_weights(const lw_material* m, double cos_o, layerw* lw) {
     lw->sum_a = lw->sum_a + a;
     if (a > 0.0 && (L->kind == LW_BSDF_DIFFUSE || L->kind == LW_BSDF_GLOSSY)) lw->nonspec = 1;
   }
+  lw->inv_sum = lw->sum_a > 0.0 ? 1.0 / lw->sum_a : 0.0;
 }
 
 static double ggx_d(double alpha, double cos_h) {
@@ -1118,7 +1119,7 @@ static v3 bsdf_eval(const lw_material* m, const layerw* lw, v3 wo, v3 wi, double
     const lw_layer* L = m->layers + l;
     double a = lw->a[l];
     if (!(a > 0.0)) continue;
-    double sel = a / lw->sum_a;
+    double sel = a * lw->inv_sum;
     if (L->kind == LW_BSDF_DIFFUSE) {
       double k = a * LW_INV_PI;
       f = add(f, mk(L->tint[0] * k, L->tint[1] * k, L->tint[2] * k));
@@ -1345,7 +1346,8 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
         v3 dl = sub(q, p);
         double dist2 = dot(dl, dl);
         double dist = sqrt(dist2);
-        wi = mk(dl.x / dist, dl.y / dist, dl.z / dist);
+        double inv_dist = 1.0 / dist;
+        wi = mk(dl.x * inv_dist, dl.y * inv_dist, dl.z * inv_dist);
         v3 ngl = normalize(cross(sub(l1, l0), sub(l2, l0)));
         double cos_l = -dot(ngl, wi);
         if (s->emit_two[le]) cos_l = fabs(cos_l);
@@ -1387,7 +1389,8 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
       if (q > 1.0) q = 1.0;
       double ur = qmc(c, bd + 4, index);
       if (!(ur < q)) break;
-      beta = mk(beta.x / q, beta.y / q, beta.z / q);
+      double inv_q = 1.0 / q;
+      beta = mk(beta.x * inv_q, beta.y * inv_q, beta.z * inv_q);
     }
     o = offset_origin(p, ngf, wi);
     d = wi;

@@ -92,8 +92,8 @@ __host__ __device__ __forceinline__ v3 cross3(v3 a, v3 b) {
   return mk3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
 }
 __host__ __device__ __forceinline__ v3 normalize3(v3 a) {
-  double l = sqrt(dot3(a, a));
-  return mk3(a.x / l, a.y / l, a.z / l);
+  double inv = 1.0 / sqrt(dot3(a, a));
+  return mk3(a.x * inv, a.y * inv, a.z * inv);
 }
 __host__ __device__ __forceinline__ v3 bary3(v3 a, v3 b, v3 c, double w, double bu, double bv) {
   return mk3((w * a.x + bu * b.x) + bv * c.x, (w * a.y + bu * b.y) + bv * c.y, (w * a.z + bu * b.z) + bv * c.z);

@@ -145,7 +145,7 @@ __device__ __forceinline__ v3 lw_to_world(const LwFrame& f, v3 v) {
 
 struct LayerW {
   double a[LW_MAX_LAYERS];
-  double sum_a;
+  double sum_a, inv_sum;
   int nonspec;
 };
 
@@ -172,6 +172,7 @@ __device__ __forceinline__ void lw_layer_weights(const lw_material& m, double co
     lw.sum_a = lw.sum_a + a;
     if (a > 0.0 && (L.kind == LW_BSDF_DIFFUSE || L.kind == LW_BSDF_GLOSSY)) lw.nonspec = 1;
   }
+  lw.inv_sum = lw.sum_a > 0.0 ? 1.0 / lw.sum_a : 0.0;
 }
 
 __device__ __forceinline__ double lw_ggx_d(double alpha, double cos_h) {
@@ -200,7 +201,7 @@ __device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& l
     const lw_layer& L = m.layers[l];
     double a = lw.a[l];
     if (!(a > 0.0)) continue;
-    double sel = a / lw.sum_a;
+    double sel = a * lw.inv_sum;
     if (L.kind == LW_BSDF_DIFFUSE) {
       double k = a * LW_INV_PI;
       f = f + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
@@ -435,7 +436,8 @@ __device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, 
       v3 dl = q - p;
       double dist2 = dot3(dl, dl);
       double dist = sqrt(dist2);
-      wi = mk3(dl.x / dist, dl.y / dist, dl.z / dist);
+      double inv_dist = 1.0 / dist;
+      wi = mk3(dl.x * inv_dist, dl.y * inv_dist, dl.z * inv_dist);
       v3 ngl = normalize3(cross3(l1 - l0, l2 - l0));
       double cos_l = -dot3(ngl, wi);
       if (S.emit_two[le]) cos_l = fabs(cos_l);
@@ -477,7 +479,8 @@ __device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, 
     if (q > 1.0) q = 1.0;
     double ur = lw_qmc_s(S, bd + 4, index);
     if (!(ur < q)) return false;
-    ps.beta = mk3(ps.beta.x / q, ps.beta.y / q, ps.beta.z / q);
+    double inv_q = 1.0 / q;
+    ps.beta = mk3(ps.beta.x * inv_q, ps.beta.y * inv_q, ps.beta.z * inv_q);
   }
   ps.o = lw_offset_origin(p, ngf, wi);
   ps.d = wi;

@@ -64,11 +64,13 @@ struct LwHit {
   long long tri;
 };
 
-// shear-space edge functions of one triangle; returns false if rejected, else t and (v, w)/det.
+// shear-space edge functions of one triangle; returns false if rejected, else t and (v, w), det.
+// The barycentrics v/det, w/det are divided only once the closest hit is final (same ops,
+// same bits as the reference, which divides on every accepted update).
 // `v` points at the 9 vertex doubles in memory (global or shared): the per-ray axis permutation
 // is applied through the load addresses, not with register selects.
 __device__ __forceinline__ bool lw_tri_eval(const double* __restrict__ v, const LwShear& s, double& t, double& bu,
-                                            double& bv) {
+                                            double& bv, double& det_out) {
   double ax = v[s.kx] - s.op[0], ay = v[s.ky] - s.op[1], az = v[s.kz] - s.op[2];
   double bx = v[3 + s.kx] - s.op[0], by = v[3 + s.ky] - s.op[1], bz = v[3 + s.kz] - s.op[2];
   double cx = v[6 + s.kx] - s.op[0], cy = v[6 + s.ky] - s.op[1], cz = v[6 + s.kz] - s.op[2];
@@ -85,28 +87,27 @@ __device__ __forceinline__ bool lw_tri_eval(const double* __restrict__ v, const 
   t = t_scaled / det;
   bu = vv;
   bv = w;
-  bu = bu / det;
-  bv = bv / det;
+  det_out = det;
   return true;
 }
 
 // _tri_hit with the closest-hit update rule (t in (tmin, best], tie -> lower id)
 __device__ __forceinline__ void lw_tri_test(const double* __restrict__ v, long long tri, const LwShear& s, double tmin,
                                             LwHit& h) {
-  double t, bu, bv;
-  if (!lw_tri_eval(v, s, t, bu, bv)) return;
+  double t, bu, bv, det;
+  if (!lw_tri_eval(v, s, t, bu, bv, det)) return;
   if (t <= tmin) return;
   if (t > h.t) return;
   if (t == h.t && h.tri >= 0 && tri >= h.tri) return;
   h.t = t;
   h.tri = tri;
-  h.bu = bu;
-  h.bv = bv;
+  h.bu = bu / det;
+  h.bv = bv / det;
 }
 
 __device__ __forceinline__ bool lw_tri_occludes(const double* __restrict__ v, const LwShear& s, double tmax) {
-  double t, bu, bv;
-  if (!lw_tri_eval(v, s, t, bu, bv)) return false;
+  double t, bu, bv, det;
+  if (!lw_tri_eval(v, s, t, bu, bv, det)) return false;
   return t > 0.0 && t < tmax;
 }
 
@@ -305,6 +306,7 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
   double stack_tn[LW_STACK];
   int sp = 0;
   int ref = bvh.root_ref;
+  double best_det = 1.0;
   for (;;) {
     while (ref >= 0 && ref != LW_REF_NONE) {
       double box[12];
@@ -333,14 +335,15 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
       int start = v >> 3, count = v & 7;
       for (int k = start; k < start + count; k++) {
         if (COUNT) cnt->tris++;
-        double t, bu, bv;
-        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv) || t <= 0.0 || t > h.t) continue;
+        double t, bu, bv, det;
+        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv, det) || t <= 0.0 || t > h.t) continue;
         long long id = bvh.tris[k].id;
         if (t == h.t && h.tri >= 0 && id >= h.tri) continue;
         h.t = t;
         h.tri = id;
-        h.bu = bu;
+        h.bu = bu;  // undivided v, w; divided by det once traversal ends
         h.bv = bv;
+        best_det = det;
       }
     }
     ref = LW_REF_NONE;
@@ -351,7 +354,11 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
         break;
       }
     }
-    if (ref == LW_REF_NONE) return;
+    if (ref == LW_REF_NONE) break;
+  }
+  if (h.tri >= 0) {
+    h.bu = h.bu / best_det;
+    h.bv = h.bv / best_det;
   }
 }
 
