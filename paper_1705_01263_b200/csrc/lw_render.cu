@@ -42,18 +42,18 @@ struct Counters {
   unsigned long long ext_nodes, ext_tris, sh_nodes, sh_tris;
 };
 
+// SoA of 16-byte vectors: slot s of every array is one LDG.128/STG.128, and a warp's 32
+// consecutive slots cover 512 contiguous bytes per array
 struct Pool {
   int size = 0;
-  double *ox, *oy, *oz, *dx, *dy, *dz;
-  double *bx, *by, *bz, *lx, *ly, *lz;
-  double* pdf_prev;
-  long long* index;
+  double2 *ray0, *ray1, *ray2;  // (o.x, o.y) (o.z, d.x) (d.y, d.z)
+  double2 *tp0, *tp1, *tp2;     // (beta.x, beta.y) (beta.z, L.x) (L.y, L.z)
+  double2* misc;                // (pdf_prev, sample index bits)
+  double2 *hit0, *hit1;         // (t, bu) (bv, tri bits)
+  double2 *sh0, *sh1, *sh2, *sh3, *sh4;  // shadow (o.x,o.y) (o.z,d.x) (d.y,d.z) (tmax,c.x) (c.y,c.z)
   int* pix;
   int* flags;  // bounce | spec_prev << 8
   unsigned char* stage;  // LW_STAGE_GENERATE / TRACE / TERMINATED
-  double *ht, *hbu, *hbv;
-  int* htri;
-  double *sox, *soy, *soz, *sdx, *sdy, *sdz, *stmax, *scx, *scy, *scz;
   int *q_ext, *q_shadow;
   void* block = nullptr;
 };
@@ -278,34 +278,45 @@ __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, uns
 #define F_BOUNCE 0xff
 #define F_SPEC (1 << 8)
 
+__device__ __forceinline__ void load_ray(const Pool& P, int s, double o[3], double d[3]) {
+  double2 a = P.ray0[s], b = P.ray1[s], c = P.ray2[s];
+  o[0] = a.x;
+  o[1] = a.y;
+  o[2] = b.x;
+  d[0] = b.y;
+  d[1] = c.x;
+  d[2] = c.y;
+}
+
 __device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) {
-  ps.o = mk3(P.ox[s], P.oy[s], P.oz[s]);
-  ps.d = mk3(P.dx[s], P.dy[s], P.dz[s]);
-  ps.beta = mk3(P.bx[s], P.by[s], P.bz[s]);
-  ps.L = mk3(P.lx[s], P.ly[s], P.lz[s]);
-  ps.pdf_prev = P.pdf_prev[s];
-  ps.index = P.index[s];
+  double2 a = P.ray0[s], b = P.ray1[s], c = P.ray2[s];
+  ps.o = mk3(a.x, a.y, b.x);
+  ps.d = mk3(b.y, c.x, c.y);
+  double2 t0 = P.tp0[s], t1 = P.tp1[s], t2 = P.tp2[s];
+  ps.beta = mk3(t0.x, t0.y, t1.x);
+  ps.L = mk3(t1.y, t2.x, t2.y);
+  double2 m = P.misc[s];
+  ps.pdf_prev = m.x;
+  ps.index = __double_as_longlong(m.y);
   int f = P.flags[s];
   ps.bounce = f & F_BOUNCE;
   ps.spec_prev = (f & F_SPEC) ? 1 : 0;
 }
 
 __device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps) {
-  P.ox[s] = ps.o.x;
-  P.oy[s] = ps.o.y;
-  P.oz[s] = ps.o.z;
-  P.dx[s] = ps.d.x;
-  P.dy[s] = ps.d.y;
-  P.dz[s] = ps.d.z;
-  P.bx[s] = ps.beta.x;
-  P.by[s] = ps.beta.y;
-  P.bz[s] = ps.beta.z;
-  P.lx[s] = ps.L.x;
-  P.ly[s] = ps.L.y;
-  P.lz[s] = ps.L.z;
-  P.pdf_prev[s] = ps.pdf_prev;
-  P.index[s] = ps.index;
+  P.ray0[s] = make_double2(ps.o.x, ps.o.y);
+  P.ray1[s] = make_double2(ps.o.z, ps.d.x);
+  P.ray2[s] = make_double2(ps.d.y, ps.d.z);
+  P.tp0[s] = make_double2(ps.beta.x, ps.beta.y);
+  P.tp1[s] = make_double2(ps.beta.z, ps.L.x);
+  P.tp2[s] = make_double2(ps.L.y, ps.L.z);
+  P.misc[s] = make_double2(ps.pdf_prev, __longlong_as_double(ps.index));
   P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0);
+}
+
+__device__ __forceinline__ v3 load_L(const Pool& P, int s) {
+  double2 t1 = P.tp1[s], t2 = P.tp2[s];
+  return mk3(t1.y, t2.x, t2.y);
 }
 
 // paper §3.1.3: regenerate only once more than regen_fraction of the pool is free (or nothing
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
     bool valid = s < P.size;
     int stage = valid ? P.stage[s] : LW_STAGE_GENERATE;
     if (regen && valid && stage == LW_STAGE_TERMINATED) {
-      bad += lw_accumulate(fb, P.pix[s], mk3(P.lx[s], P.ly[s], P.lz[s]));
+      bad += lw_accumulate(fb, P.pix[s], load_L(P, s));
       paths++;
       stage = LW_STAGE_GENERATE;
       P.stage[s] = LW_STAGE_GENERATE;
@@ -398,13 +409,12 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
     int k = base + threadIdx.x;
     if (k < n) {
       int s = P.q_ext[k];
-      double o[3] = {P.ox[s], P.oy[s], P.oz[s]}, d[3] = {P.dx[s], P.dy[s], P.dz[s]};
+      double o[3], d[3];
+      load_ray(P, s, o, d);
       LwHit h;
       lw_trace_closest<COUNT>(bvh, o, d, INFINITY, h, &tc);
-      P.ht[s] = h.t;
-      P.hbu[s] = h.bu;
-      P.hbv[s] = h.bv;
-      P.htri[s] = (int)h.tri;
+      P.hit0[s] = make_double2(h.t, h.bu);
+      P.hit1[s] = make_double2(h.bv, __longlong_as_double(h.tri));
     }
   }
   if (COUNT) {
@@ -430,10 +440,11 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
       PathState ps;
       load_state(P, s, ps);
       LwHit h;
-      h.t = P.ht[s];
-      h.bu = P.hbu[s];
-      h.bv = P.hbv[s];
-      h.tri = P.htri[s];
+      double2 h0 = P.hit0[s], h1 = P.hit1[s];
+      h.t = h0.x;
+      h.bu = h0.y;
+      h.bv = h1.x;
+      h.tri = __double_as_longlong(h1.y);
       ShadowRay sh;
       bool alive = lw_path_shade(S, ps, h, sh);
       shadow = sh.valid != 0;
@@ -441,16 +452,11 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
       P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
       alive_count += alive ? 1 : 0;
       if (shadow) {
-        P.sox[s] = sh.o.x;
-        P.soy[s] = sh.o.y;
-        P.soz[s] = sh.o.z;
-        P.sdx[s] = sh.d.x;
-        P.sdy[s] = sh.d.y;
-        P.sdz[s] = sh.d.z;
-        P.stmax[s] = sh.tmax;
-        P.scx[s] = sh.contrib.x;
-        P.scy[s] = sh.contrib.y;
-        P.scz[s] = sh.contrib.z;
+        P.sh0[s] = make_double2(sh.o.x, sh.o.y);
+        P.sh1[s] = make_double2(sh.o.z, sh.d.x);
+        P.sh2[s] = make_double2(sh.d.y, sh.d.z);
+        P.sh3[s] = make_double2(sh.tmax, sh.contrib.x);
+        P.sh4[s] = make_double2(sh.contrib.y, sh.contrib.z);
       }
     }
     int q = warp_push(&cnt->n_shadow, valid && shadow);
@@ -469,11 +475,15 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_shadow(DevScene S,
     int k = base + threadIdx.x;
     if (k < n) {
       int s = P.q_shadow[k];
-      double o[3] = {P.sox[s], P.soy[s], P.soz[s]}, d[3] = {P.sdx[s], P.sdy[s], P.sdz[s]};
-      if (!lw_trace_any<COUNT>(bvh, o, d, P.stmax[s], &tc)) {
-        P.lx[s] = P.lx[s] + P.scx[s];
-        P.ly[s] = P.ly[s] + P.scy[s];
-        P.lz[s] = P.lz[s] + P.scz[s];
+      double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
+      double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
+      if (!lw_trace_any<COUNT>(bvh, o, d, e.x, &tc)) {
+        double2 f = P.sh4[s], t1 = P.tp1[s], t2 = P.tp2[s];
+        t1.y = t1.y + e.y;
+        t2.x = t2.x + f.x;
+        t2.y = t2.y + f.y;
+        P.tp1[s] = t1;
+        P.tp2[s] = t2;
       }
     }
   }
@@ -562,26 +572,24 @@ int alloc_pool(lw_ctx* c, int size) {
   if (c->pool.size == size) return LW_OK;
   free_pool(c);
   Pool& P = c->pool;
-  size_t nd = 26, ni = 5;  // doubles and ints per slot (+ index as long long, + stage byte)
-  size_t bytes = (size_t)size * (nd * 8 + 8 + ni * 4 + 1) + 4096;
+  const size_t nvec = 14;  // double2 arrays
+  size_t bytes = (size_t)size * (nvec * 16 + 4 * 4 + 1) + 8192;
   LW_CUDA_TRY(cudaMalloc(&P.block, bytes));
   char* p = (char*)P.block;
-  auto dd = [&](double*& x) {
-    x = (double*)p;
-    p += sizeof(double) * size;
+  auto v2 = [&](double2*& x) {
+    x = (double2*)p;
+    p += sizeof(double2) * size;
   };
   auto ii = [&](int*& x) {
     x = (int*)p;
     p += sizeof(int) * size;
   };
-  dd(P.ox); dd(P.oy); dd(P.oz); dd(P.dx); dd(P.dy); dd(P.dz);
-  dd(P.bx); dd(P.by); dd(P.bz); dd(P.lx); dd(P.ly); dd(P.lz);
-  dd(P.pdf_prev);
-  P.index = (long long*)p;
-  p += sizeof(long long) * size;
-  dd(P.ht); dd(P.hbu); dd(P.hbv);
-  dd(P.sox); dd(P.soy); dd(P.soz); dd(P.sdx); dd(P.sdy); dd(P.sdz); dd(P.stmax); dd(P.scx); dd(P.scy); dd(P.scz);
-  ii(P.pix); ii(P.flags); ii(P.htri);
+  v2(P.ray0); v2(P.ray1); v2(P.ray2);
+  v2(P.tp0); v2(P.tp1); v2(P.tp2);
+  v2(P.misc);
+  v2(P.hit0); v2(P.hit1);
+  v2(P.sh0); v2(P.sh1); v2(P.sh2); v2(P.sh3); v2(P.sh4);
+  ii(P.pix); ii(P.flags);
   ii(P.q_ext); ii(P.q_shadow);
   P.stage = (unsigned char*)p;
   P.size = size;
