@@ -109,7 +109,12 @@ typedef struct lw_scene_desc {
   double cam_right[3];
   double cam_up[3];
   double tan_half_fov; /* tan(fov_y / 2), computed by the host */
+  int32_t bvh_kind;    /* render BVH: LW_BVH_SAH (default) or LW_BVH_MEDIAN (the reference's tree) */
+  int32_t reserved;
 } lw_scene_desc;
+
+#define LW_BVH_SAH 0    /* binned SAH, breadth-first */
+#define LW_BVH_MEDIAN 1 /* geometry.py:100-148 median split (built on the GPU) */
 
 typedef struct lw_render_params {
   int32_t width;

@@ -669,6 +669,187 @@ static void build_render_bvh(lwo_scene* s) {
   free(map);
 }
 
+/* Binned-SAH render tree, restating the specification of DESIGN.md §3.2 (the device builds
+ * it in csrc/lw_sah.cu): FIFO segment order, 16 centroid bins per axis, first strict minimum of
+ * A(L)nL + A(R)nR, split when n > 7 or A(B) + cost < n A(B), halve coincident centroids. */
+#define SAH_BINS 16
+#define SAH_MAXLEAF 7
+
+typedef struct {
+  int64_t start, n, parent;
+  int side;
+} sah_seg;
+
+static double sah_area(const double* lo, const double* hi) {
+  double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+  return 2.0 * ((dx * dy + dy * dz) + dz * dx);
+}
+
+static void bb_reset(double* lo, double* hi) {
+  for (int a = 0; a < 3; a++) {
+    lo[a] = INFINITY;
+    hi[a] = -INFINITY;
+  }
+}
+
+static void bb_add(double* lo, double* hi, const double* l2, const double* h2) {
+  for (int a = 0; a < 3; a++) {
+    if (l2[a] < lo[a]) lo[a] = l2[a];
+    if (h2[a] > hi[a]) hi[a] = h2[a];
+  }
+}
+
+static int sah_bin(double c, double cmin, double scale) {
+  int b = (int)((c - cmin) * scale);
+  return b > SAH_BINS - 1 ? SAH_BINS - 1 : b;
+}
+
+static void build_render_bvh_sah(lwo_scene* s) {
+  int64_t n = s->ntris;
+  s->ltri = (int64_t*)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+  s->lverts = (double*)malloc(sizeof(double) * 9 * (n > 0 ? n : 1));
+  s->rnodes = (rnode*)calloc(n > 0 ? n : 1, sizeof(rnode));
+  s->nrnodes = 0;
+  s->root_ref = leaf_ref(0, 0);
+  memset(s->root_box, 0, sizeof(s->root_box));
+  if (n == 0) return;
+  double *lo = (double*)malloc(sizeof(double) * 3 * n), *hi = (double*)malloc(sizeof(double) * 3 * n);
+  double* ce = (double*)malloc(sizeof(double) * 3 * n);
+  int64_t* spill = (int64_t*)malloc(sizeof(int64_t) * n);
+  sah_seg* q = (sah_seg*)malloc(sizeof(sah_seg) * (2 * n + 2));
+  for (int64_t i = 0; i < n; i++) {
+    for (int a = 0; a < 3; a++) {
+      const double* v = s->verts + 9 * i;
+      double l = v[a], h = v[a];
+      if (v[3 + a] < l) l = v[3 + a];
+      if (v[6 + a] < l) l = v[6 + a];
+      if (v[3 + a] > h) h = v[3 + a];
+      if (v[6 + a] > h) h = v[6 + a];
+      lo[3 * i + a] = l;
+      hi[3 * i + a] = h;
+      ce[3 * i + a] = 0.5 * (l + h);
+    }
+    s->ltri[i] = i;
+  }
+  int64_t qh = 0, qt = 0;
+  q[qt++] = (sah_seg){0, n, -1, 0};
+  while (qh < qt) {
+    sah_seg g = q[qh++];
+    int64_t* ids = s->ltri + g.start;
+    double Blo[3], Bhi[3], Clo[3], Chi[3];
+    bb_reset(Blo, Bhi);
+    bb_reset(Clo, Chi);
+    for (int64_t k = 0; k < g.n; k++) {
+      bb_add(Blo, Bhi, lo + 3 * ids[k], hi + 3 * ids[k]);
+      bb_add(Clo, Chi, ce + 3 * ids[k], ce + 3 * ids[k]);
+    }
+    if (g.parent < 0) {
+      memcpy(s->root_box, Blo, sizeof(Blo));
+      memcpy(s->root_box + 3, Bhi, sizeof(Bhi));
+    }
+    int bax = -1, bpl = -1;
+    double bcost = INFINITY, blo[2][3], bhi[2][3];
+    int64_t bnl = 0;
+    for (int a = 0; a < 3 && g.n > 1; a++) {
+      double ext = Chi[a] - Clo[a];
+      if (!(ext > 0.0)) continue;
+      double scale = (double)SAH_BINS / ext;
+      int64_t cnt[SAH_BINS];
+      double clo[SAH_BINS][3], chi[SAH_BINS][3];
+      for (int b = 0; b < SAH_BINS; b++) {
+        cnt[b] = 0;
+        bb_reset(clo[b], chi[b]);
+      }
+      for (int64_t k = 0; k < g.n; k++) {
+        int b = sah_bin(ce[3 * ids[k] + a], Clo[a], scale);
+        cnt[b]++;
+        bb_add(clo[b], chi[b], lo + 3 * ids[k], hi + 3 * ids[k]);
+      }
+      /* suffix boxes for the right side of plane p (bins p+1 .. 15) */
+      double slo[SAH_BINS][3], shi[SAH_BINS][3];
+      int64_t scnt[SAH_BINS];
+      double rlo[3], rhi[3];
+      bb_reset(rlo, rhi);
+      int64_t rc = 0;
+      for (int b = SAH_BINS - 1; b >= 1; b--) {
+        bb_add(rlo, rhi, clo[b], chi[b]);
+        rc += cnt[b];
+        memcpy(slo[b], rlo, sizeof(rlo));
+        memcpy(shi[b], rhi, sizeof(rhi));
+        scnt[b] = rc;
+      }
+      double llo[3], lhi[3];
+      bb_reset(llo, lhi);
+      int64_t lc = 0;
+      for (int p = 0; p + 1 < SAH_BINS; p++) {
+        bb_add(llo, lhi, clo[p], chi[p]);
+        lc += cnt[p];
+        if (lc == 0 || scnt[p + 1] == 0) continue;
+        double cost = sah_area(llo, lhi) * (double)lc + sah_area(slo[p + 1], shi[p + 1]) * (double)scnt[p + 1];
+        if (cost < bcost) {
+          bcost = cost;
+          bax = a;
+          bpl = p;
+          bnl = lc;
+          memcpy(blo[0], llo, sizeof(llo));
+          memcpy(bhi[0], lhi, sizeof(lhi));
+          memcpy(blo[1], slo[p + 1], sizeof(llo));
+          memcpy(bhi[1], shi[p + 1], sizeof(lhi));
+        }
+      }
+    }
+    int split = 0, halve = 0;
+    if (bax >= 0) {
+      double aB = sah_area(Blo, Bhi);
+      split = g.n > SAH_MAXLEAF || (aB + bcost) < (double)g.n * aB;
+    } else if (g.n > SAH_MAXLEAF) {
+      split = halve = 1;
+    }
+    if (!split) {
+      int32_t r = leaf_ref(g.start, g.n);
+      if (g.parent < 0)
+        s->root_ref = r;
+      else
+        s->rnodes[g.parent].ref[g.side] = r;
+      continue;
+    }
+    int64_t id = s->nrnodes++;
+    if (g.parent < 0)
+      s->root_ref = (int32_t)id;
+    else
+      s->rnodes[g.parent].ref[g.side] = (int32_t)id;
+    if (halve) {
+      bnl = g.n / 2;
+      bb_reset(blo[0], bhi[0]);
+      bb_reset(blo[1], bhi[1]);
+      for (int64_t k = 0; k < g.n; k++) bb_add(blo[k < bnl ? 0 : 1], bhi[k < bnl ? 0 : 1], lo + 3 * ids[k], hi + 3 * ids[k]);
+    } else {
+      double scale = (double)SAH_BINS / (Chi[bax] - Clo[bax]);
+      int64_t nl = 0, nr = 0;
+      for (int64_t k = 0; k < g.n; k++) {
+        int64_t t = ids[k];
+        if (sah_bin(ce[3 * t + bax], Clo[bax], scale) <= bpl)
+          ids[nl++] = t;
+        else
+          spill[nr++] = t;
+      }
+      memcpy(ids + nl, spill, sizeof(int64_t) * nr);
+    }
+    for (int c = 0; c < 2; c++) {
+      memcpy(s->rnodes[id].box[c], blo[c], sizeof(double) * 3);
+      memcpy(s->rnodes[id].box[c] + 3, bhi[c], sizeof(double) * 3);
+    }
+    q[qt++] = (sah_seg){g.start, bnl, id, 0};
+    q[qt++] = (sah_seg){g.start + bnl, g.n - bnl, id, 1};
+  }
+  for (int64_t j = 0; j < n; j++) memcpy(s->lverts + 9 * j, s->verts + 9 * s->ltri[j], sizeof(double) * 9);
+  free(lo);
+  free(hi);
+  free(ce);
+  free(spill);
+  free(q);
+}
+
 static double* dup_d(const double* p, int64_t n) {
   double* q = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
   if (n > 0) memcpy(q, p, sizeof(double) * n);
@@ -690,7 +871,10 @@ lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
   s->children = (int64_t*)malloc(sizeof(int64_t) * 2 * cap);
   s->order = (int64_t*)malloc(sizeof(int64_t) * (d->ntris > 0 ? d->ntris : 1));
   s->nnodes = lwo_build_bvh(s->verts, s->ntris, s->bounds, s->children, s->order);
-  build_render_bvh(s);
+  if (d->bvh_kind == LW_BVH_MEDIAN)
+    build_render_bvh(s);
+  else
+    build_render_bvh_sah(s);
   /* emitters */
   s->nemit = d->nemit;
   s->emit_of_tri = (int64_t*)malloc(sizeof(int64_t) * (s->ntris > 0 ? s->ntris : 1));

@@ -94,7 +94,13 @@ class LwSceneDesc(C.Structure):
         ("cam_right", C.c_double * 3),
         ("cam_up", C.c_double * 3),
         ("tan_half_fov", C.c_double),
+        ("bvh_kind", C.c_int32),
+        ("reserved", C.c_int32),
     ]
+
+
+LW_BVH_SAH = 0
+LW_BVH_MEDIAN = 1
 
 
 class LwRenderParams(C.Structure):

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(BUILD, "liblw_b200.so")
-SOURCES = ["lw_capi.cu", "lw_bvh_build.cu", "lw_render.cu"]
+SOURCES = ["lw_capi.cu", "lw_bvh_build.cu", "lw_render.cu", "lw_sah.cu"]
 HEADERS = ["lw_common.cuh", "lw_detmath.cuh", "lw_qmc.cuh", "lw_traverse.cuh", "lw_integrator.cuh", "lw_host.h",
            "lw_glibc_log_data.h", os.path.join("..", "..", "include", "lw_b200.h")]
 
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     env.pop("CXX", None)
     for src in SOURCES:
         tag = "_".join(d.replace("=", "") for d in defines)
-        obj = os.path.join(BUILD, src.replace(".cu", f"{tag}.o"))
+        obj = os.path.join(BUILD, os.path.splitext(src)[0] + f"{tag}.o")
         cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(HERE, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]

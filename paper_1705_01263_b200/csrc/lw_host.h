@@ -5,9 +5,12 @@
 
 #include <vector>
 
+#include "../../include/lw_b200.h"
 #include "lw_qmc.cuh"
 
 namespace lw {
+
+void set_error(const char* fmt, ...);
 
 // QmcDim/perm tables from the reference's DimensionTable arrays (qmc.py:274-305)
 int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_flat, int64_t perm_len,
@@ -26,5 +29,19 @@ struct DeviceBVH {
 };
 int bvh_build_device(const double* d_verts, int64_t ntris, cudaStream_t stream, DeviceBVH& out);
 int64_t bvh_node_count(int64_t ntris);
+
+// Binned-SAH render BVH built on the host (lw_sah.cpp): internal nodes in
+// breadth-first order with both children's boxes, leaf refs -(1 + (start<<3 | count)).
+struct SahNode {
+  double box[12];
+  int32_t ref[2];
+};
+struct SahBVH {
+  std::vector<SahNode> nodes;
+  std::vector<int64_t> order;  // leaf-ordered triangle ids
+  int32_t root_ref = -1;
+  double root_box[6];
+};
+int sah_build_host(const double* verts, int64_t ntris, SahBVH& out);
 
 }  // namespace lw

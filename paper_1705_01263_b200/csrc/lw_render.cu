@@ -81,6 +81,7 @@ struct lw_ctx {
   double last_total_ms = 0.0, last_trace_ms = 0.0;
   int64_t last_launches = 0;
   size_t smem_bytes = 0;  // scene bytes staged in shared memory (0 = use global/L1)
+  int nrnodes = 0;        // internal nodes of the render BVH
   cudaStream_t own_stream = nullptr;
   int instr = 0;
   std::vector<cudaEvent_t> evpool;  // pairs bracketing trace launches
@@ -567,6 +568,7 @@ __global__ void k_resolve(const unsigned long long* fb, long long n, double scal
 }
 
 int nrnodes_of(const lw_ctx* c) { return c->ref_bvh.nnodes > 1 ? (int)((c->ref_bvh.nnodes - 1) / 2) : 0; }
+int render_nodes(const lw_ctx* c) { return c->nrnodes; }
 
 int alloc_pool(lw_ctx* c, int size) {
   if (c->pool.size == size) return LW_OK;
@@ -602,7 +604,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
   LW_CHECK_ARG(c->configured, "render: lw_render_configure not called");
   cudaStream_t st = c->stream;
   const lw_render_params& p = c->params;
-  int nr = nrnodes_of(c);
+  int nr = c->nrnodes;
   int use_smem = c->smem_bytes > 0 ? 1 : 0;
   size_t smem = c->smem_bytes;
   int nsm = 148;
@@ -826,41 +828,68 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   S.normals = dn;
   S.material = dm;
   S.materials = dmat;
-  // BVH on the device (reference layout), then the render layout
+  // reference-layout BVH on the device (geometry.py:100-148 arrays; exported for parity)
   LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
   int64_t nn = c->ref_bvh.nnodes;
-  int nr = nrnodes_of(c);
+  int nr;
   RNode* rn;
   LTri* lt;
-  LW_STATUS_TRY(dev_alloc(c, rn, nr > 0 ? nr : 1));
-  LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
-  if (n > 0) {
-    int* flag;
-    int* imap;
-    LW_STATUS_TRY(dev_alloc(c, flag, nn));
-    LW_STATUS_TRY(dev_alloc(c, imap, nn));
-    k_internal_flags<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.children, nn, flag);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, imap, (int)nn, st);
-    void* tmp;
-    LW_CUDA_TRY(cudaMalloc(&tmp, tb > 0 ? tb : 16));
-    LW_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, imap, (int)nn, st));
-    k_build_rnodes<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.bounds, c->ref_bvh.children, nn, imap, rn);
-    k_build_ltris<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, c->ref_bvh.order, n, lt);
-    LW_CUDA_TRY(cudaGetLastError());
-    LW_CUDA_TRY(cudaStreamSynchronize(st));
-    cudaFree(tmp);
-  }
   double rb[6] = {0, 0, 0, 0, 0, 0};
-  long long rc[2] = {-1, 0};
-  LW_CUDA_TRY(cudaMemcpyAsync(rb, c->ref_bvh.bounds, sizeof(rb), cudaMemcpyDeviceToHost, st));
-  LW_CUDA_TRY(cudaMemcpyAsync(rc, c->ref_bvh.children, sizeof(rc), cudaMemcpyDeviceToHost, st));
-  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  if (d->bvh_kind == LW_BVH_MEDIAN) {
+    // render layout derived from the median tree on the device
+    nr = nrnodes_of(c);
+    LW_STATUS_TRY(dev_alloc(c, rn, nr > 0 ? nr : 1));
+    LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
+    if (n > 0) {
+      int* flag;
+      int* imap;
+      LW_STATUS_TRY(dev_alloc(c, flag, nn));
+      LW_STATUS_TRY(dev_alloc(c, imap, nn));
+      k_internal_flags<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.children, nn, flag);
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, imap, (int)nn, st);
+      void* tmp;
+      LW_CUDA_TRY(cudaMalloc(&tmp, tb > 0 ? tb : 16));
+      LW_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, imap, (int)nn, st));
+      k_build_rnodes<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.bounds, c->ref_bvh.children, nn, imap, rn);
+      k_build_ltris<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, c->ref_bvh.order, n, lt);
+      LW_CUDA_TRY(cudaGetLastError());
+      LW_CUDA_TRY(cudaStreamSynchronize(st));
+      cudaFree(tmp);
+    }
+    long long rc[2] = {-1, 0};
+    LW_CUDA_TRY(cudaMemcpyAsync(rb, c->ref_bvh.bounds, sizeof(rb), cudaMemcpyDeviceToHost, st));
+    LW_CUDA_TRY(cudaMemcpyAsync(rc, c->ref_bvh.children, sizeof(rc), cudaMemcpyDeviceToHost, st));
+    LW_CUDA_TRY(cudaStreamSynchronize(st));
+    S.bvh.root_ref = rc[0] >= 0 ? 0 : (int)(-(1 + ((-(rc[0] + 1)) << 3 | rc[1])));
+  } else {
+    // binned-SAH render tree (host build, lw_sah.cpp), uploaded in the device layout
+    SahBVH sb;
+    LW_STATUS_TRY(sah_build_host(d->verts, n, sb));
+    nr = (int)sb.nodes.size();
+    std::vector<RNode> hn(nr > 0 ? nr : 1);
+    for (int k = 0; k < nr; k++) {
+      memset(&hn[k], 0, sizeof(RNode));
+      memcpy(hn[k].box, sb.nodes[k].box, sizeof(double) * 12);
+      hn[k].ref[0] = sb.nodes[k].ref[0];
+      hn[k].ref[1] = sb.nodes[k].ref[1];
+    }
+    std::vector<LTri> ht(n > 0 ? n : 1);
+    for (int64_t j = 0; j < n; j++) {
+      memcpy(ht[j].v, d->verts + 9 * sb.order[j], sizeof(double) * 9);
+      ht[j].id = sb.order[j];
+    }
+    LW_STATUS_TRY(dev_upload(c, rn, hn.data(), nr > 0 ? nr : 1));
+    LW_STATUS_TRY(dev_upload(c, lt, ht.data(), n > 0 ? n : 1));
+    for (int a = 0; a < 6; a++) rb[a] = sb.root_box[a];
+    S.bvh.root_ref = sb.root_ref;
+    LW_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  c->nrnodes = nr;
   S.bvh.nodes = rn;
   S.bvh.tris = lt;
   S.bvh.ntris = n;
   for (int a = 0; a < 6; a++) S.bvh.root_box[a] = rb[a];
-  S.bvh.root_ref = rc[0] >= 0 ? 0 : (int)(-(1 + ((-(rc[0] + 1)) << 3 | rc[1])));
   // stage in shared memory when the whole render BVH fits comfortably
   size_t bytes = sizeof(RNode) * (size_t)nr + sizeof(LTri) * (size_t)n;
   c->smem_bytes = (n > 0 && bytes <= 48 * 1024) ? bytes : 0;

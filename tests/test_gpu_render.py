@@ -62,13 +62,13 @@ def _random_rays(n, lo, hi, seed):
     return o, d
 
 
-@pytest.mark.parametrize("which", ["cornell", "soup"])
-def test_render_traversal_bit_exact(gpu, oracle, which):
+@pytest.mark.parametrize("which,bvh", [("cornell", "sah"), ("cornell", "median"), ("soup", "sah"), ("soup", "median")])
+def test_render_traversal_bit_exact(gpu, oracle, which, bvh):
     if which == "cornell":
-        packed = pack_scene(scenes.cornell())
+        packed = pack_scene(scenes.cornell(), bvh=bvh)
         o, d = _random_rays(50000, np.array([0.0, 0.0, -0.5]), np.array([1.0, 1.0, 3.0]), 3)
     else:
-        packed = pack_scene(scenes.soup(1 << 16, n_materials=8))
+        packed = pack_scene(scenes.soup(1 << 16, n_materials=8), bvh=bvh)
         o, d = _random_rays(50000, np.zeros(3), np.full(3, 20.0), 4)
     tm = np.where(np.arange(len(o)) % 5 == 0, 3.0, np.inf)
     with _renderer(packed, 64, 64, 4) as r:
@@ -87,11 +87,12 @@ def test_render_traversal_bit_exact(gpu, oracle, which):
         assert np.array_equal(tri, tri3)
 
 
-@pytest.mark.parametrize("engine", ["megakernel", "wavefront"])
-def test_c1_framebuffer_bit_exact_vs_oracle(cornell_packed, oracle, engine):
+@pytest.mark.parametrize("engine,bvh", [("megakernel", "sah"), ("wavefront", "sah"), ("wavefront", "median")])
+def test_c1_framebuffer_bit_exact_vs_oracle(oracle, engine, bvh):
     """C1 (Cornell 64x64, 16 spp, depth 4): the whole accumulated framebuffer, bit for bit."""
     from paper_1705_01263_b200.render import RenderParams
 
+    cornell_packed = pack_scene(scenes.cornell(), bvh=bvh)
     with _renderer(cornell_packed, 64, 64, 4, engine=engine, pool_log2=12) as r:
         r.render_pass(0, 16)
         fb = r.framebuffer()

@@ -121,3 +121,29 @@ def test_alias_table(oracle):
     assert np.allclose(implied / len(w), pdf, atol=1e-12)
     with pytest.raises(ValueError):
         oracle.alias_build(np.zeros(4))
+
+
+@pytest.mark.parametrize("bvh", ["sah", "median"])
+def test_render_traversal_equals_brute_force(oracle, bvh):
+    """Near-first traversal with the conservative cull over either render tree == exhaustive search."""
+    from paper_1705_01263_b200 import scenes
+    from paper_1705_01263_b200.scene import pack_scene
+
+    for sc, lo, hi in ((scenes.cornell(), np.array([0.0, 0.0, -0.5]), np.array([1.0, 1.0, 3.0])),
+                       (scenes.soup(4000, n_materials=4), np.zeros(3), np.full(3, 20.0))):
+        packed = pack_scene(sc, bvh=bvh)
+        osc = oracle.OracleScene(packed)
+        rng = np.random.default_rng(5)
+        o = lo + rng.random((6000, 3)) * (hi - lo)
+        d = rng.normal(size=(6000, 3))
+        d[:300, 1] = 0.0
+        tm = np.where(np.arange(6000) % 4 == 0, 2.5, np.inf)
+        t, tri, b = osc.trace_closest(o, d, tm)
+        t2, tri2, b2 = oracle.intersect_batch(2, np.zeros((1, 6)), np.zeros((1, 2), np.int64), np.zeros(0, np.int64),
+                                              packed.verts, o, d, tm)
+        assert np.array_equal(tri, tri2) and np.array_equal(t, t2) and np.array_equal(b, b2)
+        # any-hit (0 < t < tmax) == "the exhaustive closest hit without a limit is nearer than tmax"
+        t3, tri3, _ = oracle.intersect_batch(2, np.zeros((1, 6)), np.zeros((1, 2), np.int64), np.zeros(0, np.int64),
+                                             packed.verts, o, d, np.full(len(o), np.inf))
+        occ = osc.trace_any(o, d, np.full(len(o), 3.0))
+        assert np.array_equal(occ.astype(bool), (tri3 >= 0) & (t3 < 3.0))
