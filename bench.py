@@ -16,6 +16,7 @@ restatement of the render (oracle/lw_oracle.c, OpenMP over all host threads): "k
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -120,8 +121,9 @@ class ClockSampler:
 
 # ---- CPU path (oracle restatement) ----------------------------------------------------------
 
-def cpu_render_sample(a, budget_s, threads=0):
-    """Bounded sample of the same workload on the host cores: full-width pixel rows x 1 iteration."""
+def cpu_render_sample(a, budget_s, threads=0, it0=3):
+    """Bounded sample of the same workload on the host cores (oracle/lw_oracle.c, OpenMP):
+    full-frame iterations (or a band of rows when one frame exceeds the budget)."""
     from oracle import oracle as O
     from paper_1705_01263_b200.render import RenderParams
     from paper_1705_01263_b200.scene import pack_scene
@@ -130,17 +132,21 @@ def cpu_render_sample(a, budget_s, threads=0):
     osc = O.OracleScene(packed)
     params = RenderParams(a.width, a.height, a.depth)
     threads = threads or os.cpu_count()
-    rows = 16
+    rows = min(16, a.height)
     t0 = time.perf_counter()
-    osc.render(params, 3, 4, 0, rows * a.width, nthreads=threads)
-    dt = time.perf_counter() - t0
-    rows = int(max(16, min(a.height, rows * budget_s / max(dt, 1e-6))))
+    osc.render(params, it0, it0 + 1, 0, rows * a.width, nthreads=threads)
+    per_row = (time.perf_counter() - t0) / rows
+    frame = per_row * a.height
+    if frame <= budget_s:
+        rows, its = a.height, max(1, int(budget_s / max(frame, 1e-9)))
+    else:
+        rows, its = max(1, int(budget_s / max(per_row, 1e-9))), 1
     t0 = time.perf_counter()
-    _, st = osc.render(params, 3, 4, 0, rows * a.width, nthreads=threads)
+    _, st = osc.render(params, it0, it0 + its, 0, rows * a.width, nthreads=threads)
     dt = time.perf_counter() - t0
     return {"value": st["paths"] / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{rows} rows x {a.width} px x 1 iteration (iteration 3) of the workload, "
-                      f"{st['paths']} paths in {dt:.2f} s, oracle/lw_oracle.c OpenMP",
+            "sample": f"{rows} rows x {a.width} px x {its} iterations (from iteration {it0}) of the workload: "
+                      f"{st['paths']} paths in {dt:.2f} s; oracle/lw_oracle.c (C restatement, OpenMP)",
             "mrays_per_s": (st["rays_extension"] + st["rays_shadow"]) / dt / 1e6}
 
 
@@ -150,7 +156,7 @@ def run_reference(a):
         return
     vals = []
     for step in range(a.warmup + a.steps):
-        r = cpu_render_sample(a, max(a.cpu_seconds / max(a.steps, 1), 1.0))
+        r = cpu_render_sample(a, max(a.cpu_seconds / max(a.steps, 1), 1.0), it0=3 + step)
         if step >= a.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
@@ -255,38 +261,38 @@ def run_ours(a):
     paths = a.steps * world * its * P
     value = paths / (ms_max / 1e3)
 
-    # e2e through the public API with host buffers: scene upload (H2D) + pass + resolved image (D2H)
+    # e2e through the public API, scene in -> image out every step: create the context, upload the
+    # scene from host buffers (GPU BVH builds run here), render this rank's pass, reduce, read back
+    # the resolved float32 image
     e2e = None
     if not a.no_e2e:
-        h2d = sum(getattr(packed.arrays[k], "nbytes", 0) for k in packed.arrays if packed.arrays[k] is not None)
-        img_bytes = P * 3 * 4
+        h2d = sum(v.nbytes for v in packed.arrays.values() if hasattr(v, "nbytes"))
+        h2d += C.sizeof(packed.desc) + C.sizeof(r.params.struct) + r.params.bases.nbytes + \
+            r.params.perm_flat.nbytes + r.params.perm_offset.nbytes
+        d2h = P * 3 * 4
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for s in range(a.steps):
-            r2 = Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
-                          regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail) if s == 0 else r2
-            if s > 0:
-                r2.lib.lw_scene_upload(r2.ctx, __import__("ctypes").byref(packed.desc))
-            lo, hi = partition_iterations(s * world * its, (s + 1) * world * its, rank, world)
-            r2.clear()
-            r2.render_pass(lo, hi)
-            if world > 1:
+            with Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
+                          regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail) as r2:
                 r2.set_stream(stream.cuda_stream)
-                r2.copy_framebuffer_to(tmp.data_ptr())
-                dist.all_reduce(tmp)
-                r2.load_framebuffer_from(tmp.data_ptr())
-            img = r2.image(hi - lo)
+                lo, hi = partition_iterations(s * world * its, (s + 1) * world * its, rank, world)
+                r2.render_pass(lo, hi)
+                if world > 1:
+                    r2.copy_framebuffer_to(tmp.data_ptr())
+                    dist.all_reduce(tmp)
+                    r2.load_framebuffer_from(tmp.data_ptr())
+                r2.image(world * its)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        r2.close()
         e2e = {"value": paths / float(tt[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(img_bytes), "note": "per step: scene upload + GPU BVH build + pass + resolved float32 image readback"}
-        del img
+               "d2h_bytes_per_step": int(d2h),
+               "note": "per step: context + scene upload (GPU median BVH, SAH render BVH) + pass + NCCL reduce "
+                       "(N>1) + resolved float32 image readback, host wall clock around device syncs"}
 
     peaks = load_peaks()
     nodes_per_ray = work["ext_nodes"] / max(work["ext_rays"], 1)

@@ -725,9 +725,13 @@ static void build_render_bvh_sah(lwo_scene* s) {
       if (v[6 + a] < l) l = v[6 + a];
       if (v[3 + a] > h) h = v[3 + a];
       if (v[6 + a] > h) h = v[6 + a];
+      if (l == 0.0) l = 0.0; /* canonical +0: exact min/max are then order independent */
+      if (h == 0.0) h = 0.0;
+      double c = 0.5 * (l + h);
+      if (c == 0.0) c = 0.0;
       lo[3 * i + a] = l;
       hi[3 * i + a] = h;
-      ce[3 * i + a] = 0.5 * (l + h);
+      ce[3 * i + a] = c;
     }
     s->ltri[i] = i;
   }

@@ -1,0 +1,102 @@
+"""Thin `render` command (the reference declares `lumenwave = "lumenwave.cli:main"`,
+pyproject.toml:12-13, with the flags of SPEC.md:800 but ships no cli module).
+
+    python -m paper_1705_01263_b200.cli render --config C1 --out img [--res WxH] [--iterations N]
+        [--depth D] [--snapshot-every N] [--engine wavefront|megakernel] [--metrics FILE] [--device K]
+
+Scenes come from the procedural configs (the text-format parser is out of scope);
+`--scene FILE.py` may name a Python file defining `scene()` that returns a Scene (e.g. one built
+with the reference's `load_scene`).  Outputs are numbered PFM snapshots (`--out` prefix), the
+bit-exact interchange format of SPEC.md DESIGN DECISIONS.  Exit codes per SPEC.md: 0 success,
+2 input error, 3 config error, 4 internal error.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import runpy
+import sys
+import time
+
+
+def _parse_res(text):
+    w, h = text.lower().split("x")
+    w, h = int(w), int(h)
+    if w <= 0 or h <= 0:
+        raise ValueError
+    return w, h
+
+
+def cmd_render(args) -> int:
+    from paper_1705_01263_b200 import scenes
+    from paper_1705_01263_b200.imagefiles import write_pfm
+    from paper_1705_01263_b200.render import Renderer
+
+    cfg = scenes.CONFIGS.get(args.config)
+    if args.scene:
+        try:
+            scene = runpy.run_path(args.scene)["scene"]()
+        except (OSError, KeyError) as e:
+            print(f"error: cannot load scene '{args.scene}': {e}", file=sys.stderr)
+            return 2
+    elif cfg is not None:
+        scene = cfg.builder()
+    else:
+        print(f"error: unknown config '{args.config}'", file=sys.stderr)
+        return 3
+    try:
+        w, h = _parse_res(args.res) if args.res else (cfg.width, cfg.height)
+    except ValueError:
+        print(f"error: bad --res '{args.res}' (expected WxH)", file=sys.stderr)
+        return 3
+    spp = args.iterations or (cfg.spp if cfg else 16)
+    depth = args.depth or (cfg.max_depth if cfg else 8)
+    if spp < 1:
+        print("error: --iterations must be >= 1", file=sys.stderr)
+        return 3
+    step = args.snapshot_every or spp
+    t0 = time.perf_counter()
+    with Renderer(scene, w, h, depth, device=args.device, engine=args.engine) as r:
+        done = 0
+        while done < spp:
+            k = min(step, spp - done)
+            r.render_pass(done, done + k)
+            done += k
+            write_pfm(f"{args.out}_{done:06d}.pfm", r.image(done))
+        stats = r.stats()
+    dt = time.perf_counter() - t0
+    if args.metrics:
+        stats.update({"seconds": dt, "paths_per_s": stats["paths"] / dt, "width": w, "height": h, "iterations": spp})
+        with open(args.metrics, "w") as f:
+            json.dump(stats, f, indent=1)
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="paper_1705_01263_b200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    rp = sub.add_parser("render", help="progressive render to numbered PFM snapshots")
+    rp.add_argument("--config", default="C1")
+    rp.add_argument("--scene", default=None, help="Python file defining scene() -> Scene")
+    rp.add_argument("--res", default=None)
+    rp.add_argument("--iterations", type=int, default=0)
+    rp.add_argument("--depth", type=int, default=0)
+    rp.add_argument("--snapshot-every", type=int, default=0)
+    rp.add_argument("--engine", default="wavefront", choices=["wavefront", "megakernel"])
+    rp.add_argument("--device", type=int, default=0)
+    rp.add_argument("--out", default="render")
+    rp.add_argument("--metrics", default=None)
+    args = ap.parse_args(argv)
+    try:
+        return cmd_render(args)
+    except (ValueError, NotImplementedError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 3
+    except Exception as e:  # surfaced as the SPEC's internal-error code
+        print(f"internal error: {e}", file=sys.stderr)
+        return 4
+
+
+if __name__ == "__main__":
+    sys.exit(main())

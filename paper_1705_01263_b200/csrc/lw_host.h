@@ -30,18 +30,22 @@ struct DeviceBVH {
 int bvh_build_device(const double* d_verts, int64_t ntris, cudaStream_t stream, DeviceBVH& out);
 int64_t bvh_node_count(int64_t ntris);
 
-// Binned-SAH render BVH built on the host (lw_sah.cpp): internal nodes in
-// breadth-first order with both children's boxes, leaf refs -(1 + (start<<3 | count)).
+// Binned-SAH render BVH: internal nodes in breadth-first order with both
+// children's boxes, leaf refs -(1 + (start<<3 | count)).
 struct SahNode {
   double box[12];
   int32_t ref[2];
 };
-struct SahBVH {
-  std::vector<SahNode> nodes;
-  std::vector<int64_t> order;  // leaf-ordered triangle ids
+inline int32_t leaf_ref32_host(int64_t start, int64_t count) { return (int32_t)(-(1 + ((start << 3) | count))); }
+
+// the same tree built on the GPU (lw_sah_build.cu); nodes/order are device arrays owned by the caller
+struct DeviceSah {
+  SahNode* nodes = nullptr;
+  int* order = nullptr;
+  int64_t nnodes = 0;
   int32_t root_ref = -1;
   double root_box[6];
 };
-int sah_build_host(const double* verts, int64_t ntris, SahBVH& out);
+int sah_build_device(const double* d_verts, int64_t ntris, cudaStream_t stream, DeviceSah& out);
 
 }  // namespace lw

@@ -200,6 +200,31 @@ __global__ void k_build_ltris(const double* __restrict__ verts, const long long*
   out[j] = r;
 }
 
+__global__ void k_sah_to_rnodes(const SahNode* __restrict__ in, int nr, RNode* __restrict__ out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nr) return;
+  RNode r;
+#pragma unroll
+  for (int a = 0; a < 12; a++) r.box[a] = in[k].box[a];
+  r.ref[0] = in[k].ref[0];
+  r.ref[1] = in[k].ref[1];
+#pragma unroll
+  for (int p = 0; p < 6; p++) r.pad[p] = 0;
+  out[k] = r;
+}
+
+__global__ void k_build_ltris_i32(const double* __restrict__ verts, const int* __restrict__ order, long long n,
+                                  LTri* __restrict__ out) {
+  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  long long t = order[j];
+  LTri r;
+#pragma unroll
+  for (int k = 0; k < 9; k++) r.v[k] = verts[9 * t + k];
+  r.id = t;
+  out[j] = r;
+}
+
 __global__ void k_emitters(const double* __restrict__ verts, const long long* __restrict__ emit_tri, long long nemit,
                            double* __restrict__ area, int* __restrict__ emit_of_tri) {
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -863,27 +888,25 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     LW_CUDA_TRY(cudaStreamSynchronize(st));
     S.bvh.root_ref = rc[0] >= 0 ? 0 : (int)(-(1 + ((-(rc[0] + 1)) << 3 | rc[1])));
   } else {
-    // binned-SAH render tree (host build, lw_sah.cpp), uploaded in the device layout
-    SahBVH sb;
-    LW_STATUS_TRY(sah_build_host(d->verts, n, sb));
-    nr = (int)sb.nodes.size();
-    std::vector<RNode> hn(nr > 0 ? nr : 1);
-    for (int k = 0; k < nr; k++) {
-      memset(&hn[k], 0, sizeof(RNode));
-      memcpy(hn[k].box, sb.nodes[k].box, sizeof(double) * 12);
-      hn[k].ref[0] = sb.nodes[k].ref[0];
-      hn[k].ref[1] = sb.nodes[k].ref[1];
+    // binned-SAH render tree built on the device (lw_sah_build.cu), converted to the 128-byte layout
+    DeviceSah ds;
+    int rc_sah = sah_build_device(dv, n, st, ds);
+    if (rc_sah != LW_OK) {
+      cudaFree(ds.nodes);
+      cudaFree(ds.order);
+      return rc_sah;
     }
-    std::vector<LTri> ht(n > 0 ? n : 1);
-    for (int64_t j = 0; j < n; j++) {
-      memcpy(ht[j].v, d->verts + 9 * sb.order[j], sizeof(double) * 9);
-      ht[j].id = sb.order[j];
-    }
-    LW_STATUS_TRY(dev_upload(c, rn, hn.data(), nr > 0 ? nr : 1));
-    LW_STATUS_TRY(dev_upload(c, lt, ht.data(), n > 0 ? n : 1));
-    for (int a = 0; a < 6; a++) rb[a] = sb.root_box[a];
-    S.bvh.root_ref = sb.root_ref;
+    nr = (int)ds.nnodes;
+    LW_STATUS_TRY(dev_alloc(c, rn, nr > 0 ? nr : 1));
+    LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
+    if (nr > 0) k_sah_to_rnodes<<<grid_for(nr, 256, 1 << 30), 256, 0, st>>>(ds.nodes, nr, rn);
+    if (n > 0) k_build_ltris_i32<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, ds.order, n, lt);
+    LW_CUDA_TRY(cudaGetLastError());
     LW_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(ds.nodes);
+    cudaFree(ds.order);
+    for (int a = 0; a < 6; a++) rb[a] = ds.root_box[a];
+    S.bvh.root_ref = ds.root_ref;
   }
   c->nrnodes = nr;
   S.bvh.nodes = rn;

@@ -1,0 +1,566 @@
+// lw_sah_build.cu -- binned-SAH render BVH built on the GPU.
+//
+// Produces exactly the tree of the specification restated in oracle/lw_oracle.c
+// (build_render_bvh_sah): segments processed breadth-first, internal nodes numbered in that
+// order, 16 centroid bins per axis, first strict minimum of A(L)nL + A(R)nR over (axis, plane),
+// split when n > 7 or A(B) + cost < n*A(B), coincident centroids halved in order, stable
+// partition.  Per level:
+//   1. bins of large segments (n > 32): ordered-u64 min/max + count atomics, privatised in
+//      shared memory when a 1024-position chunk lies inside one segment;
+//   2. one thread per segment: small segments bin their triangles sequentially, every segment
+//      sweeps its planes and decides leaf / split (identical FP64 formulas on both paths);
+//   3. node ids = level base + rank among splitting segments (scan), child segments at 2r, 2r+1;
+//   4. stable partition of the position list (scan + scatter) and the next position->segment map.
+// Bounds are exact (min/max), so every path reproduces the sequential specification bit for bit.
+#include <string.h>
+
+#include <algorithm>
+
+#include <cub/cub.cuh>
+
+#include "lw_common.cuh"
+#include "lw_host.h"
+
+namespace lw {
+
+namespace {
+
+constexpr int kBins = 16;
+constexpr int kMaxLeaf = 7;
+constexpr int kSmall = 32;   // segments up to this size are binned by one thread
+constexpr int kChunk = 1024; // positions per block in the large-segment binning pass
+
+struct SSeg {
+  int start, n, parent, side;
+  double B[6];  // triangle-bounds box lo xyz, hi xyz
+  double C[6];  // centroid box
+};
+
+struct SSplit {
+  int split;    // 0 leaf, 1 split
+  int axis;     // -1 = halve
+  int plane, nl;
+  double L[6], R[6], CL[6], CR[6];
+};
+
+// 13 values per bin: count, triangle box (6), centroid box (6), as order-preserving u64
+struct BinAcc {
+  unsigned long long v[13];
+};
+
+__device__ __forceinline__ unsigned long long ordd(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double unordd(unsigned long long u) {
+  unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
+  return __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ double area6(const double* b) {
+  double dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
+  return 2.0 * ((dx * dy + dy * dz) + dz * dx);
+}
+
+__device__ __forceinline__ void box_reset(double* b) {
+  b[0] = b[1] = b[2] = INFINITY;
+  b[3] = b[4] = b[5] = -INFINITY;
+}
+
+__device__ __forceinline__ void box_grow(double* b, const double* lo, const double* hi) {
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    if (lo[a] < b[a]) b[a] = lo[a];
+    if (hi[a] > b[3 + a]) b[3 + a] = hi[a];
+  }
+}
+
+__device__ __forceinline__ int bin_of(double c, double cmin, double scale) {
+  int b = (int)((c - cmin) * scale);
+  return b > kBins - 1 ? kBins - 1 : b;
+}
+
+__device__ __forceinline__ double canon(double x) { return x == 0.0 ? 0.0 : x; }
+
+__global__ void k_sah_prep(const double* __restrict__ v, int n, double* __restrict__ tb, double* __restrict__ cen,
+                           int* __restrict__ ids, int* __restrict__ pos_seg) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* p = v + 9 * (size_t)i;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    double lo = p[a], hi = p[a];
+    if (p[3 + a] < lo) lo = p[3 + a];
+    if (p[6 + a] < lo) lo = p[6 + a];
+    if (p[3 + a] > hi) hi = p[3 + a];
+    if (p[6 + a] > hi) hi = p[6 + a];
+    lo = canon(lo);
+    hi = canon(hi);
+    tb[6 * (size_t)i + a] = lo;
+    tb[6 * (size_t)i + 3 + a] = hi;
+    cen[3 * (size_t)i + a] = canon(0.5 * (lo + hi));
+  }
+  ids[i] = i;
+  pos_seg[i] = 0;
+}
+
+// root boxes: block reduction then ordered atomics (12 values)
+__global__ void k_sah_root_reduce(const double* __restrict__ tb, const double* __restrict__ cen, int n,
+                                  unsigned long long* __restrict__ acc) {
+  double v[12];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    v[k] = INFINITY;
+    v[3 + k] = -INFINITY;
+    v[6 + k] = INFINITY;
+    v[9 + k] = -INFINITY;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      v[a] = fmin(v[a], tb[6 * (size_t)i + a]);
+      v[3 + a] = fmax(v[3 + a], tb[6 * (size_t)i + 3 + a]);
+      v[6 + a] = fmin(v[6 + a], cen[3 * (size_t)i + a]);
+      v[9 + a] = fmax(v[9 + a], cen[3 * (size_t)i + a]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 12; k++) {
+    unsigned long long u = ordd(v[k]);
+    bool mn = (k % 6) < 3;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      unsigned long long o = __shfl_down_sync(0xffffffffu, u, off);
+      u = mn ? (o < u ? o : u) : (o > u ? o : u);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (mn)
+        atomicMin(acc + k, u);
+      else
+        atomicMax(acc + k, u);
+    }
+  }
+}
+
+__global__ void k_sah_root_init(unsigned long long* acc, SSeg* seg, int n) {
+  SSeg s;
+  s.start = 0;
+  s.n = n;
+  s.parent = -1;
+  s.side = 0;
+  for (int k = 0; k < 6; k++) {
+    s.B[k] = unordd(acc[k]);
+    s.C[k] = unordd(acc[6 + k]);
+  }
+  seg[0] = s;
+}
+
+__global__ void k_sah_bins_init(BinAcc* __restrict__ bins, int nbins) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbins) return;
+  BinAcc b;
+  b.v[0] = 0;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    b.v[1 + k] = ~0ULL;
+    b.v[4 + k] = 0ULL;
+    b.v[7 + k] = ~0ULL;
+    b.v[10 + k] = 0ULL;
+  }
+  bins[i] = b;
+}
+
+__device__ __forceinline__ void bin_add(unsigned long long* b, const double* tb, const double* c, bool shared_mem) {
+  // count, tri box, centroid box; atomics are exact, so the accumulation order is irrelevant
+  atomicAdd(b, 1ULL);
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    atomicMin(b + 1 + a, ordd(tb[a]));
+    atomicMax(b + 4 + a, ordd(tb[3 + a]));
+    atomicMin(b + 7 + a, ordd(c[a]));
+    atomicMax(b + 10 + a, ordd(c[a]));
+  }
+  (void)shared_mem;
+}
+
+__global__ void __launch_bounds__(256) k_sah_bin_large(const int* __restrict__ pos_seg, const int* __restrict__ ids,
+                                                       int n, const SSeg* __restrict__ seg,
+                                                       const int* __restrict__ large_rank, const double* __restrict__ tb,
+                                                       const double* __restrict__ cen, BinAcc* __restrict__ bins) {
+  __shared__ unsigned long long sb[3 * kBins * 13];
+  int c0 = blockIdx.x * kChunk;
+  if (c0 >= n) return;
+  int c1 = min(c0 + kChunk, n);
+  int s_first = pos_seg[c0], s_last = pos_seg[c1 - 1];
+  bool priv = s_first >= 0 && s_first == s_last && large_rank[s_first] >= 0;
+  if (priv) {
+    for (int k = threadIdx.x; k < 3 * kBins; k += blockDim.x) {
+      unsigned long long* b = sb + 13 * k;
+      b[0] = 0;
+      for (int a = 0; a < 3; a++) {
+        b[1 + a] = ~0ULL;
+        b[4 + a] = 0ULL;
+        b[7 + a] = ~0ULL;
+        b[10 + a] = 0ULL;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    int s = pos_seg[i];
+    if (s < 0) continue;
+    int lr = large_rank[s];
+    if (lr < 0) continue;
+    int t = ids[i];
+    const double* tbt = tb + 6 * (size_t)t;
+    const double* ct = cen + 3 * (size_t)t;
+    const SSeg& g = seg[s];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      double ext = g.C[3 + a] - g.C[a];
+      if (!(ext > 0.0)) continue;
+      int b = bin_of(ct[a], g.C[a], (double)kBins / ext);
+      unsigned long long* dst = priv ? sb + 13 * (a * kBins + b) : bins[(size_t)lr * 3 * kBins + a * kBins + b].v;
+      bin_add(dst, tbt, ct, priv);
+    }
+  }
+  if (priv) {
+    __syncthreads();
+    int lr = large_rank[s_first];
+    for (int k = threadIdx.x; k < 3 * kBins; k += blockDim.x) {
+      unsigned long long* b = sb + 13 * k;
+      if (b[0] == 0) continue;
+      unsigned long long* d = bins[(size_t)lr * 3 * kBins + k].v;
+      atomicAdd(d, b[0]);
+      for (int a = 0; a < 3; a++) {
+        atomicMin(d + 1 + a, b[1 + a]);
+        atomicMax(d + 4 + a, b[4 + a]);
+        atomicMin(d + 7 + a, b[7 + a]);
+        atomicMax(d + 10 + a, b[10 + a]);
+      }
+    }
+  }
+}
+
+// one thread per segment: bin (small segments), sweep, decide
+__global__ void k_sah_decide(const SSeg* __restrict__ seg, int nseg, const int* __restrict__ large_rank,
+                             const BinAcc* __restrict__ bins, const int* __restrict__ ids,
+                             const double* __restrict__ tb, const double* __restrict__ cen, SSplit* __restrict__ out,
+                             int* __restrict__ split_flag) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const SSeg g = seg[s];
+  SSplit r;
+  r.split = 0;
+  r.axis = -1;
+  r.plane = -1;
+  r.nl = 0;
+  double best = INFINITY;
+  if (g.n > 1) {
+    for (int a = 0; a < 3; a++) {
+      double ext = g.C[3 + a] - g.C[a];
+      if (!(ext > 0.0)) continue;
+      double scale = (double)kBins / ext;
+      int cnt[kBins];
+      double bb[kBins][6], cb[kBins][6];
+      if (large_rank[s] >= 0) {
+        const BinAcc* src = bins + (size_t)large_rank[s] * 3 * kBins + a * kBins;
+        for (int b = 0; b < kBins; b++) {
+          cnt[b] = (int)src[b].v[0];
+          for (int k = 0; k < 6; k++) {
+            bb[b][k] = unordd(src[b].v[1 + k]);
+            cb[b][k] = unordd(src[b].v[7 + k]);
+          }
+        }
+      } else {
+        for (int b = 0; b < kBins; b++) {
+          cnt[b] = 0;
+          box_reset(bb[b]);
+          box_reset(cb[b]);
+        }
+        for (int k = 0; k < g.n; k++) {
+          int t = ids[g.start + k];
+          const double* ct = cen + 3 * (size_t)t;
+          int b = bin_of(ct[a], g.C[a], scale);
+          cnt[b]++;
+          box_grow(bb[b], tb + 6 * (size_t)t, tb + 6 * (size_t)t + 3);
+          box_grow(cb[b], ct, ct);
+        }
+      }
+      // suffix (right side of plane p = bins p+1..15)
+      double rb[kBins][6], rc[kBins][6];
+      int rn[kBins];
+      double accb[6], accc[6];
+      box_reset(accb);
+      box_reset(accc);
+      int an = 0;
+      for (int b = kBins - 1; b >= 1; b--) {
+        box_grow(accb, bb[b], bb[b] + 3);
+        box_grow(accc, cb[b], cb[b] + 3);
+        an += cnt[b];
+        for (int k = 0; k < 6; k++) {
+          rb[b][k] = accb[k];
+          rc[b][k] = accc[k];
+        }
+        rn[b] = an;
+      }
+      box_reset(accb);
+      box_reset(accc);
+      an = 0;
+      for (int p = 0; p < kBins - 1; p++) {
+        box_grow(accb, bb[p], bb[p] + 3);
+        box_grow(accc, cb[p], cb[p] + 3);
+        an += cnt[p];
+        int nr = rn[p + 1];
+        if (an == 0 || nr == 0) continue;
+        double cost = area6(accb) * (double)an + area6(rb[p + 1]) * (double)nr;
+        if (cost < best) {
+          best = cost;
+          r.axis = a;
+          r.plane = p;
+          r.nl = an;
+          for (int k = 0; k < 6; k++) {
+            r.L[k] = accb[k];
+            r.CL[k] = accc[k];
+            r.R[k] = rb[p + 1][k];
+            r.CR[k] = rc[p + 1][k];
+          }
+        }
+      }
+    }
+  }
+  if (r.axis >= 0) {
+    double aB = area6(g.B);
+    r.split = (g.n > kMaxLeaf || (aB + best) < (double)g.n * aB) ? 1 : 0;
+  } else if (g.n > kMaxLeaf) {
+    r.split = 1;  // coincident centroids: halve in the current order
+    r.axis = -1;
+    r.nl = g.n / 2;
+    box_reset(r.L);
+    box_reset(r.R);
+    box_reset(r.CL);
+    box_reset(r.CR);
+    for (int k = 0; k < g.n; k++) {
+      int t = ids[g.start + k];
+      double* B = k < r.nl ? r.L : r.R;
+      double* Cc = k < r.nl ? r.CL : r.CR;
+      box_grow(B, tb + 6 * (size_t)t, tb + 6 * (size_t)t + 3);
+      box_grow(Cc, cen + 3 * (size_t)t, cen + 3 * (size_t)t);
+    }
+  }
+  out[s] = r;
+  split_flag[s] = r.split;
+}
+
+__device__ __forceinline__ int leaf_ref32(long long start, long long count) {
+  return (int)(-(1 + ((start << 3) | count)));
+}
+
+// node ids, parent refs, node boxes and the next level's segment table
+__global__ void k_sah_emit(const SSeg* __restrict__ seg, int nseg, const SSplit* __restrict__ sp,
+                           const int* __restrict__ split_rank, int node_base, SahNode* __restrict__ nodes,
+                           int* __restrict__ root_ref, SSeg* __restrict__ next) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const SSeg g = seg[s];
+  const SSplit& r = sp[s];
+  int ref;
+  if (!r.split) {
+    ref = leaf_ref32(g.start, g.n);
+  } else {
+    int rank = split_rank[s];
+    int id = node_base + rank;
+    ref = id;
+    SahNode& nd = nodes[id];
+    for (int k = 0; k < 6; k++) {
+      nd.box[k] = r.L[k];
+      nd.box[6 + k] = r.R[k];
+    }
+    SSeg L, R;
+    L.start = g.start;
+    L.n = r.nl;
+    L.parent = id;
+    L.side = 0;
+    R.start = g.start + r.nl;
+    R.n = g.n - r.nl;
+    R.parent = id;
+    R.side = 1;
+    for (int k = 0; k < 6; k++) {
+      L.B[k] = r.L[k];
+      L.C[k] = r.CL[k];
+      R.B[k] = r.R[k];
+      R.C[k] = r.CR[k];
+    }
+    next[2 * rank] = L;
+    next[2 * rank + 1] = R;
+  }
+  if (g.parent < 0)
+    *root_ref = ref;
+  else
+    nodes[g.parent].ref[g.side] = ref;
+}
+
+__global__ void k_sah_flags(const int* __restrict__ pos_seg, const int* __restrict__ ids, int n,
+                            const SSeg* __restrict__ seg, const SSplit* __restrict__ sp, const double* __restrict__ cen,
+                            int* __restrict__ left) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = pos_seg[i];
+  int f = 0;
+  if (s >= 0 && sp[s].split) {
+    const SSeg& g = seg[s];
+    const SSplit& r = sp[s];
+    if (r.axis < 0) {
+      f = (i - g.start) < r.nl;
+    } else {
+      double ext = g.C[3 + r.axis] - g.C[r.axis];
+      int b = bin_of(cen[3 * (size_t)ids[i] + r.axis], g.C[r.axis], (double)kBins / ext);
+      f = b <= r.plane;
+    }
+  }
+  left[i] = f;
+}
+
+__global__ void k_sah_scatter(const int* __restrict__ pos_seg, const int* __restrict__ ids, int n,
+                              const SSeg* __restrict__ seg, const SSplit* __restrict__ sp,
+                              const int* __restrict__ split_rank, const int* __restrict__ left,
+                              const int* __restrict__ scan, int* __restrict__ ids_out, int* __restrict__ pos_out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = pos_seg[i];
+  if (s < 0 || !sp[s].split) {
+    ids_out[i] = ids[i];
+    pos_out[i] = -1;
+    return;
+  }
+  const SSeg& g = seg[s];
+  int nl = sp[s].nl;
+  int j = i - g.start;
+  int rl = scan[i] - scan[g.start];
+  bool l = left[i] != 0;
+  int np = l ? g.start + rl : g.start + nl + (j - rl);
+  ids_out[np] = ids[i];
+  pos_out[np] = 2 * split_rank[s] + (l ? 0 : 1);
+}
+
+__global__ void k_large_flags(const SSeg* __restrict__ seg, int nseg, int* __restrict__ flag) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) flag[s] = seg[s].n > kSmall ? 1 : 0;
+}
+
+__global__ void k_large_rank(const int* __restrict__ flag, const int* __restrict__ scan, int nseg, int* __restrict__ rank) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) rank[s] = flag[s] ? scan[s] : -1;
+}
+
+}  // namespace
+
+#define TRY(x) LW_CUDA_TRY(x)
+
+int sah_build_device(const double* d_verts, int64_t n64, cudaStream_t st, DeviceSah& out) {
+  out.nnodes = 0;
+  out.root_ref = leaf_ref32_host(0, 0);
+  for (int a = 0; a < 6; a++) out.root_box[a] = 0.0;
+  int n = (int)n64;
+  LW_CHECK_ARG(n64 >= 0 && n64 < (1LL << 28), "sah build: at most 2^28 triangles");
+  TRY(cudaMalloc(&out.nodes, sizeof(SahNode) * (n > 1 ? n - 1 : 1)));
+  TRY(cudaMalloc(&out.order, sizeof(int) * (n > 0 ? n : 1)));
+  if (n == 0) return LW_OK;
+  const int B = 256;
+  int gn = (n + B - 1) / B;
+  DevBuf b_tb, b_cen, b_ids2, b_pos, b_pos2, b_left, b_scan, b_acc, b_root;
+  TRY(b_tb.alloc(sizeof(double) * 6 * (size_t)n));
+  TRY(b_cen.alloc(sizeof(double) * 3 * (size_t)n));
+  TRY(b_ids2.alloc(sizeof(int) * n));
+  TRY(b_pos.alloc(sizeof(int) * n));
+  TRY(b_pos2.alloc(sizeof(int) * n));
+  TRY(b_left.alloc(sizeof(int) * n));
+  TRY(b_scan.alloc(sizeof(int) * (n + 1)));
+  TRY(b_acc.alloc(sizeof(unsigned long long) * 12));
+  TRY(b_root.alloc(sizeof(int)));
+  int* ids = out.order;
+  int* ids2 = b_ids2.as<int>();
+  int* pos = b_pos.as<int>();
+  int* pos2 = b_pos2.as<int>();
+  k_sah_prep<<<gn, B, 0, st>>>(d_verts, n, b_tb.as<double>(), b_cen.as<double>(), ids, pos);
+  unsigned long long init[12];
+  for (int k = 0; k < 12; k++) init[k] = ((k % 6) < 3) ? ~0ULL : 0ULL;
+  TRY(cudaMemcpyAsync(b_acc.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  k_sah_root_reduce<<<std::min(gn, 1184), B, 0, st>>>(b_tb.as<double>(), b_cen.as<double>(), n,
+                                                      b_acc.as<unsigned long long>());
+  // segment tables (current / next); a level has at most n segments
+  DevBuf b_seg[2], b_split, b_sflag, b_srank, b_lflag, b_lscan, b_lrank, b_bins, b_tmp;
+  TRY(b_seg[0].alloc(sizeof(SSeg) * n));
+  TRY(b_seg[1].alloc(sizeof(SSeg) * n));
+  TRY(b_split.alloc(sizeof(SSplit) * n));
+  TRY(b_sflag.alloc(sizeof(int) * (n + 1)));
+  TRY(b_srank.alloc(sizeof(int) * (n + 1)));
+  TRY(b_lflag.alloc(sizeof(int) * (n + 1)));
+  TRY(b_lscan.alloc(sizeof(int) * (n + 1)));
+  TRY(b_lrank.alloc(sizeof(int) * (n + 1)));
+  int max_large = n / (kSmall + 1) + 1;
+  TRY(b_bins.alloc(sizeof(BinAcc) * 3 * kBins * (size_t)max_large));
+  k_sah_root_init<<<1, 1, 0, st>>>(b_acc.as<unsigned long long>(), b_seg[0].as<SSeg>(), n);
+  size_t tb1 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb1, b_left.as<int>(), b_scan.as<int>(), n + 1, st);
+  TRY(b_tmp.alloc(tb1));
+  int nseg = 1, cur = 0, node_base = 0;
+  int h_counts[2];
+  while (nseg > 0) {
+    SSeg* seg = b_seg[cur].as<SSeg>();
+    SSeg* nxt = b_seg[cur ^ 1].as<SSeg>();
+    int gs = (nseg + B - 1) / B;
+    // large-segment ranks and bins
+    k_large_flags<<<gs, B, 0, st>>>(seg, nseg, b_lflag.as<int>());
+    size_t t = b_tmp.bytes;
+    TRY(cub::DeviceScan::ExclusiveSum(b_tmp.p, t, b_lflag.as<int>(), b_lscan.as<int>(), nseg + 1, st));
+    k_large_rank<<<gs, B, 0, st>>>(b_lflag.as<int>(), b_lscan.as<int>(), nseg, b_lrank.as<int>());
+    TRY(cudaMemcpyAsync(&h_counts[0], b_lscan.as<int>() + nseg, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TRY(cudaStreamSynchronize(st));
+    int nlarge = h_counts[0];
+    if (nlarge > 0) {
+      int nb = nlarge * 3 * kBins;
+      k_sah_bins_init<<<(nb + B - 1) / B, B, 0, st>>>(b_bins.as<BinAcc>(), nb);
+      k_sah_bin_large<<<(n + kChunk - 1) / kChunk, B, 0, st>>>(pos, ids, n, seg, b_lrank.as<int>(), b_tb.as<double>(),
+                                                              b_cen.as<double>(), b_bins.as<BinAcc>());
+    }
+    k_sah_decide<<<(nseg + 63) / 64, 64, 0, st>>>(seg, nseg, b_lrank.as<int>(), b_bins.as<BinAcc>(), ids,
+                                                  b_tb.as<double>(), b_cen.as<double>(), b_split.as<SSplit>(),
+                                                  b_sflag.as<int>());
+    t = b_tmp.bytes;
+    TRY(cub::DeviceScan::ExclusiveSum(b_tmp.p, t, b_sflag.as<int>(), b_srank.as<int>(), nseg + 1, st));
+    k_sah_emit<<<gs, B, 0, st>>>(seg, nseg, b_split.as<SSplit>(), b_srank.as<int>(), node_base, out.nodes,
+                                 b_root.as<int>(), nxt);
+    k_sah_flags<<<gn, B, 0, st>>>(pos, ids, n, seg, b_split.as<SSplit>(), b_cen.as<double>(), b_left.as<int>());
+    t = b_tmp.bytes;
+    TRY(cub::DeviceScan::ExclusiveSum(b_tmp.p, t, b_left.as<int>(), b_scan.as<int>(), n, st));
+    k_sah_scatter<<<gn, B, 0, st>>>(pos, ids, n, seg, b_split.as<SSplit>(), b_srank.as<int>(), b_left.as<int>(),
+                                    b_scan.as<int>(), ids2, pos2);
+    TRY(cudaGetLastError());
+    TRY(cudaMemcpyAsync(ids, ids2, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+    std::swap(pos, pos2);
+    TRY(cudaMemcpyAsync(&h_counts[1], b_srank.as<int>() + nseg, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TRY(cudaStreamSynchronize(st));
+    int nsplit = h_counts[1];
+    node_base += nsplit;
+    nseg = 2 * nsplit;
+    cur ^= 1;
+  }
+  out.nnodes = node_base;
+  int rr = 0;
+  unsigned long long acc[12];
+  TRY(cudaMemcpyAsync(&rr, b_root.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TRY(cudaMemcpyAsync(acc, b_acc.p, sizeof(acc), cudaMemcpyDeviceToHost, st));
+  TRY(cudaStreamSynchronize(st));
+  out.root_ref = rr;
+  for (int k = 0; k < 6; k++) {
+    unsigned long long u = acc[k];
+    unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
+    double d;
+    memcpy(&d, &b, sizeof(d));
+    out.root_box[k] = d;
+  }
+  return LW_OK;
+}
+
+}  // namespace lw
