@@ -337,137 +337,165 @@ __device__ __forceinline__ void lw_path_init(const DevScene& S, long long index,
   ps.spec_prev = 1;
 }
 
-// Material / NEE stage for the hit of the current segment (oracle trace_path loop body).
-// Returns true if the path continues (ps holds the next ray).  sh.valid marks a shadow ray
-// whose contribution must be added to ps.L if unoccluded, before the path is flushed.
-__device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, const LwHit& h, ShadowRay& sh) {
+// ---- material / NEE stage (oracle trace_path loop body), split into reusable parts ----------
+// The megakernel calls lw_path_shade (all parts in order); the wavefront runs lw_shade_nee and
+// lw_shade_material as two kernels.  Both orders evaluate the same expressions on the same
+// inputs, so results are identical.
+
+struct ShadeGeom {
+  v3 p, ng, ngf, wol;
+  LwFrame fr;
+  bool front;
+  const lw_material* m;
+  LayerW lw;
+};
+
+// hit point, geometric normal, facing (needed for emission)
+__device__ __forceinline__ void lw_shade_hit(const DevScene& S, v3 d, const LwHit& h, ShadeGeom& g, double& w) {
+  const double* vv = S.verts + 9 * h.tri;
+  v3 v0 = lw_ld3(vv), v1 = lw_ld3(vv + 3), v2 = lw_ld3(vv + 6);
+  w = (1.0 - h.bu) - h.bv;
+  g.p = bary3(v0, v1, v2, w, h.bu, h.bv);
+  g.ng = normalize3(cross3(v1 - v0, v2 - v0));
+  g.front = dot3(g.ng, d) < 0.0;
+}
+
+// shading frame, material and layer weights (vertices with a scattering event)
+__device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const LwHit& h, double w, ShadeGeom& g) {
+  const double* nn = S.normals + 9 * h.tri;
+  v3 ns = bary3(lw_ld3(nn), lw_ld3(nn + 3), lw_ld3(nn + 6), w, h.bu, h.bv);
+  double nl = dot3(ns, ns);
+  ns = nl > 0.0 ? ns * (1.0 / sqrt(nl)) : g.ng;
+  v3 wo = neg3(d);
+  g.ngf = g.front ? g.ng : neg3(g.ng);
+  if (dot3(ns, g.ngf) < 0.0) ns = neg3(ns);
+  if (dot3(ns, wo) <= 0.0) ns = g.ngf;
+  g.fr = lw_make_frame(ns);
+  g.wol = lw_to_local(g.fr, wo);
+  g.m = &S.materials[S.material[h.tri]];  // read in place (no local-memory copy)
+  lw_layer_weights(*g.m, g.wol.z, g.lw);
+}
+
+// next-event estimation: fills sh (valid = 0 if no contribution)
+__device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh) {
   sh.valid = 0;
-  const int b = ps.bounce;
+  const lw_material& m = *g.m;
+  const LayerW& lw = g.lw;
+  if (!(lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE))) return;
+  const int bd = 4 + 8 * ps.bounce;
+  double ul = lw_qmc_s(S, bd + 2, ps.index), vl = lw_qmc_s(S, bd + 3, ps.index);
+  v3 wi = mk3(0.0, 0.0, 0.0), Le = mk3(0.0, 0.0, 0.0);
+  double pl = 0.0, tmax_sh = INFINITY;
+  bool ok = false;
+  if (S.env_kind != LW_ENV_NONE && ul < S.p_env) {
+    double ue = S.nemit > 0 ? ul / S.p_env : ul;
+    if (S.env_kind == LW_ENV_CONSTANT) {
+      double z = 1.0 - 2.0 * ue;
+      double r2 = 1.0 - z * z;
+      double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
+      lw_sincos2pi(vl, &sp, &cp);
+      wi = mk3(r * cp, z, r * sp);
+      pl = S.p_env * LW_INV_FOUR_PI;
+      Le = mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
+      ok = true;
+    } else {
+      double ur;
+      long long nt = (long long)S.env_w * S.env_h;
+      long long j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
+      long long row = j / S.env_w, col = j % S.env_w;
+      double uu = ((double)col + ur) / (double)S.env_w;
+      double vv2 = ((double)row + vl) / (double)S.env_h;
+      double st, ct, sp, cp;
+      lw_sincos2pi(vv2 * 0.5, &st, &ct);
+      lw_sincos2pi(uu, &sp, &cp);
+      wi = mk3(st * cp, ct, st * sp);
+      if (st > 0.0) {
+        pl = S.p_env * __ldg(S.env_pdf + j) * (double)nt / (LW_TWO_PI_SQ * st);
+        const float* px = S.env_img + 3 * j;
+        Le = mk3((double)__ldg(px) * S.env_scale, (double)__ldg(px + 1) * S.env_scale,
+                 (double)__ldg(px + 2) * S.env_scale);
+        ok = true;
+      }
+    }
+  } else if (S.nemit > 0) {
+    double ut = S.env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
+    double ur;
+    long long le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
+    const double* lv = S.verts + 9 * S.emit_tri[le];
+    v3 l0 = lw_ld3(lv), l1 = lw_ld3(lv + 3), l2 = lw_ld3(lv + 6);
+    double su = sqrt(ur);
+    double b0 = 1.0 - su, b1 = vl * su;
+    double b2 = (1.0 - b0) - b1;
+    v3 q = bary3(l0, l1, l2, b0, b1, b2);
+    v3 dl = q - g.p;
+    double dist2 = dot3(dl, dl);
+    double dist = sqrt(dist2);
+    double inv_dist = 1.0 / dist;
+    wi = mk3(dl.x * inv_dist, dl.y * inv_dist, dl.z * inv_dist);
+    v3 ngl = normalize3(cross3(l1 - l0, l2 - l0));
+    double cos_l = -dot3(ngl, wi);
+    if (S.emit_two[le]) cos_l = fabs(cos_l);
+    if (cos_l > 0.0 && dist > 0.0) {
+      pl = (S.p_tri * S.emit_pdf[le] / S.emit_area[le]) * dist2 / cos_l;
+      Le = lw_ld3(S.emit_rad + 3 * le);
+      tmax_sh = dist * (1.0 - 1e-7);
+      ok = true;
+    }
+  }
+  if (ok && pl > 0.0 && dot3(g.ngf, wi) > 0.0) {
+    v3 wil = lw_to_local(g.fr, wi);
+    double pb;
+    v3 f = lw_bsdf_eval(m, lw, g.wol, wil, pb);
+    if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
+      double wm = pl / (pl + pb);
+      double k = (wil.z * wm) / pl;
+      sh.contrib = mk3(ps.beta.x * f.x * Le.x * k, ps.beta.y * f.y * Le.y * k, ps.beta.z * f.z * Le.z * k);
+      sh.o = lw_offset_origin(g.p, g.ngf, wi);
+      sh.d = wi;
+      sh.tmax = tmax_sh;
+      sh.valid = 1;
+    }
+  }
+}
+
+// miss / emission part: returns false if the path ends before any scattering
+__device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& ps, const LwHit& h, ShadeGeom& g,
+                                                  double& w) {
   v3 d = ps.d;
   if (h.tri < 0) {
     if (S.env_kind != LW_ENV_NONE) {
       double pe;
       v3 Le = lw_env_eval(S, d, pe);
-      double w = ps.spec_prev ? 1.0 : ps.pdf_prev / (ps.pdf_prev + pe);
-      ps.L = ps.L + mk3(ps.beta.x * Le.x * w, ps.beta.y * Le.y * w, ps.beta.z * Le.z * w);
+      double wm = ps.spec_prev ? 1.0 : ps.pdf_prev / (ps.pdf_prev + pe);
+      ps.L = ps.L + mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
     }
     return false;
   }
-  const double* vv = S.verts + 9 * h.tri;
-  v3 v0 = lw_ld3(vv), v1 = lw_ld3(vv + 3), v2 = lw_ld3(vv + 6);
-  double w = (1.0 - h.bu) - h.bv;
-  v3 p = bary3(v0, v1, v2, w, h.bu, h.bv);
-  v3 e1 = v1 - v0, e2 = v2 - v0;
-  v3 ng = normalize3(cross3(e1, e2));
-  bool front = dot3(ng, d) < 0.0;
+  lw_shade_hit(S, d, h, g, w);
   int e = S.emit_of_tri[h.tri];
-  if (e >= 0 && S.nemit > 0 && (front || S.emit_two[e])) {
+  if (e >= 0 && S.nemit > 0 && (g.front || S.emit_two[e])) {
     v3 Le = lw_ld3(S.emit_rad + 3 * e);
     double wm = 1.0;
     if (!ps.spec_prev) {
-      double cos_l = fabs(dot3(ng, d));
+      double cos_l = fabs(dot3(g.ng, d));
       double pdf_area = S.p_tri * S.emit_pdf[e] / S.emit_area[e];
       double pl = pdf_area * (h.t * h.t) / cos_l;
       wm = ps.pdf_prev / (ps.pdf_prev + pl);
     }
     ps.L = ps.L + mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
   }
-  if (b == S.max_depth - 1) return false;
-  const double* nn = S.normals + 9 * h.tri;
-  v3 ns = bary3(lw_ld3(nn), lw_ld3(nn + 3), lw_ld3(nn + 6), w, h.bu, h.bv);
-  double nl = dot3(ns, ns);
-  ns = nl > 0.0 ? ns * (1.0 / sqrt(nl)) : ng;
-  v3 wo = neg3(d);
-  v3 ngf = front ? ng : neg3(ng);
-  if (dot3(ns, ngf) < 0.0) ns = neg3(ns);
-  if (dot3(ns, wo) <= 0.0) ns = ngf;
-  LwFrame fr = lw_make_frame(ns);
-  v3 wol = lw_to_local(fr, wo);
-  const lw_material& m = S.materials[S.material[h.tri]];  // read in place (no local-memory copy)
-  LayerW lw;
-  lw_layer_weights(m, wol.z, lw);
+  return ps.bounce != S.max_depth - 1;
+}
+
+// BSDF sampling, Russian roulette and the next ray; returns true if the path continues
+__device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& ps, const ShadeGeom& g) {
+  const int b = ps.bounce;
   const int bd = 4 + 8 * b;
-  const long long index = ps.index;
-  if (lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE)) {
-    double ul = lw_qmc_s(S, bd + 2, index), vl = lw_qmc_s(S, bd + 3, index);
-    v3 wi = mk3(0.0, 0.0, 0.0), Le = mk3(0.0, 0.0, 0.0);
-    double pl = 0.0, tmax_sh = INFINITY;
-    bool ok = false;
-    if (S.env_kind != LW_ENV_NONE && ul < S.p_env) {
-      double ue = S.nemit > 0 ? ul / S.p_env : ul;
-      if (S.env_kind == LW_ENV_CONSTANT) {
-        double z = 1.0 - 2.0 * ue;
-        double r2 = 1.0 - z * z;
-        double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
-        lw_sincos2pi(vl, &sp, &cp);
-        wi = mk3(r * cp, z, r * sp);
-        pl = S.p_env * LW_INV_FOUR_PI;
-        Le = mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
-        ok = true;
-      } else {
-        double ur;
-        long long nt = (long long)S.env_w * S.env_h;
-        long long j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
-        long long row = j / S.env_w, col = j % S.env_w;
-        double uu = ((double)col + ur) / (double)S.env_w;
-        double vv2 = ((double)row + vl) / (double)S.env_h;
-        double st, ct, sp, cp;
-        lw_sincos2pi(vv2 * 0.5, &st, &ct);
-        lw_sincos2pi(uu, &sp, &cp);
-        wi = mk3(st * cp, ct, st * sp);
-        if (st > 0.0) {
-          pl = S.p_env * __ldg(S.env_pdf + j) * (double)nt / (LW_TWO_PI_SQ * st);
-          const float* px = S.env_img + 3 * j;
-          Le = mk3((double)__ldg(px) * S.env_scale, (double)__ldg(px + 1) * S.env_scale,
-                   (double)__ldg(px + 2) * S.env_scale);
-          ok = true;
-        }
-      }
-    } else if (S.nemit > 0) {
-      double ut = S.env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
-      double ur;
-      long long le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
-      const double* lv = S.verts + 9 * S.emit_tri[le];
-      v3 l0 = lw_ld3(lv), l1 = lw_ld3(lv + 3), l2 = lw_ld3(lv + 6);
-      double su = sqrt(ur);
-      double b0 = 1.0 - su, b1 = vl * su;
-      double b2 = (1.0 - b0) - b1;
-      v3 q = bary3(l0, l1, l2, b0, b1, b2);
-      v3 dl = q - p;
-      double dist2 = dot3(dl, dl);
-      double dist = sqrt(dist2);
-      double inv_dist = 1.0 / dist;
-      wi = mk3(dl.x * inv_dist, dl.y * inv_dist, dl.z * inv_dist);
-      v3 ngl = normalize3(cross3(l1 - l0, l2 - l0));
-      double cos_l = -dot3(ngl, wi);
-      if (S.emit_two[le]) cos_l = fabs(cos_l);
-      if (cos_l > 0.0 && dist > 0.0) {
-        pl = (S.p_tri * S.emit_pdf[le] / S.emit_area[le]) * dist2 / cos_l;
-        Le = lw_ld3(S.emit_rad + 3 * le);
-        tmax_sh = dist * (1.0 - 1e-7);
-        ok = true;
-      }
-    }
-    if (ok && pl > 0.0 && dot3(ngf, wi) > 0.0) {
-      v3 wil = lw_to_local(fr, wi);
-      double pb;
-      v3 f = lw_bsdf_eval(m, lw, wol, wil, pb);
-      if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
-        double wm = pl / (pl + pb);
-        double k = (wil.z * wm) / pl;
-        sh.contrib = mk3(ps.beta.x * f.x * Le.x * k, ps.beta.y * f.y * Le.y * k, ps.beta.z * f.z * Le.z * k);
-        sh.o = lw_offset_origin(p, ngf, wi);
-        sh.d = wi;
-        sh.tmax = tmax_sh;
-        sh.valid = 1;
-      }
-    }
-  }
   BSample bs;
-  double ub = lw_qmc_s(S, bd + 0, index), vb = lw_qmc_s(S, bd + 1, index);
-  if (!lw_bsdf_sample(m, lw, wol, front, ub, vb, bs)) return false;
-  v3 wi = lw_to_world(fr, bs.wi);
-  double gside = dot3(ngf, wi);
+  double ub = lw_qmc_s(S, bd + 0, ps.index), vb = lw_qmc_s(S, bd + 1, ps.index);
+  if (!lw_bsdf_sample(*g.m, g.lw, g.wol, g.front, ub, vb, bs)) return false;
+  v3 wi = lw_to_world(g.fr, bs.wi);
+  double gside = dot3(g.ngf, wi);
   if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) return false;
   ps.beta = mk3(ps.beta.x * bs.weight.x, ps.beta.y * bs.weight.y, ps.beta.z * bs.weight.z);
   ps.spec_prev = bs.delta;
@@ -477,15 +505,26 @@ __device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, 
     if (ps.beta.y > q) q = ps.beta.y;
     if (ps.beta.z > q) q = ps.beta.z;
     if (q > 1.0) q = 1.0;
-    double ur = lw_qmc_s(S, bd + 4, index);
+    double ur = lw_qmc_s(S, bd + 4, ps.index);
     if (!(ur < q)) return false;
     double inv_q = 1.0 / q;
     ps.beta = mk3(ps.beta.x * inv_q, ps.beta.y * inv_q, ps.beta.z * inv_q);
   }
-  ps.o = lw_offset_origin(p, ngf, wi);
+  ps.o = lw_offset_origin(g.p, g.ngf, wi);
   ps.d = wi;
   ps.bounce = b + 1;
   return true;
+}
+
+// whole stage in the oracle's order (megakernel): emission, NEE, BSDF sampling
+__device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, const LwHit& h, ShadowRay& sh) {
+  sh.valid = 0;
+  ShadeGeom g;
+  double w;
+  if (!lw_shade_emission(S, ps, h, g, w)) return false;
+  lw_shade_frame(S, ps.d, h, w, g);
+  lw_shade_nee(S, ps, g, sh);
+  return lw_shade_material(S, ps, g);
 }
 
 // fixed-point accumulation (oracle accumulate); returns 1 if a channel was non-finite

@@ -28,7 +28,10 @@ using namespace lw;
 #define LW_TRACE_MINB 8
 #endif
 #ifndef LW_SHADE_MINB
-#define LW_SHADE_MINB 1
+#define LW_SHADE_MINB 4
+#endif
+#ifndef LW_NEE_MINB
+#define LW_NEE_MINB 4
 #endif
 
 namespace {
@@ -453,9 +456,18 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
   }
 }
 
-__global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt) {
+__device__ __forceinline__ void load_hit(const Pool& P, int s, LwHit& h) {
+  double2 h0 = P.hit0[s], h1 = P.hit1[s];
+  h.t = h0.x;
+  h.bu = h0.y;
+  h.bv = h1.x;
+  h.tri = __double_as_longlong(h1.y);
+}
+
+// NEE half of the material stage (runs before k_shade so it sees the incoming throughput):
+// light / environment sample, BSDF evaluation, shadow-ray setup
+__global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt) {
   int n = cnt->n_ext;
-  unsigned long long alive_count = 0;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
     bool valid = k < n;
@@ -463,30 +475,62 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
     bool shadow = false;
     if (valid) {
       s = P.q_ext[k];
-      PathState ps;
-      load_state(P, s, ps);
       LwHit h;
-      double2 h0 = P.hit0[s], h1 = P.hit1[s];
-      h.t = h0.x;
-      h.bu = h0.y;
-      h.bv = h1.x;
-      h.tri = __double_as_longlong(h1.y);
-      ShadowRay sh;
-      bool alive = lw_path_shade(S, ps, h, sh);
-      shadow = sh.valid != 0;
-      store_state(P, s, ps);
-      P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
-      alive_count += alive ? 1 : 0;
-      if (shadow) {
-        P.sh0[s] = make_double2(sh.o.x, sh.o.y);
-        P.sh1[s] = make_double2(sh.o.z, sh.d.x);
-        P.sh2[s] = make_double2(sh.d.y, sh.d.z);
-        P.sh3[s] = make_double2(sh.tmax, sh.contrib.x);
-        P.sh4[s] = make_double2(sh.contrib.y, sh.contrib.z);
+      load_hit(P, s, h);
+      int f = P.flags[s];
+      int bounce = f & F_BOUNCE;
+      if (h.tri >= 0 && bounce != S.max_depth - 1) {
+        PathState ps;
+        double2 a = P.ray1[s], c = P.ray2[s];
+        ps.d = mk3(a.y, c.x, c.y);
+        double2 t0 = P.tp0[s], t1 = P.tp1[s];
+        ps.beta = mk3(t0.x, t0.y, t1.x);
+        ps.index = __double_as_longlong(P.misc[s].y);
+        ps.bounce = bounce;
+        ShadeGeom g;
+        double w;
+        lw_shade_hit(S, ps.d, h, g, w);
+        lw_shade_frame(S, ps.d, h, w, g);
+        ShadowRay sh;
+        lw_shade_nee(S, ps, g, sh);
+        shadow = sh.valid != 0;
+        if (shadow) {
+          P.sh0[s] = make_double2(sh.o.x, sh.o.y);
+          P.sh1[s] = make_double2(sh.o.z, sh.d.x);
+          P.sh2[s] = make_double2(sh.d.y, sh.d.z);
+          P.sh3[s] = make_double2(sh.tmax, sh.contrib.x);
+          P.sh4[s] = make_double2(sh.contrib.y, sh.contrib.z);
+        }
       }
     }
     int q = warp_push(&cnt->n_shadow, valid && shadow);
     if (q >= 0) P.q_shadow[q] = s;
+  }
+}
+
+// material half: miss/emission (MIS), BSDF sampling, Russian roulette, next ray, stage tag
+__global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt) {
+  int n = cnt->n_ext;
+  unsigned long long alive_count = 0;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    int k = base + threadIdx.x;
+    if (k < n) {
+      int s = P.q_ext[k];
+      PathState ps;
+      load_state(P, s, ps);
+      LwHit h;
+      load_hit(P, s, h);
+      ShadeGeom g;
+      double w;
+      bool alive = false;
+      if (lw_shade_emission(S, ps, h, g, w)) {
+        lw_shade_frame(S, ps.d, h, w, g);
+        alive = lw_shade_material(S, ps, g);
+      }
+      store_state(P, s, ps);
+      P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
+      alive_count += alive ? 1 : 0;
+    }
   }
   warp_add(&cnt->n_alive_ull, alive_count);
 }
@@ -685,6 +729,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
         else
           k_trace_ext<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         if (timed) cudaEventRecord(event(), st);
+        k_shade_nee<<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
         k_shade<<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
         if (timed) {
           marks.push_back({ev, 1});
@@ -696,7 +741,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           k_trace_shadow<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         if (timed) cudaEventRecord(event(), st);
         k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
-        launches += 6;
+        launches += 7;
         waves++;
       }
       LW_CUDA_TRY(cudaGetLastError());

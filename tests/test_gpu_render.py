@@ -190,3 +190,31 @@ def test_nee_and_bsdf_agree_single_light(gpu):
         r.render_pass(64, 128)
         b = r.image().astype(np.float64)
     assert abs(a.mean() - b.mean()) / a.mean() < 0.03
+
+
+@pytest.mark.parametrize("n", [1, 5, 8, 100, 4097, 70000])
+def test_gpu_sah_tree_traversal_matches_oracle(gpu, oracle, n):
+    """The device-built SAH tree and the oracle's sequential restatement give identical hits on
+    soups that exercise small-segment, large-segment and coincident-centroid paths."""
+    sc = scenes.soup(n, n_materials=1, seed=n)
+    if n == 4097:  # coincident centroids force the halving rule
+        m = sc.meshes[0]
+        m.positions[: len(m.positions) // 2] = m.positions[0]
+    packed = pack_scene(sc, bvh="sah")
+    o, d = _random_rays(20000, np.zeros(3), np.full(3, 20.0), n)
+    with _renderer(packed, 8, 8, 2) as r:
+        t, tri, b = r.trace_closest(o, d)
+    t2, tri2, b2 = oracle.OracleScene(packed).trace_closest(o, d)
+    assert np.array_equal(tri, tri2) and np.array_equal(_bits(t), _bits(t2)) and np.array_equal(_bits(b), _bits(b2))
+
+
+def test_cli_render_writes_snapshots(gpu, tmp_path):
+    from paper_1705_01263_b200 import cli
+    from paper_1705_01263_b200.imagefiles import read_pfm
+
+    out = str(tmp_path / "c1")
+    assert cli.main(["render", "--config", "C1", "--res", "32x32", "--iterations", "4", "--snapshot-every", "2",
+                     "--out", out, "--metrics", str(tmp_path / "m.json")]) == 0
+    img = read_pfm(out + "_000004.pfm")
+    assert img.shape == (32, 32, 3) and img.sum() > 0
+    assert cli.main(["render", "--config", "C1", "--res", "bad"]) == 3
