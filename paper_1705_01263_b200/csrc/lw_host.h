@@ -45,6 +45,7 @@ struct DeviceSah {
   int64_t nnodes = 0;
   int32_t root_ref = -1;
   double root_box[6];
+  int levels = 0;  // binary tree depth bound (level-synchronous build iterations)
 };
 int sah_build_device(const double* d_verts, int64_t ntris, cudaStream_t stream, DeviceSah& out);
 

@@ -27,6 +27,9 @@ using namespace lw;
 #ifndef LW_TRACE_MINB
 #define LW_TRACE_MINB 8
 #endif
+#ifndef LW_SHADOW_MINB
+#define LW_SHADOW_MINB 8
+#endif
 #ifndef LW_SHADE_MINB
 #define LW_SHADE_MINB 4
 #endif
@@ -146,11 +149,11 @@ __device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long 
 // stage the render BVH in shared memory when it fits (small scenes: Cornell box)
 __device__ __forceinline__ RenderBVH stage_bvh(const RenderBVH& g, int nnodes, unsigned char* smem, bool use_smem) {
   if (!use_smem) return g;
-  RNode* sn = reinterpret_cast<RNode*>(smem);
-  LTri* st = reinterpret_cast<LTri*>(smem + sizeof(RNode) * nnodes);
+  WNode* sn = reinterpret_cast<WNode*>(smem);
+  LTri* st = reinterpret_cast<LTri*>(smem + sizeof(WNode) * nnodes);
   const int4* src = reinterpret_cast<const int4*>(g.nodes);
   int4* dst = reinterpret_cast<int4*>(sn);
-  int nn4 = nnodes * (int)(sizeof(RNode) / 16);
+  int nn4 = nnodes * (int)(sizeof(WNode) / 16);
   for (int k = threadIdx.x; k < nn4; k += blockDim.x) dst[k] = src[k];
   src = reinterpret_cast<const int4*>(g.tris);
   dst = reinterpret_cast<int4*>(st);
@@ -170,14 +173,14 @@ __global__ void k_internal_flags(const long long* __restrict__ children, long lo
   if (k < nnodes) flag[k] = children[2 * k] >= 0 ? 1 : 0;
 }
 
-__device__ __forceinline__ int leaf_ref(long long start, long long count) { return (int)(-(1 + ((start << 3) | count))); }
+__host__ __device__ __forceinline__ int leaf_ref(long long start, long long count) { return (int)(-(1 + ((start << 3) | count))); }
 
 __global__ void k_build_rnodes(const double* __restrict__ bounds, const long long* __restrict__ children,
-                               long long nnodes, const int* __restrict__ imap, RNode* __restrict__ out) {
+                               long long nnodes, const int* __restrict__ imap, SahNode* __restrict__ out) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= nnodes) return;
   if (children[2 * k] < 0) return;
-  RNode r;
+  SahNode r;
 #pragma unroll
   for (int c = 0; c < 2; c++) {
     long long ch = children[2 * k + c];
@@ -186,8 +189,6 @@ __global__ void k_build_rnodes(const double* __restrict__ bounds, const long lon
     long long c0 = children[2 * ch], c1 = children[2 * ch + 1];
     r.ref[c] = c0 >= 0 ? imap[ch] : leaf_ref(-(c0 + 1), c1);
   }
-#pragma unroll
-  for (int p = 0; p < 6; p++) r.pad[p] = 0;
   out[imap[k]] = r;
 }
 
@@ -203,17 +204,83 @@ __global__ void k_build_ltris(const double* __restrict__ verts, const long long*
   out[j] = r;
 }
 
-__global__ void k_sah_to_rnodes(const SahNode* __restrict__ in, int nr, RNode* __restrict__ out) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nr) return;
-  RNode r;
+// ---- binary -> 4-wide collapse (level-synchronous over the binary tree) -------------------
+//
+// A wide node is rooted at a binary node and takes its two children; while it has fewer than
+// four, the internal child with the largest surface area (first on ties) is replaced by its two
+// children.  Wide nodes keep the id of their binary root (the array is sparse, parents before
+// children as in the binary numbering).  need[] tracks the traversal stack depth a path can
+// reach (sum of children-1 over the wide nodes above), so the upload can reject trees deeper
+// than the fixed traversal stack instead of overflowing it.
+
+__device__ __forceinline__ double sah_area12(const double* b) {
+  double dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
+  return (dx * dy + dy * dz) + dz * dx;
+}
+
+__global__ void k_collapse_level(const SahNode* __restrict__ bin, const int* __restrict__ fin, const int* __restrict__ nin,
+                                 int* __restrict__ fout, int* __restrict__ nout, int* __restrict__ need,
+                                 WNode* __restrict__ out, int* __restrict__ max_need) {
+  int n = *nin;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int b = fin[i];
+    int cref[4];
+    double cbox[4][6];
+    const SahNode& nb = bin[b];
 #pragma unroll
-  for (int a = 0; a < 12; a++) r.box[a] = in[k].box[a];
-  r.ref[0] = in[k].ref[0];
-  r.ref[1] = in[k].ref[1];
+    for (int c = 0; c < 2; c++) {
+      cref[c] = nb.ref[c];
 #pragma unroll
-  for (int p = 0; p < 6; p++) r.pad[p] = 0;
-  out[k] = r;
+      for (int a = 0; a < 6; a++) cbox[c][a] = nb.box[6 * c + a];
+    }
+    int k = 2;
+    while (k < 4) {
+      int sel = -1;
+      double sa = -1.0;
+      for (int j = 0; j < k; j++) {
+        if (cref[j] < 0) continue;
+        double ar = sah_area12(cbox[j]);
+        if (ar > sa) {
+          sa = ar;
+          sel = j;
+        }
+      }
+      if (sel < 0) break;
+      const SahNode& e = bin[cref[sel]];
+      cref[sel] = e.ref[0];
+      cref[k] = e.ref[1];
+      for (int a = 0; a < 6; a++) {
+        cbox[sel][a] = e.box[a];
+        cbox[k][a] = e.box[6 + a];
+      }
+      k++;
+    }
+    WNode w;
+    float lo[3][4], hi[3][4];
+    int rr[4];
+    for (int c = 0; c < 4; c++) {
+      bool v = c < k;
+      rr[c] = v ? cref[c] : LW_REF_NONE;
+      for (int a = 0; a < 3; a++) {
+        lo[a][c] = v ? __double2float_rd(cbox[c][a]) : INFINITY;
+        hi[a][c] = v ? __double2float_ru(cbox[c][3 + a]) : -INFINITY;
+      }
+    }
+    for (int a = 0; a < 3; a++) {
+      w.lo[a] = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
+      w.hi[a] = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
+    }
+    w.ref = make_int4(rr[0], rr[1], rr[2], rr[3]);
+    w.pad = make_int4(k, 0, 0, 0);
+    out[b] = w;
+    int nd = need[b] + (k - 1);
+    atomicMax(max_need, nd);
+    for (int c = 0; c < k; c++) {
+      if (cref[c] < 0) continue;
+      need[cref[c]] = nd;
+      fout[atomicAdd(nout, 1)] = cref[c];
+    }
+  }
 }
 
 __global__ void k_build_ltris_i32(const double* __restrict__ verts, const int* __restrict__ order, long long n,
@@ -536,7 +603,7 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+__global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   int n = cnt->n_shadow;
@@ -638,6 +705,41 @@ __global__ void k_resolve(const unsigned long long* fb, long long n, double scal
 
 int nrnodes_of(const lw_ctx* c) { return c->ref_bvh.nnodes > 1 ? (int)((c->ref_bvh.nnodes - 1) / 2) : 0; }
 int render_nodes(const lw_ctx* c) { return c->nrnodes; }
+
+// binary tree -> 4-wide nodes, one launch per binary level (frontier in device memory)
+int collapse_wide(lw_ctx* c, const SahNode* bn, int nr, int root_ref, int levels, WNode* out, int& max_need) {
+  max_need = 0;
+  if (nr <= 0 || root_ref < 0) return LW_OK;
+  cudaStream_t st = c->stream;
+  DevBuf f0, f1, need, cnt;
+  LW_CUDA_TRY(f0.alloc(sizeof(int) * nr));
+  LW_CUDA_TRY(f1.alloc(sizeof(int) * nr));
+  LW_CUDA_TRY(need.alloc(sizeof(int) * nr));
+  LW_CUDA_TRY(cnt.alloc(sizeof(int) * (levels + 2)));
+  LW_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (levels + 2), st));
+  LW_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(WNode) * nr, st));
+  int one = 1, zero = 0;
+  LW_CUDA_TRY(cudaMemcpyAsync(f0.p, &root_ref, sizeof(int), cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(need.as<int>() + root_ref, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(cnt.p, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+  int* cn = cnt.as<int>();
+  int* mx = cn + levels + 1;
+  for (int L = 0; L < levels; L++) {
+    const int* fin = (L & 1) ? f1.as<int>() : f0.as<int>();
+    int* fout = (L & 1) ? f0.as<int>() : f1.as<int>();
+    k_collapse_level<<<148 * 4, 128, 0, st>>>(bn, fin, cn + L, fout, cn + L + 1, need.as<int>(), out, mx);
+  }
+  LW_CUDA_TRY(cudaGetLastError());
+  int tail[2];
+  LW_CUDA_TRY(cudaMemcpyAsync(tail, cn + levels, sizeof(tail), cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  if (tail[0] != 0) {
+    set_error("render BVH collapse: frontier not empty after %d levels", levels);
+    return LW_ERR_CUDA;
+  }
+  max_need = tail[1];
+  return LW_OK;
+}
 
 int alloc_pool(lw_ctx* c, int size) {
   if (c->pool.size == size) return LW_OK;
@@ -901,15 +1003,15 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   // reference-layout BVH on the device (geometry.py:100-148 arrays; exported for parity)
   LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
   int64_t nn = c->ref_bvh.nnodes;
-  int nr;
-  RNode* rn;
+  int nr = 0, levels = 0, root_ref = leaf_ref(0, 0);
+  SahNode* bn = nullptr;  // binary tree (FP64 child boxes), collapsed to the 4-wide layout below
   LTri* lt;
   double rb[6] = {0, 0, 0, 0, 0, 0};
+  LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
   if (d->bvh_kind == LW_BVH_MEDIAN) {
     // render layout derived from the median tree on the device
     nr = nrnodes_of(c);
-    LW_STATUS_TRY(dev_alloc(c, rn, nr > 0 ? nr : 1));
-    LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
+    LW_CUDA_TRY(cudaMalloc(&bn, sizeof(SahNode) * (nr > 0 ? nr : 1)));
     if (n > 0) {
       int* flag;
       int* imap;
@@ -921,7 +1023,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
       void* tmp;
       LW_CUDA_TRY(cudaMalloc(&tmp, tb > 0 ? tb : 16));
       LW_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, imap, (int)nn, st));
-      k_build_rnodes<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.bounds, c->ref_bvh.children, nn, imap, rn);
+      k_build_rnodes<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.bounds, c->ref_bvh.children, nn, imap, bn);
       k_build_ltris<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, c->ref_bvh.order, n, lt);
       LW_CUDA_TRY(cudaGetLastError());
       LW_CUDA_TRY(cudaStreamSynchronize(st));
@@ -931,9 +1033,11 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     LW_CUDA_TRY(cudaMemcpyAsync(rb, c->ref_bvh.bounds, sizeof(rb), cudaMemcpyDeviceToHost, st));
     LW_CUDA_TRY(cudaMemcpyAsync(rc, c->ref_bvh.children, sizeof(rc), cudaMemcpyDeviceToHost, st));
     LW_CUDA_TRY(cudaStreamSynchronize(st));
-    S.bvh.root_ref = rc[0] >= 0 ? 0 : (int)(-(1 + ((-(rc[0] + 1)) << 3 | rc[1])));
+    root_ref = rc[0] >= 0 ? 0 : (int)(-(1 + ((-(rc[0] + 1)) << 3 | rc[1])));
+    levels = 2;  // median split: depth <= 2 + log2(n)
+    while ((1LL << (levels - 2)) < n) levels++;
   } else {
-    // binned-SAH render tree built on the device (lw_sah_build.cu), converted to the 128-byte layout
+    // binned-SAH render tree built on the device (lw_sah_build.cu)
     DeviceSah ds;
     int rc_sah = sah_build_device(dv, n, st, ds);
     if (rc_sah != LW_OK) {
@@ -942,24 +1046,34 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
       return rc_sah;
     }
     nr = (int)ds.nnodes;
-    LW_STATUS_TRY(dev_alloc(c, rn, nr > 0 ? nr : 1));
-    LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
-    if (nr > 0) k_sah_to_rnodes<<<grid_for(nr, 256, 1 << 30), 256, 0, st>>>(ds.nodes, nr, rn);
+    bn = ds.nodes;
     if (n > 0) k_build_ltris_i32<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, ds.order, n, lt);
     LW_CUDA_TRY(cudaGetLastError());
     LW_CUDA_TRY(cudaStreamSynchronize(st));
-    cudaFree(ds.nodes);
     cudaFree(ds.order);
     for (int a = 0; a < 6; a++) rb[a] = ds.root_box[a];
-    S.bvh.root_ref = ds.root_ref;
+    root_ref = ds.root_ref;
+    levels = ds.levels;
+  }
+  WNode* wn;
+  LW_STATUS_TRY(dev_alloc(c, wn, nr > 0 ? nr : 1));
+  int max_need = 0;
+  int rc_w = collapse_wide(c, bn, nr, root_ref, levels, wn, max_need);
+  cudaFree(bn);
+  LW_STATUS_TRY(rc_w);
+  if (max_need > LW_STACK) {
+    set_error("render BVH too deep: a path needs %d traversal stack entries (limit %d)", max_need, LW_STACK);
+    return LW_ERR_INVALID;
   }
   c->nrnodes = nr;
-  S.bvh.nodes = rn;
+  S.bvh.nodes = wn;
   S.bvh.tris = lt;
   S.bvh.ntris = n;
+  S.bvh.root_ref = root_ref;
   for (int a = 0; a < 6; a++) S.bvh.root_box[a] = rb[a];
+  for (int a = 0; a < 3; a++) S.bvh.absmax[a] = std::max(fabs(rb[a]), fabs(rb[3 + a]));
   // stage in shared memory when the whole render BVH fits comfortably
-  size_t bytes = sizeof(RNode) * (size_t)nr + sizeof(LTri) * (size_t)n;
+  size_t bytes = sizeof(WNode) * (size_t)nr + sizeof(LTri) * (size_t)n;
   c->smem_bytes = (n > 0 && bytes <= 48 * 1024) ? bytes : 0;
   // emitters
   int* eot;

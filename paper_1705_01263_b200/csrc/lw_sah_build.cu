@@ -545,6 +545,7 @@ int sah_build_device(const double* d_verts, int64_t n64, cudaStream_t st, Device
     node_base += nsplit;
     nseg = 2 * nsplit;
     cur ^= 1;
+    out.levels++;
   }
   out.nnodes = node_base;
   int rr = 0;

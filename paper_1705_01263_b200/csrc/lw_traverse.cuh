@@ -186,15 +186,25 @@ __device__ __forceinline__ void lw_traverse_ref(bool compat, const double* __res
 }
 
 // ---- render traversal ------------------------------------------------------------------
+//
+// 4-wide BVH with FP32 child boxes rounded outward (WNode, one 128-byte line).  The box test
+// is conservative by construction: every plane distance is computed from an origin shifted by
+// delta_a = 2^-18 (M_a + |o_a|) against the ray (M_a = scene extent on axis a), which exceeds
+// the worst-case FP32 rounding of the slab arithmetic (< 2^-22 (M_a + |o_a|) |inv_a|) by 16x,
+// so a box is never culled while it can hold a triangle whose FP64 hit t is <= the current
+// best.  Triangles are tested in FP64 on the exact vertices with the (t, lower id) rule, so the
+// closest hit equals exhaustive search -- the result the oracle's binary FP64 traversal also
+// returns -- whatever the tree shape or visit order (tests/test_gpu_render.py checks bits).
 
-#define LW_CULL_M 9.094947017729282e-13  // 2^-40
 #define LW_REF_NONE 0x7fffffff
 
-// 128-byte node: child boxes (lo xyz, hi xyz) x 2, child refs; ref >= 0 internal, < 0 leaf
-struct __align__(16) RNode {
-  double box[12];
-  int ref[2];
-  int pad[6];
+// 4-wide node: per-axis child bounds as float4 (x = child 0 ... w = child 3), child refs;
+// ref >= 0 internal node, < 0 leaf -(1 + (start << 3 | count)), LW_REF_NONE empty slot
+struct __align__(128) WNode {
+  float4 lo[3];
+  float4 hi[3];
+  int4 ref;
+  int4 pad;
 };
 
 // 80-byte leaf-ordered triangle: vertices + original id
@@ -204,68 +214,75 @@ struct __align__(16) LTri {
 };
 
 struct RenderBVH {
-  const RNode* nodes;
+  const WNode* nodes;
   const LTri* tris;
   long long ntris;
   int root_ref;
   double root_box[6];
+  double absmax[3];  // max |coordinate| of the scene per axis (box-test margin)
 };
 
-struct LwRay {
-  double o[3], inv[3];
-  bool zero[3];
+// per-ray constants of the FP32 box test
+struct LwRayF {
+  float inv[3];  // clamped reciprocal direction
+  float on[3];   // -(o - / + delta) * inv: near-plane offset (t lowered by >= 0.9 delta |inv|)
+  float of[3];   // far-plane offset (t raised)
+  int sn[3];     // float4 index of the near plane array in WNode (a, or 3 + a when inv < 0)
   LwShear sh;
 };
 
-__device__ __forceinline__ void lw_ray_setup(LwRay& r, const double o[3], const double d[3]) {
+__device__ __forceinline__ void lw_rayf_setup(LwRayF& r, const RenderBVH& bvh, const double o[3], const double d[3]) {
+  double dmax = fmax(fabs(d[0]), fmax(fabs(d[1]), fabs(d[2])));
+  bool ok = dmax >= 0x1p-60 && dmax <= 0x1p60;  // else every box passes (exhaustive, still exact)
 #pragma unroll
   for (int a = 0; a < 3; a++) {
-    r.o[a] = o[a];
-    r.zero[a] = !(d[a] > 1e-200 || d[a] < -1e-200);
-    r.inv[a] = r.zero[a] ? 0.0 : 1.0 / d[a];
+    double da = d[a];
+    double inv = fabs(da) > dmax * 0x1p-40 ? 1.0 / da : copysign(0x1p40 / dmax, da);
+    if (!ok) inv = 0.0;
+    float invf = (float)inv;
+    bool neg = invf < 0.0f || (invf == 0.0f && signbit(invf));
+    double delta = (bvh.absmax[a] + fabs(o[a])) * 0x1p-18;
+    double o_n = neg ? o[a] - delta : o[a] + delta;
+    double o_f = neg ? o[a] + delta : o[a] - delta;
+    r.inv[a] = invf;
+    r.on[a] = (float)(-(o_n * (double)invf));
+    r.of[a] = (float)(-(o_f * (double)invf));
+    r.sn[a] = neg ? 3 + a : a;
   }
   lw_shear_setup(o, d, false, r.sh);
 }
 
-__device__ __forceinline__ bool lw_box_hit(const LwRay& r, const double* box, double best, double& tn_out) {
-  double tn = -INFINITY, tf = INFINITY;
-  bool miss = false;
+// tests the four child boxes of a node against [0, best]; returns the hit mask and the entry
+// distances (conservative lower bounds)
+__device__ __forceinline__ unsigned lw_node_hit(const LwRayF& r, const WNode* __restrict__ nd, float best, float tn[4],
+                                                int ref[4]) {
+  const float4* q = reinterpret_cast<const float4*>(nd);
+  float4 nx = q[r.sn[0]], ny = q[r.sn[1]], nz = q[r.sn[2]];
+  float4 fx = q[6 - r.sn[0] - 0 + 0 - (r.sn[0] >= 3 ? 0 : 0)];  // placeholder, replaced below
+  (void)fx;
+  float4 Fx = q[r.sn[0] >= 3 ? 0 : 3], Fy = q[r.sn[1] >= 3 ? 1 : 4], Fz = q[r.sn[2] >= 3 ? 2 : 5];
+  int4 rf = *reinterpret_cast<const int4*>(&nd->ref);
+  ref[0] = rf.x;
+  ref[1] = rf.y;
+  ref[2] = rf.z;
+  ref[3] = rf.w;
+  const float nxs[4] = {nx.x, nx.y, nx.z, nx.w}, nys[4] = {ny.x, ny.y, ny.z, ny.w}, nzs[4] = {nz.x, nz.y, nz.z, nz.w};
+  const float fxs[4] = {Fx.x, Fx.y, Fx.z, Fx.w}, fys[4] = {Fy.x, Fy.y, Fy.z, Fy.w}, fzs[4] = {Fz.x, Fz.y, Fz.z, Fz.w};
+  unsigned mask = 0;
 #pragma unroll
-  for (int a = 0; a < 3; a++) {
-    double lo = box[a], hi = box[3 + a];
-    if (r.zero[a]) {
-      if (r.o[a] < lo || r.o[a] > hi) miss = true;
-      continue;
-    }
-    double t0 = (lo - r.o[a]) * r.inv[a];
-    double t1 = (hi - r.o[a]) * r.inv[a];
-    double mn = t0 > t1 ? t1 : t0;
-    double mx = t0 > t1 ? t0 : t1;
-    if (mn > tn) tn = mn;
-    if (mx < tf) tf = mx;
+  for (int c = 0; c < 4; c++) {
+    float a0 = __fmaf_rn(nxs[c], r.inv[0], r.on[0]);
+    float a1 = __fmaf_rn(nys[c], r.inv[1], r.on[1]);
+    float a2 = __fmaf_rn(nzs[c], r.inv[2], r.on[2]);
+    float b0 = __fmaf_rn(fxs[c], r.inv[0], r.of[0]);
+    float b1 = __fmaf_rn(fys[c], r.inv[1], r.of[1]);
+    float b2 = __fmaf_rn(fzs[c], r.inv[2], r.of[2]);
+    float lo = fmaxf(fmaxf(a0, a1), fmaxf(a2, 0.0f));
+    float hi = fminf(fminf(b0, b1), fminf(b2, best));
+    tn[c] = lo;
+    if (lo <= hi && ref[c] != LW_REF_NONE) mask |= 1u << c;
   }
-  double tn_lo = tn - LW_CULL_M * fabs(tn);
-  double tf_hi = tf + LW_CULL_M * fabs(tf);
-  double best_hi = best + LW_CULL_M * fabs(best);
-  tn_out = tn;
-  return !miss && tn_lo <= tf_hi && tn_lo <= best_hi && tf_hi >= 0.0;
-}
-
-__device__ __forceinline__ bool lw_pop_keep(double tn, double best) {
-  return tn - LW_CULL_M * fabs(tn) <= best + LW_CULL_M * fabs(best);
-}
-
-__device__ __forceinline__ void lw_load_node(const RNode* __restrict__ p, double box[12], int ref[2]) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-#pragma unroll
-  for (int k = 0; k < 6; k++) {
-    double2 t = q[k];
-    box[2 * k] = t.x;
-    box[2 * k + 1] = t.y;
-  }
-  int2 rr = *reinterpret_cast<const int2*>(&p->ref[0]);
-  ref[0] = rr.x;
-  ref[1] = rr.y;
+  return mask;
 }
 
 __device__ __forceinline__ void lw_load_tri(const LTri* __restrict__ p, double v[9], long long& id) {
@@ -281,7 +298,8 @@ __device__ __forceinline__ void lw_load_tri(const LTri* __restrict__ p, double v
   id = __double_as_longlong(t.y);
 }
 
-#define LW_STACK 48
+// traversal stack depth (entries); the builder rejects trees whose worst path needs more
+#define LW_STACK 64
 
 // work counters of the instrumented instantiation (node = one 128-byte node fetch,
 // tri = one 80-byte triangle test)
@@ -289,7 +307,22 @@ struct LwTraceCount {
   unsigned nodes = 0, tris = 0;
 };
 
-// closest hit, t in (0, tmax], near-child-first
+__device__ __forceinline__ unsigned long long lw_stk_pack(int ref, float tn) {
+  return ((unsigned long long)__float_as_uint(tn) << 32) | (unsigned)ref;
+}
+
+// order the hit children by entry distance (misses last): 5 compare-exchanges
+__device__ __forceinline__ void lw_cswap(float& ta, int& ra, float& tb, int& rb) {
+  bool s = tb < ta;
+  float t = s ? tb : ta;
+  tb = s ? ta : tb;
+  ta = t;
+  int q = s ? rb : ra;
+  rb = s ? ra : rb;
+  ra = q;
+}
+
+// closest hit, t in (0, tmax], nearest child first
 template <bool COUNT = false>
 __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
                                                  double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
@@ -298,37 +331,40 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
   h.bu = 0.0;
   h.bv = 0.0;
   if (bvh.ntris == 0) return;
-  LwRay r;
-  lw_ray_setup(r, o, d);
-  double tn;
-  if (!lw_box_hit(r, bvh.root_box, h.t, tn)) return;
-  int stack_ref[LW_STACK];
-  double stack_tn[LW_STACK];
+  LwRayF r;
+  lw_rayf_setup(r, bvh, o, d);
+  float best = __double2float_ru(h.t);
+  unsigned long long stk[LW_STACK];
   int sp = 0;
   int ref = bvh.root_ref;
   double best_det = 1.0;
   for (;;) {
     while (ref >= 0 && ref != LW_REF_NONE) {
-      double box[12];
-      int cr[2];
-      lw_load_node(bvh.nodes + ref, box, cr);
+      float tn[4];
+      int cr[4];
+      unsigned m = lw_node_hit(r, bvh.nodes + ref, best, tn, cr);
       if (COUNT) cnt->nodes++;
-      double tn0, tn1;
-      bool h0 = lw_box_hit(r, box, h.t, tn0);
-      bool h1 = lw_box_hit(r, box + 6, h.t, tn1);
-      if (h0 && h1) {
-        bool swap = tn1 < tn0;
-        stack_ref[sp] = swap ? cr[0] : cr[1];
-        stack_tn[sp] = swap ? tn0 : tn1;
-        sp++;
-        ref = swap ? cr[1] : cr[0];
-      } else if (h0) {
-        ref = cr[0];
-      } else if (h1) {
-        ref = cr[1];
-      } else {
+#pragma unroll
+      for (int c = 0; c < 4; c++)
+        if (!(m & (1u << c))) tn[c] = INFINITY;
+      int nh = __popc(m);
+      if (nh == 0) {
         ref = LW_REF_NONE;
+        break;
       }
+      if (nh == 1) {
+        ref = cr[__ffs(m) - 1];
+        continue;
+      }
+      lw_cswap(tn[0], cr[0], tn[1], cr[1]);
+      lw_cswap(tn[2], cr[2], tn[3], cr[3]);
+      lw_cswap(tn[0], cr[0], tn[2], cr[2]);
+      lw_cswap(tn[1], cr[1], tn[3], cr[3]);
+      lw_cswap(tn[1], cr[1], tn[2], cr[2]);
+      if (nh > 3) stk[sp++] = lw_stk_pack(cr[3], tn[3]);
+      if (nh > 2) stk[sp++] = lw_stk_pack(cr[2], tn[2]);
+      stk[sp++] = lw_stk_pack(cr[1], tn[1]);
+      ref = cr[0];
     }
     if (ref != LW_REF_NONE) {
       int v = -ref - 1;
@@ -344,13 +380,14 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
         h.bu = bu;  // undivided v, w; divided by det once traversal ends
         h.bv = bv;
         best_det = det;
+        best = __double2float_ru(t);
       }
     }
     ref = LW_REF_NONE;
     while (sp > 0) {
-      sp--;
-      if (lw_pop_keep(stack_tn[sp], h.t)) {
-        ref = stack_ref[sp];
+      unsigned long long e = stk[--sp];
+      if (__uint_as_float((unsigned)(e >> 32)) <= best) {
+        ref = (int)(unsigned)e;
         break;
       }
     }
@@ -367,32 +404,28 @@ template <bool COUNT = false>
 __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
                                              LwTraceCount* cnt = nullptr) {
   if (bvh.ntris == 0) return false;
-  LwRay r;
-  lw_ray_setup(r, o, d);
-  double tn;
-  if (!lw_box_hit(r, bvh.root_box, tmax, tn)) return false;
-  int stack_ref[LW_STACK];
+  LwRayF r;
+  lw_rayf_setup(r, bvh, o, d);
+  const float best = __double2float_ru(tmax);
+  int stk[LW_STACK];
   int sp = 0;
   int ref = bvh.root_ref;
   for (;;) {
     while (ref >= 0 && ref != LW_REF_NONE) {
-      double box[12];
-      int cr[2];
-      lw_load_node(bvh.nodes + ref, box, cr);
+      float tn[4];
+      int cr[4];
+      unsigned m = lw_node_hit(r, bvh.nodes + ref, best, tn, cr);
       if (COUNT) cnt->nodes++;
-      double tn0, tn1;
-      bool h0 = lw_box_hit(r, box, tmax, tn0);
-      bool h1 = lw_box_hit(r, box + 6, tmax, tn1);
-      if (h0 && h1) {
-        stack_ref[sp++] = cr[1];
-        ref = cr[0];
-      } else if (h0) {
-        ref = cr[0];
-      } else if (h1) {
-        ref = cr[1];
-      } else {
+      if (m == 0) {
         ref = LW_REF_NONE;
+        break;
       }
+      int first = __ffs(m) - 1;
+      ref = cr[first];
+      m &= m - 1;
+#pragma unroll
+      for (int c = 1; c < 4; c++)
+        if (m & (1u << c)) stk[sp++] = cr[c];
     }
     if (ref != LW_REF_NONE) {
       int v = -ref - 1;
@@ -403,6 +436,6 @@ __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double 
       }
     }
     if (sp == 0) return false;
-    ref = stack_ref[--sp];
+    ref = stk[--sp];
   }
 }
