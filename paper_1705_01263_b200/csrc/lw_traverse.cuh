@@ -322,23 +322,34 @@ __device__ __forceinline__ void lw_cswap(float& ta, int& ra, float& tb, int& rb)
   ra = q;
 }
 
+// Resumable traversals: init() sets a ray up, step() descends to the next leaf, tests it and
+// pops the next subtree; it returns true once the ray is finished.  lw_trace_closest /
+// lw_trace_any loop step() to completion.  (A persistent dynamic-fetch variant that refilled
+// finished lanes between steps measured 4% faster on C3 and 25% slower on C2; not kept.)
+
 // closest hit, t in (0, tmax], nearest child first
-template <bool COUNT = false>
-__device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
-                                                 double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
-  h.t = tmax;
-  h.tri = -1;
-  h.bu = 0.0;
-  h.bv = 0.0;
-  if (bvh.ntris == 0) return;
+struct LwClosest {
   LwRayF r;
-  lw_rayf_setup(r, bvh, o, d);
-  float best = __double2float_ru(h.t);
+  LwHit h;
+  double best_det;
+  float best;
+  int ref, sp;
   unsigned long long stk[LW_STACK];
-  int sp = 0;
-  int ref = bvh.root_ref;
-  double best_det = 1.0;
-  for (;;) {
+
+  __device__ __forceinline__ void init(const RenderBVH& bvh, const double o[3], const double d[3], double tmax) {
+    h.t = tmax;
+    h.tri = -1;
+    h.bu = 0.0;
+    h.bv = 0.0;
+    best_det = 1.0;
+    sp = 0;
+    ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
+    lw_rayf_setup(r, bvh, o, d);
+    best = __double2float_ru(tmax);
+  }
+
+  template <bool COUNT = false>
+  __device__ __forceinline__ bool step(const RenderBVH& bvh, LwTraceCount* cnt = nullptr) {
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
@@ -377,7 +388,7 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
         if (t == h.t && h.tri >= 0 && id >= h.tri) continue;
         h.t = t;
         h.tri = id;
-        h.bu = bu;  // undivided v, w; divided by det once traversal ends
+        h.bu = bu;  // undivided v, w; divided by det in finish()
         h.bv = bv;
         best_det = det;
         best = __double2float_ru(t);
@@ -391,26 +402,37 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
         break;
       }
     }
-    if (ref == LW_REF_NONE) break;
+    return ref == LW_REF_NONE;
   }
-  if (h.tri >= 0) {
-    h.bu = h.bu / best_det;
-    h.bv = h.bv / best_det;
+
+  __device__ __forceinline__ void finish() {
+    if (h.tri >= 0) {
+      h.bu = h.bu / best_det;
+      h.bv = h.bv / best_det;
+    }
   }
-}
+};
 
 // any hit with 0 < t < tmax
-template <bool COUNT = false>
-__device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
-                                             LwTraceCount* cnt = nullptr) {
-  if (bvh.ntris == 0) return false;
+struct LwAny {
   LwRayF r;
-  lw_rayf_setup(r, bvh, o, d);
-  const float best = __double2float_ru(tmax);
+  double tmax;
+  float best;
+  int ref, sp;
+  bool occluded;
   int stk[LW_STACK];
-  int sp = 0;
-  int ref = bvh.root_ref;
-  for (;;) {
+
+  __device__ __forceinline__ void init(const RenderBVH& bvh, const double o[3], const double d[3], double tm) {
+    tmax = tm;
+    sp = 0;
+    occluded = false;
+    ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
+    lw_rayf_setup(r, bvh, o, d);
+    best = __double2float_ru(tm);
+  }
+
+  template <bool COUNT = false>
+  __device__ __forceinline__ bool step(const RenderBVH& bvh, LwTraceCount* cnt = nullptr) {
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
@@ -420,8 +442,7 @@ __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double 
         ref = LW_REF_NONE;
         break;
       }
-      int first = __ffs(m) - 1;
-      ref = cr[first];
+      ref = cr[__ffs(m) - 1];
       m &= m - 1;
 #pragma unroll
       for (int c = 1; c < 4; c++)
@@ -432,10 +453,38 @@ __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double 
       int start = v >> 3, count = v & 7;
       for (int k = start; k < start + count; k++) {
         if (COUNT) cnt->tris++;
-        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) return true;
+        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) {
+          occluded = true;
+          return true;
+        }
       }
     }
-    if (sp == 0) return false;
+    if (sp == 0) {
+      ref = LW_REF_NONE;
+      return true;
+    }
     ref = stk[--sp];
+    return false;
   }
+};
+
+template <bool COUNT = false>
+__device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
+                                                 double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
+  LwClosest q;
+  q.init(bvh, o, d, tmax);
+  while (!q.step<COUNT>(bvh, cnt)) {
+  }
+  q.finish();
+  h = q.h;
+}
+
+template <bool COUNT = false>
+__device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
+                                             LwTraceCount* cnt = nullptr) {
+  LwAny q;
+  q.init(bvh, o, d, tmax);
+  while (!q.step<COUNT>(bvh, cnt)) {
+  }
+  return q.occluded;
 }
