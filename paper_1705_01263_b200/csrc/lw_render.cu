@@ -427,69 +427,109 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
   cnt->n_alive = 0;
 }
 
-// pool order: flush TERMINATED slots, refill free slots with new (iteration, pixel) samples
-// (one work-claim atomic per warp), and compact TRACE slots into the extension queue as
-// ascending 256-slot runs (warp ballots + block prefix, one queue atomic per block iteration;
-// a per-warp atomic is 8x more same-address traffic and measured slower)
+// pool order: flush TERMINATED slots, refill free slots with new (iteration, pixel) samples and
+// compact TRACE slots into the extension queue.  Each block owns a contiguous slot range: a
+// counting pass over the stage bytes sizes its claims, so the whole block takes its work items
+// and its queue segment with two global atomics, and the writing pass assigns items and queue
+// positions in slot order from block prefixes (one barrier per 256 slots).  The generated
+// samples form the first `granted` free slots of the range, so the queue prefix of a lane is
+// trace_prefix + min(want_prefix, granted_left).
 __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
                                                   Counters* __restrict__ cnt) {
-  __shared__ int warp_off[8];
-  __shared__ int block_base;
-  const int warp = threadIdx.x >> 5;
+  __shared__ int wc[2][8][2];  // per-warp (want, trace) counts, double-buffered by iteration parity
+  __shared__ long long s_wbase;
+  __shared__ int s_ebase, s_red[8][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const bool regen = cnt->regen_now != 0;
   const long long total = w.nits * w.npix;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
+  const int per = (int)(((long long)P.size + (long long)gridDim.x * 256 - 1) / ((long long)gridDim.x * 256)) * 256;
+  const int r0 = (int)min((long long)blockIdx.x * per, (long long)P.size);
+  const int r1 = min(r0 + per, P.size);
+  // pass 1: sizes of the claims
+  int c_want = 0, c_trace = 0;
+  for (int s = r0 + threadIdx.x; s < r1; s += 256) {
+    int st = P.stage[s];
+    if (regen && st != LW_STAGE_TRACE) c_want++;
+    else if (st == LW_STAGE_TRACE) c_trace++;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    c_want += __shfl_down_sync(0xffffffffu, c_want, off);
+    c_trace += __shfl_down_sync(0xffffffffu, c_trace, off);
+  }
+  if (lane == 0) {
+    s_red[warp][0] = c_want;
+    s_red[warp][1] = c_trace;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int want = 0, trace = 0;
+    for (int k = 0; k < 8; k++) {
+      want += s_red[k][0];
+      trace += s_red[k][1];
+    }
+    long long wb = want ? (long long)atomicAdd(&cnt->work_next, (unsigned long long)want) : 0;
+    long long left = total - wb;
+    int granted = left <= 0 ? 0 : (int)min(left, (long long)want);
+    s_wbase = wb;
+    s_ebase = (trace + granted) ? atomicAdd(&cnt->n_ext, trace + granted) : 0;
+  }
+  __syncthreads();
+  long long wnext = s_wbase;  // next work item of this block
+  int enext = s_ebase;        // next queue position of this block
   unsigned long long bad = 0, paths = 0;
-  for (int base = blockIdx.x * 256; base < P.size; base += gridDim.x * 256) {
+  int it = 0;
+  for (int base = r0; base < r1; base += 256, it ^= 1) {
     int s = base + threadIdx.x;
-    bool valid = s < P.size;
+    bool valid = s < r1;
     int stage = valid ? P.stage[s] : LW_STAGE_GENERATE;
+    bool flushed = false;
     if (regen && valid && stage == LW_STAGE_TERMINATED) {
       bad += lw_accumulate(fb, P.pix[s], load_L(P, s));
       paths++;
       stage = LW_STAGE_GENERATE;
-      P.stage[s] = LW_STAGE_GENERATE;
+      flushed = true;
     }
     bool want = regen && valid && stage == LW_STAGE_GENERATE;
-    unsigned m = __ballot_sync(0xffffffffu, want);
-    if (m) {
-      unsigned long long wb = 0;
-      if (lane == 0) wb = atomicAdd(&cnt->work_next, (unsigned long long)__popc(m));
-      wb = __shfl_sync(0xffffffffu, wb, 0);
-      long long item = (long long)wb + __popc(m & lt);
-      if (want && item < total) {
+    bool trace = valid && stage == LW_STAGE_TRACE;
+    unsigned mw = __ballot_sync(0xffffffffu, want), mt = __ballot_sync(0xffffffffu, trace);
+    if (lane == 0) {
+      wc[it][warp][0] = __popc(mw);
+      wc[it][warp][1] = __popc(mt);
+    }
+    __syncthreads();
+    int pw = __popc(mw & lt), pt = __popc(mt & lt), tw = 0, tt = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      int a = wc[it][k][0], b = wc[it][k][1];
+      if (k < warp) {
+        pw += a;
+        pt += b;
+      }
+      tw += a;
+      tt += b;
+    }
+    long long left = total - wnext;
+    int avail = left <= 0 ? 0 : (int)min(left, (long long)tw);
+    if (want) {
+      if (pw < avail) {
+        long long item = wnext + pw;
         int pix;
         long long index = work_index(S, w, item, pix);
         PathState ps;
         lw_path_init(S, index, ps);
         store_state(P, s, ps);
         P.pix[s] = pix;
-        stage = LW_STAGE_TRACE;
         P.stage[s] = LW_STAGE_TRACE;
+        trace = true;
+      } else if (flushed) {
+        P.stage[s] = LW_STAGE_GENERATE;
       }
     }
-    bool ext = valid && stage == LW_STAGE_TRACE;
-    unsigned me = __ballot_sync(0xffffffffu, ext);
-    if (lane == 0) warp_off[warp] = __popc(me);
-    __syncthreads();
-    if (threadIdx.x < 32) {  // block prefix over the 8 warp counts, one atomic per block iteration
-      int c = threadIdx.x < 8 ? warp_off[threadIdx.x] : 0;
-      int incl = c;
-#pragma unroll
-      for (int off = 1; off < 8; off <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (threadIdx.x >= off) incl += v;
-      }
-      int total = __shfl_sync(0xffffffffu, incl, 7);
-      int base = 0;
-      if (threadIdx.x == 0 && total) base = atomicAdd(&cnt->n_ext, total);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (threadIdx.x < 8) warp_off[threadIdx.x] = base + incl - c;
-    }
-    __syncthreads();
-    if (ext) P.q_ext[warp_off[warp] + __popc(me & lt)] = s;
-    __syncthreads();
+    if (trace) P.q_ext[enext + pt + min(pw, avail)] = s;
+    wnext += tw;
+    enext += tt + avail;
   }
   warp_add(&cnt->nonfinite, bad);
   warp_add(&cnt->paths, paths);
