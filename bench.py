@@ -317,8 +317,8 @@ def run_ours(a):
         "dtype": "f64", "data": "synthetic procedural scene (seeded), QMC samples",
         "config": {"workload": workload(a), "engine": a.engine, "pool_slots": 1 << a.pool_log2,
                    "regen_fraction": a.regen_fraction, "parallelism": f"sample-space dp{world}",
-                   "l2": "wavefront state pool (~300 MB) + framebuffers (50 MB) exceed the 126 MB L2; the 5 KB scene "
-                         "BVH is shared-memory resident by design"},
+                   "l2": f"wavefront state pool (~{(1 << a.pool_log2) * 250 / 1e9:.1f} GB) exceeds the 126 MB L2 "
+                         "(no flush needed); Cornell-box BVHs are shared-memory resident by design"},
         "mrays_per_s": (rays_ext_all + rays_sh_all) / (ms_max / 1e3) / 1e6,
         "gsegments_per_s": rays_ext_all / (ms_max / 1e3) / 1e9,
         "gpu_launches": int(launches),
@@ -328,8 +328,10 @@ def run_ours(a):
                      "bytes_per_ray": bytes_per_ray, "nodes_per_ray": nodes_per_ray, "tris_per_ray": tris_per_ray,
                      "avg_launch_ms": avg_ms, "launches": prof_launches,
                      "trace_share_of_step": prof_ms / ms_max,
-                     "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                     "traffic": ((traffic or {}).get("configs", {}).get(a.config) or {}).get("dram_bytes_per_launch"),
+                     "traffic_source": "profiles/trace_ext_traffic.json (ncu dram__bytes_read+write per launch)",
+                     "peak_source": ("fallback 6650 GB/s (B200_PROFILING.md)" if peaks.get("fallback")
+                                     else "MEASURED_PEAKS.json hbm_gbs (measured copy)")},
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -744,7 +744,6 @@ __global__ void k_resolve(const unsigned long long* fb, long long n, double scal
 }
 
 int nrnodes_of(const lw_ctx* c) { return c->ref_bvh.nnodes > 1 ? (int)((c->ref_bvh.nnodes - 1) / 2) : 0; }
-int render_nodes(const lw_ctx* c) { return c->nrnodes; }
 
 // binary tree -> 4-wide nodes, one launch per binary level (frontier in device memory)
 int collapse_wide(lw_ctx* c, const SahNode* bn, int nr, int root_ref, int levels, WNode* out, int& max_need) {

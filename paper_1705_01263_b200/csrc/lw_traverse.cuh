@@ -227,7 +227,7 @@ struct LwRayF {
   float inv[3];  // clamped reciprocal direction
   float on[3];   // -(o - / + delta) * inv: near-plane offset (t lowered by >= 0.9 delta |inv|)
   float of[3];   // far-plane offset (t raised)
-  int sn[3];     // float4 index of the near plane array in WNode (a, or 3 + a when inv < 0)
+  int sn[3], sf[3];  // float4 index of the near / far plane arrays in WNode (lo[a] = a, hi[a] = 3 + a)
   LwShear sh;
 };
 
@@ -248,6 +248,7 @@ __device__ __forceinline__ void lw_rayf_setup(LwRayF& r, const RenderBVH& bvh, c
     r.on[a] = (float)(-(o_n * (double)invf));
     r.of[a] = (float)(-(o_f * (double)invf));
     r.sn[a] = neg ? 3 + a : a;
+    r.sf[a] = neg ? a : 3 + a;
   }
   lw_shear_setup(o, d, false, r.sh);
 }
@@ -258,9 +259,7 @@ __device__ __forceinline__ unsigned lw_node_hit(const LwRayF& r, const WNode* __
                                                 int ref[4]) {
   const float4* q = reinterpret_cast<const float4*>(nd);
   float4 nx = q[r.sn[0]], ny = q[r.sn[1]], nz = q[r.sn[2]];
-  float4 fx = q[6 - r.sn[0] - 0 + 0 - (r.sn[0] >= 3 ? 0 : 0)];  // placeholder, replaced below
-  (void)fx;
-  float4 Fx = q[r.sn[0] >= 3 ? 0 : 3], Fy = q[r.sn[1] >= 3 ? 1 : 4], Fz = q[r.sn[2] >= 3 ? 2 : 5];
+  float4 Fx = q[r.sf[0]], Fy = q[r.sf[1]], Fz = q[r.sf[2]];
   int4 rf = *reinterpret_cast<const int4*>(&nd->ref);
   ref[0] = rf.x;
   ref[1] = rf.y;

@@ -53,7 +53,10 @@ def test_halton_vs_oracle_at_scale(gpu, oracle, depth):
 
     t = qmc.DimensionTable(depth)
     rng = np.random.default_rng(depth)
-    idx = np.concatenate([np.arange(1 << 16), rng.integers(0, 1 << 31, (1 << 18) - (1 << 16))]).astype(np.int64)
+    # dense small indices, the configs' range, the 32-bit digit-block boundary and beyond it
+    edge = np.array([(1 << 32) - 2, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, (1 << 40) + 3], np.int64)
+    idx = np.concatenate([np.arange(1 << 16), rng.integers(0, 1 << 31, (1 << 18) - (1 << 16) - 4096),
+                          rng.integers(1 << 31, 1 << 32, 4096 - len(edge)), edge]).astype(np.int64)
     out = np.zeros(len(idx))
     for dim in range(4 + 8 * depth):
         kernels.halton_batch(t.bases, t.perm_flat, t.perm_offset, dim, idx, out)

@@ -25,7 +25,7 @@ METRICS = {
     "local_ld_sectors": "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum",
 }
 _BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-_TIME = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+_TIME = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 
 
 def load(path):
