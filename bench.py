@@ -266,16 +266,15 @@ def run_ours(a):
     # the resolved float32 image
     e2e = None
     if not a.no_e2e:
-        h2d = sum(v.nbytes for v in packed.arrays.values() if hasattr(v, "nbytes"))
-        h2d += C.sizeof(packed.desc) + C.sizeof(r.params.struct) + r.params.bases.nbytes + \
+        pscene = packed.pinned()  # step inputs in page-locked host memory
+        h2d = sum(v.nbytes for k, v in pscene.arrays.items() if hasattr(v, "nbytes"))
+        h2d += C.sizeof(pscene.desc) + C.sizeof(r.params.struct) + r.params.bases.nbytes + \
             r.params.perm_flat.nbytes + r.params.perm_offset.nbytes
         d2h = P * 3 * 4
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for s in range(a.steps):
-            with Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
+        img = torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True).numpy()
+
+        def e2e_step(s):
+            with Renderer(None, W, H, a.depth, device=local, packed=pscene, engine=a.engine, pool_log2=a.pool_log2,
                           regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail) as r2:
                 r2.set_stream(stream.cuda_stream)
                 lo, hi = partition_iterations(s * world * its, (s + 1) * world * its, rank, world)
@@ -284,15 +283,24 @@ def run_ours(a):
                     r2.copy_framebuffer_to(tmp.data_ptr())
                     dist.all_reduce(tmp)
                     r2.load_framebuffer_from(tmp.data_ptr())
-                r2.image(world * its)
+                r2.image(world * its, out=img)
+
+        e2e_step(0)  # untimed warm-up (first use of the device memory pool at this scene's sizes)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(a.steps):
+            e2e_step(s)
         torch.cuda.synchronize()
         tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": paths / float(tt[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "note": "per step: context + scene upload (GPU median BVH, SAH render BVH) + pass + NCCL reduce "
-                       "(N>1) + resolved float32 image readback, host wall clock around device syncs"}
+               "note": "per step: context + scene upload from pinned host buffers (GPU SAH build + 4-wide "
+                       "collapse) + pass + NCCL reduce (N>1) + resolved float32 image readback into pinned "
+                       "memory, host wall clock around device syncs"}
 
     peaks = load_peaks()
     nodes_per_ray = work["ext_nodes"] / max(work["ext_rays"], 1)

@@ -251,9 +251,9 @@ __global__ void k_root_init(SegTable t, int n, int* pos_seg_first) {
 int bvh_build_device(const double* d_verts, int64_t n, cudaStream_t st, DeviceBVH& out) {
   int64_t nnodes = bvh_node_count(n);
   out.nnodes = nnodes;
-  TRY(cudaMalloc(&out.bounds, sizeof(double) * 6 * nnodes));
-  TRY(cudaMalloc(&out.children, sizeof(long long) * 2 * nnodes));
-  TRY(cudaMalloc(&out.order, sizeof(long long) * (n > 0 ? n : 1)));
+  TRY(cudaMallocAsync(&out.bounds, sizeof(double) * 6 * nnodes, st));
+  TRY(cudaMallocAsync(&out.children, sizeof(long long) * 2 * nnodes, st));
+  TRY(cudaMallocAsync(&out.order, sizeof(long long) * (n > 0 ? n : 1), st));
   if (n == 0) {  // geometry.py:103-106
     TRY(cudaMemsetAsync(out.bounds, 0, sizeof(double) * 6, st));
     long long ch[2] = {-1, 0};
@@ -265,18 +265,18 @@ int bvh_build_device(const double* d_verts, int64_t n, cudaStream_t st, DeviceBV
   const int B = 256;
   int gn = (int)((n + B - 1) / B);
   DevBuf b_tmin, b_tmax, b_keys, b_keys_out, b_ids, b_lists, b_lists2, b_pos, b_left, b_flag, b_scan, b_cnt;
-  TRY(b_tmin.alloc(sizeof(double) * 3 * n));
-  TRY(b_tmax.alloc(sizeof(double) * 3 * n));
-  TRY(b_keys.alloc(sizeof(unsigned long long) * 3 * n));
-  TRY(b_keys_out.alloc(sizeof(unsigned long long) * n));
-  TRY(b_ids.alloc(sizeof(int) * n));
-  TRY(b_lists.alloc(sizeof(int) * 3 * n));
-  TRY(b_lists2.alloc(sizeof(int) * 3 * n));
-  TRY(b_pos.alloc(sizeof(int) * n));
-  TRY(b_left.alloc(n));
-  TRY(b_flag.alloc(sizeof(int) * n));
-  TRY(b_scan.alloc(sizeof(int) * n));
-  TRY(b_cnt.alloc(sizeof(int)));
+  TRY(b_tmin.alloc(sizeof(double) * 3 * n, st));
+  TRY(b_tmax.alloc(sizeof(double) * 3 * n, st));
+  TRY(b_keys.alloc(sizeof(unsigned long long) * 3 * n, st));
+  TRY(b_keys_out.alloc(sizeof(unsigned long long) * n, st));
+  TRY(b_ids.alloc(sizeof(int) * n, st));
+  TRY(b_lists.alloc(sizeof(int) * 3 * n, st));
+  TRY(b_lists2.alloc(sizeof(int) * 3 * n, st));
+  TRY(b_pos.alloc(sizeof(int) * n, st));
+  TRY(b_left.alloc(n, st));
+  TRY(b_flag.alloc(sizeof(int) * n, st));
+  TRY(b_scan.alloc(sizeof(int) * n, st));
+  TRY(b_cnt.alloc(sizeof(int), st));
   k_tri_prep<<<gn, B, 0, st>>>(d_verts, n, b_tmin.as<double>(), b_tmax.as<double>(), b_keys.as<unsigned long long>(),
                                b_ids.as<int>());
   TRY(cudaGetLastError());
@@ -286,7 +286,7 @@ int bvh_build_device(const double* d_verts, int64_t n, cudaStream_t st, DeviceBV
                                   b_ids.as<int>(), b_lists.as<int>(), (int)n, 0, 64, st);
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, b_flag.as<int>(), b_scan.as<int>(), (int)n, st);
   DevBuf b_tmp;
-  TRY(b_tmp.alloc(sort_bytes > scan_bytes ? sort_bytes : scan_bytes));
+  TRY(b_tmp.alloc(sort_bytes > scan_bytes ? sort_bytes : scan_bytes, st));
   int* lists[3];
   int* lists2[3];
   for (int a = 0; a < 3; a++) {
@@ -302,14 +302,14 @@ int bvh_build_device(const double* d_verts, int64_t n, cudaStream_t st, DeviceBV
   DevBuf b_seg[2], b_bmin, b_bmax, b_axis, b_child;
   SegTable tab[2];
   for (int k = 0; k < 2; k++) {
-    TRY(b_seg[k].alloc(sizeof(int) * 4 * cap));
+    TRY(b_seg[k].alloc(sizeof(int) * 4 * cap, st));
     int* p = b_seg[k].as<int>();
     tab[k] = SegTable{p, p + cap, p + 2 * cap, p + 3 * cap};
   }
-  TRY(b_bmin.alloc(sizeof(unsigned long long) * 3 * cap));
-  TRY(b_bmax.alloc(sizeof(unsigned long long) * 3 * cap));
-  TRY(b_axis.alloc(sizeof(int) * cap));
-  TRY(b_child.alloc(sizeof(int) * cap));
+  TRY(b_bmin.alloc(sizeof(unsigned long long) * 3 * cap, st));
+  TRY(b_bmax.alloc(sizeof(unsigned long long) * 3 * cap, st));
+  TRY(b_axis.alloc(sizeof(int) * cap, st));
+  TRY(b_child.alloc(sizeof(int) * cap, st));
   TRY(cudaMemsetAsync(b_pos.p, 0, sizeof(int) * n, st));
   k_root_init<<<1, 1, 0, st>>>(tab[0], (int)n, nullptr);
   int nseg = 1, cur = 0;
@@ -355,7 +355,7 @@ extern "C" int lw_bvh_build(const double* verts, int64_t ntris, double* bounds, 
   LW_CHECK_ARG(ntris >= 0 && (ntris == 0 || verts) && bounds && children && nnodes, "bad arguments");
   cudaStream_t st = cudaStreamPerThread;
   DevBuf b_v;
-  LW_CUDA_TRY(b_v.alloc(sizeof(double) * 9 * (ntris > 0 ? ntris : 1)));
+  LW_CUDA_TRY(b_v.alloc(sizeof(double) * 9 * (ntris > 0 ? ntris : 1), st));
   if (ntris > 0) LW_CUDA_TRY(cudaMemcpyAsync(b_v.p, verts, sizeof(double) * 9 * ntris, cudaMemcpyHostToDevice, st));
   DeviceBVH bvh;
   int rc = bvh_build_device(b_v.as<double>(), ntris, st, bvh);

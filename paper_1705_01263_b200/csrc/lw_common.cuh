@@ -42,19 +42,34 @@ void set_error(const char* fmt, ...);
     if (_s != LW_OK) return _s; \
   } while (0)
 
-// RAII device buffer (stateless entry points)
+// RAII device buffer.  alloc(n) is a plain cudaMalloc (stateless entry points); alloc(n, stream)
+// is stream-ordered (cudaMallocAsync from the device's default pool, whose release threshold the
+// render context raises), so builder temporaries cost neither a driver allocation nor the
+// implicit device synchronisation of cudaFree.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool async = false;
+  cudaStream_t st = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (!p) return;
+    if (async)
+      cudaFreeAsync(p, st);
+    else
+      cudaFree(p);
   }
   cudaError_t alloc(size_t n) {
     bytes = n;
     return cudaMalloc(&p, n > 0 ? n : 16);
+  }
+  cudaError_t alloc(size_t n, cudaStream_t stream) {
+    bytes = n;
+    async = true;
+    st = stream;
+    return cudaMallocAsync(&p, n > 0 ? n : 16, stream);
   }
   template <class T>
   T* as() const {

@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -73,6 +74,7 @@ struct lw_ctx {
   DevScene S;
   std::vector<void*> scene_allocs;
   DeviceBVH ref_bvh;
+  bool ref_built = false;
   int64_t ntris = 0;
   lw_render_params params;
   QmcDim* d_qdims = nullptr;
@@ -98,7 +100,7 @@ namespace {
 
 template <class T>
 int dev_upload(lw_ctx* c, T*& dst, const T* src, int64_t count) {
-  LW_CUDA_TRY(cudaMalloc(&dst, sizeof(T) * (count > 0 ? count : 1)));
+  LW_CUDA_TRY(cudaMallocAsync(&dst, sizeof(T) * (count > 0 ? count : 1), c->stream));
   c->scene_allocs.push_back(dst);
   if (count > 0) LW_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, c->stream));
   return LW_OK;
@@ -106,23 +108,24 @@ int dev_upload(lw_ctx* c, T*& dst, const T* src, int64_t count) {
 
 template <class T>
 int dev_alloc(lw_ctx* c, T*& dst, int64_t count) {
-  LW_CUDA_TRY(cudaMalloc(&dst, sizeof(T) * (count > 0 ? count : 1)));
+  LW_CUDA_TRY(cudaMallocAsync(&dst, sizeof(T) * (count > 0 ? count : 1), c->stream));
   c->scene_allocs.push_back(dst);
   return LW_OK;
 }
 
 void free_scene(lw_ctx* c) {
-  for (void* p : c->scene_allocs) cudaFree(p);
+  for (void* p : c->scene_allocs) cudaFreeAsync(p, c->stream);
   c->scene_allocs.clear();
-  cudaFree(c->ref_bvh.bounds);
-  cudaFree(c->ref_bvh.children);
-  cudaFree(c->ref_bvh.order);
+  if (c->ref_bvh.bounds) cudaFreeAsync(c->ref_bvh.bounds, c->stream);
+  if (c->ref_bvh.children) cudaFreeAsync(c->ref_bvh.children, c->stream);
+  if (c->ref_bvh.order) cudaFreeAsync(c->ref_bvh.order, c->stream);
   c->ref_bvh = DeviceBVH();
+  c->ref_built = false;
   c->has_scene = false;
 }
 
 void free_pool(lw_ctx* c) {
-  if (c->pool.block) cudaFree(c->pool.block);
+  if (c->pool.block) cudaFreeAsync(c->pool.block, c->stream);
   c->pool = Pool();
 }
 
@@ -786,7 +789,7 @@ int alloc_pool(lw_ctx* c, int size) {
   Pool& P = c->pool;
   const size_t nvec = 14;  // double2 arrays
   size_t bytes = (size_t)size * (nvec * 16 + 4 * 4 + 1) + 8192;
-  LW_CUDA_TRY(cudaMalloc(&P.block, bytes));
+  LW_CUDA_TRY(cudaMallocAsync(&P.block, bytes, c->stream));
   char* p = (char*)P.block;
   auto v2 = [&](double2*& x) {
     x = (double2*)p;
@@ -948,6 +951,59 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
 
 }  // namespace
 
+namespace {
+// Per-device cache of the fixed context resources (stream, pinned counter mirror, counters,
+// events): pinned-host allocation and stream creation cost milliseconds with large variance,
+// so a destroyed context returns them for the next one (e.g. one context per progressive job).
+struct CtxRes {
+  int device;
+  cudaStream_t stream;
+  Counters *d_cnt, *h_cnt;
+  cudaEvent_t ev0, ev1;
+};
+std::mutex g_res_mu;
+std::vector<CtxRes> g_res_free;
+constexpr size_t kResCache = 16;
+
+cudaError_t take_res(int device, CtxRes& r) {
+  {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    for (size_t k = 0; k < g_res_free.size(); k++) {
+      if (g_res_free[k].device == device) {
+        r = g_res_free[k];
+        g_res_free.erase(g_res_free.begin() + k);
+        return cudaSuccess;
+      }
+    }
+  }
+  r.device = device;
+  r.stream = nullptr;
+  r.d_cnt = r.h_cnt = nullptr;
+  r.ev0 = r.ev1 = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&r.d_cnt, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaMallocHost(&r.h_cnt, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaEventCreate(&r.ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&r.ev1);
+  return e;
+}
+
+void give_res(const CtxRes& r) {
+  {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    if (g_res_free.size() < kResCache) {
+      g_res_free.push_back(r);
+      return;
+    }
+  }
+  if (r.d_cnt) cudaFree(r.d_cnt);
+  if (r.h_cnt) cudaFreeHost(r.h_cnt);
+  if (r.ev0) cudaEventDestroy(r.ev0);
+  if (r.ev1) cudaEventDestroy(r.ev1);
+  if (r.stream) cudaStreamDestroy(r.stream);
+}
+}  // namespace
+
 extern "C" {
 
 int lw_ctx_create(int device, lw_ctx** out) {
@@ -959,17 +1015,26 @@ int lw_ctx_create(int device, lw_ctx** out) {
   memset(&c->stats, 0, sizeof(c->stats));
   memset(&c->params, 0, sizeof(c->params));
   memset(&c->prof, 0, sizeof(c->prof));
-  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-  c->stream = c->own_stream;
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_cnt, sizeof(Counters));
-  if (e == cudaSuccess) e = cudaMallocHost(&c->h_cnt, sizeof(Counters));
-  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
-  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  // scene, pool and framebuffer memory is stream-ordered from the device's default pool; keep
+  // freed blocks reserved so a new context reuses them without driver allocations
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  CtxRes r;
+  cudaError_t e = take_res(device, r);
   if (e != cudaSuccess) {
+    give_res(r);
     set_error("context creation failed: %s", cudaGetErrorString(e));
     delete c;
     return LW_ERR_CUDA;
   }
+  c->own_stream = c->stream = r.stream;
+  c->d_cnt = r.d_cnt;
+  c->h_cnt = r.h_cnt;
+  c->ev0 = r.ev0;
+  c->ev1 = r.ev1;
   *out = c;
   return LW_OK;
 }
@@ -1000,14 +1065,13 @@ int lw_ctx_destroy(lw_ctx* c) {
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   free_scene(c);
   free_pool(c);
-  cudaFree(c->d_fb);
-  cudaFree(c->d_qdims);
-  cudaFree(c->d_qperm);
-  cudaFree(c->d_cnt);
-  cudaFreeHost(c->h_cnt);
-  cudaEventDestroy(c->ev0);
-  cudaEventDestroy(c->ev1);
-  cudaStreamDestroy(c->own_stream);
+  if (c->d_fb) cudaFreeAsync(c->d_fb, c->stream);
+  cudaStreamSynchronize(c->stream);
+  if (c->d_qdims) cudaFreeAsync(c->d_qdims, c->stream);
+  if (c->d_qperm) cudaFreeAsync(c->d_qperm, c->stream);
+  cudaStreamSynchronize(c->stream);
+  CtxRes r{c->device, c->own_stream, c->d_cnt, c->h_cnt, c->ev0, c->ev1};
+  give_res(r);
   delete c;
   return LW_OK;
 }
@@ -1040,7 +1104,13 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   S.material = dm;
   S.materials = dmat;
   // reference-layout BVH on the device (geometry.py:100-148 arrays; exported for parity)
-  LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
+  // the reference-layout median tree (geometry.py:100-148 arrays) is built here only when it is
+  // the render tree; otherwise on demand by lw_ctx_bvh_info / lw_ctx_bvh_download
+  c->ref_built = false;
+  if (d->bvh_kind == LW_BVH_MEDIAN) {
+    LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
+    c->ref_built = true;
+  }
   int64_t nn = c->ref_bvh.nnodes;
   int nr = 0, levels = 0, root_ref = leaf_ref(0, 0);
   SahNode* bn = nullptr;  // binary tree (FP64 child boxes), collapsed to the 4-wide layout below
@@ -1050,7 +1120,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   if (d->bvh_kind == LW_BVH_MEDIAN) {
     // render layout derived from the median tree on the device
     nr = nrnodes_of(c);
-    LW_CUDA_TRY(cudaMalloc(&bn, sizeof(SahNode) * (nr > 0 ? nr : 1)));
+    LW_CUDA_TRY(cudaMallocAsync(&bn, sizeof(SahNode) * (nr > 0 ? nr : 1), st));
     if (n > 0) {
       int* flag;
       int* imap;
@@ -1060,13 +1130,13 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
       size_t tb = 0;
       cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, imap, (int)nn, st);
       void* tmp;
-      LW_CUDA_TRY(cudaMalloc(&tmp, tb > 0 ? tb : 16));
+      LW_CUDA_TRY(cudaMallocAsync(&tmp, tb > 0 ? tb : 16, st));
       LW_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, imap, (int)nn, st));
       k_build_rnodes<<<grid_for(nn, 256, 1 << 30), 256, 0, st>>>(c->ref_bvh.bounds, c->ref_bvh.children, nn, imap, bn);
       k_build_ltris<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, c->ref_bvh.order, n, lt);
       LW_CUDA_TRY(cudaGetLastError());
       LW_CUDA_TRY(cudaStreamSynchronize(st));
-      cudaFree(tmp);
+      cudaFreeAsync(tmp, st);
     }
     long long rc[2] = {-1, 0};
     LW_CUDA_TRY(cudaMemcpyAsync(rb, c->ref_bvh.bounds, sizeof(rb), cudaMemcpyDeviceToHost, st));
@@ -1080,8 +1150,8 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     DeviceSah ds;
     int rc_sah = sah_build_device(dv, n, st, ds);
     if (rc_sah != LW_OK) {
-      cudaFree(ds.nodes);
-      cudaFree(ds.order);
+      if (ds.nodes) cudaFreeAsync(ds.nodes, st);
+      if (ds.order) cudaFreeAsync(ds.order, st);
       return rc_sah;
     }
     nr = (int)ds.nnodes;
@@ -1089,7 +1159,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     if (n > 0) k_build_ltris_i32<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dv, ds.order, n, lt);
     LW_CUDA_TRY(cudaGetLastError());
     LW_CUDA_TRY(cudaStreamSynchronize(st));
-    cudaFree(ds.order);
+    cudaFreeAsync(ds.order, st);
     for (int a = 0; a < 6; a++) rb[a] = ds.root_box[a];
     root_ref = ds.root_ref;
     levels = ds.levels;
@@ -1098,7 +1168,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   LW_STATUS_TRY(dev_alloc(c, wn, nr > 0 ? nr : 1));
   int max_need = 0;
   int rc_w = collapse_wide(c, bn, nr, root_ref, levels, wn, max_need);
-  cudaFree(bn);
+  if (bn) cudaFreeAsync(bn, st);
   LW_STATUS_TRY(rc_w);
   if (max_need > LW_STACK) {
     set_error("render BVH too deep: a path needs %d traversal stack entries (limit %d)", max_need, LW_STACK);
@@ -1203,14 +1273,15 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   std::vector<QmcDim> dims;
   std::vector<uint16_t> perm;
   LW_STATUS_TRY(pack_qmc_tables(p->bases, p->ndims, p->perm_flat, p->perm_len, p->perm_offset, dims, perm));
-  cudaFree(c->d_qdims);
-  cudaFree(c->d_qperm);
+  if (c->d_qdims) cudaFreeAsync(c->d_qdims, c->stream);
+  if (c->d_qperm) cudaFreeAsync(c->d_qperm, c->stream);
   c->d_qdims = nullptr;
   c->d_qperm = nullptr;
-  LW_CUDA_TRY(cudaMalloc(&c->d_qdims, sizeof(QmcDim) * dims.size()));
-  LW_CUDA_TRY(cudaMalloc(&c->d_qperm, sizeof(uint16_t) * perm.size()));
-  LW_CUDA_TRY(cudaMemcpy(c->d_qdims, dims.data(), sizeof(QmcDim) * dims.size(), cudaMemcpyHostToDevice));
-  LW_CUDA_TRY(cudaMemcpy(c->d_qperm, perm.data(), sizeof(uint16_t) * perm.size(), cudaMemcpyHostToDevice));
+  LW_CUDA_TRY(cudaMallocAsync(&c->d_qdims, sizeof(QmcDim) * dims.size(), c->stream));
+  LW_CUDA_TRY(cudaMallocAsync(&c->d_qperm, sizeof(uint16_t) * perm.size(), c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(c->d_qdims, dims.data(), sizeof(QmcDim) * dims.size(), cudaMemcpyHostToDevice, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(c->d_qperm, perm.data(), sizeof(uint16_t) * perm.size(), cudaMemcpyHostToDevice, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
   c->params = *p;
   c->params.bases = nullptr;
   c->params.perm_flat = nullptr;
@@ -1223,11 +1294,11 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   c->S.rr_start = p->rr_start;
   int64_t px = (int64_t)p->width * p->height;
   if (px != c->fb_pixels) {
-    cudaFree(c->d_fb);
+    if (c->d_fb) cudaFreeAsync(c->d_fb, c->stream);
     c->d_fb = nullptr;
-    LW_CUDA_TRY(cudaMalloc(&c->d_fb, sizeof(unsigned long long) * 3 * px));
+    LW_CUDA_TRY(cudaMallocAsync(&c->d_fb, sizeof(unsigned long long) * 3 * px, c->stream));
     c->fb_pixels = px;
-    LW_CUDA_TRY(cudaMemset(c->d_fb, 0, sizeof(unsigned long long) * 3 * px));
+    LW_CUDA_TRY(cudaMemsetAsync(c->d_fb, 0, sizeof(unsigned long long) * 3 * px, c->stream));
   }
   c->configured = true;
   return LW_OK;
@@ -1381,14 +1452,23 @@ int lw_ctx_camera_rays(lw_ctx* c, const int64_t* idx, int64_t n, double* out_o, 
   return LW_OK;
 }
 
+static int ensure_ref_bvh(lw_ctx* c) {
+  if (c->ref_built) return LW_OK;
+  LW_STATUS_TRY(bvh_build_device(c->S.verts, c->ntris, c->stream, c->ref_bvh));
+  c->ref_built = true;
+  return LW_OK;
+}
+
 int lw_ctx_bvh_info(lw_ctx* c, int64_t* nnodes) {
   LW_CHECK_ARG(c && c->has_scene && nnodes, "no scene");
+  LW_STATUS_TRY(ensure_ref_bvh(c));
   *nnodes = c->ref_bvh.nnodes;
   return LW_OK;
 }
 
 int lw_ctx_bvh_download(lw_ctx* c, double* bounds, int64_t* children, int64_t* order) {
   LW_CHECK_ARG(c && c->has_scene && bounds && children, "no scene");
+  LW_STATUS_TRY(ensure_ref_bvh(c));
   int64_t nn = c->ref_bvh.nnodes;
   LW_CUDA_TRY(cudaMemcpyAsync(bounds, c->ref_bvh.bounds, sizeof(double) * 6 * nn, cudaMemcpyDeviceToHost, c->stream));
   LW_CUDA_TRY(cudaMemcpyAsync(children, c->ref_bvh.children, sizeof(long long) * 2 * nn, cudaMemcpyDeviceToHost, c->stream));

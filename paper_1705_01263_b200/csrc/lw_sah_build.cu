@@ -463,21 +463,21 @@ int sah_build_device(const double* d_verts, int64_t n64, cudaStream_t st, Device
   for (int a = 0; a < 6; a++) out.root_box[a] = 0.0;
   int n = (int)n64;
   LW_CHECK_ARG(n64 >= 0 && n64 < (1LL << 28), "sah build: at most 2^28 triangles");
-  TRY(cudaMalloc(&out.nodes, sizeof(SahNode) * (n > 1 ? n - 1 : 1)));
-  TRY(cudaMalloc(&out.order, sizeof(int) * (n > 0 ? n : 1)));
+  TRY(cudaMallocAsync(&out.nodes, sizeof(SahNode) * (n > 1 ? n - 1 : 1), st));
+  TRY(cudaMallocAsync(&out.order, sizeof(int) * (n > 0 ? n : 1), st));
   if (n == 0) return LW_OK;
   const int B = 256;
   int gn = (n + B - 1) / B;
   DevBuf b_tb, b_cen, b_ids2, b_pos, b_pos2, b_left, b_scan, b_acc, b_root;
-  TRY(b_tb.alloc(sizeof(double) * 6 * (size_t)n));
-  TRY(b_cen.alloc(sizeof(double) * 3 * (size_t)n));
-  TRY(b_ids2.alloc(sizeof(int) * n));
-  TRY(b_pos.alloc(sizeof(int) * n));
-  TRY(b_pos2.alloc(sizeof(int) * n));
-  TRY(b_left.alloc(sizeof(int) * n));
-  TRY(b_scan.alloc(sizeof(int) * (n + 1)));
-  TRY(b_acc.alloc(sizeof(unsigned long long) * 12));
-  TRY(b_root.alloc(sizeof(int)));
+  TRY(b_tb.alloc(sizeof(double) * 6 * (size_t)n, st));
+  TRY(b_cen.alloc(sizeof(double) * 3 * (size_t)n, st));
+  TRY(b_ids2.alloc(sizeof(int) * n, st));
+  TRY(b_pos.alloc(sizeof(int) * n, st));
+  TRY(b_pos2.alloc(sizeof(int) * n, st));
+  TRY(b_left.alloc(sizeof(int) * n, st));
+  TRY(b_scan.alloc(sizeof(int) * (n + 1), st));
+  TRY(b_acc.alloc(sizeof(unsigned long long) * 12, st));
+  TRY(b_root.alloc(sizeof(int), st));
   int* ids = out.order;
   int* ids2 = b_ids2.as<int>();
   int* pos = b_pos.as<int>();
@@ -490,20 +490,20 @@ int sah_build_device(const double* d_verts, int64_t n64, cudaStream_t st, Device
                                                       b_acc.as<unsigned long long>());
   // segment tables (current / next); a level has at most n segments
   DevBuf b_seg[2], b_split, b_sflag, b_srank, b_lflag, b_lscan, b_lrank, b_bins, b_tmp;
-  TRY(b_seg[0].alloc(sizeof(SSeg) * n));
-  TRY(b_seg[1].alloc(sizeof(SSeg) * n));
-  TRY(b_split.alloc(sizeof(SSplit) * n));
-  TRY(b_sflag.alloc(sizeof(int) * (n + 1)));
-  TRY(b_srank.alloc(sizeof(int) * (n + 1)));
-  TRY(b_lflag.alloc(sizeof(int) * (n + 1)));
-  TRY(b_lscan.alloc(sizeof(int) * (n + 1)));
-  TRY(b_lrank.alloc(sizeof(int) * (n + 1)));
+  TRY(b_seg[0].alloc(sizeof(SSeg) * n, st));
+  TRY(b_seg[1].alloc(sizeof(SSeg) * n, st));
+  TRY(b_split.alloc(sizeof(SSplit) * n, st));
+  TRY(b_sflag.alloc(sizeof(int) * (n + 1), st));
+  TRY(b_srank.alloc(sizeof(int) * (n + 1), st));
+  TRY(b_lflag.alloc(sizeof(int) * (n + 1), st));
+  TRY(b_lscan.alloc(sizeof(int) * (n + 1), st));
+  TRY(b_lrank.alloc(sizeof(int) * (n + 1), st));
   int max_large = n / (kSmall + 1) + 1;
-  TRY(b_bins.alloc(sizeof(BinAcc) * 3 * kBins * (size_t)max_large));
+  TRY(b_bins.alloc(sizeof(BinAcc) * 3 * kBins * (size_t)max_large, st));
   k_sah_root_init<<<1, 1, 0, st>>>(b_acc.as<unsigned long long>(), b_seg[0].as<SSeg>(), n);
   size_t tb1 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb1, b_left.as<int>(), b_scan.as<int>(), n + 1, st);
-  TRY(b_tmp.alloc(tb1));
+  TRY(b_tmp.alloc(tb1, st));
   int nseg = 1, cur = 0, node_base = 0;
   int h_counts[2];
   while (nseg > 0) {

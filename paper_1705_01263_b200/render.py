@@ -109,10 +109,16 @@ class Renderer:
         check(self.lib.lw_framebuffer_download(self.ctx, ptr(fb, C.c_int64)))
         return fb
 
-    def image(self, samples=None) -> np.ndarray:
-        """Resolved (H, W, 3) float32 radiance = framebuffer / samples per pixel (GPU resolve)."""
+    def image(self, samples=None, out=None) -> np.ndarray:
+        """Resolved (H, W, 3) float32 radiance = framebuffer / samples per pixel (GPU resolve).
+
+        `out`: optional C-contiguous float32 (H, W, 3) array to fill (e.g. a view of pinned memory)."""
         samples = self.iterations if samples is None else samples
-        out = np.empty((self.params.height, self.params.width, 3), dtype=np.float32)
+        shape = (self.params.height, self.params.width, 3)
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        if out.shape != shape or out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"image out must be a C-contiguous float32 array of shape {shape}")
         check(self.lib.lw_framebuffer_resolve(self.ctx, 1.0 / max(samples, 1), ptr(out, C.c_float)))
         return out
 

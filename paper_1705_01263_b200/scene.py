@@ -239,6 +239,33 @@ class PackedScene:
     def verts(self):
         return self.arrays["verts"]
 
+    _PIN_FIELDS = {"verts": ("verts", C.c_double), "normals": ("normals", C.c_double),
+                   "material": ("material", C.c_int32), "emit_tri": ("emit_tri", C.c_int64),
+                   "emit_rad": ("emit_radiance", C.c_double), "emit_two": ("emit_twosided", C.c_int32),
+                   "emit_w": ("emit_weight", C.c_double), "env_img": ("env_image", C.c_float),
+                   "env_w": ("env_weight", C.c_double)}
+
+    def pinned(self) -> "PackedScene":
+        """Copy whose geometry / emitter / environment arrays live in page-locked host memory, so
+        lw_scene_upload is a DMA from pinned buffers (torch pinned tensors; torch is plumbing here)."""
+        import torch
+
+        arrays = dict(self.arrays)
+        desc = type(self.desc).from_buffer_copy(self.desc)
+        keep = []
+        for key, (field, ctype) in self._PIN_FIELDS.items():
+            a = arrays.get(key)
+            if not isinstance(a, np.ndarray) or a.size == 0:
+                continue
+            if key in ("env_img", "env_w") and desc.env_kind != _abi.LW_ENV_IMAGE:
+                continue
+            t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            arrays[key] = t.numpy()
+            keep.append(t)
+            setattr(desc, field, ptr(arrays[key], ctype))
+        arrays["_pinned"] = keep
+        return PackedScene(desc=desc, arrays=arrays, geometry=self.geometry, ntris=self.ntris, nemit=self.nemit)
+
 
 def _tri_areas(v):
     p = v.reshape(-1, 3, 3)
