@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--pool-log2", type=int, default=22)
     ap.add_argument("--regen-fraction", type=float, default=0.5)
     ap.add_argument("--megakernel-tail", type=int, default=0)
+    ap.add_argument("--lights", default="alias", choices=["alias", "tree"],
+                    help="NEE emitter selection: alias table (BASELINE configs) or the light hierarchy")
     ap.add_argument("--width", type=int, default=0)
     ap.add_argument("--height", type=int, default=0)
     ap.add_argument("--depth", type=int, default=0)
@@ -121,14 +123,16 @@ class ClockSampler:
 
 # ---- CPU path (oracle restatement) ----------------------------------------------------------
 
-def cpu_render_sample(a, budget_s, threads=0, it0=3):
+def cpu_render_sample(a, budget_s, threads=0, it0=3, gpu=None):
     """Bounded sample of the same workload on the host cores (oracle/lw_oracle.c, OpenMP):
-    full-frame iterations (or a band of rows when one frame exceeds the budget)."""
+    full-frame iterations (or a band of rows when one frame exceeds the budget).  With `gpu` (the
+    bench's Renderer) the same sample is rendered on the GPU and compared with the CPU framebuffer
+    (the "RMSE vs ref" half of the metric)."""
     from oracle import oracle as O
     from paper_1705_01263_b200.render import RenderParams
     from paper_1705_01263_b200.scene import pack_scene
 
-    packed = pack_scene(build_scene(a))
+    packed = pack_scene(build_scene(a), lights=a.lights)
     osc = O.OracleScene(packed)
     params = RenderParams(a.width, a.height, a.depth)
     threads = threads or os.cpu_count()
@@ -142,12 +146,24 @@ def cpu_render_sample(a, budget_s, threads=0, it0=3):
     else:
         rows, its = max(1, int(budget_s / max(per_row, 1e-9))), 1
     t0 = time.perf_counter()
-    _, st = osc.render(params, it0, it0 + its, 0, rows * a.width, nthreads=threads)
+    fb_cpu, st = osc.render(params, it0, it0 + its, 0, rows * a.width, nthreads=threads)
     dt = time.perf_counter() - t0
-    return {"value": st["paths"] / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{rows} rows x {a.width} px x {its} iterations (from iteration {it0}) of the workload: "
-                      f"{st['paths']} paths in {dt:.2f} s; oracle/lw_oracle.c (C restatement, OpenMP)",
-            "mrays_per_s": (st["rays_extension"] + st["rays_shadow"]) / dt / 1e6}
+    out = {"value": st["paths"] / dt, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{rows} rows x {a.width} px x {its} iterations (from iteration {it0}) of the workload: "
+                     f"{st['paths']} paths in {dt:.2f} s; oracle/lw_oracle.c (C restatement, OpenMP)",
+           "mrays_per_s": (st["rays_extension"] + st["rays_shadow"]) / dt / 1e6}
+    if gpu is not None:
+        import numpy as np
+
+        gpu.clear()
+        gpu.render_pass(it0, it0 + its, 0, rows * a.width)
+        fb_gpu = gpu.framebuffer()
+        scale = 1.0 / (its * 1048576.0)
+        diff = (fb_gpu[: rows * a.width].astype(np.float64) - fb_cpu[: rows * a.width].astype(np.float64)) * scale
+        out["parity"] = {"bit_exact": bool(np.array_equal(fb_gpu, fb_cpu)), "rmse": float(np.sqrt((diff ** 2).mean())),
+                         "mean_radiance": float(fb_cpu[: rows * a.width].astype(np.float64).mean() * scale),
+                         "sample": "the cpu_baseline sample rendered on the GPU vs the CPU oracle (int64 framebuffers)"}
+    return out
 
 
 def run_reference(a):
@@ -200,7 +216,7 @@ def run_ours(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    packed = pack_scene(build_scene(a))
+    packed = pack_scene(build_scene(a), lights=a.lights)
     W, H, P = a.width, a.height, a.width * a.height
     its = a.pass_iterations
     r = Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
@@ -323,7 +339,7 @@ def run_ours(a):
         "metric": metric_name(a), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic procedural scene (seeded), QMC samples",
-        "config": {"workload": workload(a), "engine": a.engine, "pool_slots": 1 << a.pool_log2,
+        "config": {"workload": workload(a), "engine": a.engine, "lights": a.lights, "pool_slots": 1 << a.pool_log2,
                    "regen_fraction": a.regen_fraction, "parallelism": f"sample-space dp{world}",
                    "l2": f"wavefront state pool (~{(1 << a.pool_log2) * 250 / 1e9:.1f} GB) exceeds the 126 MB L2 "
                          "(no flush needed); Cornell-box BVHs are shared-memory resident by design"},
@@ -343,7 +359,9 @@ def run_ours(a):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = {k: v for k, v in cpu_render_sample(a, a.cpu_seconds).items() if k != "mrays_per_s"}
+        cb = cpu_render_sample(a, a.cpu_seconds, gpu=r)
+        line["parity_vs_cpu_reference"] = cb.pop("parity")
+        line["cpu_baseline"] = {k: v for k, v in cb.items() if k != "mrays_per_s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     r.close()

@@ -110,8 +110,12 @@ typedef struct lw_scene_desc {
   double cam_up[3];
   double tan_half_fov; /* tan(fov_y / 2), computed by the host */
   int32_t bvh_kind;    /* render BVH: LW_BVH_SAH (default) or LW_BVH_MEDIAN (the reference's tree) */
-  int32_t reserved;
+  int32_t light_sampler; /* NEE emitter selection: LW_LIGHTS_ALIAS (flat alias table over weights)
+                            or LW_LIGHTS_TREE (light hierarchy) */
 } lw_scene_desc;
+
+#define LW_LIGHTS_ALIAS 0
+#define LW_LIGHTS_TREE 1
 
 #define LW_BVH_SAH 0    /* binned SAH, breadth-first */
 #define LW_BVH_MEDIAN 1 /* geometry.py:100-148 median split (built on the GPU) */
@@ -232,6 +236,18 @@ int lw_ctx_trace_closest(lw_ctx* ctx, const double* origins, const double* dirs,
 int lw_ctx_trace_any(lw_ctx* ctx, const double* origins, const double* dirs, const double* tmaxs, int64_t n,
                      int32_t* out_occluded);
 int lw_ctx_camera_rays(lw_ctx* ctx, const int64_t* sample_index, int64_t n, double* out_o, double* out_d);
+/* Light hierarchy of the uploaded scene (LW_LIGHTS_TREE; PAPER.md:215-253, SPEC.md:196-221
+ * LightHierarchy / sample_light / light_pdf).  info: node count (0 = alias-table selection).
+ * download: nodes as 15 doubles (lo[3] hi[3] tot flux[8]) + right child (leaf: -(emitter+1)),
+ * per-emitter branch bits and depth (-1 = weight 0, not in the tree).  sample: emitter, selection
+ * probability and rescaled uniform for points x with unit normals nrm.  pdf: selection
+ * probability of emitter e from (x, nrm), the MIS counterpart of sample. */
+int lw_ctx_light_tree_info(lw_ctx* ctx, int64_t* nnodes);
+int lw_ctx_light_tree_download(lw_ctx* ctx, double* nodes15, int32_t* right, uint64_t* path, int32_t* depth);
+int lw_ctx_light_sample(lw_ctx* ctx, const double* x, const double* nrm, const double* u, int64_t n,
+                        int64_t* out_e, double* out_psel, double* out_u);
+int lw_ctx_light_pdf(lw_ctx* ctx, const int64_t* e, const double* x, const double* nrm, int64_t n,
+                     double* out_psel);
 /* BVH arrays the context built (reference layout), for parity checks */
 int lw_ctx_bvh_info(lw_ctx* ctx, int64_t* nnodes);
 int lw_ctx_bvh_download(lw_ctx* ctx, double* bounds, int64_t* children, int64_t* order);

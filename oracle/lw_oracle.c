@@ -598,6 +598,14 @@ typedef struct {
   int32_t ref[2];   /* >= 0 internal node index; < 0 leaf: -(1 + (start << 3 | count)) */
 } rnode;
 
+/* light hierarchy node (device: LwLightNode) */
+typedef struct {
+  double lo[3], hi[3];
+  double tot;
+  double flux[8];
+  int32_t right;
+} lt_node;
+
 struct lwo_scene {
   lw_scene_desc d;
   int64_t ntris;
@@ -635,6 +643,11 @@ struct lwo_scene {
   int32_t* env_alias;
   double* env_pdf;
   double p_env, p_tri;
+  /* light hierarchy (light_sampler == LW_LIGHTS_TREE) */
+  int64_t lt_n;
+  lt_node* lt;
+  uint64_t* lt_path;
+  int32_t* lt_depth;
 };
 
 static int32_t leaf_ref(int64_t start, int64_t count) { return (int32_t)(-(1 + ((start << 3) | count))); }
@@ -860,6 +873,119 @@ static double* dup_d(const double* p, int64_t n) {
   return q;
 }
 
+/* ---- light hierarchy: build (restating the library's light_tree_build) --------------------
+ * Emitters of positive weight; median split (n/2 to the left) of the (centroid, emitter) order
+ * along the axis of largest centroid extent (first on ties); single-emitter leaves; depth-first
+ * node ids (left = node + 1, right = node + 2 * nleft).  Leaf: triangle box, tot = weight,
+ * flux[k] = weight * max cos of the (two-sided: either) normal towards emission octant k. */
+static double lt_octant_cos(int k, double nx, double ny, double nz) {
+  double a = (k & 1) ? -nx : nx, b = (k & 2) ? -ny : ny, c = (k & 4) ? -nz : nz;
+  a = a > 0.0 ? a : 0.0;
+  b = b > 0.0 ? b : 0.0;
+  c = c > 0.0 ? c : 0.0;
+  return sqrt((a * a + b * b) + c * c);
+}
+
+typedef struct {
+  const lw_scene_desc* d;
+  double* cen;
+  int64_t* items;
+  lwo_scene* s;
+} lt_ctx;
+
+static const double* g_lt_cen; /* comparator key (oracle build is single-threaded) */
+static int g_lt_axis;
+static int lt_cmp(const void* pa, const void* pb) {
+  int64_t x = *(const int64_t*)pa, y = *(const int64_t*)pb;
+  double cx = g_lt_cen[3 * x + g_lt_axis], cy = g_lt_cen[3 * y + g_lt_axis];
+  if (cx < cy) return -1;
+  if (cx > cy) return 1;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+static void lt_rec(lt_ctx* c, int64_t begin, int64_t end, int64_t node, uint64_t bits, int dep) {
+  lt_node* N = c->s->lt + node;
+  int64_t n = end - begin;
+  if (n == 1) {
+    int64_t e = c->items[begin];
+    const double* v = c->s->verts + 9 * c->d->emit_tri[e];
+    for (int a = 0; a < 3; a++) {
+      double lo = v[a], hi = v[a];
+      if (v[3 + a] < lo) lo = v[3 + a];
+      if (v[6 + a] < lo) lo = v[6 + a];
+      if (v[3 + a] > hi) hi = v[3 + a];
+      if (v[6 + a] > hi) hi = v[6 + a];
+      N->lo[a] = lo;
+      N->hi[a] = hi;
+    }
+    double e1x = v[3] - v[0], e1y = v[4] - v[1], e1z = v[5] - v[2];
+    double e2x = v[6] - v[0], e2y = v[7] - v[1], e2z = v[8] - v[2];
+    double cx = e1y * e2z - e1z * e2y, cy = e1z * e2x - e1x * e2z, cz = e1x * e2y - e1y * e2x;
+    double inv = 1.0 / sqrt((cx * cx + cy * cy) + cz * cz);
+    double nx = cx * inv, ny = cy * inv, nz = cz * inv;
+    double w = c->d->emit_weight[e];
+    N->tot = w;
+    for (int k = 0; k < 8; k++) {
+      double cc = lt_octant_cos(k, nx, ny, nz);
+      if (c->d->emit_twosided[e]) {
+        double c2 = lt_octant_cos(k, -nx, -ny, -nz);
+        if (c2 > cc) cc = c2;
+      }
+      N->flux[k] = w * cc;
+    }
+    N->right = (int32_t)(-(e + 1));
+    c->s->lt_path[e] = bits;
+    c->s->lt_depth[e] = dep;
+    return;
+  }
+  double cmin[3] = {INFINITY, INFINITY, INFINITY}, cmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = begin; i < end; i++)
+    for (int a = 0; a < 3; a++) {
+      double cv = c->cen[3 * c->items[i] + a];
+      if (cv < cmin[a]) cmin[a] = cv;
+      if (cv > cmax[a]) cmax[a] = cv;
+    }
+  int axis = 0;
+  for (int a = 1; a < 3; a++)
+    if (cmax[a] - cmin[a] > cmax[axis] - cmin[axis]) axis = a;
+  g_lt_cen = c->cen;
+  g_lt_axis = axis;
+  qsort(c->items + begin, (size_t)n, sizeof(int64_t), lt_cmp);
+  int64_t nl = n / 2;
+  int64_t left = node + 1, right = node + 2 * nl;
+  lt_rec(c, begin, begin + nl, left, bits, dep + 1);
+  lt_rec(c, begin + nl, end, right, bits | (1ULL << dep), dep + 1);
+  const lt_node *L = c->s->lt + left, *R = c->s->lt + right;
+  N = c->s->lt + node;
+  for (int a = 0; a < 3; a++) {
+    N->lo[a] = L->lo[a] < R->lo[a] ? L->lo[a] : R->lo[a];
+    N->hi[a] = L->hi[a] > R->hi[a] ? L->hi[a] : R->hi[a];
+  }
+  N->tot = L->tot + R->tot;
+  for (int k = 0; k < 8; k++) N->flux[k] = L->flux[k] + R->flux[k];
+  N->right = (int32_t)right;
+}
+
+static void lt_build(lwo_scene* s, const lw_scene_desc* d) {
+  int64_t ne = d->nemit;
+  lt_ctx c = {d, (double*)malloc(sizeof(double) * 3 * (ne > 0 ? ne : 1)),
+              (int64_t*)malloc(sizeof(int64_t) * (ne > 0 ? ne : 1)), s};
+  s->lt_path = (uint64_t*)calloc(ne > 0 ? ne : 1, sizeof(uint64_t));
+  s->lt_depth = (int32_t*)malloc(sizeof(int32_t) * (ne > 0 ? ne : 1));
+  int64_t m = 0;
+  for (int64_t e = 0; e < ne; e++) {
+    const double* v = s->verts + 9 * d->emit_tri[e];
+    for (int a = 0; a < 3; a++) c.cen[3 * e + a] = ((v[a] + v[3 + a]) + v[6 + a]) / 3.0;
+    s->lt_depth[e] = -1;
+    if (d->emit_weight[e] > 0.0) c.items[m++] = e;
+  }
+  s->lt_n = m > 0 ? 2 * m - 1 : 0;
+  s->lt = (lt_node*)calloc(s->lt_n > 0 ? s->lt_n : 1, sizeof(lt_node));
+  if (m > 0) lt_rec(&c, 0, m, 0, 0ULL, 0);
+  free(c.cen);
+  free(c.items);
+}
+
 lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
   lwo_scene* s = (lwo_scene*)calloc(1, sizeof(lwo_scene));
   s->d = *d;
@@ -904,6 +1030,7 @@ lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
     }
     if (lwo_alias_build(d->emit_weight, s->nemit, s->emit_prob, s->emit_alias, s->emit_pdf)) s->nemit = 0;
   }
+  if (d->light_sampler == LW_LIGHTS_TREE && s->nemit > 0) lt_build(s, d);
   s->env_kind = d->env_kind;
   s->env_w = d->env_width;
   s->env_h = d->env_height;
@@ -947,6 +1074,9 @@ void lwo_scene_destroy(lwo_scene* s) {
   free(s->env_prob);
   free(s->env_alias);
   free(s->env_pdf);
+  free(s->lt);
+  free(s->lt_path);
+  free(s->lt_depth);
   free(s);
 }
 
@@ -1202,6 +1332,123 @@ static v3 offset_origin(v3 p, v3 n, v3 dir) {
   return mk(p.x + n.x * sgn, p.y + n.y * sgn, p.z + n.z * sgn);
 }
 
+/* ---- light hierarchy: sample_light / light_pdf (device: lw_lighttree.cuh) ---------------- */
+#define LT_PMIN 0.015625 /* 1/64: branch probabilities clamped to [PMIN, 1 - PMIN] */
+
+static double lt_importance(const lt_node* N, v3 x, v3 n) {
+  v3 c = mk((N->lo[0] + N->hi[0]) * 0.5, (N->lo[1] + N->hi[1]) * 0.5, (N->lo[2] + N->hi[2]) * 0.5);
+  v3 dx = sub(c, x);
+  double d2 = dot(dx, dx);
+  v3 ext = mk(N->hi[0] - N->lo[0], N->hi[1] - N->lo[1], N->hi[2] - N->lo[2]);
+  double r2 = dot(ext, ext) * 0.25;
+  double dist2 = d2 > r2 ? d2 : r2;
+  int inside = x.x >= N->lo[0] && x.x <= N->hi[0] && x.y >= N->lo[1] && x.y <= N->hi[1] && x.z >= N->lo[2] &&
+               x.z <= N->hi[2];
+  if (inside || !(d2 > r2)) return dist2 > 0.0 ? N->tot / dist2 : N->tot;
+  int oct = (dx.x > 0.0 ? 1 : 0) | (dx.y > 0.0 ? 2 : 0) | (dx.z > 0.0 ? 4 : 0); /* signs of x - c */
+  double d = sqrt(d2);
+  double cos_t = dot(n, dx) / d;
+  double sin2a = r2 / d2;
+  double cos_a = sqrt(1.0 - sin2a);
+  double cosb = 1.0;
+  if (cos_t < cos_a) { /* cos(theta - alpha), the largest cosine over the box's bounding cone */
+    double s2 = 1.0 - cos_t * cos_t;
+    double sin_t = sqrt(s2 > 0.0 ? s2 : 0.0);
+    cosb = cos_t * cos_a + sin_t * sqrt(sin2a);
+    if (cosb < 0.0) cosb = 0.0;
+  }
+  return N->flux[oct] * cosb / dist2;
+}
+
+static double lt_pleft(const lwo_scene* s, int64_t k, v3 x, v3 n) {
+  double il = lt_importance(s->lt + k + 1, x, n);
+  double ir = lt_importance(s->lt + s->lt[k].right, x, n);
+  double sum = il + ir;
+  double pl = sum > 0.0 ? il / sum : 0.5;
+  if (pl < LT_PMIN) pl = LT_PMIN;
+  if (pl > 1.0 - LT_PMIN) pl = 1.0 - LT_PMIN;
+  return pl;
+}
+
+static int64_t lt_sample(const lwo_scene* s, v3 x, v3 n, double u, double* psel, double* u_out) {
+  int64_t k = 0;
+  double p = 1.0;
+  while (s->lt[k].right >= 0) {
+    double pl = lt_pleft(s, k, x, n);
+    if (u < pl) {
+      u = u / pl;
+      p = p * pl;
+      k = k + 1;
+    } else {
+      u = (u - pl) / (1.0 - pl);
+      p = p * (1.0 - pl);
+      k = s->lt[k].right;
+    }
+  }
+  if (u >= 1.0) u = 0.9999999999999999;
+  if (u < 0.0) u = 0.0;
+  *psel = p;
+  *u_out = u;
+  return -(int64_t)s->lt[k].right - 1;
+}
+
+static double lt_pdf(const lwo_scene* s, int64_t e, v3 x, v3 n) {
+  int dep = s->lt_depth[e];
+  if (dep < 0) return 0.0;
+  uint64_t bits = s->lt_path[e];
+  int64_t k = 0;
+  double p = 1.0;
+  for (int l = 0; l < dep; l++) {
+    double pl = lt_pleft(s, k, x, n);
+    if (((bits >> l) & 1ULL) == 0) {
+      p = p * pl;
+      k = k + 1;
+    } else {
+      p = p * (1.0 - pl);
+      k = s->lt[k].right;
+    }
+  }
+  return p;
+}
+
+/* reference normal of the estimates: the facing geometric normal through the octahedral packing */
+static v3 lt_ref_normal(int64_t packed) {
+  double o[3];
+  lwo_oct_decode(packed, o);
+  return normalize(mk(o[0], o[1], o[2]));
+}
+
+int64_t lwo_light_tree(const lwo_scene* s, double* nodes15, int32_t* right, uint64_t* path, int32_t* depth) {
+  if (!s->lt) return 0;
+  for (int64_t k = 0; nodes15 && k < s->lt_n; k++) {
+    const lt_node* N = s->lt + k;
+    double* o = nodes15 + 15 * k;
+    for (int a = 0; a < 3; a++) {
+      o[a] = N->lo[a];
+      o[3 + a] = N->hi[a];
+    }
+    o[6] = N->tot;
+    for (int b = 0; b < 8; b++) o[7 + b] = N->flux[b];
+    if (right) right[k] = N->right;
+  }
+  for (int64_t e = 0; path && e < s->d.nemit; e++) {
+    path[e] = s->lt_path[e];
+    depth[e] = s->lt_depth[e];
+  }
+  return s->lt_n;
+}
+
+void lwo_light_sample_batch(const lwo_scene* s, const double* x, const double* nrm, const double* u, int64_t n,
+                            int64_t* out_e, double* out_psel, double* out_u) {
+  for (int64_t i = 0; i < n; i++)
+    out_e[i] = lt_sample(s, ld3(x + 3 * i), ld3(nrm + 3 * i), u[i], out_psel + i, out_u + i);
+}
+
+void lwo_light_pdf_batch(const lwo_scene* s, const int64_t* e, const double* x, const double* nrm, int64_t n,
+                         double* out_psel) {
+  for (int64_t i = 0; i < n; i++) out_psel[i] = lt_pdf(s, e[i], ld3(x + 3 * i), ld3(nrm + 3 * i));
+}
+
 /* environment lookup: lat-long, y up, row 0 at +y */
 static v3 env_eval(const lwo_scene* s, v3 d, double* pdf) {
   if (s->env_kind == LW_ENV_CONSTANT) {
@@ -1438,6 +1685,7 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
   v3 beta = mk(1, 1, 1), L = mk(0, 0, 0);
   int spec_prev = 1;
   double pdf_prev = 0.0;
+  int64_t nprev = 0; /* packed facing normal of the previous vertex (light-tree MIS) */
   for (int b = 0; b < depth; b++) {
     hitrec h;
     trace_closest(s, &o.x, &d.x, INFINITY, &h);
@@ -1465,7 +1713,8 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
       double wm = 1.0;
       if (!spec_prev) {
         double cos_l = fabs(dot(ng, d));
-        double pdf_area = s->p_tri * s->emit_pdf[e] / s->emit_area[e];
+        double psel = s->lt ? lt_pdf(s, e, o, lt_ref_normal(nprev)) : s->emit_pdf[e];
+        double pdf_area = s->p_tri * psel / s->emit_area[e];
         double pl = pdf_area * (h.t * h.t) / cos_l;
         wm = pdf_prev / (pdf_prev + pl);
       }
@@ -1523,8 +1772,16 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
         }
       } else if (s->nemit > 0) {
         double ut = s->env_kind != LW_ENV_NONE ? (ul - s->p_env) / (1.0 - s->p_env) : ul;
-        double ur;
-        int64_t le = alias_sample(s->emit_prob, s->emit_alias, s->nemit, ut, &ur);
+        double ur, psel;
+        int64_t le;
+        if (s->lt) {
+          v3 xr = offset_origin(p, ngf, ngf);
+          v3 nr = lt_ref_normal(lwo_oct_encode(ngf.x, ngf.y, ngf.z));
+          le = lt_sample(s, xr, nr, ut, &psel, &ur);
+        } else {
+          le = alias_sample(s->emit_prob, s->emit_alias, s->nemit, ut, &ur);
+          psel = s->emit_pdf[le];
+        }
         const double* lv = s->verts + 9 * s->emit_tri[le];
         v3 l0 = ld3(lv), l1 = ld3(lv + 3), l2 = ld3(lv + 6);
         double su = sqrt(ur);
@@ -1540,7 +1797,7 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
         double cos_l = -dot(ngl, wi);
         if (s->emit_two[le]) cos_l = fabs(cos_l);
         if (cos_l > 0.0 && dist > 0.0) {
-          pl = (s->p_tri * s->emit_pdf[le] / s->emit_area[le]) * dist2 / cos_l;
+          pl = (s->p_tri * psel / s->emit_area[le]) * dist2 / cos_l;
           Le = ld3(s->emit_rad + 3 * le);
           tmax_sh = dist * (1.0 - 1e-7);
           ok = 1;
@@ -1582,6 +1839,7 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
     }
     o = offset_origin(p, ngf, wi);
     d = wi;
+    nprev = lwo_oct_encode(ngf.x, ngf.y, ngf.z);
   }
   return L;
 }

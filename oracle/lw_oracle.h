@@ -61,6 +61,17 @@ void lwo_camera_rays(const lwo_scene* s, const lw_render_params* p, const int64_
 void lwo_render(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin, int64_t pix_end,
                 int64_t it_begin, int64_t it_end, int64_t* fb, int nthreads, lw_render_stats* stats);
 
+/* Light hierarchy (device: lw_lighttree.cuh).  Node record =
+ * lo[3] hi[3] tot flux[8] as 15 doubles + right child (or -(emitter+1) at a leaf).
+ * lwo_light_tree: node count (0 when the scene uses the alias table); copies when outputs given. */
+int64_t lwo_light_tree(const lwo_scene* s, double* nodes15, int32_t* right, uint64_t* path, int32_t* depth);
+/* sample_light from points x with unit normals nrm and uniforms u: emitter, selection probability,
+ * rescaled uniform.  light_pdf: selection probability of emitter e from (x, nrm). */
+void lwo_light_sample_batch(const lwo_scene* s, const double* x, const double* nrm, const double* u, int64_t n,
+                            int64_t* out_e, double* out_psel, double* out_u);
+void lwo_light_pdf_batch(const lwo_scene* s, const int64_t* e, const double* x, const double* nrm, int64_t n,
+                         double* out_psel);
+
 /* Deterministic math shared by oracle and device (restated independently in lw_detmath.cuh). */
 void lwo_sincos2pi(double u, double* s, double* c);
 double lwo_atan2(double y, double x);

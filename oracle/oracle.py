@@ -45,6 +45,9 @@ _SIG = {
     "lwo_trace_closest_batch": (None, [_V, _pd, _pd, _pd, C.c_int64, _pd, _pi64, _pd]),
     "lwo_trace_any_batch": (None, [_V, _pd, _pd, _pd, C.c_int64, _pi32]),
     "lwo_camera_rays": (None, [_V, C.POINTER(LwRenderParams), _pi64, C.c_int64, _pd, _pd]),
+    "lwo_light_tree": (C.c_int64, [_V, _pd, _pi32, C.POINTER(C.c_uint64), _pi32]),
+    "lwo_light_sample_batch": (None, [_V, _pd, _pd, _pd, C.c_int64, _pi64, _pd, _pd]),
+    "lwo_light_pdf_batch": (None, [_V, _pi64, _pd, _pd, C.c_int64, _pd]),
     "lwo_render": (None, [_V, C.POINTER(LwRenderParams), C.c_int64, C.c_int64, C.c_int64, C.c_int64, _pi64, C.c_int, C.POINTER(LwRenderStats)]),
     "lwo_sincos2pi": (None, [C.c_double, _pd, _pd]),
     "lwo_atan2": (C.c_double, [C.c_double, C.c_double]),
@@ -202,6 +205,39 @@ class OracleScene:
         lib().lwo_trace_any_batch(self.h, ptr(o, C.c_double), ptr(d, C.c_double), ptr(tm, C.c_double), n,
                                   ptr(occ, C.c_int32))
         return occ
+
+    def light_tree(self):
+        """Light hierarchy (oracle lt_build): (nodes [n,15], right [n], path, depth) or None."""
+        n = lib().lwo_light_tree(self.h, None, None, None, None)
+        if n == 0:
+            return None
+        ne = self.packed.nemit
+        nodes = np.empty((n, 15))
+        right = np.empty(n, np.int32)
+        path = np.empty(max(ne, 1), np.uint64)
+        depth = np.empty(max(ne, 1), np.int32)
+        lib().lwo_light_tree(self.h, ptr(nodes, C.c_double), ptr(right, C.c_int32), ptr(path, C.c_uint64),
+                             ptr(depth, C.c_int32))
+        return nodes, right, path[:ne], depth[:ne]
+
+    def light_sample(self, x, nrm, u):
+        x = np.ascontiguousarray(x, np.float64)
+        nrm = np.ascontiguousarray(nrm, np.float64)
+        u = np.ascontiguousarray(u, np.float64)
+        n = len(u)
+        e, p, uo = np.empty(n, np.int64), np.empty(n), np.empty(n)
+        lib().lwo_light_sample_batch(self.h, ptr(x, C.c_double), ptr(nrm, C.c_double), ptr(u, C.c_double), n,
+                                     ptr(e, C.c_int64), ptr(p, C.c_double), ptr(uo, C.c_double))
+        return e, p, uo
+
+    def light_pdf(self, e, x, nrm):
+        e = np.ascontiguousarray(e, np.int64)
+        x = np.ascontiguousarray(x, np.float64)
+        nrm = np.ascontiguousarray(nrm, np.float64)
+        p = np.empty(len(e))
+        lib().lwo_light_pdf_batch(self.h, ptr(e, C.c_int64), ptr(x, C.c_double), ptr(nrm, C.c_double), len(e),
+                                  ptr(p, C.c_double))
+        return p
 
     def camera_rays(self, params, sample_index):
         idx = np.ascontiguousarray(sample_index, np.int64)

@@ -95,10 +95,12 @@ class LwSceneDesc(C.Structure):
         ("cam_up", C.c_double * 3),
         ("tan_half_fov", C.c_double),
         ("bvh_kind", C.c_int32),
-        ("reserved", C.c_int32),
+        ("light_sampler", C.c_int32),
     ]
 
 
+LW_LIGHTS_ALIAS = 0
+LW_LIGHTS_TREE = 1
 LW_BVH_SAH = 0
 LW_BVH_MEDIAN = 1
 
@@ -210,6 +212,10 @@ SIGNATURES = {
     "lw_ctx_trace_closest": (C.c_int, [_V, _pd, _pd, _pd, C.c_int64, _pd, _pi64, _pd]),
     "lw_ctx_trace_any": (C.c_int, [_V, _pd, _pd, _pd, C.c_int64, _pi32]),
     "lw_ctx_camera_rays": (C.c_int, [_V, _pi64, C.c_int64, _pd, _pd]),
+    "lw_ctx_light_tree_info": (C.c_int, [_V, _pi64]),
+    "lw_ctx_light_tree_download": (C.c_int, [_V, _pd, _pi32, C.POINTER(C.c_uint64), _pi32]),
+    "lw_ctx_light_sample": (C.c_int, [_V, _pd, _pd, _pd, C.c_int64, _pi64, _pd, _pd]),
+    "lw_ctx_light_pdf": (C.c_int, [_V, _pi64, _pd, _pd, C.c_int64, _pd]),
     "lw_ctx_bvh_info": (C.c_int, [_V, _pi64]),
     "lw_ctx_bvh_download": (C.c_int, [_V, _pd, _pi64, _pi64]),
     "lw_ctx_last_pass_timing": (C.c_int, [_V, _pd, _pd, _pi64]),

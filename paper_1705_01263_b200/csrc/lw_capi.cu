@@ -7,6 +7,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "lw_common.cuh"
@@ -85,6 +86,117 @@ int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_fla
     for (uint64_t v = 0xffffffffULL; v; v /= (uint64_t)b) nd++;
     q.digits32 = (b != 2 && perm_flat[perm_offset[k]] == 0) ? nd : 0;
   }
+  return LW_OK;
+}
+
+// ---- light hierarchy (oracle lt_build) ------------------------------------------------------
+namespace {
+struct LtBuild {
+  const double* verts;
+  const int64_t* tri;
+  const double* w;
+  const int32_t* two;
+  std::vector<double> cen;  // [nemit*3]
+  std::vector<int64_t> items;
+  std::vector<LwLightNode>* nodes;
+  std::vector<unsigned long long>* path;
+  std::vector<int>* depth;
+};
+
+void lt_leaf(LtBuild& b, int64_t e, LwLightNode& N) {
+  const double* v = b.verts + 9 * b.tri[e];
+  for (int a = 0; a < 3; a++) {
+    double lo = v[a], hi = v[a];
+    if (v[3 + a] < lo) lo = v[3 + a];
+    if (v[6 + a] < lo) lo = v[6 + a];
+    if (v[3 + a] > hi) hi = v[3 + a];
+    if (v[6 + a] > hi) hi = v[6 + a];
+    N.lo[a] = lo;
+    N.hi[a] = hi;
+  }
+  double e1x = v[3] - v[0], e1y = v[4] - v[1], e1z = v[5] - v[2];
+  double e2x = v[6] - v[0], e2y = v[7] - v[1], e2z = v[8] - v[2];
+  double cx = e1y * e2z - e1z * e2y, cy = e1z * e2x - e1x * e2z, cz = e1x * e2y - e1y * e2x;
+  double inv = 1.0 / sqrt((cx * cx + cy * cy) + cz * cz);
+  double nx = cx * inv, ny = cy * inv, nz = cz * inv;
+  N.tot = b.w[e];
+  for (int k = 0; k < 8; k++) {
+    double c = lw_lt_octant_cos(k, nx, ny, nz);
+    if (b.two[e]) {
+      double c2 = lw_lt_octant_cos(k, -nx, -ny, -nz);
+      if (c2 > c) c = c2;
+    }
+    N.flux[k] = b.w[e] * c;
+  }
+  N.right = (int)(-(e + 1));
+  N.pad = 0;
+}
+
+void lt_rec(LtBuild& b, int64_t begin, int64_t end, int64_t node, unsigned long long bits, int dep) {
+  LwLightNode& N = (*b.nodes)[node];
+  int64_t n = end - begin;
+  if (n == 1) {
+    int64_t e = b.items[begin];
+    lt_leaf(b, e, N);
+    (*b.path)[e] = bits;
+    (*b.depth)[e] = dep;
+    return;
+  }
+  double cmin[3] = {INFINITY, INFINITY, INFINITY}, cmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = begin; i < end; i++)
+    for (int a = 0; a < 3; a++) {
+      double c = b.cen[3 * b.items[i] + a];
+      if (c < cmin[a]) cmin[a] = c;
+      if (c > cmax[a]) cmax[a] = c;
+    }
+  int axis = 0;
+  for (int a = 1; a < 3; a++)
+    if (cmax[a] - cmin[a] > cmax[axis] - cmin[axis]) axis = a;
+  const double* cen = b.cen.data();
+  std::sort(b.items.begin() + begin, b.items.begin() + end, [cen, axis](int64_t x, int64_t y) {
+    double cx = cen[3 * x + axis], cy = cen[3 * y + axis];
+    return cx < cy || (cx == cy && x < y);
+  });
+  int64_t nl = n / 2;
+  int64_t left = node + 1, right = node + 2 * nl;
+  lt_rec(b, begin, begin + nl, left, bits, dep + 1);
+  lt_rec(b, begin + nl, end, right, bits | (1ULL << dep), dep + 1);
+  const LwLightNode &L = (*b.nodes)[left], &R = (*b.nodes)[right];
+  LwLightNode& M = (*b.nodes)[node];
+  for (int a = 0; a < 3; a++) {
+    M.lo[a] = L.lo[a] < R.lo[a] ? L.lo[a] : R.lo[a];
+    M.hi[a] = L.hi[a] > R.hi[a] ? L.hi[a] : R.hi[a];
+  }
+  M.tot = L.tot + R.tot;
+  for (int k = 0; k < 8; k++) M.flux[k] = L.flux[k] + R.flux[k];
+  M.right = (int)right;
+  M.pad = 0;
+}
+}  // namespace
+
+int light_tree_build(const double* verts, const int64_t* emit_tri, const double* weight, const int32_t* twosided,
+                     int64_t nemit, std::vector<LwLightNode>& nodes, std::vector<unsigned long long>& path,
+                     std::vector<int>& depth) {
+  LtBuild b;
+  b.verts = verts;
+  b.tri = emit_tri;
+  b.w = weight;
+  b.two = twosided;
+  b.cen.resize(3 * (size_t)(nemit > 0 ? nemit : 1));
+  path.assign(nemit > 0 ? nemit : 1, 0ULL);
+  depth.assign(nemit > 0 ? nemit : 1, -1);
+  for (int64_t e = 0; e < nemit; e++) {
+    const double* v = verts + 9 * emit_tri[e];
+    for (int a = 0; a < 3; a++) b.cen[3 * e + a] = ((v[a] + v[3 + a]) + v[6 + a]) / 3.0;
+    if (weight[e] > 0.0) b.items.push_back(e);
+  }
+  int64_t m = (int64_t)b.items.size();
+  nodes.assign(m > 0 ? 2 * m - 1 : 0, LwLightNode());
+  LW_CHECK_ARG(m < (1LL << 30), "light tree: too many emitters");
+  b.nodes = &nodes;
+  b.path = &path;
+  b.depth = &depth;
+  if (m > 0) lt_rec(b, 0, m, 0, 0ULL, 0);
   return LW_OK;
 }
 

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/lw_b200.h"
+#include "lw_lighttree.cuh"
 #include "lw_qmc.cuh"
 
 namespace lw {
@@ -18,6 +19,12 @@ int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_fla
 
 // Vose alias table; same operation order as the oracle
 int alias_build(const double* w, int64_t n, double* prob, int32_t* alias, double* pdf);
+
+// light hierarchy over the emitters of positive weight (lw_lighttree.cuh; oracle lt_build):
+// depth-first nodes, per-emitter branch bits and depth (-1 = not in the tree)
+int light_tree_build(const double* verts, const int64_t* emit_tri, const double* weight, const int32_t* twosided,
+                     int64_t nemit, std::vector<LwLightNode>& nodes, std::vector<unsigned long long>& path,
+                     std::vector<int>& depth);
 
 // Device BVH build (geometry.py:100-148 semantics).  d_verts [ntris*9] on the device.
 // Outputs are device arrays owned by the caller after the call (cudaFree).

@@ -9,6 +9,7 @@
 #pragma once
 #include "lw_common.cuh"
 #include "lw_detmath.cuh"
+#include "lw_lighttree.cuh"
 #include "lw_qmc.cuh"
 #include "lw_traverse.cuh"
 
@@ -27,6 +28,11 @@ struct DevScene {
   const double* emit_prob;
   const double* emit_pdf;
   const int* emit_alias;
+  // light hierarchy (light_mode == LW_LIGHTS_TREE)
+  const LwLightNode* lt_nodes;
+  const unsigned long long* lt_path;
+  const int* lt_depth;
+  int light_mode;
   int env_kind;
   int env_w, env_h;
   const float* env_img;
@@ -50,6 +56,7 @@ struct PathState {
   long long index;
   int bounce;
   int spec_prev;
+  int nprev;  // octahedral-packed facing geometric normal of the previous vertex (light-tree MIS)
 };
 
 struct ShadowRay {
@@ -335,7 +342,13 @@ __device__ __forceinline__ void lw_path_init(const DevScene& S, long long index,
   ps.index = index;
   ps.bounce = 0;
   ps.spec_prev = 1;
+  ps.nprev = 0;
 }
+
+// reference point and normal of the light-hierarchy estimates at a vertex: the reflection-side
+// offset point (the origin of NEE and of reflected continuation rays) and the facing geometric
+// normal rounded through the octahedral packing, which is what the next vertex sees for MIS
+__device__ __forceinline__ v3 lw_lt_ref_normal(int packed) { return normalize3(lw_oct_decode((long long)packed)); }
 
 // ---- material / NEE stage (oracle trace_path loop body), split into reusable parts ----------
 // The megakernel calls lw_path_shade (all parts in order); the wavefront runs lw_shade_nee and
@@ -419,8 +432,16 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
     }
   } else if (S.nemit > 0) {
     double ut = S.env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
-    double ur;
-    long long le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
+    double ur, psel;
+    long long le;
+    if (S.light_mode == LW_LIGHTS_TREE) {
+      v3 xr = lw_offset_origin(g.p, g.ngf, g.ngf);
+      v3 nr = lw_lt_ref_normal((int)lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z));
+      le = lw_lt_sample(S.lt_nodes, xr, nr, ut, psel, ur);
+    } else {
+      le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
+      psel = S.emit_pdf[le];
+    }
     const double* lv = S.verts + 9 * S.emit_tri[le];
     v3 l0 = lw_ld3(lv), l1 = lw_ld3(lv + 3), l2 = lw_ld3(lv + 6);
     double su = sqrt(ur);
@@ -436,7 +457,7 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
     double cos_l = -dot3(ngl, wi);
     if (S.emit_two[le]) cos_l = fabs(cos_l);
     if (cos_l > 0.0 && dist > 0.0) {
-      pl = (S.p_tri * S.emit_pdf[le] / S.emit_area[le]) * dist2 / cos_l;
+      pl = (S.p_tri * psel / S.emit_area[le]) * dist2 / cos_l;
       Le = lw_ld3(S.emit_rad + 3 * le);
       tmax_sh = dist * (1.0 - 1e-7);
       ok = true;
@@ -478,7 +499,10 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
     double wm = 1.0;
     if (!ps.spec_prev) {
       double cos_l = fabs(dot3(g.ng, d));
-      double pdf_area = S.p_tri * S.emit_pdf[e] / S.emit_area[e];
+      double psel = S.light_mode == LW_LIGHTS_TREE
+                        ? lw_lt_pdf(S.lt_nodes, S.lt_path, S.lt_depth, e, ps.o, lw_lt_ref_normal(ps.nprev))
+                        : S.emit_pdf[e];
+      double pdf_area = S.p_tri * psel / S.emit_area[e];
       double pl = pdf_area * (h.t * h.t) / cos_l;
       wm = ps.pdf_prev / (ps.pdf_prev + pl);
     }
@@ -513,6 +537,7 @@ __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& 
   ps.o = lw_offset_origin(g.p, g.ngf, wi);
   ps.d = wi;
   ps.bounce = b + 1;
+  ps.nprev = (int)lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z);
   return true;
 }
 

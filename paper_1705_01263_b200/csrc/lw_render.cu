@@ -60,6 +60,7 @@ struct Pool {
   double2 *sh0, *sh1, *sh2, *sh3, *sh4;  // shadow (o.x,o.y) (o.z,d.x) (d.y,d.z) (tmax,c.x) (c.y,c.z)
   int* pix;
   int* flags;  // bounce | spec_prev << 8
+  int* nprev;  // octahedral-packed facing normal of the previous vertex (light-tree MIS)
   unsigned char* stage;  // LW_STAGE_GENERATE / TRACE / TERMINATED
   int *q_ext, *q_shadow;
   void* block = nullptr;
@@ -75,6 +76,7 @@ struct lw_ctx {
   std::vector<void*> scene_allocs;
   DeviceBVH ref_bvh;
   bool ref_built = false;
+  int64_t lt_nodes = 0;  // light hierarchy nodes (0 = alias-table light selection)
   int64_t ntris = 0;
   lw_render_params params;
   QmcDim* d_qdims = nullptr;
@@ -121,6 +123,7 @@ void free_scene(lw_ctx* c) {
   if (c->ref_bvh.order) cudaFreeAsync(c->ref_bvh.order, c->stream);
   c->ref_bvh = DeviceBVH();
   c->ref_built = false;
+  c->lt_nodes = 0;
   c->has_scene = false;
 }
 
@@ -400,6 +403,7 @@ __device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) 
   int f = P.flags[s];
   ps.bounce = f & F_BOUNCE;
   ps.spec_prev = (f & F_SPEC) ? 1 : 0;
+  ps.nprev = P.nprev[s];
 }
 
 __device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps) {
@@ -411,6 +415,7 @@ __device__ __forceinline__ void store_state(const Pool& P, int s, const PathStat
   P.tp2[s] = make_double2(ps.L.y, ps.L.z);
   P.misc[s] = make_double2(ps.pdf_prev, __longlong_as_double(ps.index));
   P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0);
+  P.nprev[s] = ps.nprev;
 }
 
 __device__ __forceinline__ v3 load_L(const Pool& P, int s) {
@@ -741,6 +746,23 @@ __global__ void k_camera_dbg(DevScene S, const long long* idx, long long n, doub
   od[3 * i + 2] = d.z;
 }
 
+__global__ void k_light_sample_dbg(DevScene S, const double* x, const double* nrm, const double* u, long long n,
+                                   long long* oe, double* op, double* ou) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ps, uo;
+  oe[i] = lw_lt_sample(S.lt_nodes, lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i), u[i], ps, uo);
+  op[i] = ps;
+  ou[i] = uo;
+}
+
+__global__ void k_light_pdf_dbg(DevScene S, const long long* e, const double* x, const double* nrm, long long n,
+                                double* op) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  op[i] = lw_lt_pdf(S.lt_nodes, S.lt_path, S.lt_depth, e[i], lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i));
+}
+
 __global__ void k_resolve(const unsigned long long* fb, long long n, double scale, float* out) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[i] = (float)((double)(long long)fb[i] * scale);
@@ -788,7 +810,7 @@ int alloc_pool(lw_ctx* c, int size) {
   free_pool(c);
   Pool& P = c->pool;
   const size_t nvec = 14;  // double2 arrays
-  size_t bytes = (size_t)size * (nvec * 16 + 4 * 4 + 1) + 8192;
+  size_t bytes = (size_t)size * (nvec * 16 + 5 * 4 + 1) + 8192;
   LW_CUDA_TRY(cudaMallocAsync(&P.block, bytes, c->stream));
   char* p = (char*)P.block;
   auto v2 = [&](double2*& x) {
@@ -804,7 +826,7 @@ int alloc_pool(lw_ctx* c, int size) {
   v2(P.misc);
   v2(P.hit0); v2(P.hit1);
   v2(P.sh0); v2(P.sh1); v2(P.sh2); v2(P.sh3); v2(P.sh4);
-  ii(P.pix); ii(P.flags);
+  ii(P.pix); ii(P.flags); ii(P.nprev);
   ii(P.q_ext); ii(P.q_shadow);
   P.stage = (unsigned char*)p;
   P.size = size;
@@ -1217,6 +1239,29 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     S.emit_alias = eal;
     LW_CUDA_TRY(cudaStreamSynchronize(st));
   }
+  // light hierarchy, built on the host like the alias tables
+  S.light_mode = LW_LIGHTS_ALIAS;
+  S.lt_nodes = nullptr;
+  S.lt_path = nullptr;
+  S.lt_depth = nullptr;
+  if (d->light_sampler == LW_LIGHTS_TREE && S.nemit > 0) {
+    std::vector<LwLightNode> ln;
+    std::vector<unsigned long long> lp;
+    std::vector<int> ld;
+    LW_STATUS_TRY(light_tree_build(d->verts, d->emit_tri, d->emit_weight, d->emit_twosided, d->nemit, ln, lp, ld));
+    LwLightNode* dn;
+    unsigned long long* dp;
+    int* dd;
+    LW_STATUS_TRY(dev_upload(c, dn, ln.data(), (int64_t)ln.size()));
+    LW_STATUS_TRY(dev_upload(c, dp, lp.data(), (int64_t)lp.size()));
+    LW_STATUS_TRY(dev_upload(c, dd, ld.data(), (int64_t)ld.size()));
+    LW_CUDA_TRY(cudaStreamSynchronize(st));  // host vectors go out of scope
+    S.lt_nodes = dn;
+    S.lt_path = dp;
+    S.lt_depth = dd;
+    S.light_mode = LW_LIGHTS_TREE;
+    c->lt_nodes = (int64_t)ln.size();
+  }
   // environment
   S.env_kind = d->env_kind;
   S.env_w = d->env_width;
@@ -1475,6 +1520,85 @@ int lw_ctx_bvh_download(lw_ctx* c, double* bounds, int64_t* children, int64_t* o
   if (c->ntris > 0 && order)
     LW_CUDA_TRY(cudaMemcpyAsync(order, c->ref_bvh.order, sizeof(long long) * c->ntris, cudaMemcpyDeviceToHost, c->stream));
   LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_light_tree_info(lw_ctx* c, int64_t* nnodes) {
+  LW_CHECK_ARG(c && c->has_scene && nnodes, "no scene");
+  *nnodes = c->lt_nodes;
+  return LW_OK;
+}
+
+int lw_ctx_light_tree_download(lw_ctx* c, double* nodes15, int32_t* right, uint64_t* path, int32_t* depth) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  if (c->lt_nodes == 0) return LW_OK;
+  std::vector<LwLightNode> h(c->lt_nodes);
+  LW_CUDA_TRY(cudaMemcpyAsync(h.data(), c->S.lt_nodes, sizeof(LwLightNode) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+  if (path) LW_CUDA_TRY(cudaMemcpyAsync(path, c->S.lt_path, sizeof(uint64_t) * c->S.nemit, cudaMemcpyDeviceToHost, c->stream));
+  if (depth) LW_CUDA_TRY(cudaMemcpyAsync(depth, c->S.lt_depth, sizeof(int32_t) * c->S.nemit, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (size_t k = 0; k < h.size(); k++) {
+    double* o = nodes15 ? nodes15 + 15 * k : nullptr;
+    if (o) {
+      for (int a = 0; a < 3; a++) {
+        o[a] = h[k].lo[a];
+        o[3 + a] = h[k].hi[a];
+      }
+      o[6] = h[k].tot;
+      for (int b = 0; b < 8; b++) o[7 + b] = h[k].flux[b];
+    }
+    if (right) right[k] = h[k].right;
+  }
+  return LW_OK;
+}
+
+int lw_ctx_light_sample(lw_ctx* c, const double* x, const double* nrm, const double* u, int64_t n, int64_t* out_e,
+                        double* out_psel, double* out_u) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  LW_CHECK_ARG(c->lt_nodes > 0, "the scene has no light hierarchy (pack_scene(..., lights='tree'))");
+  if (n <= 0) return LW_OK;
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  DevBuf bx, bn, bu, be, bp, bo;
+  LW_CUDA_TRY(bx.alloc(sizeof(double) * 3 * n, st));
+  LW_CUDA_TRY(bn.alloc(sizeof(double) * 3 * n, st));
+  LW_CUDA_TRY(bu.alloc(sizeof(double) * n, st));
+  LW_CUDA_TRY(be.alloc(sizeof(long long) * n, st));
+  LW_CUDA_TRY(bp.alloc(sizeof(double) * n, st));
+  LW_CUDA_TRY(bo.alloc(sizeof(double) * n, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bx.p, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bn.p, nrm, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bu.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  k_light_sample_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->S, bx.as<double>(), bn.as<double>(), bu.as<double>(),
+                                                                 n, be.as<long long>(), bp.as<double>(), bo.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_e, be.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_psel, bp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_u, bo.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_ctx_light_pdf(lw_ctx* c, const int64_t* e, const double* x, const double* nrm, int64_t n, double* out_psel) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  LW_CHECK_ARG(c->lt_nodes > 0, "the scene has no light hierarchy (pack_scene(..., lights='tree'))");
+  if (n <= 0) return LW_OK;
+  for (int64_t i = 0; i < n; i++) LW_CHECK_ARG(e[i] >= 0 && e[i] < c->S.nemit, "emitter index out of range");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  DevBuf be, bx, bn, bp;
+  LW_CUDA_TRY(be.alloc(sizeof(long long) * n, st));
+  LW_CUDA_TRY(bx.alloc(sizeof(double) * 3 * n, st));
+  LW_CUDA_TRY(bn.alloc(sizeof(double) * 3 * n, st));
+  LW_CUDA_TRY(bp.alloc(sizeof(double) * n, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(be.p, e, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bx.p, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bn.p, nrm, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  k_light_pdf_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->S, be.as<long long>(), bx.as<double>(), bn.as<double>(),
+                                                              n, bp.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_psel, bp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
   return LW_OK;
 }
 

@@ -175,6 +175,43 @@ class Renderer:
                                         ptr(occ, C.c_int32)))
         return occ
 
+    # -- light hierarchy (scenes packed with lights="tree")
+    def light_tree(self):
+        """(nodes [n,15] = lo hi tot flux[8], right [n], path [nemit], depth [nemit]) or None."""
+        nn = C.c_int64()
+        check(self.lib.lw_ctx_light_tree_info(self.ctx, C.byref(nn)))
+        if nn.value == 0:
+            return None
+        ne = self.packed.nemit
+        nodes = np.empty((nn.value, 15))
+        right = np.empty(nn.value, np.int32)
+        path = np.empty(max(ne, 1), np.uint64)
+        depth = np.empty(max(ne, 1), np.int32)
+        check(self.lib.lw_ctx_light_tree_download(self.ctx, ptr(nodes, C.c_double), ptr(right, C.c_int32),
+                                                  ptr(path, C.c_uint64), ptr(depth, C.c_int32)))
+        return nodes, right, path[:ne], depth[:ne]
+
+    def light_sample(self, x, nrm, u):
+        """sample_light: emitter, selection probability, rescaled uniform."""
+        x = np.ascontiguousarray(x, np.float64)
+        nrm = np.ascontiguousarray(nrm, np.float64)
+        u = np.ascontiguousarray(u, np.float64)
+        n = len(u)
+        e, p, uo = np.empty(n, np.int64), np.empty(n), np.empty(n)
+        check(self.lib.lw_ctx_light_sample(self.ctx, ptr(x, C.c_double), ptr(nrm, C.c_double), ptr(u, C.c_double), n,
+                                           ptr(e, C.c_int64), ptr(p, C.c_double), ptr(uo, C.c_double)))
+        return e, p, uo
+
+    def light_pdf(self, e, x, nrm):
+        """light_pdf's selection factor of emitter e seen from (x, nrm)."""
+        e = np.ascontiguousarray(e, np.int64)
+        x = np.ascontiguousarray(x, np.float64)
+        nrm = np.ascontiguousarray(nrm, np.float64)
+        p = np.empty(len(e))
+        check(self.lib.lw_ctx_light_pdf(self.ctx, ptr(e, C.c_int64), ptr(x, C.c_double), ptr(nrm, C.c_double), len(e),
+                                        ptr(p, C.c_double)))
+        return p
+
     def camera_rays(self, sample_index):
         idx = np.ascontiguousarray(sample_index, np.int64)
         o = np.empty((len(idx), 3))
