@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--pool-log2", type=int, default=22)
     ap.add_argument("--regen-fraction", type=float, default=0.5)
     ap.add_argument("--megakernel-tail", type=int, default=0)
+    ap.add_argument("--env-sampling", default="alias", choices=["alias", "pyramid"],
+                    help="environment-image sampling: alias table (BASELINE configs) or the normal-binned pyramid")
     ap.add_argument("--lights", default="alias", choices=["alias", "tree"],
                     help="NEE emitter selection: alias table (BASELINE configs) or the light hierarchy")
     ap.add_argument("--width", type=int, default=0)
@@ -132,7 +134,7 @@ def cpu_render_sample(a, budget_s, threads=0, it0=3, gpu=None):
     from paper_1705_01263_b200.render import RenderParams
     from paper_1705_01263_b200.scene import pack_scene
 
-    packed = pack_scene(build_scene(a), lights=a.lights)
+    packed = pack_scene(build_scene(a), lights=a.lights, env_sampling=a.env_sampling)
     osc = O.OracleScene(packed)
     params = RenderParams(a.width, a.height, a.depth)
     threads = threads or os.cpu_count()
@@ -216,7 +218,7 @@ def run_ours(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    packed = pack_scene(build_scene(a), lights=a.lights)
+    packed = pack_scene(build_scene(a), lights=a.lights, env_sampling=a.env_sampling)
     W, H, P = a.width, a.height, a.width * a.height
     its = a.pass_iterations
     r = Renderer(None, W, H, a.depth, device=local, packed=packed, engine=a.engine, pool_log2=a.pool_log2,
@@ -339,7 +341,7 @@ def run_ours(a):
         "metric": metric_name(a), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic procedural scene (seeded), QMC samples",
-        "config": {"workload": workload(a), "engine": a.engine, "lights": a.lights, "pool_slots": 1 << a.pool_log2,
+        "config": {"workload": workload(a), "engine": a.engine, "lights": a.lights, "env_sampling": a.env_sampling, "pool_slots": 1 << a.pool_log2,
                    "regen_fraction": a.regen_fraction, "parallelism": f"sample-space dp{world}",
                    "l2": f"wavefront state pool (~{(1 << a.pool_log2) * 250 / 1e9:.1f} GB) exceeds the 126 MB L2 "
                          "(no flush needed); Cornell-box BVHs are shared-memory resident by design"},

@@ -110,12 +110,15 @@ typedef struct lw_scene_desc {
   double cam_up[3];
   double tan_half_fov; /* tan(fov_y / 2), computed by the host */
   int32_t bvh_kind;    /* render BVH: LW_BVH_SAH (default) or LW_BVH_MEDIAN (the reference's tree) */
-  int32_t light_sampler; /* NEE emitter selection: LW_LIGHTS_ALIAS (flat alias table over weights)
-                            or LW_LIGHTS_TREE (light hierarchy) */
+  int32_t light_sampler; /* NEE light selection flags: 0 = LW_LIGHTS_ALIAS (flat alias tables over
+                            emitter and texel weights); | LW_LIGHTS_TREE: light hierarchy over the
+                            emitters; | LW_LIGHTS_ENV_PYRAMID: environment pyramid
+                            with normal-binned top levels */
 } lw_scene_desc;
 
 #define LW_LIGHTS_ALIAS 0
 #define LW_LIGHTS_TREE 1
+#define LW_LIGHTS_ENV_PYRAMID 2
 
 #define LW_BVH_SAH 0    /* binned SAH, breadth-first */
 #define LW_BVH_MEDIAN 1 /* geometry.py:100-148 median split (built on the GPU) */
@@ -248,6 +251,14 @@ int lw_ctx_light_sample(lw_ctx* ctx, const double* x, const double* nrm, const d
                         int64_t* out_e, double* out_psel, double* out_u);
 int lw_ctx_light_pdf(lw_ctx* ctx, const int64_t* e, const double* x, const double* nrm, int64_t n,
                      double* out_psel);
+/* Environment pyramid (LW_LIGHTS_ENV_PYRAMID; PAPER.md:262-276, SPEC.md:222-230 sample_env /
+ * env_pdf): levels (0 = not built).  sample: base texel index (row * width + col), its probability
+ * and the in-texel (u, v) for octahedral-packed facing normals and uniforms uv [n,2]; pdf: texel
+ * probability for the packed normal. */
+int lw_ctx_env_pyramid_info(lw_ctx* ctx, int32_t* nlevels);
+int lw_ctx_env_sample(lw_ctx* ctx, const int64_t* packed_normal, const double* uv, int64_t n, int64_t* out_texel,
+                      double* out_p, double* out_uv);
+int lw_ctx_env_pdf(lw_ctx* ctx, const int64_t* packed_normal, const int64_t* texel, int64_t n, double* out_p);
 /* BVH arrays the context built (reference layout), for parity checks */
 int lw_ctx_bvh_info(lw_ctx* ctx, int64_t* nnodes);
 int lw_ctx_bvh_download(lw_ctx* ctx, double* bounds, int64_t* children, int64_t* order);

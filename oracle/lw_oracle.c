@@ -643,7 +643,12 @@ struct lwo_scene {
   int32_t* env_alias;
   double* env_pdf;
   double p_env, p_tri;
-  /* light hierarchy (light_sampler == LW_LIGHTS_TREE) */
+  /* environment pyramid (light_sampler & LW_LIGHTS_ENV_PYRAMID) */
+  int ep_on, ep_nl, ep_ntop;
+  double* ep_lvl;
+  double* ep_top;
+  int64_t ep_off[24], ep_toff[24], ep_stride;
+  /* light hierarchy (light_sampler & LW_LIGHTS_TREE) */
   int64_t lt_n;
   lt_node* lt;
   uint64_t* lt_path;
@@ -986,6 +991,8 @@ static void lt_build(lwo_scene* s, const lw_scene_desc* d) {
   free(c.items);
 }
 
+static void ep_build(lwo_scene* s, const lw_scene_desc* d);
+
 lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
   lwo_scene* s = (lwo_scene*)calloc(1, sizeof(lwo_scene));
   s->d = *d;
@@ -1030,7 +1037,7 @@ lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
     }
     if (lwo_alias_build(d->emit_weight, s->nemit, s->emit_prob, s->emit_alias, s->emit_pdf)) s->nemit = 0;
   }
-  if (d->light_sampler == LW_LIGHTS_TREE && s->nemit > 0) lt_build(s, d);
+  if ((d->light_sampler & LW_LIGHTS_TREE) && s->nemit > 0) lt_build(s, d);
   s->env_kind = d->env_kind;
   s->env_w = d->env_width;
   s->env_h = d->env_height;
@@ -1043,6 +1050,7 @@ lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
     s->env_pdf = (double*)malloc(sizeof(double) * nt);
     if (lwo_alias_build(d->env_weight, nt, s->env_prob, s->env_alias, s->env_pdf)) s->env_kind = LW_ENV_NONE;
   }
+  if (s->env_kind == LW_ENV_IMAGE && (d->light_sampler & LW_LIGHTS_ENV_PYRAMID)) ep_build(s, d);
   int has_env = s->env_kind != LW_ENV_NONE;
   int has_tri = s->nemit > 0;
   s->p_env = has_env ? (has_tri ? d->p_env : 1.0) : 0.0;
@@ -1074,6 +1082,8 @@ void lwo_scene_destroy(lwo_scene* s) {
   free(s->env_prob);
   free(s->env_alias);
   free(s->env_pdf);
+  free(s->ep_lvl);
+  free(s->ep_top);
   free(s->lt);
   free(s->lt_path);
   free(s->lt_depth);
@@ -1449,8 +1459,249 @@ void lwo_light_pdf_batch(const lwo_scene* s, const int64_t* e, const double* x, 
   for (int64_t i = 0; i < n; i++) out_psel[i] = lt_pdf(s, e[i], ld3(x + 3 * i), ld3(nrm + 3 * i));
 }
 
+/* ---- environment pyramid (device: lw_envpyr.cuh; library host build: env_pyramid_build) ----
+ * Level 0 = texel weights (luminance * sin theta); level l+1 = sums of 2x2 children up to a 1 x 2
+ * top; the top EP_TOP levels are replicated per normal bin (4 x 4 octahedral cells of the facing
+ * geometric normal) with weights scaled by a conservative cosine bound floored at 1/64.
+ * Sampling: column half with u, row half with v, both rescaled; pdf = product of conditionals. */
+#define EP_BINS 16
+#define EP_TOP 5
+#define EP_CWMIN 0.015625
+
+static int ep_bin(int64_t packed) { return (int)(((packed >> 30) & 3) * 4 + ((packed >> 14) & 3)); }
+
+static v3 ep_dir(double phi_turns, double theta_turns) {
+  double st, ct, sp, cp;
+  lwo_sincos2pi(theta_turns, &st, &ct);
+  lwo_sincos2pi(phi_turns, &sp, &cp);
+  return mk(st * cp, ct, st * sp);
+}
+
+static v3 ep_decode_n(int64_t packed) {
+  double o[3];
+  lwo_oct_decode(packed, o);
+  return normalize(mk(o[0], o[1], o[2]));
+}
+
+static void ep_bin_cone(int b, v3* axis, double* cosb) {
+  int64_t bu = b / 4, bv = b % 4;
+  *axis = ep_decode_n(((bu * 16384 + 8192) << 16) | (bv * 16384 + 8192));
+  double m = 1.0;
+  for (int k = 0; k <= 8; k++) {
+    int64_t t = k * 2048;
+    int64_t e0[4][2] = {{bu * 16384 + t, bv * 16384}, {bu * 16384 + t, bv * 16384 + 16384},
+                        {bu * 16384, bv * 16384 + t}, {bu * 16384 + 16384, bv * 16384 + t}};
+    for (int q = 0; q < 4; q++) {
+      int64_t eu = e0[q][0] > 65535 ? 65535 : e0[q][0], ev = e0[q][1] > 65535 ? 65535 : e0[q][1];
+      double c = dot(*axis, ep_decode_n((eu << 16) | ev));
+      if (c < m) m = c;
+    }
+  }
+  *cosb = m - 0.02;
+}
+
+static void ep_texel_cone(int64_t r, int64_t c, int64_t Hl, int64_t Wl, v3* ctr, double* cosg) {
+  double f0 = (double)c / (double)Wl, f1 = (double)(c + 1) / (double)Wl;
+  double t0 = (double)r / (double)Hl * 0.5, t1 = (double)(r + 1) / (double)Hl * 0.5;
+  *ctr = ep_dir((f0 + f1) * 0.5, (t0 + t1) * 0.5);
+  double m = 1.0;
+  for (int k = 0; k <= 8; k++) {
+    double a = (double)k / 8.0;
+    double fk = f0 + (f1 - f0) * a, tk = t0 + (t1 - t0) * a;
+    v3 sm[4] = {ep_dir(fk, t0), ep_dir(fk, t1), ep_dir(f0, tk), ep_dir(f1, tk)};
+    for (int q = 0; q < 4; q++) {
+      double cq = dot(*ctr, sm[q]);
+      if (cq < m) m = cq;
+    }
+  }
+  *cosg = m - 0.02;
+}
+
+static double ep_cos_bound(v3 axis, double cosb, v3 ctr, double cosg) {
+  if (cosb <= 0.0 || cosg <= 0.0) return 1.0;
+  double sinb = sqrt(1.0 - cosb * cosb), sing = sqrt(1.0 - cosg * cosg);
+  double cosd = cosb * cosg - sinb * sing, sind = sinb * cosg + cosb * sing;
+  if (sind <= 0.0) return 1.0;
+  double cosa = dot(axis, ctr);
+  if (cosa >= cosd) return 1.0;
+  double s2 = 1.0 - cosa * cosa;
+  double sina = sqrt(s2 > 0.0 ? s2 : 0.0);
+  double cw = cosa * cosd + sina * sind;
+  return cw > 0.0 ? cw : 0.0;
+}
+
+static void ep_build(lwo_scene* s, const lw_scene_desc* d) {
+  int64_t W = d->env_width, H = d->env_height;
+  if (!(H >= 1 && W == 2 * H && (H & (H - 1)) == 0)) return; /* library rejects the scene */
+  int nl = 1;
+  while ((H >> (nl - 1)) > 1) nl++;
+  s->ep_nl = nl;
+  int64_t tot = 0;
+  for (int l = 0; l < nl; l++) {
+    s->ep_off[l] = tot;
+    tot += (H >> l) * (W >> l);
+  }
+  s->ep_lvl = (double*)malloc(sizeof(double) * tot);
+  for (int64_t k = 0; k < W * H; k++) s->ep_lvl[k] = d->env_weight[k];
+  for (int l = 1; l < nl; l++) {
+    int64_t Hl = H >> l, Wl = W >> l, Wc = Wl * 2;
+    const double* ch = s->ep_lvl + s->ep_off[l - 1];
+    double* o = s->ep_lvl + s->ep_off[l];
+    for (int64_t r = 0; r < Hl; r++)
+      for (int64_t c = 0; c < Wl; c++)
+        o[r * Wl + c] = ((ch[(2 * r) * Wc + 2 * c] + ch[(2 * r) * Wc + 2 * c + 1]) + ch[(2 * r + 1) * Wc + 2 * c]) +
+                        ch[(2 * r + 1) * Wc + 2 * c + 1];
+  }
+  s->ep_ntop = nl < EP_TOP ? nl : EP_TOP;
+  int64_t ts = 0;
+  for (int l = nl - s->ep_ntop; l < nl; l++) {
+    s->ep_toff[l] = ts;
+    ts += (H >> l) * (W >> l);
+  }
+  s->ep_stride = ts;
+  s->ep_top = (double*)malloc(sizeof(double) * EP_BINS * ts);
+  for (int b = 0; b < EP_BINS; b++) {
+    v3 axis;
+    double cosb;
+    ep_bin_cone(b, &axis, &cosb);
+    for (int l = nl - s->ep_ntop; l < nl; l++) {
+      int64_t Hl = H >> l, Wl = W >> l;
+      for (int64_t r = 0; r < Hl; r++)
+        for (int64_t c = 0; c < Wl; c++) {
+          v3 ctr;
+          double cosg;
+          ep_texel_cone(r, c, Hl, Wl, &ctr, &cosg);
+          double cw = ep_cos_bound(axis, cosb, ctr, cosg);
+          if (cw < EP_CWMIN) cw = EP_CWMIN;
+          s->ep_top[b * ts + s->ep_toff[l] + r * Wl + c] = s->ep_lvl[s->ep_off[l] + r * Wl + c] * cw;
+        }
+    }
+  }
+  s->ep_on = 1;
+}
+
+static double ep_w(const lwo_scene* s, int bin, int l, int64_t r, int64_t c) {
+  int64_t wl = (int64_t)s->env_w >> l;
+  if (l >= s->ep_nl - s->ep_ntop) return s->ep_top[bin * s->ep_stride + s->ep_toff[l] + r * wl + c];
+  return s->ep_lvl[s->ep_off[l] + r * wl + c];
+}
+
+static void ep_sample(const lwo_scene* s, int bin, double u, double v, int64_t* row, int64_t* col, double* p_out,
+                      double* u_out, double* v_out) {
+  int l = s->ep_nl - 1;
+  double w0 = ep_w(s, bin, l, 0, 0), w1 = ep_w(s, bin, l, 0, 1);
+  double sm = w0 + w1;
+  double p0 = sm > 0.0 ? w0 / sm : 0.5;
+  int64_t r = 0, c;
+  double p;
+  if (u < p0) {
+    u = u / p0;
+    p = p0;
+    c = 0;
+  } else {
+    u = (u - p0) / (1.0 - p0);
+    p = 1.0 - p0;
+    c = 1;
+  }
+  for (; l > 0; l--) {
+    double a = ep_w(s, bin, l - 1, 2 * r, 2 * c), b = ep_w(s, bin, l - 1, 2 * r, 2 * c + 1);
+    double cc = ep_w(s, bin, l - 1, 2 * r + 1, 2 * c), dd = ep_w(s, bin, l - 1, 2 * r + 1, 2 * c + 1);
+    double top = a + b, bot = cc + dd;
+    double st = top + bot;
+    double pt = st > 0.0 ? top / st : 0.5;
+    double left, right;
+    if (v < pt) {
+      v = v / pt;
+      p = p * pt;
+      r = 2 * r;
+      left = a;
+      right = b;
+    } else {
+      v = (v - pt) / (1.0 - pt);
+      p = p * (1.0 - pt);
+      r = 2 * r + 1;
+      left = cc;
+      right = dd;
+    }
+    double sl = left + right;
+    double pl = sl > 0.0 ? left / sl : 0.5;
+    if (u < pl) {
+      u = u / pl;
+      p = p * pl;
+      c = 2 * c;
+    } else {
+      u = (u - pl) / (1.0 - pl);
+      p = p * (1.0 - pl);
+      c = 2 * c + 1;
+    }
+  }
+  if (u >= 1.0) u = 0.9999999999999999;
+  if (u < 0.0) u = 0.0;
+  if (v >= 1.0) v = 0.9999999999999999;
+  if (v < 0.0) v = 0.0;
+  *row = r;
+  *col = c;
+  *p_out = p;
+  *u_out = u;
+  *v_out = v;
+}
+
+static double ep_pdf(const lwo_scene* s, int bin, int64_t row, int64_t col) {
+  int l = s->ep_nl - 1;
+  double w0 = ep_w(s, bin, l, 0, 0), w1 = ep_w(s, bin, l, 0, 1);
+  double sm = w0 + w1;
+  double p0 = sm > 0.0 ? w0 / sm : 0.5;
+  int64_t r = 0, c = col >> l;
+  double p = c == 0 ? p0 : 1.0 - p0;
+  for (; l > 0; l--) {
+    double a = ep_w(s, bin, l - 1, 2 * r, 2 * c), b = ep_w(s, bin, l - 1, 2 * r, 2 * c + 1);
+    double cc = ep_w(s, bin, l - 1, 2 * r + 1, 2 * c), dd = ep_w(s, bin, l - 1, 2 * r + 1, 2 * c + 1);
+    double top = a + b, bot = cc + dd;
+    double st = top + bot;
+    double pt = st > 0.0 ? top / st : 0.5;
+    int64_t rb = (row >> (l - 1)) & 1, cb = (col >> (l - 1)) & 1;
+    double left, right;
+    if (rb == 0) {
+      p = p * pt;
+      left = a;
+      right = b;
+    } else {
+      p = p * (1.0 - pt);
+      left = cc;
+      right = dd;
+    }
+    double sl = left + right;
+    double pl = sl > 0.0 ? left / sl : 0.5;
+    p = cb == 0 ? p * pl : p * (1.0 - pl);
+    r = 2 * r + rb;
+    c = 2 * c + cb;
+  }
+  return p;
+}
+
+int lwo_env_pyramid_info(const lwo_scene* s, int32_t* nlevels) {
+  if (nlevels) *nlevels = s->ep_on ? s->ep_nl : 0;
+  return s->ep_on;
+}
+
+void lwo_env_sample_batch(const lwo_scene* s, const int64_t* packed_normal, const double* uv, int64_t n,
+                          int64_t* out_texel, double* out_p, double* out_uv) {
+  for (int64_t i = 0; i < n; i++) {
+    int64_t row, col;
+    ep_sample(s, ep_bin(packed_normal[i]), uv[2 * i], uv[2 * i + 1], &row, &col, out_p + i, out_uv + 2 * i,
+              out_uv + 2 * i + 1);
+    out_texel[i] = row * s->env_w + col;
+  }
+}
+
+void lwo_env_pdf_batch(const lwo_scene* s, const int64_t* packed_normal, const int64_t* texel, int64_t n,
+                       double* out_p) {
+  for (int64_t i = 0; i < n; i++)
+    out_p[i] = ep_pdf(s, ep_bin(packed_normal[i]), texel[i] / s->env_w, texel[i] % s->env_w);
+}
+
 /* environment lookup: lat-long, y up, row 0 at +y */
-static v3 env_eval(const lwo_scene* s, v3 d, double* pdf) {
+static v3 env_eval(const lwo_scene* s, v3 d, int64_t nprev, double* pdf) {
   if (s->env_kind == LW_ENV_CONSTANT) {
     *pdf = s->p_env * LW_INV_FOUR_PI;
     return scl(ld3(s->d.env_constant), s->d.env_scale);
@@ -1468,7 +1719,8 @@ static v3 env_eval(const lwo_scene* s, v3 d, double* pdf) {
     if (col < 0) col = 0;
     if (row < 0) row = 0;
     int64_t j = row * W + col;
-    *pdf = sin_t > 0.0 ? s->p_env * s->env_pdf[j] * (double)(W * H) / (LW_TWO_PI_SQ * sin_t) : 0.0;
+    double pt = s->ep_on ? ep_pdf(s, ep_bin(nprev), row, col) : s->env_pdf[j];
+    *pdf = sin_t > 0.0 ? s->p_env * pt * (double)(W * H) / (LW_TWO_PI_SQ * sin_t) : 0.0;
     const float* px = s->env_img + 3 * j;
     return mk((double)px[0] * s->d.env_scale, (double)px[1] * s->d.env_scale, (double)px[2] * s->d.env_scale);
   }
@@ -1693,7 +1945,7 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
     if (h.tri < 0) {
       if (s->env_kind != LW_ENV_NONE) {
         double pe;
-        v3 Le = env_eval(s, d, &pe);
+        v3 Le = env_eval(s, d, nprev, &pe);
         double w = spec_prev ? 1.0 : pdf_prev / (pdf_prev + pe);
         L = add(L, mk(beta.x * Le.x * w, beta.y * Le.y * w, beta.z * Le.z * w));
       }
@@ -1754,17 +2006,26 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
           Le = scl(ld3(s->d.env_constant), s->d.env_scale);
           ok = 1;
         } else {
-          double ur;
-          int64_t j = alias_sample(s->env_prob, s->env_alias, (int64_t)s->env_w * s->env_h, ue, &ur);
-          int64_t row = j / s->env_w, col = j % s->env_w;
+          double ur, vr, pt;
+          int64_t j, row, col;
+          if (s->ep_on) {
+            ep_sample(s, ep_bin(lwo_oct_encode(ngf.x, ngf.y, ngf.z)), ue, vl, &row, &col, &pt, &ur, &vr);
+            j = row * s->env_w + col;
+          } else {
+            j = alias_sample(s->env_prob, s->env_alias, (int64_t)s->env_w * s->env_h, ue, &ur);
+            row = j / s->env_w;
+            col = j % s->env_w;
+            vr = vl;
+            pt = s->env_pdf[j];
+          }
           double uu = ((double)col + ur) / (double)s->env_w;
-          double vv2 = ((double)row + vl) / (double)s->env_h;
+          double vv2 = ((double)row + vr) / (double)s->env_h;
           double st_, ct, sp, cp;
           lwo_sincos2pi(vv2 * 0.5, &st_, &ct);
           lwo_sincos2pi(uu, &sp, &cp);
           wi = mk(st_ * cp, ct, st_ * sp);
           if (st_ > 0.0) {
-            pl = s->p_env * s->env_pdf[j] * (double)((int64_t)s->env_w * s->env_h) / (LW_TWO_PI_SQ * st_);
+            pl = s->p_env * pt * (double)((int64_t)s->env_w * s->env_h) / (LW_TWO_PI_SQ * st_);
             const float* px = s->env_img + 3 * j;
             Le = mk((double)px[0] * s->d.env_scale, (double)px[1] * s->d.env_scale, (double)px[2] * s->d.env_scale);
             ok = 1;

@@ -72,6 +72,15 @@ void lwo_light_sample_batch(const lwo_scene* s, const double* x, const double* n
 void lwo_light_pdf_batch(const lwo_scene* s, const int64_t* e, const double* x, const double* nrm, int64_t n,
                          double* out_psel);
 
+/* Environment pyramid (device: lw_envpyr.cuh).  info: 1 if built (levels out).
+ * sample: base texel index, its probability and the in-texel (u, v) for octahedral-packed normals
+ * and uniforms uv [n,2].  pdf: probability of texel for the packed normal. */
+int lwo_env_pyramid_info(const lwo_scene* s, int32_t* nlevels);
+void lwo_env_sample_batch(const lwo_scene* s, const int64_t* packed_normal, const double* uv, int64_t n,
+                          int64_t* out_texel, double* out_p, double* out_uv);
+void lwo_env_pdf_batch(const lwo_scene* s, const int64_t* packed_normal, const int64_t* texel, int64_t n,
+                       double* out_p);
+
 /* Deterministic math shared by oracle and device (restated independently in lw_detmath.cuh). */
 void lwo_sincos2pi(double u, double* s, double* c);
 double lwo_atan2(double y, double x);

@@ -48,6 +48,9 @@ _SIG = {
     "lwo_light_tree": (C.c_int64, [_V, _pd, _pi32, C.POINTER(C.c_uint64), _pi32]),
     "lwo_light_sample_batch": (None, [_V, _pd, _pd, _pd, C.c_int64, _pi64, _pd, _pd]),
     "lwo_light_pdf_batch": (None, [_V, _pi64, _pd, _pd, C.c_int64, _pd]),
+    "lwo_env_pyramid_info": (C.c_int, [_V, _pi32]),
+    "lwo_env_sample_batch": (None, [_V, _pi64, _pd, C.c_int64, _pi64, _pd, _pd]),
+    "lwo_env_pdf_batch": (None, [_V, _pi64, _pi64, C.c_int64, _pd]),
     "lwo_render": (None, [_V, C.POINTER(LwRenderParams), C.c_int64, C.c_int64, C.c_int64, C.c_int64, _pi64, C.c_int, C.POINTER(LwRenderStats)]),
     "lwo_sincos2pi": (None, [C.c_double, _pd, _pd]),
     "lwo_atan2": (C.c_double, [C.c_double, C.c_double]),
@@ -237,6 +240,27 @@ class OracleScene:
         p = np.empty(len(e))
         lib().lwo_light_pdf_batch(self.h, ptr(e, C.c_int64), ptr(x, C.c_double), ptr(nrm, C.c_double), len(e),
                                   ptr(p, C.c_double))
+        return p
+
+    def env_pyramid_levels(self):
+        n = C.c_int32()
+        lib().lwo_env_pyramid_info(self.h, C.byref(n))
+        return n.value
+
+    def env_sample(self, packed_normal, uv):
+        pk = np.ascontiguousarray(packed_normal, np.int64)
+        uv = np.ascontiguousarray(uv, np.float64)
+        n = len(pk)
+        t, p, o = np.empty(n, np.int64), np.empty(n), np.empty((n, 2))
+        lib().lwo_env_sample_batch(self.h, ptr(pk, C.c_int64), ptr(uv, C.c_double), n, ptr(t, C.c_int64),
+                                   ptr(p, C.c_double), ptr(o, C.c_double))
+        return t, p, o
+
+    def env_pdf(self, packed_normal, texel):
+        pk = np.ascontiguousarray(packed_normal, np.int64)
+        tx = np.ascontiguousarray(texel, np.int64)
+        p = np.empty(len(pk))
+        lib().lwo_env_pdf_batch(self.h, ptr(pk, C.c_int64), ptr(tx, C.c_int64), len(pk), ptr(p, C.c_double))
         return p
 
     def camera_rays(self, params, sample_index):

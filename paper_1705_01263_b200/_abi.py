@@ -101,6 +101,7 @@ class LwSceneDesc(C.Structure):
 
 LW_LIGHTS_ALIAS = 0
 LW_LIGHTS_TREE = 1
+LW_LIGHTS_ENV_PYRAMID = 2
 LW_BVH_SAH = 0
 LW_BVH_MEDIAN = 1
 
@@ -216,6 +217,9 @@ SIGNATURES = {
     "lw_ctx_light_tree_download": (C.c_int, [_V, _pd, _pi32, C.POINTER(C.c_uint64), _pi32]),
     "lw_ctx_light_sample": (C.c_int, [_V, _pd, _pd, _pd, C.c_int64, _pi64, _pd, _pd]),
     "lw_ctx_light_pdf": (C.c_int, [_V, _pi64, _pd, _pd, C.c_int64, _pd]),
+    "lw_ctx_env_pyramid_info": (C.c_int, [_V, _pi32]),
+    "lw_ctx_env_sample": (C.c_int, [_V, _pi64, _pd, C.c_int64, _pi64, _pd, _pd]),
+    "lw_ctx_env_pdf": (C.c_int, [_V, _pi64, _pi64, C.c_int64, _pd]),
     "lw_ctx_bvh_info": (C.c_int, [_V, _pi64]),
     "lw_ctx_bvh_download": (C.c_int, [_V, _pd, _pi64, _pi64]),
     "lw_ctx_last_pass_timing": (C.c_int, [_V, _pd, _pd, _pi64]),

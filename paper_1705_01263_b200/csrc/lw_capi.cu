@@ -89,6 +89,120 @@ int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_fla
   return LW_OK;
 }
 
+// ---- environment pyramid (oracle ep_build) -------------------------------------------------
+namespace {
+v3 ep_dir(double phi_turns, double theta_turns) {
+  double st, ct, sp, cp;
+  lw_sincos2pi(theta_turns, &st, &ct);
+  lw_sincos2pi(phi_turns, &sp, &cp);
+  return mk3(st * cp, ct, st * sp);
+}
+
+// axis and conservative cos(half-angle) of normal bin b (4 x 4 cells of the octahedral map)
+void ep_bin_cone(int b, v3& axis, double& cosb) {
+  long long bu = b / 4, bv = b % 4;
+  axis = normalize3(lw_oct_decode(((bu * 16384 + 8192) << 16) | (bv * 16384 + 8192)));
+  double m = 1.0;
+  for (int k = 0; k <= 8; k++) {
+    long long t = k * 2048;
+    long long e0[4][2] = {{bu * 16384 + t, bv * 16384}, {bu * 16384 + t, bv * 16384 + 16384},
+                          {bu * 16384, bv * 16384 + t}, {bu * 16384 + 16384, bv * 16384 + t}};
+    for (int q = 0; q < 4; q++) {
+      long long eu = e0[q][0] > 65535 ? 65535 : e0[q][0], ev = e0[q][1] > 65535 ? 65535 : e0[q][1];
+      double c = dot3(axis, normalize3(lw_oct_decode((eu << 16) | ev)));
+      if (c < m) m = c;
+    }
+  }
+  cosb = m - 0.02;
+}
+
+// center direction and conservative cos(half-angle) of texel (r, c) of a (Hl x Wl) level
+void ep_texel_cone(long long r, long long c, long long Hl, long long Wl, v3& ctr, double& cosg) {
+  double f0 = (double)c / (double)Wl, f1 = (double)(c + 1) / (double)Wl;
+  double t0 = (double)r / (double)Hl * 0.5, t1 = (double)(r + 1) / (double)Hl * 0.5;
+  ctr = ep_dir((f0 + f1) * 0.5, (t0 + t1) * 0.5);
+  double m = 1.0;
+  for (int k = 0; k <= 8; k++) {
+    double a = (double)k / 8.0;
+    double fk = f0 + (f1 - f0) * a, tk = t0 + (t1 - t0) * a;
+    v3 s[4] = {ep_dir(fk, t0), ep_dir(fk, t1), ep_dir(f0, tk), ep_dir(f1, tk)};
+    for (int q = 0; q < 4; q++) {
+      double cq = dot3(ctr, s[q]);
+      if (cq < m) m = cq;
+    }
+  }
+  cosg = m - 0.02;
+}
+
+// upper bound of max(0, n . w) over normals in the bin cone and directions in the texel cone
+double ep_cos_bound(v3 axis, double cosb, v3 ctr, double cosg) {
+  if (cosb <= 0.0 || cosg <= 0.0) return 1.0;
+  double sinb = sqrt(1.0 - cosb * cosb), sing = sqrt(1.0 - cosg * cosg);
+  double cosd = cosb * cosg - sinb * sing, sind = sinb * cosg + cosb * sing;
+  if (sind <= 0.0) return 1.0;  // combined half-angle beyond pi
+  double cosa = dot3(axis, ctr);
+  if (cosa >= cosd) return 1.0;
+  double s2 = 1.0 - cosa * cosa;
+  double sina = sqrt(s2 > 0.0 ? s2 : 0.0);
+  double cw = cosa * cosd + sina * sind;
+  return cw > 0.0 ? cw : 0.0;
+}
+}  // namespace
+
+int env_pyramid_build(int W, int H, const double* w, std::vector<double>& lvl, std::vector<double>& top,
+                      LwEnvPyr& P) {
+  LW_CHECK_ARG(H >= 1 && W == 2 * H && (H & (H - 1)) == 0, "environment pyramid: image must be 2H x H, H a power of 2");
+  memset(&P, 0, sizeof(P));
+  int nl = 1;
+  while ((H >> (nl - 1)) > 1) nl++;
+  LW_CHECK_ARG(nl <= LW_EP_MAXLEV, "environment pyramid: image too large");
+  P.nl = nl;
+  P.W = W;
+  P.H = H;
+  long long tot = 0;
+  for (int l = 0; l < nl; l++) {
+    P.off[l] = tot;
+    tot += (long long)(H >> l) * (W >> l);
+  }
+  lvl.assign(tot, 0.0);
+  for (long long k = 0; k < (long long)W * H; k++) lvl[k] = w[k];
+  for (int l = 1; l < nl; l++) {
+    long long Hl = H >> l, Wl = W >> l, Wc = Wl * 2;
+    const double* ch = lvl.data() + P.off[l - 1];
+    double* o = lvl.data() + P.off[l];
+    for (long long r = 0; r < Hl; r++)
+      for (long long c = 0; c < Wl; c++)
+        o[r * Wl + c] = ((ch[(2 * r) * Wc + 2 * c] + ch[(2 * r) * Wc + 2 * c + 1]) + ch[(2 * r + 1) * Wc + 2 * c]) +
+                        ch[(2 * r + 1) * Wc + 2 * c + 1];
+  }
+  P.ntop = nl < LW_EP_TOP ? nl : LW_EP_TOP;
+  long long ts = 0;
+  for (int l = nl - P.ntop; l < nl; l++) {
+    P.toff[l] = ts;
+    ts += (long long)(H >> l) * (W >> l);
+  }
+  P.top_stride = ts;
+  top.assign((size_t)LW_EP_BINS * ts, 0.0);
+  for (int b = 0; b < LW_EP_BINS; b++) {
+    v3 axis;
+    double cosb;
+    ep_bin_cone(b, axis, cosb);
+    for (int l = nl - P.ntop; l < nl; l++) {
+      long long Hl = H >> l, Wl = W >> l;
+      for (long long r = 0; r < Hl; r++)
+        for (long long c = 0; c < Wl; c++) {
+          v3 ctr;
+          double cosg;
+          ep_texel_cone(r, c, Hl, Wl, ctr, cosg);
+          double cw = ep_cos_bound(axis, cosb, ctr, cosg);
+          if (cw < LW_EP_CWMIN) cw = LW_EP_CWMIN;
+          top[b * ts + P.toff[l] + r * Wl + c] = lvl[P.off[l] + r * Wl + c] * cw;
+        }
+    }
+  }
+  return LW_OK;
+}
+
 // ---- light hierarchy (oracle lt_build) ------------------------------------------------------
 namespace {
 struct LtBuild {

@@ -78,7 +78,7 @@ __device__ __forceinline__ double lw_gauss_filter_offset(double u) {
 #define LW_TWO_PI_SQ 19.739208802178716
 
 // sin/cos of 2*pi*u (oracle: lwo_sincos2pi)
-__device__ __forceinline__ void lw_sincos2pi(double u, double* s, double* c) {
+__host__ __device__ __forceinline__ void lw_sincos2pi(double u, double* s, double* c) {
   double k = floor(u * 4.0 + 0.5);
   double r = u - k * 0.25;
   double x = r * LW_TWO_PI;
@@ -125,7 +125,7 @@ __device__ __forceinline__ double lw_atan2(double y, double x) {
 }
 
 // octahedral packing, _kernels.py:233-299
-__device__ __forceinline__ long long lw_oct_encode(double x, double y, double z) {
+__host__ __device__ __forceinline__ long long lw_oct_encode(double x, double y, double z) {
   double ax = fabs(x), ay = fabs(y), az = fabs(z);
   double norm = ax + ay + az;
   if (norm <= 0.0) return 0;
@@ -143,7 +143,7 @@ __device__ __forceinline__ long long lw_oct_encode(double x, double y, double z)
   return (eu << 16) | ev;
 }
 
-__device__ __forceinline__ v3 lw_oct_decode(long long packed) {
+__host__ __device__ __forceinline__ v3 lw_oct_decode(long long packed) {
   long long eu = (packed >> 16) & 0xFFFF, ev = packed & 0xFFFF;
   double u = (double)eu / 65535.0 * 2.0 - 1.0;
   double v = (double)ev / 65535.0 * 2.0 - 1.0;

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/lw_b200.h"
+#include "lw_envpyr.cuh"
 #include "lw_lighttree.cuh"
 #include "lw_qmc.cuh"
 
@@ -19,6 +20,11 @@ int pack_qmc_tables(const int64_t* bases, int64_t ndims, const int64_t* perm_fla
 
 // Vose alias table; same operation order as the oracle
 int alias_build(const double* w, int64_t n, double* prob, int32_t* alias, double* pdf);
+
+// environment pyramid (lw_envpyr.cuh; oracle ep_build): levels and per-bin top levels; `meta`
+// gets sizes and offsets (its pointers are set by the caller after upload)
+int env_pyramid_build(int W, int H, const double* weight, std::vector<double>& lvl, std::vector<double>& top,
+                      LwEnvPyr& meta);
 
 // light hierarchy over the emitters of positive weight (lw_lighttree.cuh; oracle lt_build):
 // depth-first nodes, per-emitter branch bits and depth (-1 = not in the tree)

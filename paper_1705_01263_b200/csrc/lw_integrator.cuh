@@ -9,6 +9,7 @@
 #pragma once
 #include "lw_common.cuh"
 #include "lw_detmath.cuh"
+#include "lw_envpyr.cuh"
 #include "lw_lighttree.cuh"
 #include "lw_qmc.cuh"
 #include "lw_traverse.cuh"
@@ -33,6 +34,9 @@ struct DevScene {
   const unsigned long long* lt_path;
   const int* lt_depth;
   int light_mode;
+  // environment pyramid (env_mode == LW_LIGHTS_ENV_PYRAMID)
+  LwEnvPyr env_pyr;
+  int env_mode;
   int env_kind;
   int env_w, env_h;
   const float* env_img;
@@ -102,7 +106,8 @@ __device__ __forceinline__ v3 lw_offset_origin(v3 p, v3 n, v3 dir) {
   return mk3(p.x + n.x * sgn, p.y + n.y * sgn, p.z + n.z * sgn);
 }
 
-__device__ __forceinline__ v3 lw_env_eval(const DevScene& S, v3 d, double& pdf) {
+// nprev: packed facing normal of the vertex the ray left (selects the pyramid's top levels)
+__device__ __forceinline__ v3 lw_env_eval(const DevScene& S, v3 d, int nprev, double& pdf) {
   if (S.env_kind == LW_ENV_CONSTANT) {
     pdf = S.p_env * LW_INV_FOUR_PI;
     return mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
@@ -120,7 +125,9 @@ __device__ __forceinline__ v3 lw_env_eval(const DevScene& S, v3 d, double& pdf) 
     if (col < 0) col = 0;
     if (row < 0) row = 0;
     long long j = row * W + col;
-    pdf = sin_t > 0.0 ? S.p_env * __ldg(S.env_pdf + j) * (double)(W * H) / (LW_TWO_PI_SQ * sin_t) : 0.0;
+    double pt = S.env_mode == LW_LIGHTS_ENV_PYRAMID ? lw_ep_pdf(S.env_pyr, lw_ep_bin(nprev), row, col)
+                                                     : __ldg(S.env_pdf + j);
+    pdf = sin_t > 0.0 ? S.p_env * pt * (double)(W * H) / (LW_TWO_PI_SQ * sin_t) : 0.0;
     const float* px = S.env_img + 3 * j;
     return mk3((double)__ldg(px) * S.env_scale, (double)__ldg(px + 1) * S.env_scale, (double)__ldg(px + 2) * S.env_scale);
   }
@@ -412,18 +419,27 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
       Le = mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
       ok = true;
     } else {
-      double ur;
+      double ur, vr, pt;
       long long nt = (long long)S.env_w * S.env_h;
-      long long j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
-      long long row = j / S.env_w, col = j % S.env_w;
+      long long j, row, col;
+      if (S.env_mode == LW_LIGHTS_ENV_PYRAMID) {
+        lw_ep_sample(S.env_pyr, lw_ep_bin(lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z)), ue, vl, row, col, pt, ur, vr);
+        j = row * S.env_w + col;
+      } else {
+        j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
+        row = j / S.env_w;
+        col = j % S.env_w;
+        vr = vl;
+        pt = __ldg(S.env_pdf + j);
+      }
       double uu = ((double)col + ur) / (double)S.env_w;
-      double vv2 = ((double)row + vl) / (double)S.env_h;
+      double vv2 = ((double)row + vr) / (double)S.env_h;
       double st, ct, sp, cp;
       lw_sincos2pi(vv2 * 0.5, &st, &ct);
       lw_sincos2pi(uu, &sp, &cp);
       wi = mk3(st * cp, ct, st * sp);
       if (st > 0.0) {
-        pl = S.p_env * __ldg(S.env_pdf + j) * (double)nt / (LW_TWO_PI_SQ * st);
+        pl = S.p_env * pt * (double)nt / (LW_TWO_PI_SQ * st);
         const float* px = S.env_img + 3 * j;
         Le = mk3((double)__ldg(px) * S.env_scale, (double)__ldg(px + 1) * S.env_scale,
                  (double)__ldg(px + 2) * S.env_scale);
@@ -486,7 +502,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
   if (h.tri < 0) {
     if (S.env_kind != LW_ENV_NONE) {
       double pe;
-      v3 Le = lw_env_eval(S, d, pe);
+      v3 Le = lw_env_eval(S, d, ps.nprev, pe);
       double wm = ps.spec_prev ? 1.0 : ps.pdf_prev / (ps.pdf_prev + pe);
       ps.L = ps.L + mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
     }

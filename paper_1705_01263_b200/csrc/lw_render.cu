@@ -763,6 +763,25 @@ __global__ void k_light_pdf_dbg(DevScene S, const long long* e, const double* x,
   op[i] = lw_lt_pdf(S.lt_nodes, S.lt_path, S.lt_depth, e[i], lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i));
 }
 
+__global__ void k_env_sample_dbg(DevScene S, const long long* pk, const double* uv, long long n, long long* ot,
+                                 double* op, double* ouv) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long row, col;
+  double p, u, v;
+  lw_ep_sample(S.env_pyr, lw_ep_bin(pk[i]), uv[2 * i], uv[2 * i + 1], row, col, p, u, v);
+  ot[i] = row * S.env_w + col;
+  op[i] = p;
+  ouv[2 * i] = u;
+  ouv[2 * i + 1] = v;
+}
+
+__global__ void k_env_pdf_dbg(DevScene S, const long long* pk, const long long* tx, long long n, double* op) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  op[i] = lw_ep_pdf(S.env_pyr, lw_ep_bin(pk[i]), tx[i] / S.env_w, tx[i] % S.env_w);
+}
+
 __global__ void k_resolve(const unsigned long long* fb, long long n, double scale, float* out) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[i] = (float)((double)(long long)fb[i] * scale);
@@ -1244,7 +1263,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   S.lt_nodes = nullptr;
   S.lt_path = nullptr;
   S.lt_depth = nullptr;
-  if (d->light_sampler == LW_LIGHTS_TREE && S.nemit > 0) {
+  if ((d->light_sampler & LW_LIGHTS_TREE) && S.nemit > 0) {
     std::vector<LwLightNode> ln;
     std::vector<unsigned long long> lp;
     std::vector<int> ld;
@@ -1288,8 +1307,22 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
       S.env_pdf = pd;
       S.env_alias = pa;
     }
-  } else if (d->env_kind != LW_ENV_CONSTANT) {
-    S.env_kind = LW_ENV_NONE;
+  }
+  if (d->env_kind != LW_ENV_IMAGE && d->env_kind != LW_ENV_CONSTANT) S.env_kind = LW_ENV_NONE;
+  S.env_mode = 0;
+  memset(&S.env_pyr, 0, sizeof(S.env_pyr));
+  if (S.env_kind == LW_ENV_IMAGE && (d->light_sampler & LW_LIGHTS_ENV_PYRAMID)) {
+    std::vector<double> lvl, top;
+    LwEnvPyr ep;
+    LW_STATUS_TRY(env_pyramid_build(d->env_width, d->env_height, d->env_weight, lvl, top, ep));
+    double *dl, *dt;
+    LW_STATUS_TRY(dev_upload(c, dl, lvl.data(), (int64_t)lvl.size()));
+    LW_STATUS_TRY(dev_upload(c, dt, top.data(), (int64_t)top.size()));
+    LW_CUDA_TRY(cudaStreamSynchronize(st));  // host vectors go out of scope
+    ep.lvl = dl;
+    ep.top = dt;
+    S.env_pyr = ep;
+    S.env_mode = LW_LIGHTS_ENV_PYRAMID;
   }
   bool has_env = S.env_kind != LW_ENV_NONE, has_tri = S.nemit > 0;
   S.p_env = has_env ? (has_tri ? d->p_env : 1.0) : 0.0;
@@ -1598,6 +1631,59 @@ int lw_ctx_light_pdf(lw_ctx* c, const int64_t* e, const double* x, const double*
                                                               n, bp.as<double>());
   LW_CUDA_TRY(cudaGetLastError());
   LW_CUDA_TRY(cudaMemcpyAsync(out_psel, bp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_ctx_env_pyramid_info(lw_ctx* c, int32_t* nlevels) {
+  LW_CHECK_ARG(c && c->has_scene && nlevels, "no scene");
+  *nlevels = c->S.env_mode == LW_LIGHTS_ENV_PYRAMID ? c->S.env_pyr.nl : 0;
+  return LW_OK;
+}
+
+int lw_ctx_env_sample(lw_ctx* c, const int64_t* pk, const double* uv, int64_t n, int64_t* out_t, double* out_p,
+                      double* out_uv) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  LW_CHECK_ARG(c->S.env_mode == LW_LIGHTS_ENV_PYRAMID, "the scene has no environment pyramid (pack_scene(..., env_sampling='pyramid'))");
+  if (n <= 0) return LW_OK;
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  DevBuf bk, bu, bt, bp, bo;
+  LW_CUDA_TRY(bk.alloc(sizeof(long long) * n, st));
+  LW_CUDA_TRY(bu.alloc(sizeof(double) * 2 * n, st));
+  LW_CUDA_TRY(bt.alloc(sizeof(long long) * n, st));
+  LW_CUDA_TRY(bp.alloc(sizeof(double) * n, st));
+  LW_CUDA_TRY(bo.alloc(sizeof(double) * 2 * n, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bk.p, pk, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bu.p, uv, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
+  k_env_sample_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->S, bk.as<long long>(), bu.as<double>(), n,
+                                                               bt.as<long long>(), bp.as<double>(), bo.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_t, bt.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_p, bp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_uv, bo.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_ctx_env_pdf(lw_ctx* c, const int64_t* pk, const int64_t* tx, int64_t n, double* out_p) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  LW_CHECK_ARG(c->S.env_mode == LW_LIGHTS_ENV_PYRAMID, "the scene has no environment pyramid (pack_scene(..., env_sampling='pyramid'))");
+  if (n <= 0) return LW_OK;
+  int64_t nt = (int64_t)c->S.env_w * c->S.env_h;
+  for (int64_t i = 0; i < n; i++) LW_CHECK_ARG(tx[i] >= 0 && tx[i] < nt, "texel index out of range");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  DevBuf bk, bt, bp;
+  LW_CUDA_TRY(bk.alloc(sizeof(long long) * n, st));
+  LW_CUDA_TRY(bt.alloc(sizeof(long long) * n, st));
+  LW_CUDA_TRY(bp.alloc(sizeof(double) * n, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bk.p, pk, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(bt.p, tx, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  k_env_pdf_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->S, bk.as<long long>(), bt.as<long long>(), n,
+                                                            bp.as<double>());
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_p, bp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   LW_CUDA_TRY(cudaStreamSynchronize(st));
   return LW_OK;
 }

@@ -212,6 +212,29 @@ class Renderer:
                                         ptr(p, C.c_double)))
         return p
 
+    # -- environment pyramid (scenes packed with env="pyramid")
+    def env_pyramid_levels(self) -> int:
+        n = C.c_int32()
+        check(self.lib.lw_ctx_env_pyramid_info(self.ctx, C.byref(n)))
+        return n.value
+
+    def env_sample(self, packed_normal, uv):
+        """sample_env: base texel, its probability, in-texel (u, v)."""
+        pk = np.ascontiguousarray(packed_normal, np.int64)
+        uv = np.ascontiguousarray(uv, np.float64)
+        n = len(pk)
+        t, p, o = np.empty(n, np.int64), np.empty(n), np.empty((n, 2))
+        check(self.lib.lw_ctx_env_sample(self.ctx, ptr(pk, C.c_int64), ptr(uv, C.c_double), n, ptr(t, C.c_int64),
+                                         ptr(p, C.c_double), ptr(o, C.c_double)))
+        return t, p, o
+
+    def env_pdf(self, packed_normal, texel):
+        pk = np.ascontiguousarray(packed_normal, np.int64)
+        tx = np.ascontiguousarray(texel, np.int64)
+        p = np.empty(len(pk))
+        check(self.lib.lw_ctx_env_pdf(self.ctx, ptr(pk, C.c_int64), ptr(tx, C.c_int64), len(pk), ptr(p, C.c_double)))
+        return p
+
     def camera_rays(self, sample_index):
         idx = np.ascontiguousarray(sample_index, np.int64)
         o = np.empty((len(idx), 3))

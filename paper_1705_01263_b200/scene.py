@@ -272,17 +272,22 @@ def _tri_areas(v):
     return 0.5 * np.linalg.norm(np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), axis=1)
 
 
-def pack_scene(scene, time: float = 0.0, p_env: float = 0.5, bvh: str = "sah", lights: str = "alias") -> PackedScene:
+def pack_scene(scene, time: float = 0.0, p_env: float = 0.5, bvh: str = "sah", lights: str = "alias",
+               env_sampling: str = "alias") -> PackedScene:
     """Flatten `scene` (reference or local dataclasses) into the C-ABI scene description.
 
     bvh: render acceleration structure, "sah" (binned SAH, default) or "median" (the reference's tree).
     lights: NEE emitter selection, "alias" (flat alias table over luminance * area) or "tree" (the
     light hierarchy of PAPER.md:215-253, importance by flux, distance and orientation).
+    env_sampling: environment-image sampling, "alias" (alias table over texels) or "pyramid" (PAPER.md:262-276
+    image pyramid with normal-binned top levels; needs a 2H x H image, H a power of two).
     """
     if bvh not in ("sah", "median"):
         raise ValueError("bvh must be 'sah' or 'median'")
     if lights not in ("alias", "tree"):
         raise ValueError("lights must be 'alias' or 'tree'")
+    if env_sampling not in ("alias", "pyramid"):
+        raise ValueError("env_sampling must be 'alias' or 'pyramid'")
     geo = flatten_instances(scene, time)
     ntris = len(geo.verts)
     verts = np.ascontiguousarray(geo.verts, dtype=np.float64)
@@ -382,5 +387,6 @@ def pack_scene(scene, time: float = 0.0, p_env: float = 0.5, bvh: str = "sah", l
         d.cam_up[k] = float(cam.up[k])
     d.tan_half_fov = math.tan(math.radians(float(cam.fov_y)) * 0.5)
     d.bvh_kind = _abi.LW_BVH_SAH if bvh == "sah" else _abi.LW_BVH_MEDIAN
-    d.light_sampler = _abi.LW_LIGHTS_TREE if lights == "tree" else _abi.LW_LIGHTS_ALIAS
+    d.light_sampler = (_abi.LW_LIGHTS_TREE if lights == "tree" else 0) | \
+        (_abi.LW_LIGHTS_ENV_PYRAMID if env_sampling == "pyramid" else 0)
     return PackedScene(desc=d, arrays=arrays, geometry=geo, ntris=ntris, nemit=len(emit_tri))

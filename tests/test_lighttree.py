@@ -146,3 +146,73 @@ def test_render_with_light_tree_bit_exact(gpu, oracle, engine):
         fb = r.framebuffer()
     fb2, _ = oracle.OracleScene(packed).render(RenderParams(W, H, c.max_depth), 0, 3)
     assert np.array_equal(fb, fb2) and fb.sum() > 0
+
+
+# ---- environment pyramid --------------
+
+def _env_scene(w=256, h=128):
+    return scenes.envmap_scene(w, h, sphere_subdiv=3)
+
+
+def test_env_pyramid_probabilities(oracle):
+    packed = pack_scene(_env_scene(), env_sampling="pyramid")
+    os_ = oracle.OracleScene(packed)
+    assert os_.env_pyramid_levels() == 8
+    nt = 256 * 128
+    w = packed.arrays["env_w"].reshape(-1)
+    rng = np.random.default_rng(2)
+    for pk in [0, 0xFFFFFFFF, 0x7FFF7FFF, int(rng.integers(0, 2 ** 32))]:
+        pe = os_.env_pdf(np.full(nt, pk), np.arange(nt))
+        assert abs(pe.sum() - 1.0) < 1e-12
+        assert np.array_equal(pe > 0, w > 0)  # coverage: never zero where there is radiance
+        uv = rng.random((4000, 2))
+        t, ps, uvo = os_.env_sample(np.full(4000, pk), uv)
+        assert np.array_equal(_bits(ps), _bits(os_.env_pdf(np.full(4000, pk), t)))
+        assert uvo.min() >= 0.0 and uvo.max() < 1.0
+
+
+def test_env_pyramid_single_texel(oracle):
+    """a single nonzero texel is sampled with probability 1."""
+    from paper_1705_01263_b200.scene import Environment
+
+    sc = _env_scene(64, 32)
+    img = np.zeros((32, 64, 3))
+    img[9, 41] = (5.0, 4.0, 3.0)
+    sc.environment = Environment(image=img, scale=1.0)
+    os_ = oracle.OracleScene(pack_scene(sc, env_sampling="pyramid"))
+    t, p, _ = os_.env_sample(np.zeros(100, np.int64), np.random.default_rng(0).random((100, 2)))
+    assert np.all(t == 9 * 64 + 41) and np.all(p == 1.0)
+
+
+@pytest.mark.gpu
+def test_env_sample_and_pdf_bit_exact(gpu, oracle):
+    from paper_1705_01263_b200.render import Renderer
+
+    packed = pack_scene(_env_scene(512, 256), env_sampling="pyramid")
+    rng = np.random.default_rng(8)
+    n = 40000
+    pk = rng.integers(0, 2 ** 32, n)
+    uv = rng.random((n, 2))
+    tx = rng.integers(0, 512 * 256, n)
+    os_ = oracle.OracleScene(packed)
+    with Renderer(None, 16, 16, 4, packed=packed) as r:
+        assert r.env_pyramid_levels() == 9
+        t, p, o = r.env_sample(pk, uv)
+        q = r.env_pdf(pk, tx)
+    t2, p2, o2 = os_.env_sample(pk, uv)
+    assert np.array_equal(t, t2) and np.array_equal(_bits(p), _bits(p2)) and np.array_equal(_bits(o), _bits(o2))
+    assert np.array_equal(_bits(q), _bits(os_.env_pdf(pk, tx)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["wavefront", "megakernel"])
+def test_render_with_env_pyramid_bit_exact(gpu, oracle, engine):
+    from paper_1705_01263_b200.render import Renderer, RenderParams
+
+    packed = pack_scene(_env_scene(512, 256), env_sampling="pyramid", lights="tree")
+    W, H = 96, 54
+    with Renderer(None, W, H, 8, packed=packed, engine=engine) as r:
+        r.render_pass(0, 3)
+        fb = r.framebuffer()
+    fb2, _ = oracle.OracleScene(packed).render(RenderParams(W, H, 8), 0, 3)
+    assert np.array_equal(fb, fb2) and fb.sum() > 0
