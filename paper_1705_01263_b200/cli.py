@@ -3,6 +3,8 @@ pyproject.toml:12-13, with the flags of SPEC.md:800 but ships no cli module).
 
     python -m paper_1705_01263_b200.cli render --config C1 --out img [--res WxH] [--iterations N]
         [--depth D] [--snapshot-every N] [--engine wavefront|megakernel] [--metrics FILE] [--device K]
+        [--lights alias|tree] [--env-sampling alias|pyramid]
+        [--devices N [--contexts-per-device C] [--fail DEV@ITER ...]]   # batch scheduler
 
 Scenes come from the procedural configs (the text-format parser is out of scope, SURVEY.md §2.1);
 `--scene FILE.py` may name a Python file defining `scene()` that returns a Scene (e.g. one built
@@ -55,9 +57,14 @@ def cmd_render(args) -> int:
     if spp < 1:
         print("error: --iterations must be >= 1", file=sys.stderr)
         return 3
+    from paper_1705_01263_b200.scene import pack_scene
+
+    packed = pack_scene(scene, lights=args.lights, env_sampling=args.env_sampling)
+    if args.devices > 1 or args.fail or args.contexts_per_device > 1:
+        return _render_batch(args, packed, w, h, depth, spp)
     step = args.snapshot_every or spp
     t0 = time.perf_counter()
-    with Renderer(scene, w, h, depth, device=args.device, engine=args.engine) as r:
+    with Renderer(None, w, h, depth, device=args.device, engine=args.engine, packed=packed) as r:
         done = 0
         while done < spp:
             k = min(step, spp - done)
@@ -70,6 +77,44 @@ def cmd_render(args) -> int:
         stats.update({"seconds": dt, "paths_per_s": stats["paths"] / dt, "width": w, "height": h, "iterations": spp})
         with open(args.metrics, "w") as f:
             json.dump(stats, f, indent=1)
+    return 0
+
+
+def _render_batch(args, packed, w, h, depth, spp) -> int:
+    """Batch mode: dynamic iteration sets over all device contexts, throttled
+    merges, `--fail DEV@ITER` failure injection; one final snapshot."""
+    import numpy as np
+
+    from paper_1705_01263_b200.imagefiles import write_pfm
+    from paper_1705_01263_b200.render import Renderer
+    from paper_1705_01263_b200.scheduler import BatchScheduler, SchedulerError, WorkerProfile
+
+    slots = [d for d in range(max(args.devices, 1)) for _ in range(max(args.contexts_per_device, 1))]
+    fails = {}
+    for f in args.fail or []:
+        try:
+            dev, it = f.split("@")
+            fails[int(dev)] = int(it)
+        except ValueError:
+            print(f"error: bad --fail '{f}' (expected DEV@ITER)", file=sys.stderr)
+            return 3
+    profiles = [WorkerProfile(k, fail_after=fails.get(k)) for k in range(len(slots))]
+    t0 = time.perf_counter()
+    sch = BatchScheduler(lambda k: Renderer(None, w, h, depth, device=slots[k], engine=args.engine, packed=packed),
+                         profiles)
+    try:
+        fb = sch.run(0, spp)
+    except SchedulerError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 4
+    img = (fb.astype(np.float64) * (1.0 / (1048576.0 * spp))).astype(np.float32).reshape(h, w, 3)
+    write_pfm(f"{args.out}_{spp:06d}.pfm", img)
+    dt = time.perf_counter() - t0
+    if args.metrics:
+        m = sch.ledger.metrics()
+        m.update({"seconds": dt, "paths_per_s": w * h * spp / dt, "width": w, "height": h, "iterations": spp})
+        with open(args.metrics, "w") as f:
+            json.dump(m, f, indent=1, default=str)
     return 0
 
 
@@ -87,6 +132,11 @@ def main(argv=None) -> int:
     rp.add_argument("--device", type=int, default=0)
     rp.add_argument("--out", default="render")
     rp.add_argument("--metrics", default=None)
+    rp.add_argument("--lights", default="alias", choices=["alias", "tree"])
+    rp.add_argument("--env-sampling", default="alias", choices=["alias", "pyramid"])
+    rp.add_argument("--devices", type=int, default=1, help="batch scheduler over GPUs 0..N-1")
+    rp.add_argument("--contexts-per-device", type=int, default=1, help="simulated devices per GPU")
+    rp.add_argument("--fail", action="append", default=None, help="inject a failure: DEV@ITER (SPEC.md:800)")
     args = ap.parse_args(argv)
     try:
         return cmd_render(args)

@@ -264,3 +264,19 @@ def render(scene, width, height, spp, max_depth=8, device=0, pass_iterations=16,
             r.render_pass(done, done + step)
             done += step
             yield done, r.image(done)
+
+
+def render_batch(packed, width, height, max_depth, it_begin, it_end, devices=(0,), contexts_per_device=1,
+                 cap=64, **renderer_kw):
+    """Batch-mode multi-device render of iterations [it_begin, it_end) (scheduler.BatchScheduler,
+    PAPER.md:779-817): dynamic iteration sets, throttled merges, failure re-render.  Returns the
+    master int64 framebuffer (H*W, 3) and the ledger metrics.  The image is bit-identical to a
+    single-context render of the same iterations."""
+    from paper_1705_01263_b200.scheduler import BatchScheduler, WorkerProfile
+
+    slots = [d for d in devices for _ in range(contexts_per_device)]
+    profiles = [WorkerProfile(k) for k in range(len(slots))]
+    sch = BatchScheduler(lambda w: Renderer(None, width, height, max_depth, device=slots[w], packed=packed,
+                                            **renderer_kw), profiles, cap=cap)
+    fb = sch.run(it_begin, it_end)
+    return fb, sch.ledger.metrics()
