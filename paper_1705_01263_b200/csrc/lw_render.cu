@@ -152,22 +152,31 @@ __device__ __forceinline__ void warp_add(unsigned long long* ctr, unsigned long 
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, v);
 }
 
-// stage the render BVH in shared memory when it fits (small scenes: Cornell box)
+// stage the render BVH in shared memory when it fits (small scenes: Cornell box); nodes are laid
+// out with an LW_SNODE-byte stride (RenderBVH::nstride): with 144 bytes, lanes reading the same
+// field of different nodes hit different banks instead of the same four
+#ifndef LW_SNODE
+#define LW_SNODE 144
+#endif
+__host__ __device__ __forceinline__ size_t smem_bvh_bytes(long long nnodes, long long ntris) {
+  return (size_t)nnodes * LW_SNODE + (size_t)ntris * sizeof(LTri);
+}
+
 __device__ __forceinline__ RenderBVH stage_bvh(const RenderBVH& g, int nnodes, unsigned char* smem, bool use_smem) {
   if (!use_smem) return g;
-  WNode* sn = reinterpret_cast<WNode*>(smem);
-  LTri* st = reinterpret_cast<LTri*>(smem + sizeof(WNode) * nnodes);
   const int4* src = reinterpret_cast<const int4*>(g.nodes);
-  int4* dst = reinterpret_cast<int4*>(sn);
-  int nn4 = nnodes * (int)(sizeof(WNode) / 16);
-  for (int k = threadIdx.x; k < nn4; k += blockDim.x) dst[k] = src[k];
+  const int per = (int)(sizeof(WNode) / 16), sper = LW_SNODE / 16;
+  int4* dst = reinterpret_cast<int4*>(smem);
+  for (int k = threadIdx.x; k < nnodes * per; k += blockDim.x) dst[(k / per) * sper + k % per] = src[k];
+  LTri* st = reinterpret_cast<LTri*>(smem + (size_t)nnodes * LW_SNODE);
   src = reinterpret_cast<const int4*>(g.tris);
   dst = reinterpret_cast<int4*>(st);
   int nt4 = (int)g.ntris * (int)(sizeof(LTri) / 16);
   for (int k = threadIdx.x; k < nt4; k += blockDim.x) dst[k] = src[k];
   __syncthreads();
   RenderBVH b = g;
-  b.nodes = sn;
+  b.nodes = reinterpret_cast<const WNode*>(smem);
+  b.nstride = LW_SNODE;
   b.tris = st;
   return b;
 }
@@ -390,7 +399,10 @@ __device__ __forceinline__ void load_ray(const Pool& P, int s, double o[3], doub
   d[2] = c.y;
 }
 
-__device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) {
+// nprev (previous vertex normal) is only consumed by the light hierarchy / environment pyramid MIS
+__device__ __forceinline__ bool needs_nprev(const DevScene& S) { return S.light_mode != 0 || S.env_mode != 0; }
+
+__device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps, bool nprev) {
   double2 a = P.ray0[s], b = P.ray1[s], c = P.ray2[s];
   ps.o = mk3(a.x, a.y, b.x);
   ps.d = mk3(b.y, c.x, c.y);
@@ -403,10 +415,10 @@ __device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps) 
   int f = P.flags[s];
   ps.bounce = f & F_BOUNCE;
   ps.spec_prev = (f & F_SPEC) ? 1 : 0;
-  ps.nprev = P.nprev[s];
+  ps.nprev = nprev ? P.nprev[s] : 0;
 }
 
-__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps) {
+__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps, bool nprev) {
   P.ray0[s] = make_double2(ps.o.x, ps.o.y);
   P.ray1[s] = make_double2(ps.o.z, ps.d.x);
   P.ray2[s] = make_double2(ps.d.y, ps.d.z);
@@ -415,7 +427,7 @@ __device__ __forceinline__ void store_state(const Pool& P, int s, const PathStat
   P.tp2[s] = make_double2(ps.L.y, ps.L.z);
   P.misc[s] = make_double2(ps.pdf_prev, __longlong_as_double(ps.index));
   P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0);
-  P.nprev[s] = ps.nprev;
+  if (nprev) P.nprev[s] = ps.nprev;
 }
 
 __device__ __forceinline__ v3 load_L(const Pool& P, int s) {
@@ -527,7 +539,7 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
         long long index = work_index(S, w, item, pix);
         PathState ps;
         lw_path_init(S, index, ps);
-        store_state(P, s, ps);
+        store_state(P, s, ps, needs_nprev(S));
         P.pix[s] = pix;
         P.stage[s] = LW_STAGE_TRACE;
         trace = true;
@@ -632,7 +644,7 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
     if (k < n) {
       int s = P.q_ext[k];
       PathState ps;
-      load_state(P, s, ps);
+      load_state(P, s, ps, needs_nprev(S));
       LwHit h;
       load_hit(P, s, h);
       ShadeGeom g;
@@ -642,7 +654,7 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
         lw_shade_frame(S, ps.d, h, w, g);
         alive = lw_shade_material(S, ps, g);
       }
-      store_state(P, s, ps);
+      store_state(P, s, ps, needs_nprev(S));
       P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
       alive_count += alive ? 1 : 0;
     }
@@ -695,7 +707,7 @@ __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned 
     int s = base + threadIdx.x;
     if (s < P.size && P.stage[s] == LW_STAGE_TRACE) {
       PathState ps;
-      load_state(P, s, ps);
+      load_state(P, s, ps, needs_nprev(S));
       run_to_completion(S, bvh, ps, next, nsh);
       bad += lw_accumulate(fb, P.pix[s], ps.L);
       paths++;
@@ -1223,7 +1235,8 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   for (int a = 0; a < 6; a++) S.bvh.root_box[a] = rb[a];
   for (int a = 0; a < 3; a++) S.bvh.absmax[a] = std::max(fabs(rb[a]), fabs(rb[3 + a]));
   // stage in shared memory when the whole render BVH fits comfortably
-  size_t bytes = sizeof(WNode) * (size_t)nr + sizeof(LTri) * (size_t)n;
+  S.bvh.nstride = (int)sizeof(WNode);
+  size_t bytes = smem_bvh_bytes(nr, n);
   c->smem_bytes = (n > 0 && bytes <= 48 * 1024) ? bytes : 0;
   // emitters
   int* eot;

@@ -215,6 +215,7 @@ struct __align__(16) LTri {
 
 struct RenderBVH {
   const WNode* nodes;
+  int nstride;  // bytes between nodes: 128 in global memory, LW_SNODE when staged in shared memory
   const LTri* tris;
   long long ntris;
   int root_ref;
@@ -282,6 +283,10 @@ __device__ __forceinline__ unsigned lw_node_hit(const LwRayF& r, const WNode* __
     if (lo <= hi && ref[c] != LW_REF_NONE) mask |= 1u << c;
   }
   return mask;
+}
+
+__device__ __forceinline__ const WNode* lw_node_at(const RenderBVH& bvh, int ref) {
+  return reinterpret_cast<const WNode*>(reinterpret_cast<const char*>(bvh.nodes) + (size_t)ref * bvh.nstride);
 }
 
 __device__ __forceinline__ void lw_load_tri(const LTri* __restrict__ p, double v[9], long long& id) {
@@ -352,7 +357,7 @@ struct LwClosest {
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_hit(r, bvh.nodes + ref, best, tn, cr);
+      unsigned m = lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
       if (COUNT) cnt->nodes++;
 #pragma unroll
       for (int c = 0; c < 4; c++)
@@ -435,7 +440,7 @@ struct LwAny {
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_hit(r, bvh.nodes + ref, best, tn, cr);
+      unsigned m = lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
       if (COUNT) cnt->nodes++;
       if (m == 0) {
         ref = LW_REF_NONE;

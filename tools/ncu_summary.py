@@ -23,6 +23,10 @@ METRICS = {
     "threads_per_warp_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
     "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "local_ld_sectors": "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum",
+    "l1tex_throughput_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
+    "l2_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+    "warp_instructions": "smsp__inst_executed.sum",
 }
 _BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 _TIME = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
@@ -48,6 +52,14 @@ def load(path):
             u = unit.get(m, "")
             x *= _TIME.get(u, 1.0) if k == "duration_us" else _BYTES.get(u, 1.0)
             rec[k] = round(x, 4)
+        stalls = []
+        for h in hdr:
+            if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(d[h].replace(",", "")), h[34:-23]))
+                except ValueError:
+                    pass
+        rec["top_stalls_per_issue"] = {n: round(v, 3) for v, n in sorted(stalls, reverse=True)[:5]}
         res.append(rec)
     return res
 
