@@ -57,6 +57,16 @@ extern "C" {
 #define LW_BSDF_SPECULAR_TRANSMIT 3
 #define LW_MAX_LAYERS 4 /* sceneformat.py:225 */
 
+/* light-path-expression events (paper_1705_01263_b200/lpe.py) */
+#define LW_EV_C 0  /* camera */
+#define LW_EV_RD 1 /* diffuse reflection */
+#define LW_EV_RG 2 /* glossy reflection */
+#define LW_EV_RS 3 /* specular reflection */
+#define LW_EV_TS 4 /* specular transmission */
+#define LW_EV_L 5  /* emissive triangle */
+#define LW_EV_E 6  /* environment */
+#define LW_EV_COUNT 7
+
 /* environment kinds (sceneformat.py:304-309) */
 #define LW_ENV_NONE 0
 #define LW_ENV_CONSTANT 1
@@ -255,6 +265,14 @@ int lw_ctx_light_pdf(lw_ctx* ctx, const int64_t* e, const double* x, const doubl
  * env_pdf): levels (0 = not built).  sample: base texel index (row * width + col), its probability
  * and the in-texel (u, v) for octahedral-packed facing normals and uniforms uv [n,2]; pdf: texel
  * probability for the packed normal. */
+/* Light path expressions: the product automaton of lpe.compile_layers
+ * (trans [nstates, LW_EV_COUNT], per-state accepting-layer bit mask, start state).  While set, the
+ * megakernel engine routes every radiance contribution to the layers whose expression accepts the
+ * contribution's event string (int64 fixed-point layer framebuffers, cleared with the main one);
+ * nlayers = 0 removes the layers.  The wavefront engine rejects passes while layers are set. */
+int lw_ctx_set_lpe(lw_ctx* ctx, int32_t nlayers, int32_t nstates, const int16_t* trans, const uint8_t* accept,
+                   int32_t start);
+int lw_ctx_lpe_download(lw_ctx* ctx, int32_t layer, int64_t* fb);
 int lw_ctx_env_pyramid_info(lw_ctx* ctx, int32_t* nlevels);
 int lw_ctx_env_sample(lw_ctx* ctx, const int64_t* packed_normal, const double* uv, int64_t n, int64_t* out_texel,
                       double* out_p, double* out_uv);

@@ -1825,6 +1825,29 @@ static v3 bsdf_eval(const lw_material* m, const layerw* lw, v3 wo, v3 wi, double
   return f;
 }
 
+/* the diffuse and glossy parts of bsdf_eval's f (LPE routing of NEE contributions) */
+static void bsdf_eval_split(const lw_material* m, const layerw* lw, v3 wo, v3 wi, v3* fd, v3* fg) {
+  *fd = mk(0, 0, 0);
+  *fg = mk(0, 0, 0);
+  if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw->sum_a > 0.0)) return;
+  for (int l = 0; l < m->nlayers; l++) {
+    const lw_layer* L = m->layers + l;
+    double a = lw->a[l];
+    if (!(a > 0.0)) continue;
+    if (L->kind == LW_BSDF_DIFFUSE) {
+      double k = a * LW_INV_PI;
+      *fd = add(*fd, mk(L->tint[0] * k, L->tint[1] * k, L->tint[2] * k));
+    } else if (L->kind == LW_BSDF_GLOSSY) {
+      double al = alpha_of(L);
+      v3 h = normalize(add(wo, wi));
+      double D = ggx_d(al, h.z);
+      double G = ggx_g1(al, wo.z) * ggx_g1(al, wi.z);
+      double k = a * (D * G / (4.0 * wo.z * wi.z));
+      *fg = add(*fg, mk(L->tint[0] * k, L->tint[1] * k, L->tint[2] * k));
+    }
+  }
+}
+
 static double fresnel_dielectric(double cos_i, double eta) { /* eta = eta_i / eta_t */
   double sin2t = eta * eta * (1.0 - cos_i * cos_i);
   if (sin2t >= 1.0) return 1.0;
@@ -1840,6 +1863,7 @@ typedef struct {
   double pdf;  /* mixture pdf (non-delta) */
   int delta;
   int transmit;
+  int event; /* LPE event of the sampled lobe */
 } bsample;
 
 /* returns 0 if no valid sample */
@@ -1862,6 +1886,7 @@ static int bsdf_sample(const lw_material* m, const layerw* lw, v3 wo, int front,
   const lw_layer* L = m->layers + pick;
   bs->delta = 0;
   bs->transmit = 0;
+  bs->event = L->kind == LW_BSDF_DIFFUSE ? LW_EV_RD : (L->kind == LW_BSDF_GLOSSY ? LW_EV_RG : LW_EV_RS);
   if (L->kind == LW_BSDF_DIFFUSE) {
     double r = sqrt(ur), sp, cp;
     lwo_sincos2pi(v, &sp, &cp);
@@ -1897,6 +1922,7 @@ static int bsdf_sample(const lw_material* m, const layerw* lw, v3 wo, int front,
       double cos_t = sqrt(1.0 - sin2t);
       bs->wi = mk(-eta * wo.x, -eta * wo.y, -cos_t);
       bs->transmit = 1;
+      bs->event = LW_EV_TS;
       double k = lw->sum_a * (eta * eta);
       bs->weight = mk(k * L->tint[0], k * L->tint[1], k * L->tint[2]);
     }
@@ -1929,7 +1955,39 @@ static void accumulate(int64_t* fb, int64_t pix, v3 L, lw_render_stats* st) {
 }
 
 /* one path, DESIGN.md §4 (SPEC.md:385-402 trace_eye_path / next_event) */
-static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
+/* light-path-expression layers (lwo_render_lpe): product DFA + layer framebuffers */
+typedef struct {
+  const int16_t* trans;
+  const uint8_t* accept;
+  int start, nlayers;
+  int64_t* fb;
+  int64_t npix;
+} lpe_ctx;
+
+static int lpe_step(const lpe_ctx* x, int state, int ev) { return x->trans[state * LW_EV_COUNT + ev]; }
+
+/* same per-contribution fixed-point rule as the device (lw_lpe_route) */
+static void lpe_route(const lpe_ctx* x, int state, int64_t pix, v3 c) {
+  int m = x->accept[state];
+  if (!m) return;
+  double v[3] = {c.x, c.y, c.z};
+  int64_t q[3];
+  for (int k = 0; k < 3; k++) {
+    double y = v[k];
+    if (!(y == y) || y == INFINITY || y == -INFINITY || y < 0.0) y = 0.0;
+    if (y > LW_FB_SAMPLE_CLAMP) y = LW_FB_SAMPLE_CLAMP;
+    q[k] = (int64_t)llrint(y * 1048576.0);
+  }
+  for (int l = 0; l < x->nlayers; l++)
+    if ((m >> l) & 1)
+      for (int k = 0; k < 3; k++) x->fb[(int64_t)l * x->npix * 3 + 3 * pix + k] += q[k];
+}
+
+static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, const lpe_ctx* lpe, int64_t pix);
+
+static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) { return trace_path_lpe(c, index, st, NULL, 0); }
+
+static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, const lpe_ctx* lpe, int64_t pix) {
   const lwo_scene* s = c->s;
   int depth = c->p->max_depth;
   v3 o, d;
@@ -1938,6 +1996,7 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
   int spec_prev = 1;
   double pdf_prev = 0.0;
   int64_t nprev = 0; /* packed facing normal of the previous vertex (light-tree MIS) */
+  int lst = lpe ? lpe_step(lpe, lpe->start, LW_EV_C) : 0; /* LPE automaton state */
   for (int b = 0; b < depth; b++) {
     hitrec h;
     trace_closest(s, &o.x, &d.x, INFINITY, &h);
@@ -1947,7 +2006,9 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
         double pe;
         v3 Le = env_eval(s, d, nprev, &pe);
         double w = spec_prev ? 1.0 : pdf_prev / (pdf_prev + pe);
-        L = add(L, mk(beta.x * Le.x * w, beta.y * Le.y * w, beta.z * Le.z * w));
+        v3 cc = mk(beta.x * Le.x * w, beta.y * Le.y * w, beta.z * Le.z * w);
+        L = add(L, cc);
+        if (lpe) lpe_route(lpe, lpe_step(lpe, lst, LW_EV_E), pix, cc);
       }
       break;
     }
@@ -1970,7 +2031,9 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
         double pl = pdf_area * (h.t * h.t) / cos_l;
         wm = pdf_prev / (pdf_prev + pl);
       }
-      L = add(L, mk(beta.x * Le.x * wm, beta.y * Le.y * wm, beta.z * Le.z * wm));
+      v3 cc = mk(beta.x * Le.x * wm, beta.y * Le.y * wm, beta.z * Le.z * wm);
+      L = add(L, cc);
+      if (lpe) lpe_route(lpe, lpe_step(lpe, lst, LW_EV_L), pix, cc);
     }
     if (b == depth - 1) break;
     /* shading frame */
@@ -2074,7 +2137,18 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
           v3 contrib = mk(beta.x * f.x * Le.x * k, beta.y * f.y * Le.y * k, beta.z * f.z * Le.z * k);
           v3 so = offset_origin(p, ngf, wi);
           if (st) st->rays_shadow++;
-          if (!trace_any(s, &so.x, &wi.x, tmax_sh)) L = add(L, contrib);
+          if (!trace_any(s, &so.x, &wi.x, tmax_sh)) {
+            L = add(L, contrib);
+            if (lpe) { /* diffuse and glossy parts, terminal L (triangle) or E (environment) */
+              v3 fd, fg;
+              bsdf_eval_split(m, &lw, wol, wil, &fd, &fg);
+              int term = tmax_sh == INFINITY ? LW_EV_E : LW_EV_L;
+              lpe_route(lpe, lpe_step(lpe, lpe_step(lpe, lst, LW_EV_RD), term), pix,
+                        mk(beta.x * fd.x * Le.x * k, beta.y * fd.y * Le.y * k, beta.z * fd.z * Le.z * k));
+              lpe_route(lpe, lpe_step(lpe, lpe_step(lpe, lst, LW_EV_RG), term), pix,
+                        mk(beta.x * fg.x * Le.x * k, beta.y * fg.y * Le.y * k, beta.z * fg.z * Le.z * k));
+            }
+          }
         }
       }
     }
@@ -2082,6 +2156,7 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
     bsample bs;
     double ub = qmc(c, bd + 0, index), vb = qmc(c, bd + 1, index);
     if (!bsdf_sample(m, &lw, wol, front, ub, vb, &bs)) break;
+    if (lpe) lst = lpe_step(lpe, lst, bs.event);
     v3 wi = to_world(&fr, bs.wi);
     double gside = dot(ngf, wi);
     if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) break;
@@ -2103,6 +2178,38 @@ static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) {
     nprev = lwo_oct_encode(ngf.x, ngf.y, ngf.z);
   }
   return L;
+}
+
+void lwo_render_lpe(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin, int64_t pix_end,
+                    int64_t it_begin, int64_t it_end, int64_t* fb, int nlayers, int nstates, const int16_t* trans,
+                    const uint8_t* accept, int start, int64_t* layer_fb, int nthreads, lw_render_stats* stats) {
+  rctx c = {s, p};
+  int64_t P = (int64_t)p->width * p->height;
+  lpe_ctx x = {trans, accept, start, nlayers, layer_fb, P};
+  (void)nstates;
+  int64_t ext = 0, shd = 0, nonf = 0;
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads) reduction(+ : ext, shd, nonf)
+#endif
+  for (int64_t pix = pix_begin; pix < pix_end; pix++) {
+    lw_render_stats st;
+    memset(&st, 0, sizeof(st));
+    for (int64_t it = it_begin; it < it_end; it++) {
+      v3 L = trace_path_lpe(&c, it * P + pix, &st, &x, pix);
+      accumulate(fb, pix, L, &st);
+    }
+    ext += st.rays_extension;
+    shd += st.rays_shadow;
+    nonf += st.nonfinite;
+  }
+  (void)nthreads;
+  if (stats) {
+    stats->paths += (pix_end - pix_begin) * (it_end - it_begin);
+    stats->rays_extension += ext;
+    stats->rays_shadow += shd;
+    stats->nonfinite += nonf;
+  }
 }
 
 void lwo_render(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin, int64_t pix_end, int64_t it_begin,

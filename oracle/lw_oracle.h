@@ -81,6 +81,12 @@ void lwo_env_sample_batch(const lwo_scene* s, const int64_t* packed_normal, cons
 void lwo_env_pdf_batch(const lwo_scene* s, const int64_t* packed_normal, const int64_t* texel, int64_t n,
                        double* out_p);
 
+/* lwo_render plus light-path-expression layers: product-DFA tables from
+ * lpe.compile_layers; layer_fb holds nlayers int64 framebuffers of W*H*3. */
+void lwo_render_lpe(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin, int64_t pix_end,
+                    int64_t it_begin, int64_t it_end, int64_t* fb, int nlayers, int nstates, const int16_t* trans,
+                    const uint8_t* accept, int start, int64_t* layer_fb, int nthreads, lw_render_stats* stats);
+
 /* Deterministic math shared by oracle and device (restated independently in lw_detmath.cuh). */
 void lwo_sincos2pi(double u, double* s, double* c);
 double lwo_atan2(double y, double x);

@@ -52,6 +52,9 @@ _SIG = {
     "lwo_env_sample_batch": (None, [_V, _pi64, _pd, C.c_int64, _pi64, _pd, _pd]),
     "lwo_env_pdf_batch": (None, [_V, _pi64, _pi64, C.c_int64, _pd]),
     "lwo_render": (None, [_V, C.POINTER(LwRenderParams), C.c_int64, C.c_int64, C.c_int64, C.c_int64, _pi64, C.c_int, C.POINTER(LwRenderStats)]),
+    "lwo_render_lpe": (None, [_V, C.POINTER(LwRenderParams), C.c_int64, C.c_int64, C.c_int64, C.c_int64, _pi64,
+                               C.c_int, C.c_int, C.POINTER(C.c_int16), C.POINTER(C.c_uint8), C.c_int, _pi64, C.c_int,
+                               C.POINTER(LwRenderStats)]),
     "lwo_sincos2pi": (None, [C.c_double, _pd, _pd]),
     "lwo_atan2": (C.c_double, [C.c_double, C.c_double]),
 }
@@ -270,6 +273,22 @@ class OracleScene:
         lib().lwo_camera_rays(self.h, C.byref(params.struct), ptr(idx, C.c_int64), len(idx), ptr(o, C.c_double),
                               ptr(d, C.c_double))
         return o, d
+
+    def render_lpe(self, params, it_begin, it_end, tables, pix_begin=0, pix_end=None, nthreads=0):
+        """render() plus LPE layers (tables = lpe.compile_layers(...)): (fb, {name: layer fb}, stats)."""
+        W, H = params.width, params.height
+        if pix_end is None:
+            pix_end = W * H
+        fb = np.zeros((H * W, 3), np.int64)
+        nl = len(tables.names)
+        lfb = np.zeros((nl, H * W, 3), np.int64)
+        tr = np.ascontiguousarray(tables.trans, np.int16)
+        ac = np.ascontiguousarray(tables.accept, np.uint8)
+        st = LwRenderStats()
+        lib().lwo_render_lpe(self.h, C.byref(params.struct), int(pix_begin), int(pix_end), int(it_begin), int(it_end),
+                             ptr(fb, C.c_int64), nl, len(tr), ptr(tr, C.c_int16), ptr(ac, C.c_uint8),
+                             int(tables.start), ptr(lfb, C.c_int64), int(nthreads), C.byref(st))
+        return fb, {n: lfb[k] for k, n in enumerate(tables.names)}, st.as_dict()
 
     def render(self, params, it_begin, it_end, pix_begin=0, pix_end=None, nthreads=0):
         W, H = params.width, params.height

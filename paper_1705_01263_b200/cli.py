@@ -5,6 +5,8 @@ pyproject.toml:12-13, with the flags of SPEC.md:800 but ships no cli module).
         [--depth D] [--snapshot-every N] [--engine wavefront|megakernel] [--metrics FILE] [--device K]
         [--lights alias|tree] [--env-sampling alias|pyramid]
         [--devices N [--contexts-per-device C] [--fail DEV@ITER ...]]   # batch scheduler
+        [--layer NAME=EXPR ...]                                          # LPE layers (megakernel)
+    python -m paper_1705_01263_b200.cli composite --layers a.pfm b.pfm --gains 1 2 --out c.pfm
 
 Scenes come from the procedural configs (the text-format parser is out of scope, SURVEY.md §2.1);
 `--scene FILE.py` may name a Python file defining `scene()` that returns a Scene (e.g. one built
@@ -62,15 +64,33 @@ def cmd_render(args) -> int:
     packed = pack_scene(scene, lights=args.lights, env_sampling=args.env_sampling)
     if args.devices > 1 or args.fail or args.contexts_per_device > 1:
         return _render_batch(args, packed, w, h, depth, spp)
+    layers = {}
+    for spec in args.layer or []:
+        name, _, expr = spec.partition("=")
+        if not name or not expr:
+            print(f"error: bad --layer '{spec}' (expected NAME=EXPR)", file=sys.stderr)
+            return 3
+        layers[name] = expr
+    engine = "megakernel" if layers else args.engine  # LPE layers are routed by the megakernel engine
     step = args.snapshot_every or spp
     t0 = time.perf_counter()
-    with Renderer(None, w, h, depth, device=args.device, engine=args.engine, packed=packed) as r:
+    with Renderer(None, w, h, depth, device=args.device, engine=engine, packed=packed) as r:
+        if layers:
+            from paper_1705_01263_b200.lpe import LpeError
+
+            try:
+                r.set_lpe_layers(layers)
+            except LpeError as e:
+                print(f"error: --layer: {e}", file=sys.stderr)
+                return 2
         done = 0
         while done < spp:
             k = min(step, spp - done)
             r.render_pass(done, done + k)
             done += k
             write_pfm(f"{args.out}_{done:06d}.pfm", r.image(done))
+            for name, img in (r.layer_images(done).items() if layers else []):
+                write_pfm(f"{args.out}_{name}_{done:06d}.pfm", img)
         stats = r.stats()
     dt = time.perf_counter() - t0
     if args.metrics:
@@ -118,6 +138,27 @@ def _render_batch(args, packed, w, h, depth, spp) -> int:
     return 0
 
 
+def cmd_composite(args) -> int:
+    """Linear recombination of layer PFMs: out = sum gain_k * layer_k."""
+    from paper_1705_01263_b200.imagefiles import read_pfm, write_pfm
+    from paper_1705_01263_b200.lpe import composite
+
+    gains = args.gains or [1.0] * len(args.layers)
+    if len(gains) != len(args.layers):
+        print("error: one gain per layer", file=sys.stderr)
+        return 3
+    try:
+        imgs = {k: read_pfm(p) for k, p in enumerate(args.layers)}
+    except (OSError, ValueError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2
+    if len({im.shape for im in imgs.values()}) != 1:
+        print("error: layer resolutions differ", file=sys.stderr)
+        return 2
+    write_pfm(args.out, composite(imgs, dict(enumerate(gains))).astype("float32"))
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_1705_01263_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -137,9 +178,15 @@ def main(argv=None) -> int:
     rp.add_argument("--devices", type=int, default=1, help="batch scheduler over GPUs 0..N-1")
     rp.add_argument("--contexts-per-device", type=int, default=1, help="simulated devices per GPU")
     rp.add_argument("--fail", action="append", default=None, help="inject a failure: DEV@ITER (SPEC.md:800)")
+    rp.add_argument("--layer", action="append", default=None,
+                    help="light-path-expression output layer NAME=EXPR (lpe.py syntax), repeatable")
+    cp = sub.add_parser("composite", help="sum of gain * layer PFMs")
+    cp.add_argument("--layers", nargs="+", required=True)
+    cp.add_argument("--gains", nargs="+", type=float, default=None)
+    cp.add_argument("--out", required=True)
     args = ap.parse_args(argv)
     try:
-        return cmd_render(args)
+        return cmd_composite(args) if args.cmd == "composite" else cmd_render(args)
     except (ValueError, NotImplementedError) as e:
         print(f"error: {e}", file=sys.stderr)
         return 3

@@ -61,6 +61,7 @@ struct PathState {
   int bounce;
   int spec_prev;
   int nprev;  // octahedral-packed facing geometric normal of the previous vertex (light-tree MIS)
+  int lpe;    // light-path-expression automaton state (megakernel with layers)
 };
 
 struct ShadowRay {
@@ -68,7 +69,46 @@ struct ShadowRay {
   double tmax;
   v3 contrib;
   int valid;
+  v3 c_diffuse, c_glossy;  // LPE: the contribution's diffuse / glossy parts
+  int term;                // LPE: terminal event (LW_EV_L / LW_EV_E)
+  int lpe;                 // LPE: automaton state at the NEE vertex
 };
+
+// light-path-expression layers (megakernel engine): product DFA + layer framebuffers
+struct LwLpe {
+  const short* trans;           // [nstates * LW_EV_COUNT]
+  const unsigned char* accept;  // [nstates] bit k: layer k accepts
+  int start, nlayers;
+  unsigned long long* fb;       // [nlayers][npix * 3] int64 fixed point
+  long long npix;
+};
+
+__device__ __forceinline__ int lw_lpe_step(const LwLpe* lpe, int state, int ev) {
+  return lpe->trans[state * LW_EV_COUNT + ev];
+}
+
+// add one contribution to every layer accepting `state` (same fixed-point rule as the beauty, per
+// contribution: clamp to [0, 2^32], non-finite -> 0, round(v * 2^20))
+__device__ __forceinline__ void lw_lpe_route(const LwLpe* lpe, int state, long long pix, v3 c) {
+  int m = lpe->accept[state];
+  if (!m) return;
+  double v[3] = {c.x, c.y, c.z};
+  long long q[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    double x = v[k];
+    if (!(x == x) || x == INFINITY || x == -INFINITY || x < 0.0) x = 0.0;
+    if (x > LW_FB_SAMPLE_CLAMP) x = LW_FB_SAMPLE_CLAMP;
+    q[k] = __double2ll_rn(x * 1048576.0);
+  }
+  for (int l = 0; l < lpe->nlayers; l++) {
+    if (!((m >> l) & 1)) continue;
+    unsigned long long* f = lpe->fb + (size_t)l * lpe->npix * 3 + 3 * pix;
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      if (q[k]) atomicAdd(f + k, (unsigned long long)q[k]);
+  }
+}
 
 __device__ __forceinline__ double lw_qmc_s(const DevScene& S, int dim, long long index) {
   return lw_halton(S.qdims, S.qperm, dim, index);
@@ -234,6 +274,32 @@ __device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& l
   return f;
 }
 
+// the diffuse and glossy parts of lw_bsdf_eval's f (LPE routing of NEE contributions)
+__device__ __forceinline__ void lw_bsdf_eval_split(const lw_material& m, const LayerW& lw, v3 wo, v3 wi, v3& fd,
+                                                   v3& fg) {
+  fd = mk3(0.0, 0.0, 0.0);
+  fg = mk3(0.0, 0.0, 0.0);
+  if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return;
+#pragma unroll
+  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+    if (l >= m.nlayers) break;
+    const lw_layer& L = m.layers[l];
+    double a = lw.a[l];
+    if (!(a > 0.0)) continue;
+    if (L.kind == LW_BSDF_DIFFUSE) {
+      double k = a * LW_INV_PI;
+      fd = fd + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
+    } else if (L.kind == LW_BSDF_GLOSSY) {
+      double al = lw_alpha_of(L);
+      v3 h = normalize3(wo + wi);
+      double D = lw_ggx_d(al, h.z);
+      double G = lw_ggx_g1(al, wo.z) * lw_ggx_g1(al, wi.z);
+      double k = a * (D * G / (4.0 * wo.z * wi.z));
+      fg = fg + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
+    }
+  }
+}
+
 __device__ __forceinline__ double lw_fresnel_dielectric(double cos_i, double eta) {
   double sin2t = eta * eta * (1.0 - cos_i * cos_i);
   if (sin2t >= 1.0) return 1.0;
@@ -247,6 +313,7 @@ struct BSample {
   v3 wi, weight;
   double pdf;
   int delta, transmit;
+  int event;  // LPE event of the sampled lobe (LW_EV_RD / RG / RS / TS)
 };
 
 __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const LayerW& lw, v3 wo, bool front, double u,
@@ -272,6 +339,7 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
   const lw_layer& L = m.layers[pick];
   bs.delta = 0;
   bs.transmit = 0;
+  bs.event = L.kind == LW_BSDF_DIFFUSE ? LW_EV_RD : (L.kind == LW_BSDF_GLOSSY ? LW_EV_RG : LW_EV_RS);
   if (L.kind == LW_BSDF_DIFFUSE) {
     double r = sqrt(ur), sp, cp;
     lw_sincos2pi(v, &sp, &cp);
@@ -307,6 +375,7 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
       double cos_t = sqrt(1.0 - sin2t);
       bs.wi = mk3(-eta * wo.x, -eta * wo.y, -cos_t);
       bs.transmit = 1;
+      bs.event = LW_EV_TS;
       double k = lw.sum_a * (eta * eta);
       bs.weight = mk3(k * L.tint[0], k * L.tint[1], k * L.tint[2]);
     }
@@ -350,6 +419,7 @@ __device__ __forceinline__ void lw_path_init(const DevScene& S, long long index,
   ps.bounce = 0;
   ps.spec_prev = 1;
   ps.nprev = 0;
+  ps.lpe = 0;
 }
 
 // reference point and normal of the light-hierarchy estimates at a vertex: the reflection-side
@@ -397,7 +467,8 @@ __device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const Lw
 }
 
 // next-event estimation: fills sh (valid = 0 if no contribution)
-__device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh) {
+__device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh,
+                                             const LwLpe* lpe = nullptr) {
   sh.valid = 0;
   const lw_material& m = *g.m;
   const LayerW& lw = g.lw;
@@ -491,20 +562,31 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
       sh.d = wi;
       sh.tmax = tmax_sh;
       sh.valid = 1;
+      if (lpe) {  // the diffuse and glossy parts, routed after the shadow test
+        v3 fd, fg;
+        lw_bsdf_eval_split(m, lw, g.wol, wil, fd, fg);
+        sh.c_diffuse = mk3(ps.beta.x * fd.x * Le.x * k, ps.beta.y * fd.y * Le.y * k, ps.beta.z * fd.z * Le.z * k);
+        sh.c_glossy = mk3(ps.beta.x * fg.x * Le.x * k, ps.beta.y * fg.y * Le.y * k, ps.beta.z * fg.z * Le.z * k);
+        sh.term = tmax_sh == INFINITY ? LW_EV_E : LW_EV_L;
+        sh.lpe = ps.lpe;
+      }
     }
   }
 }
 
 // miss / emission part: returns false if the path ends before any scattering
+// lpe (megakernel with LPE layers): routes the emission to the layers accepting ... L / ... E
 __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& ps, const LwHit& h, ShadeGeom& g,
-                                                  double& w) {
+                                                  double& w, const LwLpe* lpe = nullptr, long long pix = 0) {
   v3 d = ps.d;
   if (h.tri < 0) {
     if (S.env_kind != LW_ENV_NONE) {
       double pe;
       v3 Le = lw_env_eval(S, d, ps.nprev, pe);
       double wm = ps.spec_prev ? 1.0 : ps.pdf_prev / (ps.pdf_prev + pe);
-      ps.L = ps.L + mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
+      v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
+      ps.L = ps.L + c;
+      if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_E), pix, c);
     }
     return false;
   }
@@ -522,18 +604,22 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
       double pl = pdf_area * (h.t * h.t) / cos_l;
       wm = ps.pdf_prev / (ps.pdf_prev + pl);
     }
-    ps.L = ps.L + mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
+    v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
+    ps.L = ps.L + c;
+    if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_L), pix, c);
   }
   return ps.bounce != S.max_depth - 1;
 }
 
 // BSDF sampling, Russian roulette and the next ray; returns true if the path continues
-__device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& ps, const ShadeGeom& g) {
+__device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& ps, const ShadeGeom& g,
+                                                  const LwLpe* lpe = nullptr) {
   const int b = ps.bounce;
   const int bd = 4 + 8 * b;
   BSample bs;
   double ub = lw_qmc_s(S, bd + 0, ps.index), vb = lw_qmc_s(S, bd + 1, ps.index);
   if (!lw_bsdf_sample(*g.m, g.lw, g.wol, g.front, ub, vb, bs)) return false;
+  if (lpe) ps.lpe = lw_lpe_step(lpe, ps.lpe, bs.event);
   v3 wi = lw_to_world(g.fr, bs.wi);
   double gside = dot3(g.ngf, wi);
   if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) return false;
@@ -558,14 +644,15 @@ __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& 
 }
 
 // whole stage in the oracle's order (megakernel): emission, NEE, BSDF sampling
-__device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, const LwHit& h, ShadowRay& sh) {
+__device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, const LwHit& h, ShadowRay& sh,
+                                              const LwLpe* lpe = nullptr, long long pix = 0) {
   sh.valid = 0;
   ShadeGeom g;
   double w;
-  if (!lw_shade_emission(S, ps, h, g, w)) return false;
+  if (!lw_shade_emission(S, ps, h, g, w, lpe, pix)) return false;
   lw_shade_frame(S, ps.d, h, w, g);
-  lw_shade_nee(S, ps, g, sh);
-  return lw_shade_material(S, ps, g);
+  lw_shade_nee(S, ps, g, sh, lpe);
+  return lw_shade_material(S, ps, g, lpe);
 }
 
 // fixed-point accumulation (oracle accumulate); returns 1 if a channel was non-finite

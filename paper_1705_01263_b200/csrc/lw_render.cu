@@ -77,6 +77,7 @@ struct lw_ctx {
   DeviceBVH ref_bvh;
   bool ref_built = false;
   int64_t lt_nodes = 0;  // light hierarchy nodes (0 = alias-table light selection)
+  LwLpe lpe = {nullptr, nullptr, 0, 0, nullptr, 0};  // light-path-expression layers (megakernel)
   int64_t ntris = 0;
   lw_render_params params;
   QmcDim* d_qdims = nullptr;
@@ -97,6 +98,13 @@ struct lw_ctx {
   std::vector<cudaEvent_t> evpool;  // pairs bracketing trace launches
   lw_kernel_profile prof;
 };
+
+void free_lpe(lw_ctx* c) {
+  if (c->lpe.trans) cudaFreeAsync((void*)c->lpe.trans, c->stream);
+  if (c->lpe.accept) cudaFreeAsync((void*)c->lpe.accept, c->stream);
+  if (c->lpe.fb) cudaFreeAsync(c->lpe.fb, c->stream);
+  c->lpe = LwLpe{nullptr, nullptr, 0, 0, nullptr, 0};
+}
 
 namespace {
 
@@ -336,25 +344,34 @@ __device__ __forceinline__ long long work_index(const DevScene& S, const WorkRan
 }
 
 __device__ __forceinline__ void run_to_completion(const DevScene& S, const RenderBVH& bvh, PathState& ps,
-                                                  unsigned long long& next, unsigned long long& nsh) {
+                                                  unsigned long long& next, unsigned long long& nsh,
+                                                  const LwLpe* lpe = nullptr, long long pix = 0) {
   for (;;) {
     double o[3] = {ps.o.x, ps.o.y, ps.o.z}, d[3] = {ps.d.x, ps.d.y, ps.d.z};
     LwHit h;
     lw_trace_closest(bvh, o, d, INFINITY, h);
     next++;
     ShadowRay sh;
-    bool alive = lw_path_shade(S, ps, h, sh);
+    bool alive = lw_path_shade(S, ps, h, sh, lpe, pix);
     if (sh.valid) {
       double so[3] = {sh.o.x, sh.o.y, sh.o.z}, sd[3] = {sh.d.x, sh.d.y, sh.d.z};
       nsh++;
-      if (!lw_trace_any(bvh, so, sd, sh.tmax)) ps.L = ps.L + sh.contrib;
+      if (!lw_trace_any(bvh, so, sd, sh.tmax)) {
+        ps.L = ps.L + sh.contrib;
+        if (lpe) {
+          lw_lpe_route(lpe, lw_lpe_step(lpe, lw_lpe_step(lpe, sh.lpe, LW_EV_RD), sh.term), pix, sh.c_diffuse);
+          lw_lpe_route(lpe, lw_lpe_step(lpe, lw_lpe_step(lpe, sh.lpe, LW_EV_RG), sh.term), pix, sh.c_glossy);
+        }
+      }
     }
     if (!alive) break;
   }
 }
 
+// LPE = true: every contribution is also routed to the light-path-expression layers
+template <bool LPE>
 __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, unsigned long long* __restrict__ fb,
-                                                    Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+                                                    Counters* __restrict__ cnt, int nrnodes, int use_smem, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   long long total = w.nits * w.npix;
@@ -366,7 +383,8 @@ __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, uns
       long long index = work_index(S, w, item, pix);
       PathState ps;
       lw_path_init(S, index, ps);
-      run_to_completion(S, bvh, ps, next, nsh);
+      if (LPE) ps.lpe = lw_lpe_step(&lpe, lpe.start, LW_EV_C);
+      run_to_completion(S, bvh, ps, next, nsh, LPE ? &lpe : nullptr, pix);
       bad += lw_accumulate(fb, pix, ps.L);
       paths++;
     }
@@ -886,10 +904,14 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     int grid = nsm * 8;
     long long need = (total + 127) / 128;
     if (need < grid) grid = (int)std::max<long long>(1, need);
-    k_megakernel<<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem);
+    if (c->lpe.nlayers > 0)
+      k_megakernel<true><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+    else
+      k_megakernel<false><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
     LW_CUDA_TRY(cudaGetLastError());
     launches = 1;
   } else {
+    LW_CHECK_ARG(c->lpe.nlayers == 0, "light-path-expression layers need the megakernel engine");
     int pool = 1 << p.pool_log2;
     if ((long long)pool > total) {
       long long r = 1;
@@ -1119,6 +1141,7 @@ int lw_ctx_destroy(lw_ctx* c) {
   free_scene(c);
   free_pool(c);
   if (c->d_fb) cudaFreeAsync(c->d_fb, c->stream);
+  free_lpe(c);
   cudaStreamSynchronize(c->stream);
   if (c->d_qdims) cudaFreeAsync(c->d_qdims, c->stream);
   if (c->d_qperm) cudaFreeAsync(c->d_qperm, c->stream);
@@ -1385,6 +1408,7 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   c->S.rr_start = p->rr_start;
   int64_t px = (int64_t)p->width * p->height;
   if (px != c->fb_pixels) {
+    free_lpe(c);  // layer framebuffers have the old size
     if (c->d_fb) cudaFreeAsync(c->d_fb, c->stream);
     c->d_fb = nullptr;
     LW_CUDA_TRY(cudaMallocAsync(&c->d_fb, sizeof(unsigned long long) * 3 * px, c->stream));
@@ -1398,6 +1422,8 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
 int lw_framebuffer_clear(lw_ctx* c) {
   LW_CHECK_ARG(c && c->configured, "not configured");
   LW_CUDA_TRY(cudaMemsetAsync(c->d_fb, 0, sizeof(unsigned long long) * 3 * c->fb_pixels, c->stream));
+  if (c->lpe.nlayers > 0)
+    LW_CUDA_TRY(cudaMemsetAsync(c->lpe.fb, 0, sizeof(unsigned long long) * 3 * c->lpe.npix * c->lpe.nlayers, c->stream));
   memset(&c->stats, 0, sizeof(c->stats));
   return LW_OK;
 }
@@ -1698,6 +1724,39 @@ int lw_ctx_env_pdf(lw_ctx* c, const int64_t* pk, const int64_t* tx, int64_t n, d
   LW_CUDA_TRY(cudaGetLastError());
   LW_CUDA_TRY(cudaMemcpyAsync(out_p, bp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_ctx_set_lpe(lw_ctx* c, int32_t nlayers, int32_t nstates, const int16_t* trans, const uint8_t* accept,
+                   int32_t start) {
+  LW_CHECK_ARG(c && c->configured, "lw_render_configure must precede lw_ctx_set_lpe");
+  cudaSetDevice(c->device);
+  free_lpe(c);
+  if (nlayers == 0) return LW_OK;
+  LW_CHECK_ARG(nlayers > 0 && nlayers <= 8 && nstates > 0 && trans && accept && start >= 0 && start < nstates,
+               "bad LPE tables");
+  for (int64_t k = 0; k < (int64_t)nstates * LW_EV_COUNT; k++)
+    LW_CHECK_ARG(trans[k] >= 0 && trans[k] < nstates, "LPE transition out of range");
+  short* dt;
+  unsigned char* da;
+  unsigned long long* dfb;
+  cudaStream_t st = c->stream;
+  LW_CUDA_TRY(cudaMallocAsync((void**)&dt, sizeof(short) * nstates * LW_EV_COUNT, st));
+  LW_CUDA_TRY(cudaMallocAsync((void**)&da, nstates, st));
+  LW_CUDA_TRY(cudaMallocAsync((void**)&dfb, sizeof(unsigned long long) * 3 * c->fb_pixels * nlayers, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(dt, trans, sizeof(short) * nstates * LW_EV_COUNT, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(da, accept, nstates, cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaMemsetAsync(dfb, 0, sizeof(unsigned long long) * 3 * c->fb_pixels * nlayers, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  c->lpe = LwLpe{dt, da, start, nlayers, dfb, c->fb_pixels};
+  return LW_OK;
+}
+
+int lw_ctx_lpe_download(lw_ctx* c, int32_t layer, int64_t* fb) {
+  LW_CHECK_ARG(c && fb && layer >= 0 && layer < c->lpe.nlayers, "no such LPE layer");
+  LW_CUDA_TRY(cudaMemcpyAsync(fb, c->lpe.fb + (size_t)layer * 3 * c->lpe.npix,
+                              sizeof(int64_t) * 3 * c->lpe.npix, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return LW_OK;
 }
 

@@ -175,6 +175,41 @@ class Renderer:
                                         ptr(occ, C.c_int32)))
         return occ
 
+    # -- light path expressions (megakernel engine)
+    def set_lpe_layers(self, layers: dict | None):
+        """Route contributions to output layers {name: expression} (lpe.py syntax); None removes them.
+        Layers need engine="megakernel"; they are cleared with clear()."""
+        from paper_1705_01263_b200.lpe import compile_layers
+
+        if not layers:
+            check(self.lib.lw_ctx_set_lpe(self.ctx, 0, 0, None, None, 0))
+            self.lpe = None
+            return None
+        if self.params.engine != "megakernel":
+            raise ValueError("light-path-expression layers need engine='megakernel'")
+        t = compile_layers(layers)
+        tr = np.ascontiguousarray(t.trans, np.int16)
+        ac = np.ascontiguousarray(t.accept, np.uint8)
+        check(self.lib.lw_ctx_set_lpe(self.ctx, len(t.names), len(tr), ptr(tr, C.c_int16), ptr(ac, C.c_uint8),
+                                      int(t.start)))
+        self.lpe = t
+        return t
+
+    def layer_framebuffers(self) -> dict:
+        """{name: int64 (H*W, 3) fixed-point layer framebuffer}."""
+        out = {}
+        for k, n in enumerate(self.lpe.names if getattr(self, "lpe", None) else []):
+            fb = np.empty((self.params.pixels, 3), dtype=np.int64)
+            check(self.lib.lw_ctx_lpe_download(self.ctx, k, ptr(fb, C.c_int64)))
+            out[n] = fb
+        return out
+
+    def layer_images(self, samples=None) -> dict:
+        samples = self.iterations if samples is None else samples
+        scale = 1.0 / (1048576.0 * max(samples, 1))
+        h, w = self.params.height, self.params.width
+        return {n: (fb * scale).astype(np.float32).reshape(h, w, 3) for n, fb in self.layer_framebuffers().items()}
+
     # -- light hierarchy (scenes packed with lights="tree")
     def light_tree(self):
         """(nodes [n,15] = lo hi tot flux[8], right [n], path [nemit], depth [nemit]) or None."""
