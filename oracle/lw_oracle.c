@@ -598,13 +598,17 @@ typedef struct {
   int32_t ref[2];   /* >= 0 internal node index; < 0 leaf: -(1 + (start << 3 | count)) */
 } rnode;
 
-/* light hierarchy node (device: LwLightNode) */
+/* light hierarchy node (device: LwLightNode): FP32 record of FP64 build sums */
 typedef struct {
-  double lo[3], hi[3];
-  double tot;
-  double flux[8];
+  float lo[3], hi[3];
+  float tot;
+  float flux[8];
   int32_t right;
 } lt_node;
+
+typedef struct {
+  double lo[3], hi[3], tot, flux[8];
+} lt_acc;
 
 struct lwo_scene {
   lw_scene_desc d;
@@ -908,9 +912,19 @@ static int lt_cmp(const void* pa, const void* pb) {
   return x < y ? -1 : (x > y ? 1 : 0);
 }
 
-static void lt_rec(lt_ctx* c, int64_t begin, int64_t end, int64_t node, uint64_t bits, int dep) {
-  lt_node* N = c->s->lt + node;
+static void lt_store(const lt_acc* A, int32_t right, lt_node* N) {
+  for (int a = 0; a < 3; a++) {
+    N->lo[a] = (float)A->lo[a];
+    N->hi[a] = (float)A->hi[a];
+  }
+  N->tot = (float)A->tot;
+  for (int k = 0; k < 8; k++) N->flux[k] = (float)A->flux[k];
+  N->right = right;
+}
+
+static lt_acc lt_rec(lt_ctx* c, int64_t begin, int64_t end, int64_t node, uint64_t bits, int dep) {
   int64_t n = end - begin;
+  lt_acc M;
   if (n == 1) {
     int64_t e = c->items[begin];
     const double* v = c->s->verts + 9 * c->d->emit_tri[e];
@@ -920,8 +934,8 @@ static void lt_rec(lt_ctx* c, int64_t begin, int64_t end, int64_t node, uint64_t
       if (v[6 + a] < lo) lo = v[6 + a];
       if (v[3 + a] > hi) hi = v[3 + a];
       if (v[6 + a] > hi) hi = v[6 + a];
-      N->lo[a] = lo;
-      N->hi[a] = hi;
+      M.lo[a] = lo;
+      M.hi[a] = hi;
     }
     double e1x = v[3] - v[0], e1y = v[4] - v[1], e1z = v[5] - v[2];
     double e2x = v[6] - v[0], e2y = v[7] - v[1], e2z = v[8] - v[2];
@@ -929,19 +943,19 @@ static void lt_rec(lt_ctx* c, int64_t begin, int64_t end, int64_t node, uint64_t
     double inv = 1.0 / sqrt((cx * cx + cy * cy) + cz * cz);
     double nx = cx * inv, ny = cy * inv, nz = cz * inv;
     double w = c->d->emit_weight[e];
-    N->tot = w;
+    M.tot = w;
     for (int k = 0; k < 8; k++) {
       double cc = lt_octant_cos(k, nx, ny, nz);
       if (c->d->emit_twosided[e]) {
         double c2 = lt_octant_cos(k, -nx, -ny, -nz);
         if (c2 > cc) cc = c2;
       }
-      N->flux[k] = w * cc;
+      M.flux[k] = w * cc;
     }
-    N->right = (int32_t)(-(e + 1));
+    lt_store(&M, (int32_t)(-(e + 1)), c->s->lt + node);
     c->s->lt_path[e] = bits;
     c->s->lt_depth[e] = dep;
-    return;
+    return M;
   }
   double cmin[3] = {INFINITY, INFINITY, INFINITY}, cmax[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = begin; i < end; i++)
@@ -958,17 +972,16 @@ static void lt_rec(lt_ctx* c, int64_t begin, int64_t end, int64_t node, uint64_t
   qsort(c->items + begin, (size_t)n, sizeof(int64_t), lt_cmp);
   int64_t nl = n / 2;
   int64_t left = node + 1, right = node + 2 * nl;
-  lt_rec(c, begin, begin + nl, left, bits, dep + 1);
-  lt_rec(c, begin + nl, end, right, bits | (1ULL << dep), dep + 1);
-  const lt_node *L = c->s->lt + left, *R = c->s->lt + right;
-  N = c->s->lt + node;
+  lt_acc L = lt_rec(c, begin, begin + nl, left, bits, dep + 1);
+  lt_acc R = lt_rec(c, begin + nl, end, right, bits | (1ULL << dep), dep + 1);
   for (int a = 0; a < 3; a++) {
-    N->lo[a] = L->lo[a] < R->lo[a] ? L->lo[a] : R->lo[a];
-    N->hi[a] = L->hi[a] > R->hi[a] ? L->hi[a] : R->hi[a];
+    M.lo[a] = L.lo[a] < R.lo[a] ? L.lo[a] : R.lo[a];
+    M.hi[a] = L.hi[a] > R.hi[a] ? L.hi[a] : R.hi[a];
   }
-  N->tot = L->tot + R->tot;
-  for (int k = 0; k < 8; k++) N->flux[k] = L->flux[k] + R->flux[k];
-  N->right = (int32_t)right;
+  M.tot = L.tot + R.tot;
+  for (int k = 0; k < 8; k++) M.flux[k] = L.flux[k] + R.flux[k];
+  lt_store(&M, (int32_t)right, c->s->lt + node);
+  return M;
 }
 
 static void lt_build(lwo_scene* s, const lw_scene_desc* d) {
@@ -1345,39 +1358,40 @@ static v3 offset_origin(v3 p, v3 n, v3 dir) {
 /* ---- light hierarchy: sample_light / light_pdf (device: lw_lighttree.cuh) ---------------- */
 #define LT_PMIN 0.015625 /* 1/64: branch probabilities clamped to [PMIN, 1 - PMIN] */
 
-static double lt_importance(const lt_node* N, v3 x, v3 n) {
-  v3 c = mk((N->lo[0] + N->hi[0]) * 0.5, (N->lo[1] + N->hi[1]) * 0.5, (N->lo[2] + N->hi[2]) * 0.5);
-  v3 dx = sub(c, x);
-  double d2 = dot(dx, dx);
-  v3 ext = mk(N->hi[0] - N->lo[0], N->hi[1] - N->lo[1], N->hi[2] - N->lo[2]);
-  double r2 = dot(ext, ext) * 0.25;
-  double dist2 = d2 > r2 ? d2 : r2;
-  int inside = x.x >= N->lo[0] && x.x <= N->hi[0] && x.y >= N->lo[1] && x.y <= N->hi[1] && x.z >= N->lo[2] &&
-               x.z <= N->hi[2];
-  if (inside || !(d2 > r2)) return dist2 > 0.0 ? N->tot / dist2 : N->tot;
-  int oct = (dx.x > 0.0 ? 1 : 0) | (dx.y > 0.0 ? 2 : 0) | (dx.z > 0.0 ? 4 : 0); /* signs of x - c */
-  double d = sqrt(d2);
-  double cos_t = dot(n, dx) / d;
-  double sin2a = r2 / d2;
-  double cos_a = sqrt(1.0 - sin2a);
-  double cosb = 1.0;
+static float lt_importance(const lt_node* N, float x0, float x1, float x2, float n0, float n1, float n2) {
+  float cx = (N->lo[0] + N->hi[0]) * 0.5f, cy = (N->lo[1] + N->hi[1]) * 0.5f, cz = (N->lo[2] + N->hi[2]) * 0.5f;
+  float dx = cx - x0, dy = cy - x1, dz = cz - x2;
+  float d2 = (dx * dx + dy * dy) + dz * dz;
+  float ex = N->hi[0] - N->lo[0], ey = N->hi[1] - N->lo[1], ez = N->hi[2] - N->lo[2];
+  float r2 = ((ex * ex + ey * ey) + ez * ez) * 0.25f;
+  float dist2 = d2 > r2 ? d2 : r2;
+  int inside = x0 >= N->lo[0] && x0 <= N->hi[0] && x1 >= N->lo[1] && x1 <= N->hi[1] && x2 >= N->lo[2] &&
+               x2 <= N->hi[2];
+  if (inside || !(d2 > r2)) return dist2 > 0.0f ? N->tot / dist2 : N->tot;
+  int oct = (dx > 0.0f ? 1 : 0) | (dy > 0.0f ? 2 : 0) | (dz > 0.0f ? 4 : 0); /* signs of x - c */
+  float d = sqrtf(d2);
+  float cos_t = ((n0 * dx + n1 * dy) + n2 * dz) / d;
+  float sin2a = r2 / d2;
+  float cos_a = sqrtf(1.0f - sin2a);
+  float cosb = 1.0f;
   if (cos_t < cos_a) { /* cos(theta - alpha), the largest cosine over the box's bounding cone */
-    double s2 = 1.0 - cos_t * cos_t;
-    double sin_t = sqrt(s2 > 0.0 ? s2 : 0.0);
-    cosb = cos_t * cos_a + sin_t * sqrt(sin2a);
-    if (cosb < 0.0) cosb = 0.0;
+    float s2 = 1.0f - cos_t * cos_t;
+    float sin_t = sqrtf(s2 > 0.0f ? s2 : 0.0f);
+    cosb = cos_t * cos_a + sin_t * sqrtf(sin2a);
+    if (cosb < 0.0f) cosb = 0.0f;
   }
   return N->flux[oct] * cosb / dist2;
 }
 
 static double lt_pleft(const lwo_scene* s, int64_t k, v3 x, v3 n) {
-  double il = lt_importance(s->lt + k + 1, x, n);
-  double ir = lt_importance(s->lt + s->lt[k].right, x, n);
-  double sum = il + ir;
-  double pl = sum > 0.0 ? il / sum : 0.5;
-  if (pl < LT_PMIN) pl = LT_PMIN;
-  if (pl > 1.0 - LT_PMIN) pl = 1.0 - LT_PMIN;
-  return pl;
+  float x0 = (float)x.x, x1 = (float)x.y, x2 = (float)x.z, n0 = (float)n.x, n1 = (float)n.y, n2 = (float)n.z;
+  float il = lt_importance(s->lt + k + 1, x0, x1, x2, n0, n1, n2);
+  float ir = lt_importance(s->lt + s->lt[k].right, x0, x1, x2, n0, n1, n2);
+  float sum = il + ir;
+  float pl = sum > 0.0f ? il / sum : 0.5f;
+  if (pl < (float)LT_PMIN) pl = (float)LT_PMIN;
+  if (pl > 1.0f - (float)LT_PMIN) pl = 1.0f - (float)LT_PMIN;
+  return (double)pl;
 }
 
 static int64_t lt_sample(const lwo_scene* s, v3 x, v3 n, double u, double* psel, double* u_out) {

@@ -217,7 +217,12 @@ struct LtBuild {
   std::vector<int>* depth;
 };
 
-void lt_leaf(LtBuild& b, int64_t e, LwLightNode& N) {
+// FP64 accumulation, FP32 node record (rounded to nearest once)
+struct LtAcc {
+  double lo[3], hi[3], tot, flux[8];
+};
+
+void lt_leaf(LtBuild& b, int64_t e, LtAcc& A) {
   const double* v = b.verts + 9 * b.tri[e];
   for (int a = 0; a < 3; a++) {
     double lo = v[a], hi = v[a];
@@ -225,36 +230,45 @@ void lt_leaf(LtBuild& b, int64_t e, LwLightNode& N) {
     if (v[6 + a] < lo) lo = v[6 + a];
     if (v[3 + a] > hi) hi = v[3 + a];
     if (v[6 + a] > hi) hi = v[6 + a];
-    N.lo[a] = lo;
-    N.hi[a] = hi;
+    A.lo[a] = lo;
+    A.hi[a] = hi;
   }
   double e1x = v[3] - v[0], e1y = v[4] - v[1], e1z = v[5] - v[2];
   double e2x = v[6] - v[0], e2y = v[7] - v[1], e2z = v[8] - v[2];
   double cx = e1y * e2z - e1z * e2y, cy = e1z * e2x - e1x * e2z, cz = e1x * e2y - e1y * e2x;
   double inv = 1.0 / sqrt((cx * cx + cy * cy) + cz * cz);
   double nx = cx * inv, ny = cy * inv, nz = cz * inv;
-  N.tot = b.w[e];
+  A.tot = b.w[e];
   for (int k = 0; k < 8; k++) {
     double c = lw_lt_octant_cos(k, nx, ny, nz);
     if (b.two[e]) {
       double c2 = lw_lt_octant_cos(k, -nx, -ny, -nz);
       if (c2 > c) c = c2;
     }
-    N.flux[k] = b.w[e] * c;
+    A.flux[k] = b.w[e] * c;
   }
-  N.right = (int)(-(e + 1));
-  N.pad = 0;
 }
 
-void lt_rec(LtBuild& b, int64_t begin, int64_t end, int64_t node, unsigned long long bits, int dep) {
-  LwLightNode& N = (*b.nodes)[node];
+void lt_store(const LtAcc& A, int right, LwLightNode& N) {
+  for (int a = 0; a < 3; a++) {
+    N.lo[a] = (float)A.lo[a];
+    N.hi[a] = (float)A.hi[a];
+  }
+  N.tot = (float)A.tot;
+  for (int k = 0; k < 8; k++) N.flux[k] = (float)A.flux[k];
+  N.right = right;
+}
+
+LtAcc lt_rec(LtBuild& b, int64_t begin, int64_t end, int64_t node, unsigned long long bits, int dep) {
   int64_t n = end - begin;
+  LtAcc M;
   if (n == 1) {
     int64_t e = b.items[begin];
-    lt_leaf(b, e, N);
+    lt_leaf(b, e, M);
+    lt_store(M, (int)(-(e + 1)), (*b.nodes)[node]);
     (*b.path)[e] = bits;
     (*b.depth)[e] = dep;
-    return;
+    return M;
   }
   double cmin[3] = {INFINITY, INFINITY, INFINITY}, cmax[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = begin; i < end; i++)
@@ -273,18 +287,16 @@ void lt_rec(LtBuild& b, int64_t begin, int64_t end, int64_t node, unsigned long 
   });
   int64_t nl = n / 2;
   int64_t left = node + 1, right = node + 2 * nl;
-  lt_rec(b, begin, begin + nl, left, bits, dep + 1);
-  lt_rec(b, begin + nl, end, right, bits | (1ULL << dep), dep + 1);
-  const LwLightNode &L = (*b.nodes)[left], &R = (*b.nodes)[right];
-  LwLightNode& M = (*b.nodes)[node];
+  LtAcc L = lt_rec(b, begin, begin + nl, left, bits, dep + 1);
+  LtAcc R = lt_rec(b, begin + nl, end, right, bits | (1ULL << dep), dep + 1);
   for (int a = 0; a < 3; a++) {
     M.lo[a] = L.lo[a] < R.lo[a] ? L.lo[a] : R.lo[a];
     M.hi[a] = L.hi[a] > R.hi[a] ? L.hi[a] : R.hi[a];
   }
   M.tot = L.tot + R.tot;
   for (int k = 0; k < 8; k++) M.flux[k] = L.flux[k] + R.flux[k];
-  M.right = (int)right;
-  M.pad = 0;
+  lt_store(M, (int)right, (*b.nodes)[node]);
+  return M;
 }
 }  // namespace
 

@@ -16,16 +16,18 @@
 
 #define LW_LT_PMIN 0.015625  // 1/64
 
-// 128-byte node, depth-first order: left child = node + 1, right child = `right`
+// 64-byte node, depth-first order: left child = node + 1, right child = `right`.  The estimates
+// are heuristics (clamped branch probabilities keep the estimator unbiased), so the node data and
+// the importance arithmetic are FP32: IEEE single operations with correctly rounded division and
+// square root give the same bits on the host (oracle, -ffp-contract=off) and the device.
 struct __align__(16) LwLightNode {
-  double lo[3], hi[3];
-  double tot;      // sum of emitter weights (luminance(L) * area) below the node
-  double flux[8];  // per emission octant: sum of weight * max cos towards that octant
-  int right;       // internal: right child index; leaf: -(emitter + 1)
-  int pad;
+  float lo[3], hi[3];
+  float tot;      // sum of emitter weights (luminance(L) * area) below the node
+  float flux[8];  // per emission octant: sum of weight * max cos towards that octant
+  int right;      // internal: right child index; leaf: -(emitter + 1)
 };
 
-// max over unit directions w in octant k (bit a set = negative axis a) of max(0, n . w)
+// max over unit directions w in octant k (bit a set = negative axis a) of max(0, n . w) (FP64, build)
 __host__ __device__ inline double lw_lt_octant_cos(int k, double nx, double ny, double nz) {
   double a = (k & 1) ? -nx : nx, b = (k & 2) ? -ny : ny, c = (k & 4) ? -nz : nz;
   a = a > 0.0 ? a : 0.0;
@@ -34,41 +36,42 @@ __host__ __device__ inline double lw_lt_octant_cos(int k, double nx, double ny, 
   return sqrt((a * a + b * b) + c * c);
 }
 
-// contribution estimate of a node at point x with (unit) normal n
-__device__ __forceinline__ double lw_lt_importance(const LwLightNode& N, v3 x, v3 n) {
-  v3 c = mk3((N.lo[0] + N.hi[0]) * 0.5, (N.lo[1] + N.hi[1]) * 0.5, (N.lo[2] + N.hi[2]) * 0.5);
-  v3 dx = c - x;
-  double d2 = dot3(dx, dx);
-  v3 ext = mk3(N.hi[0] - N.lo[0], N.hi[1] - N.lo[1], N.hi[2] - N.lo[2]);
-  double r2 = dot3(ext, ext) * 0.25;
-  double dist2 = d2 > r2 ? d2 : r2;
-  bool inside = x.x >= N.lo[0] && x.x <= N.hi[0] && x.y >= N.lo[1] && x.y <= N.hi[1] && x.z >= N.lo[2] &&
-                x.z <= N.hi[2];
-  if (inside || !(d2 > r2)) return dist2 > 0.0 ? N.tot / dist2 : N.tot;
-  int oct = (dx.x > 0.0 ? 1 : 0) | (dx.y > 0.0 ? 2 : 0) | (dx.z > 0.0 ? 4 : 0);  // signs of x - c
-  double d = sqrt(d2);
-  double cos_t = dot3(n, dx) / d;
-  double sin2a = r2 / d2;
-  double cos_a = sqrt(1.0 - sin2a);
-  double cosb = 1.0;
+// contribution estimate of a node at point x with (unit) normal n (FP32)
+__device__ __forceinline__ float lw_lt_importance(const LwLightNode& N, float x0, float x1, float x2, float n0,
+                                                  float n1, float n2) {
+  float cx = (N.lo[0] + N.hi[0]) * 0.5f, cy = (N.lo[1] + N.hi[1]) * 0.5f, cz = (N.lo[2] + N.hi[2]) * 0.5f;
+  float dx = cx - x0, dy = cy - x1, dz = cz - x2;
+  float d2 = (dx * dx + dy * dy) + dz * dz;
+  float ex = N.hi[0] - N.lo[0], ey = N.hi[1] - N.lo[1], ez = N.hi[2] - N.lo[2];
+  float r2 = ((ex * ex + ey * ey) + ez * ez) * 0.25f;
+  float dist2 = d2 > r2 ? d2 : r2;
+  bool inside = x0 >= N.lo[0] && x0 <= N.hi[0] && x1 >= N.lo[1] && x1 <= N.hi[1] && x2 >= N.lo[2] && x2 <= N.hi[2];
+  if (inside || !(d2 > r2)) return dist2 > 0.0f ? N.tot / dist2 : N.tot;
+  int oct = (dx > 0.0f ? 1 : 0) | (dy > 0.0f ? 2 : 0) | (dz > 0.0f ? 4 : 0);  // signs of x - c
+  float d = sqrtf(d2);
+  float cos_t = ((n0 * dx + n1 * dy) + n2 * dz) / d;
+  float sin2a = r2 / d2;
+  float cos_a = sqrtf(1.0f - sin2a);
+  float cosb = 1.0f;
   if (cos_t < cos_a) {
-    double s2 = 1.0 - cos_t * cos_t;
-    double sin_t = sqrt(s2 > 0.0 ? s2 : 0.0);
-    cosb = cos_t * cos_a + sin_t * sqrt(sin2a);
-    if (cosb < 0.0) cosb = 0.0;
+    float s2 = 1.0f - cos_t * cos_t;
+    float sin_t = sqrtf(s2 > 0.0f ? s2 : 0.0f);
+    cosb = cos_t * cos_a + sin_t * sqrtf(sin2a);
+    if (cosb < 0.0f) cosb = 0.0f;
   }
   return N.flux[oct] * cosb / dist2;
 }
 
 // probability of descending into the left child of internal node `k`
 __device__ __forceinline__ double lw_lt_pleft(const LwLightNode* __restrict__ nodes, int k, v3 x, v3 n) {
-  double il = lw_lt_importance(nodes[k + 1], x, n);
-  double ir = lw_lt_importance(nodes[nodes[k].right], x, n);
-  double s = il + ir;
-  double pl = s > 0.0 ? il / s : 0.5;
-  if (pl < LW_LT_PMIN) pl = LW_LT_PMIN;
-  if (pl > 1.0 - LW_LT_PMIN) pl = 1.0 - LW_LT_PMIN;
-  return pl;
+  float x0 = (float)x.x, x1 = (float)x.y, x2 = (float)x.z, n0 = (float)n.x, n1 = (float)n.y, n2 = (float)n.z;
+  float il = lw_lt_importance(nodes[k + 1], x0, x1, x2, n0, n1, n2);
+  float ir = lw_lt_importance(nodes[nodes[k].right], x0, x1, x2, n0, n1, n2);
+  float s = il + ir;
+  float pl = s > 0.0f ? il / s : 0.5f;
+  if (pl < (float)LW_LT_PMIN) pl = (float)LW_LT_PMIN;
+  if (pl > 1.0f - (float)LW_LT_PMIN) pl = 1.0f - (float)LW_LT_PMIN;
+  return (double)pl;
 }
 
 // sample_light: emitter index, selection probability, and the rescaled remaining uniform

@@ -62,7 +62,7 @@ def test_many_lights_probabilities(oracle):
     nodes, right, path, depth = os_.light_tree()
     ne = packed.nemit
     assert nodes.shape[0] == 2 * int((depth >= 0).sum()) - 1
-    assert np.allclose(nodes[0, 6], nodes[1:][right[1:] < 0, 6].sum(), rtol=1e-12)
+    assert np.allclose(nodes[0, 6], nodes[1:][right[1:] < 0, 6].sum(), rtol=1e-6)  # FP32 node records
     rng = np.random.default_rng(3)
     v = packed.verts.reshape(-1, 3)
     lo, hi = v.min(0), v.max(0)
