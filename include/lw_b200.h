@@ -267,9 +267,9 @@ int lw_ctx_light_pdf(lw_ctx* ctx, const int64_t* e, const double* x, const doubl
  * probability for the packed normal. */
 /* Light path expressions: the product automaton of lpe.compile_layers
  * (trans [nstates, LW_EV_COUNT], per-state accepting-layer bit mask, start state).  While set, the
- * megakernel engine routes every radiance contribution to the layers whose expression accepts the
+ * renderer routes every radiance contribution to the layers whose expression accepts the
  * contribution's event string (int64 fixed-point layer framebuffers, cleared with the main one);
- * nlayers = 0 removes the layers.  The wavefront engine rejects passes while layers are set. */
+ * nlayers = 0 removes the layers.  Both engines route (the stage kernels' LPE instantiations). */
 int lw_ctx_set_lpe(lw_ctx* ctx, int32_t nlayers, int32_t nstates, const int16_t* trans, const uint8_t* accept,
                    int32_t start);
 int lw_ctx_lpe_download(lw_ctx* ctx, int32_t layer, int64_t* fb);

@@ -5,7 +5,7 @@ pyproject.toml:12-13, with the flags of SPEC.md:800 but ships no cli module).
         [--depth D] [--snapshot-every N] [--engine wavefront|megakernel] [--metrics FILE] [--device K]
         [--lights alias|tree] [--env-sampling alias|pyramid]
         [--devices N [--contexts-per-device C] [--fail DEV@ITER ...]]   # batch scheduler
-        [--layer NAME=EXPR ...]                                          # LPE layers (megakernel)
+        [--layer NAME=EXPR ...]                                          # LPE output layers
     python -m paper_1705_01263_b200.cli composite --layers a.pfm b.pfm --gains 1 2 --out c.pfm
 
 Scenes come from the procedural configs (the text-format parser is out of scope, SURVEY.md §2.1);
@@ -71,7 +71,7 @@ def cmd_render(args) -> int:
             print(f"error: bad --layer '{spec}' (expected NAME=EXPR)", file=sys.stderr)
             return 3
         layers[name] = expr
-    engine = "megakernel" if layers else args.engine  # LPE layers are routed by the megakernel engine
+    engine = args.engine
     step = args.snapshot_every or spp
     t0 = time.perf_counter()
     with Renderer(None, w, h, depth, device=args.device, engine=engine, packed=packed) as r:

@@ -61,6 +61,10 @@ struct Pool {
   int* pix;
   int* flags;  // bounce | spec_prev << 8
   int* nprev;  // octahedral-packed facing normal of the previous vertex (light-tree MIS)
+  // light-path-expression layers (only touched by the LPE instantiations of the stage kernels)
+  int* lpe_state;            // automaton state of the path
+  double2 *sh5, *sh6, *sh7;  // NEE contribution split: (d.x, d.y) (d.z, g.x) (g.y, g.z)
+  int* sh_lpe;               // automaton state at the NEE vertex | terminal event << 16
   unsigned char* stage;  // LW_STAGE_GENERATE / TRACE / TERMINATED
   int *q_ext, *q_shadow;
   void* block = nullptr;
@@ -472,8 +476,9 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
 // positions in slot order from block prefixes (one barrier per 256 slots).  The generated
 // samples form the first `granted` free slots of the range, so the queue prefix of a lane is
 // trace_prefix + min(want_prefix, granted_left).
+template <bool LPE>
 __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
-                                                  Counters* __restrict__ cnt) {
+                                                  Counters* __restrict__ cnt, LwLpe lpe) {
   __shared__ int wc[2][8][2];  // per-warp (want, trace) counts, double-buffered by iteration parity
   __shared__ long long s_wbase;
   __shared__ int s_ebase, s_red[8][2];
@@ -558,6 +563,7 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
         PathState ps;
         lw_path_init(S, index, ps);
         store_state(P, s, ps, needs_nprev(S));
+        if (LPE) P.lpe_state[s] = lw_lpe_step(&lpe, lpe.start, LW_EV_C);
         P.pix[s] = pix;
         P.stage[s] = LW_STAGE_TRACE;
         trace = true;
@@ -611,7 +617,9 @@ __device__ __forceinline__ void load_hit(const Pool& P, int s, LwHit& h) {
 
 // NEE half of the material stage (runs before k_shade so it sees the incoming throughput):
 // light / environment sample, BSDF evaluation, shadow-ray setup
-__global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt) {
+template <bool LPE>
+__global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt,
+                                                                LwLpe lpe) {
   int n = cnt->n_ext;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
@@ -632,13 +640,20 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
         ps.beta = mk3(t0.x, t0.y, t1.x);
         ps.index = __double_as_longlong(P.misc[s].y);
         ps.bounce = bounce;
+        if (LPE) ps.lpe = P.lpe_state[s];
         ShadeGeom g;
         double w;
         lw_shade_hit(S, ps.d, h, g, w);
         lw_shade_frame(S, ps.d, h, w, g);
         ShadowRay sh;
-        lw_shade_nee(S, ps, g, sh);
+        lw_shade_nee(S, ps, g, sh, LPE ? &lpe : nullptr);
         shadow = sh.valid != 0;
+        if (LPE && shadow) {
+          P.sh5[s] = make_double2(sh.c_diffuse.x, sh.c_diffuse.y);
+          P.sh6[s] = make_double2(sh.c_diffuse.z, sh.c_glossy.x);
+          P.sh7[s] = make_double2(sh.c_glossy.y, sh.c_glossy.z);
+          P.sh_lpe[s] = sh.lpe | (sh.term << 16);
+        }
         if (shadow) {
           P.sh0[s] = make_double2(sh.o.x, sh.o.y);
           P.sh1[s] = make_double2(sh.o.z, sh.d.x);
@@ -654,7 +669,8 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
 }
 
 // material half: miss/emission (MIS), BSDF sampling, Russian roulette, next ray, stage tag
-__global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt) {
+template <bool LPE>
+__global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt, LwLpe lpe) {
   int n = cnt->n_ext;
   unsigned long long alive_count = 0;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
@@ -668,11 +684,13 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
       ShadeGeom g;
       double w;
       bool alive = false;
-      if (lw_shade_emission(S, ps, h, g, w)) {
+      if (LPE) ps.lpe = P.lpe_state[s];
+      if (lw_shade_emission(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0)) {
         lw_shade_frame(S, ps.d, h, w, g);
-        alive = lw_shade_material(S, ps, g);
+        alive = lw_shade_material(S, ps, g, LPE ? &lpe : nullptr);
       }
       store_state(P, s, ps, needs_nprev(S));
+      if (LPE) P.lpe_state[s] = ps.lpe;
       P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
       alive_count += alive ? 1 : 0;
     }
@@ -680,8 +698,9 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
   warp_add(&cnt->n_alive_ull, alive_count);
 }
 
-template <bool COUNT>
-__global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+template <bool COUNT, bool LPE>
+__global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem,
+                                                                      LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   int n = cnt->n_shadow;
@@ -699,6 +718,13 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S
         t2.y = t2.y + f.y;
         P.tp1[s] = t1;
         P.tp2[s] = t2;
+        if (LPE) {
+          double2 a5 = P.sh5[s], a6 = P.sh6[s], a7 = P.sh7[s];
+          int sl = P.sh_lpe[s], st0 = sl & 0xffff, term = sl >> 16;
+          long long pix = P.pix[s];
+          lw_lpe_route(&lpe, lw_lpe_step(&lpe, lw_lpe_step(&lpe, st0, LW_EV_RD), term), pix, mk3(a5.x, a5.y, a6.x));
+          lw_lpe_route(&lpe, lw_lpe_step(&lpe, lw_lpe_step(&lpe, st0, LW_EV_RG), term), pix, mk3(a6.y, a7.x, a7.y));
+        }
       }
     }
   }
@@ -716,8 +742,9 @@ __global__ void k_wave_end(Counters* cnt) {
 }
 
 // megakernel tail: run every in-flight path to completion, in pool order
+template <bool LPE>
 __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned long long* __restrict__ fb,
-                                                   Counters* __restrict__ cnt, int nrnodes, int use_smem) {
+                                                   Counters* __restrict__ cnt, int nrnodes, int use_smem, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   unsigned long long next = 0, nsh = 0, bad = 0, paths = 0;
@@ -726,7 +753,8 @@ __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned 
     if (s < P.size && P.stage[s] == LW_STAGE_TRACE) {
       PathState ps;
       load_state(P, s, ps, needs_nprev(S));
-      run_to_completion(S, bvh, ps, next, nsh);
+      if (LPE) ps.lpe = P.lpe_state[s];
+      run_to_completion(S, bvh, ps, next, nsh, LPE ? &lpe : nullptr, P.pix[s]);
       bad += lw_accumulate(fb, P.pix[s], ps.L);
       paths++;
       P.stage[s] = LW_STAGE_GENERATE;
@@ -858,8 +886,8 @@ int alloc_pool(lw_ctx* c, int size) {
   if (c->pool.size == size) return LW_OK;
   free_pool(c);
   Pool& P = c->pool;
-  const size_t nvec = 14;  // double2 arrays
-  size_t bytes = (size_t)size * (nvec * 16 + 5 * 4 + 1) + 8192;
+  const size_t nvec = 17;  // double2 arrays
+  size_t bytes = (size_t)size * (nvec * 16 + 7 * 4 + 1) + 8192;
   LW_CUDA_TRY(cudaMallocAsync(&P.block, bytes, c->stream));
   char* p = (char*)P.block;
   auto v2 = [&](double2*& x) {
@@ -875,7 +903,8 @@ int alloc_pool(lw_ctx* c, int size) {
   v2(P.misc);
   v2(P.hit0); v2(P.hit1);
   v2(P.sh0); v2(P.sh1); v2(P.sh2); v2(P.sh3); v2(P.sh4);
-  ii(P.pix); ii(P.flags); ii(P.nprev);
+  v2(P.sh5); v2(P.sh6); v2(P.sh7);
+  ii(P.pix); ii(P.flags); ii(P.nprev); ii(P.lpe_state); ii(P.sh_lpe);
   ii(P.q_ext); ii(P.q_shadow);
   P.stage = (unsigned char*)p;
   P.size = size;
@@ -911,7 +940,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     LW_CUDA_TRY(cudaGetLastError());
     launches = 1;
   } else {
-    LW_CHECK_ARG(c->lpe.nlayers == 0, "light-path-expression layers need the megakernel engine");
+    const bool lpe_on = c->lpe.nlayers > 0;
     int pool = 1 << p.pool_log2;
     if ((long long)pool > total) {
       long long r = 1;
@@ -938,7 +967,10 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     for (;;) {
       for (int k = 0; k < check_every; k++) {
         k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0);
-        k_generate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
+        if (lpe_on)
+          k_generate<true><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
+        else
+          k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
         if (timed) {
           marks.push_back({ev, 0});
           cudaEventRecord(event(), st);
@@ -948,16 +980,23 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
         else
           k_trace_ext<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         if (timed) cudaEventRecord(event(), st);
-        k_shade_nee<<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
-        k_shade<<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
+        if (lpe_on) {
+          k_shade_nee<true><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<true><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        } else {
+          k_shade_nee<false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        }
         if (timed) {
           marks.push_back({ev, 1});
           cudaEventRecord(event(), st);
         }
-        if (count)
-          k_trace_shadow<true><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        if (lpe_on)
+          k_trace_shadow<false, true><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+        else if (count)
+          k_trace_shadow<true, false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
         else
-          k_trace_shadow<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+          k_trace_shadow<false, false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
         if (timed) cudaEventRecord(event(), st);
         k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 7;
@@ -970,7 +1009,10 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       bool work_left = h.work_next < (unsigned long long)total;
       if (!work_left && h.n_alive == 0) break;
       if (!work_left && p.megakernel_tail > 0 && h.n_alive < p.megakernel_tail) {
-        k_mega_tail<<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem);
+        if (lpe_on)
+          k_mega_tail<true><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+        else
+          k_mega_tail<false><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
         k_tail_done<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 2;
         break;
@@ -982,7 +1024,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     }
     // flush the remaining finished paths
     k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1);
-    k_generate<<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt);
+    k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
     launches += 2;
   }
   LW_CUDA_TRY(cudaGetLastError());

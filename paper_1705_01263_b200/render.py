@@ -175,18 +175,16 @@ class Renderer:
                                         ptr(occ, C.c_int32)))
         return occ
 
-    # -- light path expressions (megakernel engine)
+    # -- light path expressions
     def set_lpe_layers(self, layers: dict | None):
         """Route contributions to output layers {name: expression} (lpe.py syntax); None removes them.
-        Layers need engine="megakernel"; they are cleared with clear()."""
+        Layers are cleared with clear(); both engines route them."""
         from paper_1705_01263_b200.lpe import compile_layers
 
         if not layers:
             check(self.lib.lw_ctx_set_lpe(self.ctx, 0, 0, None, None, 0))
             self.lpe = None
             return None
-        if self.params.engine != "megakernel":
-            raise ValueError("light-path-expression layers need engine='megakernel'")
         t = compile_layers(layers)
         tr = np.ascontiguousarray(t.trans, np.int16)
         ac = np.ascontiguousarray(t.accept, np.uint8)

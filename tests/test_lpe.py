@@ -100,8 +100,9 @@ def test_oracle_layers_partition_beauty(oracle):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("which", ["cornell", "env"])
-def test_gpu_lpe_layers_bit_exact(gpu, oracle, which):
+@pytest.mark.parametrize("which,engine", [("cornell", "megakernel"), ("env", "megakernel"), ("cornell", "wavefront"),
+                                          ("env", "wavefront")])
+def test_gpu_lpe_layers_bit_exact(gpu, oracle, which, engine):
     from paper_1705_01263_b200.render import Renderer, RenderParams
 
     if which == "cornell":
@@ -111,7 +112,7 @@ def test_gpu_lpe_layers_bit_exact(gpu, oracle, which):
     layers = {"beauty": "C.*[LE]", "diffuse": "CD.*[LE]", "caustic": "C[GS]+D.*L", "direct": "C.?[LE]",
               "env": "C.*E"}
     W, H = 64, 48
-    with Renderer(None, W, H, depth, packed=packed, engine="megakernel") as r:
+    with Renderer(None, W, H, depth, packed=packed, engine=engine, pool_log2=12) as r:
         t = r.set_lpe_layers(layers)
         r.render_pass(0, 4)
         fb = r.framebuffer()
