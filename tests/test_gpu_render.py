@@ -218,3 +218,42 @@ def test_cli_render_writes_snapshots(gpu, tmp_path):
     img = read_pfm(out + "_000004.pfm")
     assert img.shape == (32, 32, 3) and img.sum() > 0
     assert cli.main(["render", "--config", "C1", "--res", "bad"]) == 3
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_full_size_config_band_bit_exact(gpu, oracle, cfg):
+    """BASELINE configs at full scene size and resolution (2^20-triangle soup, 4K x 2K environment,
+    10k emitters): a band of rows x 2 iterations bit-exact vs the oracle, with the alias samplers
+    of the configs and with the light hierarchy / environment pyramid."""
+    from paper_1705_01263_b200.render import RenderParams
+
+    c = scenes.CONFIGS[cfg]
+    sc = c.builder()
+    W, H = c.width, c.height
+    pb, pe = 530 * W, 534 * W
+    for kw in ({}, {"lights": "tree", "env_sampling": "pyramid"}):
+        if kw and cfg == "C3":
+            continue
+        packed = pack_scene(sc, **kw)
+        with _renderer(packed, W, H, c.max_depth) as r:
+            r.render_pass(7, 9, pb, pe)
+            fb = r.framebuffer()
+        fb2, _ = oracle.OracleScene(packed).render(RenderParams(W, H, c.max_depth), 7, 9, pb, pe)
+        assert np.array_equal(fb, fb2), (cfg, kw)
+        assert fb[pb:pe].sum() > 0
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_full_frame_pass_split_and_pool_invariance(gpu, cfg):
+    """Size-independent properties at the full resolution: one pass of 4 iterations equals two
+    passes of 2 (int64 accumulation is associative) and does not depend on the pool size."""
+    c = scenes.CONFIGS[cfg]
+    packed = pack_scene(c.builder())
+    outs = []
+    for pool, splits in ((22, [(0, 4)]), (22, [(0, 2), (2, 4)]), (18, [(0, 4)])):
+        with _renderer(packed, c.width, c.height, c.max_depth, pool_log2=pool) as r:
+            for a, b in splits:
+                r.render_pass(a, b)
+            outs.append(r.framebuffer())
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
