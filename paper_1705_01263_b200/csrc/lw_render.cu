@@ -1221,21 +1221,26 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   S.normals = dn;
   S.material = dm;
   S.materials = dmat;
-  // reference-layout BVH on the device (geometry.py:100-148 arrays; exported for parity)
   // the reference-layout median tree (geometry.py:100-148 arrays) is built here only when it is
   // the render tree; otherwise on demand by lw_ctx_bvh_info / lw_ctx_bvh_download
   c->ref_built = false;
-  if (d->bvh_kind == LW_BVH_MEDIAN) {
-    LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
-    c->ref_built = true;
-  }
-  int64_t nn = c->ref_bvh.nnodes;
+  // render tree: the requested kind; a SAH tree whose worst path would overflow the traversal
+  // stack (pathological, e.g. exponentially spaced triangles) is replaced by the median tree
+  // (depth <= 2 + log2 n).  Hits do not depend on the tree, so the image is unchanged.
+  int kind = d->bvh_kind;
   int nr = 0, levels = 0, root_ref = leaf_ref(0, 0);
-  SahNode* bn = nullptr;  // binary tree (FP64 child boxes), collapsed to the 4-wide layout below
   LTri* lt;
+  WNode* wn = nullptr;
   double rb[6] = {0, 0, 0, 0, 0, 0};
   LW_STATUS_TRY(dev_alloc(c, lt, n > 0 ? n : 1));
-  if (d->bvh_kind == LW_BVH_MEDIAN) {
+  for (;;) {
+  SahNode* bn = nullptr;  // binary tree (FP64 child boxes), collapsed to the 4-wide layout below
+  if (kind == LW_BVH_MEDIAN) {
+    if (!c->ref_built) {
+      LW_STATUS_TRY(bvh_build_device(dv, n, st, c->ref_bvh));
+      c->ref_built = true;
+    }
+    int64_t nn = c->ref_bvh.nnodes;
     // render layout derived from the median tree on the device
     nr = nrnodes_of(c);
     LW_CUDA_TRY(cudaMallocAsync(&bn, sizeof(SahNode) * (nr > 0 ? nr : 1), st));
@@ -1282,15 +1287,18 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     root_ref = ds.root_ref;
     levels = ds.levels;
   }
-  WNode* wn;
   LW_STATUS_TRY(dev_alloc(c, wn, nr > 0 ? nr : 1));
   int max_need = 0;
   int rc_w = collapse_wide(c, bn, nr, root_ref, levels, wn, max_need);
   if (bn) cudaFreeAsync(bn, st);
   LW_STATUS_TRY(rc_w);
-  if (max_need > LW_STACK) {
-    set_error("render BVH too deep: a path needs %d traversal stack entries (limit %d)", max_need, LW_STACK);
-    return LW_ERR_INVALID;
+  if (max_need <= LW_STACK) break;
+  if (kind != LW_BVH_MEDIAN) {
+    kind = LW_BVH_MEDIAN;
+    continue;
+  }
+  set_error("render BVH too deep: a path needs %d traversal stack entries (limit %d)", max_need, LW_STACK);
+  return LW_ERR_INVALID;
   }
   c->nrnodes = nr;
   S.bvh.nodes = wn;

@@ -257,3 +257,26 @@ def test_full_frame_pass_split_and_pool_invariance(gpu, cfg):
             outs.append(r.framebuffer())
     for o in outs[1:]:
         assert np.array_equal(outs[0], o)
+
+
+def test_degenerate_deep_sah_tree_falls_back_to_median(gpu, oracle):
+    """A SAH tree deeper than the traversal stack (exponentially spaced triangles) is replaced by the
+    median tree at upload; hits do not depend on the tree, so the image still matches the oracle."""
+    from paper_1705_01263_b200.render import RenderParams
+    from paper_1705_01263_b200.scenes import _mesh, diffuse_material
+    from paper_1705_01263_b200.scene import Instance, Scene, make_camera
+
+    n = 300
+    x = np.cumsum(1.5 ** np.arange(n) * 1e-6)  # exponential spacing: SAH peels one triangle per level
+    pos = np.concatenate([np.stack([x, np.zeros(n), np.zeros(n)], 1), np.stack([x, np.full(n, 1e-7), np.zeros(n)], 1),
+                          np.stack([x, np.zeros(n), np.full(n, 1e-7)], 1)])
+    tris = np.stack([np.arange(n), np.arange(n) + n, np.arange(n) + 2 * n], 1)
+    sc = Scene(camera=make_camera((0, 0, 5), (0, 0, 0)), meshes=[_mesh("comb", pos, np.zeros_like(pos), np.zeros_like(pos), tris)],
+               instances=[Instance("comb", 0, 0)], materials=[diffuse_material("m", (0.5, 0.5, 0.5))], emitters=[],
+               environment=scenes.Environment(constant=(1.0, 1.0, 1.0)))
+    packed = pack_scene(sc)
+    with _renderer(packed, 16, 16, 2) as r:
+        r.render_pass(0, 2)
+        fb = r.framebuffer()
+    fb2, _ = oracle.OracleScene(packed).render(RenderParams(16, 16, 2), 0, 2)
+    assert np.array_equal(fb, fb2)
