@@ -198,6 +198,22 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
+def load_stage_profile(config):
+    """ncu --set full summary of this config's k_trace_ext (profiles/r01_ncu_stage_kernels.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_stage_kernels.json")))
+    except OSError:
+        return None
+    k = (d.get("kernels") or {}).get(f"{config}_trace_ext")
+    if not k:
+        return None
+    return {"l1tex_throughput_pct": k.get("l1tex_throughput_pct"), "issue_active_pct": k.get("issue_active_pct"),
+            "dram_throughput_gbs": round((k["dram_read_bytes"] + k["dram_write_bytes"]) / k["duration_us"] / 1e3, 1),
+            "threads_per_warp_inst": k.get("threads_per_warp_inst"),
+            "note": "measured limiter of this kernel: L1TEX throughput (local-memory stack, shared/global node "
+                    "loads of divergent lanes), not HBM; source profiles/r01_ncu_stage_kernels.json"}
+
+
 def load_traffic():
     try:
         return json.load(open(os.path.join(ROOT, "profiles", "trace_ext_traffic.json")))
@@ -356,6 +372,7 @@ def run_ours(a):
                      "trace_share_of_step": prof_ms / ms_max,
                      "traffic": ((traffic or {}).get("configs", {}).get(a.config) or {}).get("dram_bytes_per_launch"),
                      "traffic_source": "profiles/trace_ext_traffic.json (ncu dram__bytes_read+write per launch)",
+                     "ncu": load_stage_profile(a.config),
                      "peak_source": ("fallback 6650 GB/s (B200_PROFILING.md)" if peaks.get("fallback")
                                      else "MEASURED_PEAKS.json hbm_gbs (measured copy)")},
         "e2e": e2e,
