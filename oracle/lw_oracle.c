@@ -1358,7 +1358,9 @@ static v3 offset_origin(v3 p, v3 n, v3 dir) {
 /* ---- light hierarchy: sample_light / light_pdf (device: lw_lighttree.cuh) ---------------- */
 #define LT_PMIN 0.015625 /* 1/64: branch probabilities clamped to [PMIN, 1 - PMIN] */
 
-static float lt_importance(const lt_node* N, float x0, float x1, float x2, float n0, float n1, float n2) {
+/* importance as a fraction num / den (den > 0); lt_pleft combines two fractions with one division */
+static void lt_importance(const lt_node* N, float x0, float x1, float x2, float n0, float n1, float n2, float* num,
+                          float* den) {
   float cx = (N->lo[0] + N->hi[0]) * 0.5f, cy = (N->lo[1] + N->hi[1]) * 0.5f, cz = (N->lo[2] + N->hi[2]) * 0.5f;
   float dx = cx - x0, dy = cy - x1, dz = cz - x2;
   float d2 = (dx * dx + dy * dy) + dz * dz;
@@ -1367,26 +1369,34 @@ static float lt_importance(const lt_node* N, float x0, float x1, float x2, float
   float dist2 = d2 > r2 ? d2 : r2;
   int inside = x0 >= N->lo[0] && x0 <= N->hi[0] && x1 >= N->lo[1] && x1 <= N->hi[1] && x2 >= N->lo[2] &&
                x2 <= N->hi[2];
-  if (inside || !(d2 > r2)) return dist2 > 0.0f ? N->tot / dist2 : N->tot;
-  int oct = (dx > 0.0f ? 1 : 0) | (dy > 0.0f ? 2 : 0) | (dz > 0.0f ? 4 : 0); /* signs of x - c */
-  float d = sqrtf(d2);
-  float cos_t = ((n0 * dx + n1 * dy) + n2 * dz) / d;
-  float sin2a = r2 / d2;
-  float cos_a = sqrtf(1.0f - sin2a);
-  float cosb = 1.0f;
-  if (cos_t < cos_a) { /* cos(theta - alpha), the largest cosine over the box's bounding cone */
-    float s2 = 1.0f - cos_t * cos_t;
-    float sin_t = sqrtf(s2 > 0.0f ? s2 : 0.0f);
-    cosb = cos_t * cos_a + sin_t * sqrtf(sin2a);
-    if (cosb < 0.0f) cosb = 0.0f;
+  if (inside || !(d2 > r2)) {
+    *num = N->tot;
+    *den = dist2 > 0.0f ? dist2 : 1.0f;
+    return;
   }
-  return N->flux[oct] * cosb / dist2;
+  int oct = (dx > 0.0f ? 1 : 0) | (dy > 0.0f ? 2 : 0) | (dz > 0.0f ? 4 : 0); /* signs of x - c */
+  /* cos(max(0, theta - alpha)) * d^2 with cos theta = dt / d, cos alpha = sqrt(d2 - r2) / d,
+   * sin alpha = r / d: (dt sqrt(d2 - r2) + sqrt(d2 - dt^2) r) / d^2, 1 when theta <= alpha */
+  float dt = (n0 * dx + n1 * dy) + n2 * dz;
+  float s1 = sqrtf(d2 - r2);
+  if (dt >= s1) {
+    *num = N->flux[oct];
+    *den = dist2;
+    return;
+  }
+  float s2 = d2 - dt * dt;
+  float t = dt * s1 + sqrtf(s2 > 0.0f ? s2 : 0.0f) * sqrtf(r2);
+  if (t < 0.0f) t = 0.0f;
+  *num = N->flux[oct] * t;
+  *den = d2 * dist2;
 }
 
 static double lt_pleft(const lwo_scene* s, int64_t k, v3 x, v3 n) {
   float x0 = (float)x.x, x1 = (float)x.y, x2 = (float)x.z, n0 = (float)n.x, n1 = (float)n.y, n2 = (float)n.z;
-  float il = lt_importance(s->lt + k + 1, x0, x1, x2, n0, n1, n2);
-  float ir = lt_importance(s->lt + s->lt[k].right, x0, x1, x2, n0, n1, n2);
+  float nl, dl, nr, dr;
+  lt_importance(s->lt + k + 1, x0, x1, x2, n0, n1, n2, &nl, &dl);
+  lt_importance(s->lt + s->lt[k].right, x0, x1, x2, n0, n1, n2, &nr, &dr);
+  float il = nl * dr, ir = nr * dl; /* importances scaled by the common factor dl * dr */
   float sum = il + ir;
   float pl = sum > 0.0f ? il / sum : 0.5f;
   if (pl < (float)LT_PMIN) pl = (float)LT_PMIN;

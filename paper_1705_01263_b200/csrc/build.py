@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(BUILD, "liblw_b200.so")
 SOURCES = ["lw_capi.cu", "lw_bvh_build.cu", "lw_render.cu", "lw_sah_build.cu"]
-HEADERS = ["lw_common.cuh", "lw_detmath.cuh", "lw_qmc.cuh", "lw_traverse.cuh", "lw_integrator.cuh", "lw_host.h",
-           "lw_glibc_log_data.h", os.path.join("..", "..", "include", "lw_b200.h")]
+# every header of the library (any change rebuilds all translation units)
+HEADERS = sorted(f for f in os.listdir(HERE) if f.endswith((".cuh", ".h"))) + [os.path.join("..", "..", "include", "lw_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

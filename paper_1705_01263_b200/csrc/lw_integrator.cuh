@@ -30,9 +30,8 @@ struct DevScene {
   const double* emit_pdf;
   const int* emit_alias;
   // light hierarchy (light_mode == LW_LIGHTS_TREE)
-  const LwLightNode* lt_nodes;
-  const unsigned long long* lt_path;
-  const int* lt_depth;
+  LwLightTree lt;
+  int lt_nheap;  // heap slots of lt.nodes
   int light_mode;
   // environment pyramid (env_mode == LW_LIGHTS_ENV_PYRAMID)
   LwEnvPyr env_pyr;
@@ -467,8 +466,9 @@ __device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const Lw
 }
 
 // next-event estimation: fills sh (valid = 0 if no contribution)
+// lt: the light hierarchy with its top staged in shared memory (nullptr: S.lt, global memory)
 __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh,
-                                             const LwLpe* lpe = nullptr) {
+                                             const LwLpe* lpe = nullptr, const LwLightTree* lt = nullptr) {
   sh.valid = 0;
   const lw_material& m = *g.m;
   const LayerW& lw = g.lw;
@@ -524,7 +524,7 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
     if (S.light_mode == LW_LIGHTS_TREE) {
       v3 xr = lw_offset_origin(g.p, g.ngf, g.ngf);
       v3 nr = lw_lt_ref_normal((int)lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z));
-      le = lw_lt_sample(S.lt_nodes, xr, nr, ut, psel, ur);
+      le = lw_lt_sample(lt ? *lt : S.lt, xr, nr, ut, psel, ur);
     } else {
       le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
       psel = S.emit_pdf[le];
@@ -577,7 +577,8 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
 // miss / emission part: returns false if the path ends before any scattering
 // lpe (megakernel with LPE layers): routes the emission to the layers accepting ... L / ... E
 __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& ps, const LwHit& h, ShadeGeom& g,
-                                                  double& w, const LwLpe* lpe = nullptr, long long pix = 0) {
+                                                  double& w, const LwLpe* lpe = nullptr, long long pix = 0,
+                                                  const LwLightTree* lt = nullptr) {
   v3 d = ps.d;
   if (h.tri < 0) {
     if (S.env_kind != LW_ENV_NONE) {
@@ -598,7 +599,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
     if (!ps.spec_prev) {
       double cos_l = fabs(dot3(g.ng, d));
       double psel = S.light_mode == LW_LIGHTS_TREE
-                        ? lw_lt_pdf(S.lt_nodes, S.lt_path, S.lt_depth, e, ps.o, lw_lt_ref_normal(ps.nprev))
+                        ? lw_lt_pdf(lt ? *lt : S.lt, e, ps.o, lw_lt_ref_normal(ps.nprev))
                         : S.emit_pdf[e];
       double pdf_area = S.p_tri * psel / S.emit_area[e];
       double pl = pdf_area * (h.t * h.t) / cos_l;

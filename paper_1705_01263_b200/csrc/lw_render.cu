@@ -81,6 +81,9 @@ struct lw_ctx {
   DeviceBVH ref_bvh;
   bool ref_built = false;
   int64_t lt_nodes = 0;  // light hierarchy nodes (0 = alias-table light selection)
+  std::vector<LwLightNode> lt_dfs;  // the hierarchy as built (depth-first), for lw_ctx_light_tree_download
+  std::vector<unsigned long long> lt_path;
+  std::vector<int> lt_depth;
   LwLpe lpe = {nullptr, nullptr, 0, 0, nullptr, 0};  // light-path-expression layers (megakernel)
   int64_t ntris = 0;
   lw_render_params params;
@@ -617,9 +620,12 @@ __device__ __forceinline__ void load_hit(const Pool& P, int s, LwHit& h) {
 
 // NEE half of the material stage (runs before k_shade so it sees the incoming throughput):
 // light / environment sample, BSDF evaluation, shadow-ray setup
-template <bool LPE>
+template <bool LPE, bool LT>
 __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt,
                                                                 LwLpe lpe) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  LwLightTree lt;
+  if (LT) lt = lw_lt_stage(S.lt, S.lt_nheap, smem);
   int n = cnt->n_ext;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
@@ -646,7 +652,7 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
         lw_shade_hit(S, ps.d, h, g, w);
         lw_shade_frame(S, ps.d, h, w, g);
         ShadowRay sh;
-        lw_shade_nee(S, ps, g, sh, LPE ? &lpe : nullptr);
+        lw_shade_nee(S, ps, g, sh, LPE ? &lpe : nullptr, LT ? &lt : nullptr);
         shadow = sh.valid != 0;
         if (LPE && shadow) {
           P.sh5[s] = make_double2(sh.c_diffuse.x, sh.c_diffuse.y);
@@ -669,8 +675,11 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
 }
 
 // material half: miss/emission (MIS), BSDF sampling, Russian roulette, next ray, stage tag
-template <bool LPE>
+template <bool LPE, bool LT>
 __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt, LwLpe lpe) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  LwLightTree lt;
+  if (LT) lt = lw_lt_stage(S.lt, S.lt_nheap, smem);
   int n = cnt->n_ext;
   unsigned long long alive_count = 0;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
@@ -685,7 +694,7 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
       double w;
       bool alive = false;
       if (LPE) ps.lpe = P.lpe_state[s];
-      if (lw_shade_emission(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0)) {
+      if (lw_shade_emission(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0, LT ? &lt : nullptr)) {
         lw_shade_frame(S, ps.d, h, w, g);
         alive = lw_shade_material(S, ps, g, LPE ? &lpe : nullptr);
       }
@@ -806,10 +815,12 @@ __global__ void k_camera_dbg(DevScene S, const long long* idx, long long n, doub
 
 __global__ void k_light_sample_dbg(DevScene S, const double* x, const double* nrm, const double* u, long long n,
                                    long long* oe, double* op, double* ou) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  LwLightTree T = lw_lt_stage(S.lt, S.lt_nheap, smem);
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ps, uo;
-  oe[i] = lw_lt_sample(S.lt_nodes, lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i), u[i], ps, uo);
+  oe[i] = lw_lt_sample(T, lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i), u[i], ps, uo);
   op[i] = ps;
   ou[i] = uo;
 }
@@ -818,7 +829,7 @@ __global__ void k_light_pdf_dbg(DevScene S, const long long* e, const double* x,
                                 double* op) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  op[i] = lw_lt_pdf(S.lt_nodes, S.lt_path, S.lt_depth, e[i], lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i));
+  op[i] = lw_lt_pdf(S.lt, e[i], lw_ld3(x + 3 * i), lw_ld3(nrm + 3 * i));  // global nodes only
 }
 
 __global__ void k_env_sample_dbg(DevScene S, const long long* pk, const double* uv, long long n, long long* ot,
@@ -843,6 +854,12 @@ __global__ void k_env_pdf_dbg(DevScene S, const long long* pk, const long long* 
 __global__ void k_resolve(const unsigned long long* fb, long long n, double scale, float* out) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) out[i] = (float)((double)(long long)fb[i] * scale);
+}
+
+// dynamic shared memory of the light-hierarchy top (0 without a hierarchy)
+size_t lt_smem_bytes(const lw_ctx* c) {
+  if (c->S.light_mode != LW_LIGHTS_TREE) return 0;
+  return sizeof(LwLightNode) * (size_t)std::min(c->S.lt_nheap, LW_LT_SMEM_NODES);
 }
 
 int nrnodes_of(const lw_ctx* c) { return c->ref_bvh.nnodes > 1 ? (int)((c->ref_bvh.nnodes - 1) / 2) : 0; }
@@ -941,6 +958,8 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     launches = 1;
   } else {
     const bool lpe_on = c->lpe.nlayers > 0;
+    const size_t ltsm = lt_smem_bytes(c);  // light-hierarchy top staged by the shading kernels
+    const bool ltm = ltsm > 0;
     int pool = 1 << p.pool_log2;
     if ((long long)pool > total) {
       long long r = 1;
@@ -980,12 +999,18 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
         else
           k_trace_ext<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         if (timed) cudaEventRecord(event(), st);
-        if (lpe_on) {
-          k_shade_nee<true><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-          k_shade<true><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        if (lpe_on && ltm) {
+          k_shade_nee<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        } else if (lpe_on) {
+          k_shade_nee<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        } else if (ltm) {
+          k_shade_nee<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         } else {
-          k_shade_nee<false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-          k_shade<false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade_nee<false, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<false, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         }
         if (timed) {
           marks.push_back({ev, 1});
@@ -1346,26 +1371,51 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   }
   // light hierarchy, built on the host like the alias tables
   S.light_mode = LW_LIGHTS_ALIAS;
-  S.lt_nodes = nullptr;
-  S.lt_path = nullptr;
-  S.lt_depth = nullptr;
+  memset(&S.lt, 0, sizeof(S.lt));
+  S.lt_nheap = 0;
+  c->lt_dfs.clear();
+  c->lt_path.clear();
+  c->lt_depth.clear();
   if ((d->light_sampler & LW_LIGHTS_TREE) && S.nemit > 0) {
     std::vector<LwLightNode> ln;
     std::vector<unsigned long long> lp;
     std::vector<int> ld;
     LW_STATUS_TRY(light_tree_build(d->verts, d->emit_tri, d->emit_weight, d->emit_twosided, d->nemit, ln, lp, ld));
+    // heap order for the device (children 2i+1, 2i+2): the top levels become a contiguous prefix
+    int dmax = 0;
+    for (int v : ld) dmax = std::max(dmax, v);
+    LW_CHECK_ARG(dmax <= 26, "light tree too deep for the heap layout (more than 2^26 emitters)");
+    int64_t nheap = (2LL << dmax) - 1;
+    std::vector<LwLightNode> hp(nheap);
+    std::vector<std::pair<int64_t, int64_t>> todo{{0, 0}};  // (dfs id, heap id)
+    while (!todo.empty()) {
+      auto [di, hi] = todo.back();
+      todo.pop_back();
+      hp[hi] = ln[di];
+      if (ln[di].right >= 0) {
+        todo.push_back({ln[di].right, 2 * hi + 2});
+        todo.push_back({di + 1, 2 * hi + 1});
+        hp[hi].right = 1;
+      }
+    }
     LwLightNode* dn;
     unsigned long long* dp;
     int* dd;
-    LW_STATUS_TRY(dev_upload(c, dn, ln.data(), (int64_t)ln.size()));
+    LW_STATUS_TRY(dev_upload(c, dn, hp.data(), nheap));
     LW_STATUS_TRY(dev_upload(c, dp, lp.data(), (int64_t)lp.size()));
     LW_STATUS_TRY(dev_upload(c, dd, ld.data(), (int64_t)ld.size()));
     LW_CUDA_TRY(cudaStreamSynchronize(st));  // host vectors go out of scope
-    S.lt_nodes = dn;
-    S.lt_path = dp;
-    S.lt_depth = dd;
+    S.lt.nodes = dn;
+    S.lt.top = dn;
+    S.lt.ntop = 0;
+    S.lt.path = dp;
+    S.lt.depth = dd;
+    S.lt_nheap = (int)nheap;
     S.light_mode = LW_LIGHTS_TREE;
     c->lt_nodes = (int64_t)ln.size();
+    c->lt_dfs = std::move(ln);
+    c->lt_path = std::move(lp);
+    c->lt_depth = std::move(ld);
   }
   // environment
   S.env_kind = d->env_kind;
@@ -1654,11 +1704,7 @@ int lw_ctx_light_tree_info(lw_ctx* c, int64_t* nnodes) {
 int lw_ctx_light_tree_download(lw_ctx* c, double* nodes15, int32_t* right, uint64_t* path, int32_t* depth) {
   LW_CHECK_ARG(c && c->has_scene, "no scene");
   if (c->lt_nodes == 0) return LW_OK;
-  std::vector<LwLightNode> h(c->lt_nodes);
-  LW_CUDA_TRY(cudaMemcpyAsync(h.data(), c->S.lt_nodes, sizeof(LwLightNode) * h.size(), cudaMemcpyDeviceToHost, c->stream));
-  if (path) LW_CUDA_TRY(cudaMemcpyAsync(path, c->S.lt_path, sizeof(uint64_t) * c->S.nemit, cudaMemcpyDeviceToHost, c->stream));
-  if (depth) LW_CUDA_TRY(cudaMemcpyAsync(depth, c->S.lt_depth, sizeof(int32_t) * c->S.nemit, cudaMemcpyDeviceToHost, c->stream));
-  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const std::vector<LwLightNode>& h = c->lt_dfs;
   for (size_t k = 0; k < h.size(); k++) {
     double* o = nodes15 ? nodes15 + 15 * k : nullptr;
     if (o) {
@@ -1670,6 +1716,10 @@ int lw_ctx_light_tree_download(lw_ctx* c, double* nodes15, int32_t* right, uint6
       for (int b = 0; b < 8; b++) o[7 + b] = h[k].flux[b];
     }
     if (right) right[k] = h[k].right;
+  }
+  for (int64_t e = 0; e < c->S.nemit; e++) {
+    if (path) path[e] = c->lt_path[e];
+    if (depth) depth[e] = c->lt_depth[e];
   }
   return LW_OK;
 }
@@ -1691,7 +1741,7 @@ int lw_ctx_light_sample(lw_ctx* c, const double* x, const double* nrm, const dou
   LW_CUDA_TRY(cudaMemcpyAsync(bx.p, x, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
   LW_CUDA_TRY(cudaMemcpyAsync(bn.p, nrm, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
   LW_CUDA_TRY(cudaMemcpyAsync(bu.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-  k_light_sample_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->S, bx.as<double>(), bn.as<double>(), bu.as<double>(),
+  k_light_sample_dbg<<<grid_for(n, 128, 1 << 30), 128, lt_smem_bytes(c), st>>>(c->S, bx.as<double>(), bn.as<double>(), bu.as<double>(),
                                                                  n, be.as<long long>(), bp.as<double>(), bo.as<double>());
   LW_CUDA_TRY(cudaGetLastError());
   LW_CUDA_TRY(cudaMemcpyAsync(out_e, be.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
