@@ -474,7 +474,8 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
   const LayerW& lw = g.lw;
   if (!(lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE))) return;
   const int bd = 4 + 8 * ps.bounce;
-  double ul = lw_qmc_s(S, bd + 2, ps.index), vl = lw_qmc_s(S, bd + 3, ps.index);
+  double ul, vl;
+  lw_halton2(S.qdims, S.qperm, bd + 2, bd + 3, ps.index, ul, vl);
   v3 wi = mk3(0.0, 0.0, 0.0), Le = mk3(0.0, 0.0, 0.0);
   double pl = 0.0, tmax_sh = INFINITY;
   bool ok = false;
@@ -618,7 +619,8 @@ __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& 
   const int b = ps.bounce;
   const int bd = 4 + 8 * b;
   BSample bs;
-  double ub = lw_qmc_s(S, bd + 0, ps.index), vb = lw_qmc_s(S, bd + 1, ps.index);
+  double ub, vb;
+  lw_halton2(S.qdims, S.qperm, bd + 0, bd + 1, ps.index, ub, vb);
   if (!lw_bsdf_sample(*g.m, g.lw, g.wol, g.front, ub, vb, bs)) return false;
   if (lpe) ps.lpe = lw_lpe_step(lpe, ps.lpe, bs.event);
   v3 wi = lw_to_world(g.fr, bs.wi);

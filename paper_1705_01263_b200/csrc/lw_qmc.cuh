@@ -104,3 +104,42 @@ __device__ __forceinline__ double lw_halton(const QmcDim* __restrict__ dims, con
   }
   return rev / scale;
 }
+
+// Two dimensions of the same index with interleaved digit loops: the two dependent
+// divide-and-accumulate chains run side by side (instruction-level parallelism for the
+// latency-bound shading kernels).  Same integers and the same final divisions as lw_halton, so
+// the same bits; falls back to lw_halton outside the fixed-digit 32-bit regime.
+__device__ __forceinline__ void lw_halton2(const QmcDim* __restrict__ dims, const uint16_t* __restrict__ perm, int dimA,
+                                           int dimB, long long index, double& a, double& b) {
+  QmcDim A = dims[dimA], B = dims[dimB];
+  uint64_t n = (uint64_t)index;
+  if (index <= 0 || A.base == 2 || B.base == 2 || !A.digits32 || !B.digits32 || (n >> 32) || n > A.exact_limit ||
+      n > B.exact_limit) {
+    a = lw_halton(dims, perm, dimA, index);
+    b = lw_halton(dims, perm, dimB, index);
+    return;
+  }
+  const uint16_t *pa = perm + A.perm_off, *pb = perm + B.perm_off;
+  uint32_t ma = (uint32_t)n, mb = (uint32_t)n;
+  uint64_t ra = 0, sa = 1, rb = 0, sb = 1;
+  const uint32_t kmax = A.digits32 > B.digits32 ? A.digits32 : B.digits32;
+#pragma unroll 2
+  for (uint32_t k = 0; k < kmax; k++) {
+    if (k < A.digits32) {
+      uint32_t q = lw_div32(ma, A);
+      uint32_t digit = ma - q * A.base;
+      ra = ra * A.base + __ldg(pa + digit);
+      sa *= A.base;
+      ma = q;
+    }
+    if (k < B.digits32) {
+      uint32_t q = lw_div32(mb, B);
+      uint32_t digit = mb - q * B.base;
+      rb = rb * B.base + __ldg(pb + digit);
+      sb *= B.base;
+      mb = q;
+    }
+  }
+  a = (double)ra / (double)sa;
+  b = (double)rb / (double)sb;
+}
