@@ -242,6 +242,7 @@ int lw_framebuffer_download(lw_ctx* ctx, int64_t* host_fb);           /* W*H*3 i
 int lw_framebuffer_resolve(lw_ctx* ctx, double inv_samples, float* host_rgb); /* W*H*3 float32 */
 int lw_framebuffer_copy_device(lw_ctx* ctx, void* dst_device);         /* D2D copy for NCCL reduction */
 int lw_framebuffer_load_device(lw_ctx* ctx, const void* src_device);   /* D2D copy back after reduction */
+int lw_framebuffer_upload(lw_ctx* ctx, const int64_t* host_fb);       /* H2D: resume from a checkpoint */
 int lw_get_stats(lw_ctx* ctx, lw_render_stats* stats);
 /* debug/parity surface of the render traversal (near-first, conservative cull) */
 int lw_ctx_trace_closest(lw_ctx* ctx, const double* origins, const double* dirs, const double* tmaxs, int64_t n,

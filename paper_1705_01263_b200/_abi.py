@@ -217,6 +217,7 @@ SIGNATURES = {
     "lw_ctx_light_tree_download": (C.c_int, [_V, _pd, _pi32, C.POINTER(C.c_uint64), _pi32]),
     "lw_ctx_light_sample": (C.c_int, [_V, _pd, _pd, _pd, C.c_int64, _pi64, _pd, _pd]),
     "lw_ctx_light_pdf": (C.c_int, [_V, _pi64, _pd, _pd, C.c_int64, _pd]),
+    "lw_framebuffer_upload": (C.c_int, [_V, _pi64]),
     "lw_ctx_set_lpe": (C.c_int, [_V, C.c_int32, C.c_int32, C.POINTER(C.c_int16), C.POINTER(C.c_uint8), C.c_int32]),
     "lw_ctx_lpe_download": (C.c_int, [_V, C.c_int32, _pi64]),
     "lw_ctx_env_pyramid_info": (C.c_int, [_V, _pi32]),

@@ -6,6 +6,7 @@ pyproject.toml:12-13, with the flags of SPEC.md:800 but ships no cli module).
         [--lights alias|tree] [--env-sampling alias|pyramid]
         [--devices N [--contexts-per-device C] [--fail DEV@ITER ...]]   # batch scheduler
         [--layer NAME=EXPR ...]                                          # LPE output layers
+        [--checkpoint state.npz] [--resume state.npz]                    # progressive state
     python -m paper_1705_01263_b200.cli composite --layers a.pfm b.pfm --gains 1 2 --out c.pfm
 
 Scenes come from the procedural configs (the text-format parser is out of scope, SURVEY.md §2.1);
@@ -75,6 +76,14 @@ def cmd_render(args) -> int:
     step = args.snapshot_every or spp
     t0 = time.perf_counter()
     with Renderer(None, w, h, depth, device=args.device, engine=engine, packed=packed) as r:
+        done0 = 0
+        if args.resume:
+            try:
+                r.load_checkpoint(args.resume)
+            except (OSError, ValueError, KeyError) as e:
+                print(f"error: cannot resume from '{args.resume}': {e}", file=sys.stderr)
+                return 2
+            done0 = r.iterations
         if layers:
             from paper_1705_01263_b200.lpe import LpeError
 
@@ -83,12 +92,14 @@ def cmd_render(args) -> int:
             except LpeError as e:
                 print(f"error: --layer: {e}", file=sys.stderr)
                 return 2
-        done = 0
+        done = done0
         while done < spp:
             k = min(step, spp - done)
             r.render_pass(done, done + k)
             done += k
             write_pfm(f"{args.out}_{done:06d}.pfm", r.image(done))
+            if args.checkpoint:
+                r.save_checkpoint(args.checkpoint)
             for name, img in (r.layer_images(done).items() if layers else []):
                 write_pfm(f"{args.out}_{name}_{done:06d}.pfm", img)
         stats = r.stats()
@@ -178,6 +189,8 @@ def main(argv=None) -> int:
     rp.add_argument("--devices", type=int, default=1, help="batch scheduler over GPUs 0..N-1")
     rp.add_argument("--contexts-per-device", type=int, default=1, help="simulated devices per GPU")
     rp.add_argument("--fail", action="append", default=None, help="inject a failure: DEV@ITER (SPEC.md:800)")
+    rp.add_argument("--checkpoint", default=None, help="save the progressive state (.npz) after every snapshot")
+    rp.add_argument("--resume", default=None, help="continue from a checkpoint written by --checkpoint")
     rp.add_argument("--layer", action="append", default=None,
                     help="light-path-expression output layer NAME=EXPR (lpe.py syntax), repeatable")
     cp = sub.add_parser("composite", help="sum of gain * layer PFMs")

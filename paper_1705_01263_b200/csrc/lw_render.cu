@@ -1583,6 +1583,13 @@ int lw_framebuffer_copy_device(lw_ctx* c, void* dst) {
   return LW_OK;
 }
 
+int lw_framebuffer_upload(lw_ctx* c, const int64_t* host_fb) {
+  LW_CHECK_ARG(c && c->configured && host_fb, "bad arguments");
+  LW_CUDA_TRY(cudaMemcpyAsync(c->d_fb, host_fb, sizeof(int64_t) * 3 * c->fb_pixels, cudaMemcpyHostToDevice, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
 int lw_framebuffer_load_device(lw_ctx* c, const void* src) {
   LW_CHECK_ARG(c && c->configured && src, "bad arguments");
   LW_CUDA_TRY(cudaMemcpyAsync(c->d_fb, src, sizeof(int64_t) * 3 * c->fb_pixels, cudaMemcpyDeviceToDevice, c->stream));

@@ -122,6 +122,32 @@ class Renderer:
         check(self.lib.lw_framebuffer_resolve(self.ctx, 1.0 / max(samples, 1), ptr(out, C.c_float)))
         return out
 
+    # -- checkpoint / resume (progressive state = int64 framebuffer + iteration count)
+    def _fingerprint(self) -> str:
+        import hashlib
+
+        h = hashlib.sha256()
+        for k in ("verts", "normals", "material", "emit_tri", "emit_rad"):
+            a = self.packed.arrays.get(k)
+            if isinstance(a, np.ndarray):
+                h.update(np.ascontiguousarray(a).tobytes())
+        p = self.params
+        h.update(f"{p.width}x{p.height}d{p.max_depth}".encode())
+        return h.hexdigest()
+
+    def save_checkpoint(self, path):
+        """Framebuffer + progressive state; load_checkpoint on a renderer of the same scene and
+        parameters continues the render bit-identically (int64 accumulation)."""
+        np.savez(path, fb=self.framebuffer(), iterations=self.iterations, fingerprint=self._fingerprint())
+
+    def load_checkpoint(self, path):
+        z = np.load(path)
+        if str(z["fingerprint"]) != self._fingerprint():
+            raise ValueError("checkpoint belongs to a different scene or resolution/depth")
+        fb = np.ascontiguousarray(z["fb"], np.int64)
+        check(self.lib.lw_framebuffer_upload(self.ctx, ptr(fb, C.c_int64)))
+        self.iterations = int(z["iterations"])
+
     def copy_framebuffer_to(self, device_ptr: int):
         check(self.lib.lw_framebuffer_copy_device(self.ctx, C.c_void_p(device_ptr)))
 

@@ -280,3 +280,35 @@ def test_degenerate_deep_sah_tree_falls_back_to_median(gpu, oracle):
         fb = r.framebuffer()
     fb2, _ = oracle.OracleScene(packed).render(RenderParams(16, 16, 2), 0, 2)
     assert np.array_equal(fb, fb2)
+
+
+def test_checkpoint_resume_bit_exact(cornell_packed, tmp_path):
+    """save after iterations [0, 6), resume in a new context, render [6, 12): identical
+    to rendering [0, 12) in one context; a checkpoint of another scene is refused."""
+    ck = str(tmp_path / "ck.npz")
+    with _renderer(cornell_packed, 48, 32, 5) as r:
+        r.render_pass(0, 6)
+        r.save_checkpoint(ck)
+    with _renderer(cornell_packed, 48, 32, 5) as r:
+        r.load_checkpoint(ck)
+        assert r.iterations == 6
+        r.render_pass(6, 12)
+        resumed = r.framebuffer()
+    with _renderer(cornell_packed, 48, 32, 5) as r:
+        r.render_pass(0, 12)
+        assert np.array_equal(r.framebuffer(), resumed)
+    with _renderer(pack_scene(scenes.soup(64, seed=1)), 48, 32, 5) as r:
+        with pytest.raises(ValueError):
+            r.load_checkpoint(ck)
+
+
+def test_cli_checkpoint_resume(gpu, tmp_path):
+    from paper_1705_01263_b200 import cli
+    from paper_1705_01263_b200.imagefiles import read_pfm
+
+    a, b, ck = str(tmp_path / "a"), str(tmp_path / "b"), str(tmp_path / "ck.npz")
+    base = ["render", "--config", "C1", "--res", "24x16"]
+    assert cli.main(base + ["--iterations", "8", "--out", a]) == 0
+    assert cli.main(base + ["--iterations", "4", "--out", b, "--checkpoint", ck]) == 0
+    assert cli.main(base + ["--iterations", "8", "--out", b, "--resume", ck]) == 0
+    assert (read_pfm(a + "_000008.pfm") == read_pfm(b + "_000008.pfm")).all()
