@@ -285,6 +285,47 @@ __device__ __forceinline__ unsigned lw_node_hit(const LwRayF& r, const WNode* __
   return mask;
 }
 
+// 256-bit read-only loads (sm_100 LDG.E.ENL2.256): a 128-byte node in four load instructions
+// (3 x 32 B planes + the refs) instead of seven 16-byte ones; the trace kernels are bound by L1TEX
+// wavefronts, which scale with load instructions of divergent lanes
+__device__ __forceinline__ void lw_ldg256(const void* p, float v[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
+__device__ __forceinline__ unsigned lw_node_hit_g(const LwRayF& r, const WNode* __restrict__ nd, float best, float tn[4],
+                                                  int ref[4]) {
+  float w[24];
+  lw_ldg256(reinterpret_cast<const char*>(nd), w);
+  lw_ldg256(reinterpret_cast<const char*>(nd) + 32, w + 8);
+  lw_ldg256(reinterpret_cast<const char*>(nd) + 64, w + 16);
+  int4 rf = __ldg(&nd->ref);
+  ref[0] = rf.x;
+  ref[1] = rf.y;
+  ref[2] = rf.z;
+  ref[3] = rf.w;
+  unsigned mask = 0;
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    // w[4 a + c] = lo[a].c, w[12 + 4 a + c] = hi[a].c
+    float nx = r.sn[0] >= 3 ? w[12 + c] : w[c], fx = r.sn[0] >= 3 ? w[c] : w[12 + c];
+    float ny = r.sn[1] >= 3 ? w[16 + c] : w[4 + c], fy = r.sn[1] >= 3 ? w[4 + c] : w[16 + c];
+    float nz = r.sn[2] >= 3 ? w[20 + c] : w[8 + c], fz = r.sn[2] >= 3 ? w[8 + c] : w[20 + c];
+    float a0 = __fmaf_rn(nx, r.inv[0], r.on[0]);
+    float a1 = __fmaf_rn(ny, r.inv[1], r.on[1]);
+    float a2 = __fmaf_rn(nz, r.inv[2], r.on[2]);
+    float b0 = __fmaf_rn(fx, r.inv[0], r.of[0]);
+    float b1 = __fmaf_rn(fy, r.inv[1], r.of[1]);
+    float b2 = __fmaf_rn(fz, r.inv[2], r.of[2]);
+    float lo = fmaxf(fmaxf(a0, a1), fmaxf(a2, 0.0f));
+    float hi = fminf(fminf(b0, b1), fminf(b2, best));
+    tn[c] = lo;
+    if (lo <= hi && ref[c] != LW_REF_NONE) mask |= 1u << c;
+  }
+  return mask;
+}
+
 __device__ __forceinline__ const WNode* lw_node_at(const RenderBVH& bvh, int ref) {
   return reinterpret_cast<const WNode*>(reinterpret_cast<const char*>(bvh.nodes) + (size_t)ref * bvh.nstride);
 }
@@ -357,7 +398,8 @@ struct LwClosest {
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
+      unsigned m = bvh.nstride == (int)sizeof(WNode) ? lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr)
+                                                     : lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
       if (COUNT) cnt->nodes++;
 #pragma unroll
       for (int c = 0; c < 4; c++)
@@ -440,7 +482,8 @@ struct LwAny {
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
+      unsigned m = bvh.nstride == (int)sizeof(WNode) ? lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr)
+                                                     : lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
       if (COUNT) cnt->nodes++;
       if (m == 0) {
         ref = LW_REF_NONE;
