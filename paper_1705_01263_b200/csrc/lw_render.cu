@@ -1317,6 +1317,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   int rc_w = collapse_wide(c, bn, nr, root_ref, levels, wn, max_need);
   if (bn) cudaFreeAsync(bn, st);
   LW_STATUS_TRY(rc_w);
+  if (getenv("LW_DEBUG_STACK")) fprintf(stderr, "render BVH kind %d: %d wide nodes, stack need %d\n", kind, nr, max_need);
   if (max_need <= LW_STACK) break;
   if (kind != LW_BVH_MEDIAN) {
     kind = LW_BVH_MEDIAN;

@@ -367,52 +367,51 @@ __device__ __forceinline__ void lw_cswap(float& ta, int& ra, float& tb, int& rb)
   ra = q;
 }
 
-// Resumable traversals: init() sets a ray up, step() descends to the next leaf, tests it and
-// pops the next subtree; it returns true once the ray is finished.  lw_trace_closest /
-// lw_trace_any loop step() to completion.  (A persistent dynamic-fetch variant that refilled
-// finished lanes between steps measured 4% faster on C3 and 25% slower on C2; not kept.)
+// The traversals are flat loops over scalar locals: only the stack is an addressable array.
+// (Written as a resumable object with init()/step() the whole object -- ray constants, hit
+// record, stack pointer -- lived in local memory and was re-read on every node visit, and a
+// dynamically indexed child array forced a local store per node: ~3x the L1TEX requests of the
+// node fetches themselves.  A persistent dynamic-fetch variant that refilled finished lanes between
+// leaves measured 4% faster on C3 and 25% slower on C2; not kept.)
+
+__device__ __forceinline__ unsigned lw_node_test(const RenderBVH& bvh, const LwRayF& r, int ref, float best, float tn[4],
+                                                 int cr[4]) {
+  return bvh.nstride == (int)sizeof(WNode) ? lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr)
+                                           : lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
+}
+
+// the single hit child of mask m (no dynamic register-array index)
+__device__ __forceinline__ int lw_pick(unsigned m, const int cr[4]) {
+  return (m & 1u) ? cr[0] : (m & 2u) ? cr[1] : (m & 4u) ? cr[2] : cr[3];
+}
 
 // closest hit, t in (0, tmax], nearest child first
-struct LwClosest {
+template <bool COUNT = false>
+__device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
+                                                 double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
   LwRayF r;
-  LwHit h;
-  double best_det;
-  float best;
-  int ref, sp;
+  lw_rayf_setup(r, bvh, o, d);
+  double ht = tmax, hu = 0.0, hv = 0.0, best_det = 1.0;
+  long long htri = -1;
+  float best = __double2float_ru(tmax);
+  int ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
+  int sp = 0;
   unsigned long long stk[LW_STACK];
-
-  __device__ __forceinline__ void init(const RenderBVH& bvh, const double o[3], const double d[3], double tmax) {
-    h.t = tmax;
-    h.tri = -1;
-    h.bu = 0.0;
-    h.bv = 0.0;
-    best_det = 1.0;
-    sp = 0;
-    ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
-    lw_rayf_setup(r, bvh, o, d);
-    best = __double2float_ru(tmax);
-  }
-
-  template <bool COUNT = false>
-  __device__ __forceinline__ bool step(const RenderBVH& bvh, LwTraceCount* cnt = nullptr) {
-    while (ref >= 0 && ref != LW_REF_NONE) {
+  while (ref != LW_REF_NONE) {
+    while (ref >= 0) {
       float tn[4];
       int cr[4];
-      unsigned m = bvh.nstride == (int)sizeof(WNode) ? lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr)
-                                                     : lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
+      unsigned m = lw_node_test(bvh, r, ref, best, tn, cr);
       if (COUNT) cnt->nodes++;
+      int nh = __popc(m);
+      if (nh <= 1) {
+        ref = nh == 0 ? LW_REF_NONE : lw_pick(m, cr);
+        if (nh == 0) break;
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 4; c++)
         if (!(m & (1u << c))) tn[c] = INFINITY;
-      int nh = __popc(m);
-      if (nh == 0) {
-        ref = LW_REF_NONE;
-        break;
-      }
-      if (nh == 1) {
-        ref = cr[__ffs(m) - 1];
-        continue;
-      }
       lw_cswap(tn[0], cr[0], tn[1], cr[1]);
       lw_cswap(tn[2], cr[2], tn[3], cr[3]);
       lw_cswap(tn[0], cr[0], tn[2], cr[2]);
@@ -429,13 +428,13 @@ struct LwClosest {
       for (int k = start; k < start + count; k++) {
         if (COUNT) cnt->tris++;
         double t, bu, bv, det;
-        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv, det) || t <= 0.0 || t > h.t) continue;
+        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv, det) || t <= 0.0 || t > ht) continue;
         long long id = bvh.tris[k].id;
-        if (t == h.t && h.tri >= 0 && id >= h.tri) continue;
-        h.t = t;
-        h.tri = id;
-        h.bu = bu;  // undivided v, w; divided by det in finish()
-        h.bv = bv;
+        if (t == ht && htri >= 0 && id >= htri) continue;
+        ht = t;
+        htri = id;
+        hu = bu;  // undivided v, w; divided by det once the hit is final
+        hv = bv;
         best_det = det;
         best = __double2float_ru(t);
       }
@@ -448,48 +447,34 @@ struct LwClosest {
         break;
       }
     }
-    return ref == LW_REF_NONE;
   }
-
-  __device__ __forceinline__ void finish() {
-    if (h.tri >= 0) {
-      h.bu = h.bu / best_det;
-      h.bv = h.bv / best_det;
-    }
-  }
-};
+  h.t = ht;
+  h.tri = htri;
+  h.bu = htri >= 0 ? hu / best_det : 0.0;
+  h.bv = htri >= 0 ? hv / best_det : 0.0;
+}
 
 // any hit with 0 < t < tmax
-struct LwAny {
+template <bool COUNT = false>
+__device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
+                                             LwTraceCount* cnt = nullptr) {
   LwRayF r;
-  double tmax;
-  float best;
-  int ref, sp;
-  bool occluded;
+  lw_rayf_setup(r, bvh, o, d);
+  float best = __double2float_ru(tmax);
+  int ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
+  int sp = 0;
   int stk[LW_STACK];
-
-  __device__ __forceinline__ void init(const RenderBVH& bvh, const double o[3], const double d[3], double tm) {
-    tmax = tm;
-    sp = 0;
-    occluded = false;
-    ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
-    lw_rayf_setup(r, bvh, o, d);
-    best = __double2float_ru(tm);
-  }
-
-  template <bool COUNT = false>
-  __device__ __forceinline__ bool step(const RenderBVH& bvh, LwTraceCount* cnt = nullptr) {
-    while (ref >= 0 && ref != LW_REF_NONE) {
+  while (ref != LW_REF_NONE) {
+    while (ref >= 0) {
       float tn[4];
       int cr[4];
-      unsigned m = bvh.nstride == (int)sizeof(WNode) ? lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr)
-                                                     : lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
+      unsigned m = lw_node_test(bvh, r, ref, best, tn, cr);
       if (COUNT) cnt->nodes++;
       if (m == 0) {
         ref = LW_REF_NONE;
         break;
       }
-      ref = cr[__ffs(m) - 1];
+      ref = lw_pick(m, cr);
       m &= m - 1;
 #pragma unroll
       for (int c = 1; c < 4; c++)
@@ -500,38 +485,10 @@ struct LwAny {
       int start = v >> 3, count = v & 7;
       for (int k = start; k < start + count; k++) {
         if (COUNT) cnt->tris++;
-        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) {
-          occluded = true;
-          return true;
-        }
+        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) return true;
       }
     }
-    if (sp == 0) {
-      ref = LW_REF_NONE;
-      return true;
-    }
-    ref = stk[--sp];
-    return false;
+    ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
   }
-};
-
-template <bool COUNT = false>
-__device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
-                                                 double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
-  LwClosest q;
-  q.init(bvh, o, d, tmax);
-  while (!q.step<COUNT>(bvh, cnt)) {
-  }
-  q.finish();
-  h = q.h;
-}
-
-template <bool COUNT = false>
-__device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
-                                             LwTraceCount* cnt = nullptr) {
-  LwAny q;
-  q.init(bvh, o, d, tmax);
-  while (!q.step<COUNT>(bvh, cnt)) {
-  }
-  return q.occluded;
+  return false;
 }
