@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
   warp_add(&cnt->paths, paths);
 }
 
-template <bool COUNT>
+template <bool COUNT, int NODES>
 __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
       double o[3], d[3];
       load_ray(P, s, o, d);
       LwHit h;
-      lw_trace_closest<COUNT>(bvh, o, d, INFINITY, h, &tc);
+      lw_trace_closest<COUNT, NODES>(bvh, o, d, INFINITY, h, &tc);
       P.hit0[s] = make_double2(h.t, h.bu);
       P.hit1[s] = make_double2(h.bv, __longlong_as_double(h.tri));
     }
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
   warp_add(&cnt->n_alive_ull, alive_count);
 }
 
-template <bool COUNT, bool LPE>
+template <bool COUNT, bool LPE, int NODES>
 __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem,
                                                                       LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S
       int s = P.q_shadow[k];
       double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
       double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
-      if (!lw_trace_any<COUNT>(bvh, o, d, e.x, &tc)) {
+      if (!lw_trace_any<COUNT, NODES>(bvh, o, d, e.x, &tc)) {
         double2 f = P.sh4[s], t1 = P.tp1[s], t2 = P.tp2[s];
         t1.y = t1.y + e.y;
         t2.x = t2.x + f.x;
@@ -929,6 +929,18 @@ int alloc_pool(lw_ctx* c, int size) {
   return LW_OK;
 }
 
+template <int NODES>
+void launch_shadow(lw_ctx* c, int grid, size_t smem, int nr, bool lpe_on, bool count) {
+  cudaStream_t st = c->stream;
+  int use_smem = NODES == LW_NODES_SMEM ? 1 : 0;
+  if (lpe_on)
+    k_trace_shadow<false, true, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+  else if (count)
+    k_trace_shadow<true, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+  else
+    k_trace_shadow<false, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+}
+
 int run_pass(lw_ctx* c, const WorkRange& w) {
   LW_CHECK_ARG(c->has_scene, "render: no scene uploaded");
   LW_CHECK_ARG(c->configured, "render: lw_render_configure not called");
@@ -994,10 +1006,17 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           marks.push_back({ev, 0});
           cudaEventRecord(event(), st);
         }
-        if (count)
-          k_trace_ext<true><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
-        else
-          k_trace_ext<false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        if (use_smem) {
+          if (count)
+            k_trace_ext<true, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+          else
+            k_trace_ext<false, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        } else {
+          if (count)
+            k_trace_ext<true, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+          else
+            k_trace_ext<false, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+        }
         if (timed) cudaEventRecord(event(), st);
         if (lpe_on && ltm) {
           k_shade_nee<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
@@ -1016,12 +1035,10 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           marks.push_back({ev, 1});
           cudaEventRecord(event(), st);
         }
-        if (lpe_on)
-          k_trace_shadow<false, true><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
-        else if (count)
-          k_trace_shadow<true, false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+        if (use_smem)
+          launch_shadow<LW_NODES_SMEM>(c, gT, smem, nr, lpe_on, count);
         else
-          k_trace_shadow<false, false><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+          launch_shadow<LW_NODES_GLOBAL>(c, gT, smem, nr, lpe_on, count);
         if (timed) cudaEventRecord(event(), st);
         k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 7;

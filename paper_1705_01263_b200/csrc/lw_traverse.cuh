@@ -226,9 +226,8 @@ struct RenderBVH {
 // per-ray constants of the FP32 box test
 struct LwRayF {
   float inv[3];  // clamped reciprocal direction
-  float on[3];   // -(o - / + delta) * inv: near-plane offset (t lowered by >= 0.9 delta |inv|)
-  float of[3];   // far-plane offset (t raised)
-  int sn[3], sf[3];  // float4 index of the near / far plane arrays in WNode (lo[a] = a, hi[a] = 3 + a)
+  float olo[3];  // offset of the lo planes: near-plane offset -(o + delta) * inv when inv >= 0,
+  float ohi[3];  // far-plane offset -(o - delta) * inv otherwise (ohi: the other one)
   LwShear sh;
 };
 
@@ -245,43 +244,44 @@ __device__ __forceinline__ void lw_rayf_setup(LwRayF& r, const RenderBVH& bvh, c
     double delta = (bvh.absmax[a] + fabs(o[a])) * 0x1p-18;
     double o_n = neg ? o[a] - delta : o[a] + delta;
     double o_f = neg ? o[a] + delta : o[a] - delta;
+    float on = (float)(-(o_n * (double)invf)), of = (float)(-(o_f * (double)invf));
     r.inv[a] = invf;
-    r.on[a] = (float)(-(o_n * (double)invf));
-    r.of[a] = (float)(-(o_f * (double)invf));
-    r.sn[a] = neg ? 3 + a : a;
-    r.sf[a] = neg ? a : 3 + a;
+    r.olo[a] = neg ? of : on;
+    r.ohi[a] = neg ? on : of;
   }
   lw_shear_setup(o, d, false, r.sh);
+}
+
+// slab test of one child from its lo / hi planes.  The near plane's entry distance is the smaller
+// of the two (lo * inv + olo <= hi * inv + ohi for inv >= 0 and the reverse for inv < 0, exactly:
+// lo <= hi, the offsets are ordered and rounding is monotone), so min / max pick near and far
+// without per-ray plane indices (fewer live registers in the node loop).
+__device__ __forceinline__ bool lw_slab(const LwRayF& r, float lx, float ly, float lz, float hx, float hy, float hz,
+                                        float best, float& tn) {
+  float a0 = __fmaf_rn(lx, r.inv[0], r.olo[0]), b0 = __fmaf_rn(hx, r.inv[0], r.ohi[0]);
+  float a1 = __fmaf_rn(ly, r.inv[1], r.olo[1]), b1 = __fmaf_rn(hy, r.inv[1], r.ohi[1]);
+  float a2 = __fmaf_rn(lz, r.inv[2], r.olo[2]), b2 = __fmaf_rn(hz, r.inv[2], r.ohi[2]);
+  float lo = fmaxf(fmaxf(fminf(a0, b0), fminf(a1, b1)), fmaxf(fminf(a2, b2), 0.0f));
+  float hi = fminf(fminf(fmaxf(a0, b0), fmaxf(a1, b1)), fminf(fmaxf(a2, b2), best));
+  tn = lo;
+  return lo <= hi;
 }
 
 // tests the four child boxes of a node against [0, best]; returns the hit mask and the entry
 // distances (conservative lower bounds)
 __device__ __forceinline__ unsigned lw_node_hit(const LwRayF& r, const WNode* __restrict__ nd, float best, float tn[4],
                                                 int ref[4]) {
-  const float4* q = reinterpret_cast<const float4*>(nd);
-  float4 nx = q[r.sn[0]], ny = q[r.sn[1]], nz = q[r.sn[2]];
-  float4 Fx = q[r.sf[0]], Fy = q[r.sf[1]], Fz = q[r.sf[2]];
-  int4 rf = *reinterpret_cast<const int4*>(&nd->ref);
+  float4 lx = nd->lo[0], ly = nd->lo[1], lz = nd->lo[2], hx = nd->hi[0], hy = nd->hi[1], hz = nd->hi[2];
+  int4 rf = nd->ref;
   ref[0] = rf.x;
   ref[1] = rf.y;
   ref[2] = rf.z;
   ref[3] = rf.w;
-  const float nxs[4] = {nx.x, nx.y, nx.z, nx.w}, nys[4] = {ny.x, ny.y, ny.z, ny.w}, nzs[4] = {nz.x, nz.y, nz.z, nz.w};
-  const float fxs[4] = {Fx.x, Fx.y, Fx.z, Fx.w}, fys[4] = {Fy.x, Fy.y, Fy.z, Fy.w}, fzs[4] = {Fz.x, Fz.y, Fz.z, Fz.w};
   unsigned mask = 0;
-#pragma unroll
-  for (int c = 0; c < 4; c++) {
-    float a0 = __fmaf_rn(nxs[c], r.inv[0], r.on[0]);
-    float a1 = __fmaf_rn(nys[c], r.inv[1], r.on[1]);
-    float a2 = __fmaf_rn(nzs[c], r.inv[2], r.on[2]);
-    float b0 = __fmaf_rn(fxs[c], r.inv[0], r.of[0]);
-    float b1 = __fmaf_rn(fys[c], r.inv[1], r.of[1]);
-    float b2 = __fmaf_rn(fzs[c], r.inv[2], r.of[2]);
-    float lo = fmaxf(fmaxf(a0, a1), fmaxf(a2, 0.0f));
-    float hi = fminf(fminf(b0, b1), fminf(b2, best));
-    tn[c] = lo;
-    if (lo <= hi && ref[c] != LW_REF_NONE) mask |= 1u << c;
-  }
+  if (lw_slab(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, best, tn[0]) && ref[0] != LW_REF_NONE) mask |= 1u;
+  if (lw_slab(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, best, tn[1]) && ref[1] != LW_REF_NONE) mask |= 2u;
+  if (lw_slab(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, best, tn[2]) && ref[2] != LW_REF_NONE) mask |= 4u;
+  if (lw_slab(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, best, tn[3]) && ref[3] != LW_REF_NONE) mask |= 8u;
   return mask;
 }
 
@@ -296,7 +296,7 @@ __device__ __forceinline__ void lw_ldg256(const void* p, float v[8]) {
 
 __device__ __forceinline__ unsigned lw_node_hit_g(const LwRayF& r, const WNode* __restrict__ nd, float best, float tn[4],
                                                   int ref[4]) {
-  float w[24];
+  float w[24];  // w[4 a + c] = lo[a].c, w[12 + 4 a + c] = hi[a].c
   lw_ldg256(reinterpret_cast<const char*>(nd), w);
   lw_ldg256(reinterpret_cast<const char*>(nd) + 32, w + 8);
   lw_ldg256(reinterpret_cast<const char*>(nd) + 64, w + 16);
@@ -307,22 +307,9 @@ __device__ __forceinline__ unsigned lw_node_hit_g(const LwRayF& r, const WNode* 
   ref[3] = rf.w;
   unsigned mask = 0;
 #pragma unroll
-  for (int c = 0; c < 4; c++) {
-    // w[4 a + c] = lo[a].c, w[12 + 4 a + c] = hi[a].c
-    float nx = r.sn[0] >= 3 ? w[12 + c] : w[c], fx = r.sn[0] >= 3 ? w[c] : w[12 + c];
-    float ny = r.sn[1] >= 3 ? w[16 + c] : w[4 + c], fy = r.sn[1] >= 3 ? w[4 + c] : w[16 + c];
-    float nz = r.sn[2] >= 3 ? w[20 + c] : w[8 + c], fz = r.sn[2] >= 3 ? w[8 + c] : w[20 + c];
-    float a0 = __fmaf_rn(nx, r.inv[0], r.on[0]);
-    float a1 = __fmaf_rn(ny, r.inv[1], r.on[1]);
-    float a2 = __fmaf_rn(nz, r.inv[2], r.on[2]);
-    float b0 = __fmaf_rn(fx, r.inv[0], r.of[0]);
-    float b1 = __fmaf_rn(fy, r.inv[1], r.of[1]);
-    float b2 = __fmaf_rn(fz, r.inv[2], r.of[2]);
-    float lo = fmaxf(fmaxf(a0, a1), fmaxf(a2, 0.0f));
-    float hi = fminf(fminf(b0, b1), fminf(b2, best));
-    tn[c] = lo;
-    if (lo <= hi && ref[c] != LW_REF_NONE) mask |= 1u << c;
-  }
+  for (int c = 0; c < 4; c++)
+    if (lw_slab(r, w[c], w[4 + c], w[8 + c], w[12 + c], w[16 + c], w[20 + c], best, tn[c]) && ref[c] != LW_REF_NONE)
+      mask |= 1u << c;
   return mask;
 }
 
@@ -374,8 +361,16 @@ __device__ __forceinline__ void lw_cswap(float& ta, int& ra, float& tb, int& rb)
 // node fetches themselves.  A persistent dynamic-fetch variant that refilled finished lanes between
 // leaves measured 4% faster on C3 and 25% slower on C2; not kept.)
 
+// node placement of the trace: LW_NODES_ANY decides per node fetch (stateless / megakernel paths),
+// the wavefront trace kernels are instantiated for one placement so only that path is compiled
+#define LW_NODES_ANY 0
+#define LW_NODES_GLOBAL 1
+#define LW_NODES_SMEM 2
+template <int NODES>
 __device__ __forceinline__ unsigned lw_node_test(const RenderBVH& bvh, const LwRayF& r, int ref, float best, float tn[4],
                                                  int cr[4]) {
+  if (NODES == LW_NODES_GLOBAL) return lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr);
+  if (NODES == LW_NODES_SMEM) return lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
   return bvh.nstride == (int)sizeof(WNode) ? lw_node_hit_g(r, lw_node_at(bvh, ref), best, tn, cr)
                                            : lw_node_hit(r, lw_node_at(bvh, ref), best, tn, cr);
 }
@@ -386,7 +381,7 @@ __device__ __forceinline__ int lw_pick(unsigned m, const int cr[4]) {
 }
 
 // closest hit, t in (0, tmax], nearest child first
-template <bool COUNT = false>
+template <bool COUNT = false, int NODES = LW_NODES_ANY>
 __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
                                                  double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
   LwRayF r;
@@ -401,7 +396,7 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
     while (ref >= 0) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_test(bvh, r, ref, best, tn, cr);
+      unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
       if (COUNT) cnt->nodes++;
       int nh = __popc(m);
       if (nh <= 1) {
@@ -455,7 +450,7 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
 }
 
 // any hit with 0 < t < tmax
-template <bool COUNT = false>
+template <bool COUNT = false, int NODES = LW_NODES_ANY>
 __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
                                              LwTraceCount* cnt = nullptr) {
   LwRayF r;
@@ -468,7 +463,7 @@ __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double 
     while (ref >= 0) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_test(bvh, r, ref, best, tn, cr);
+      unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
       if (COUNT) cnt->nodes++;
       if (m == 0) {
         ref = LW_REF_NONE;
