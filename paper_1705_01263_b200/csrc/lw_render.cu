@@ -47,6 +47,7 @@ struct Counters {
   unsigned long long n_alive_ull;
   unsigned long long rays_ext, rays_shadow, paths, nonfinite, regens, waves;
   unsigned long long ext_nodes, ext_tris, sh_nodes, sh_tris;
+  int ext_next, sh_next;  // queue heads of the persistent trace kernels
 };
 
 // SoA of 16-byte vectors: slot s of every array is one LDG.128/STG.128, and a warp's 32
@@ -99,6 +100,11 @@ struct lw_ctx {
   double last_total_ms = 0.0, last_trace_ms = 0.0;
   int64_t last_launches = 0;
   size_t smem_bytes = 0;  // scene bytes staged in shared memory (0 = use global/L1)
+  // persistent lane-refill trace kernels for global-memory BVHs (bit 0: extension, bit 1: shadow);
+  // LW_TRACE_PERSIST=<mask> overrides (A/B measurements)
+  int persist_mask = getenv("LW_TRACE_PERSIST") ? atoi(getenv("LW_TRACE_PERSIST")) : 3;
+  bool persist = (persist_mask & 1) != 0;
+  bool persist_sh = (persist_mask & 2) != 0;
   int nrnodes = 0;        // internal nodes of the render BVH
   cudaStream_t own_stream = nullptr;
   int instr = 0;
@@ -470,6 +476,8 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
   cnt->n_ext = 0;
   cnt->n_shadow = 0;
   cnt->n_alive = 0;
+  cnt->ext_next = 0;
+  cnt->sh_next = 0;
 }
 
 // pool order: flush TERMINATED slots, refill free slots with new (iteration, pixel) samples and
@@ -610,6 +618,120 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
   }
 }
 
+#ifndef LW_REFILL
+#define LW_REFILL 8
+#endif
+// Persistent extension trace over a global-memory BVH with lane refill (Aila & Laine 2009): a lane
+// whose ray is finished takes the next queue entry (one warp-aggregated atomic per refill) instead
+// of idling until the slowest lane of its warp is done, so the warp's SIMT efficiency does not
+// collapse on incoherent rays.  The traversal is the same as lw_trace_closest (same visit order,
+// same hits); the loop yields after every leaf so that refills can happen.
+template <bool COUNT>
+__global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, Pool P, Counters* __restrict__ cnt) {
+  const RenderBVH& bvh = S.bvh;
+  const int n = cnt->n_ext;
+  const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+  LwTraceCount tc;
+  int s = -1;
+  LwRayF r;
+  double ht = 0.0, hu = 0.0, hv = 0.0, best_det = 1.0;
+  long long htri = -1;
+  float best = 0.0f;
+  int ref = LW_REF_NONE, sp = 0;
+  unsigned long long stk[LW_STACK];
+  bool more = true;
+  for (;;) {
+    unsigned idle = __ballot_sync(0xffffffffu, s < 0);
+    if (more && __popc(idle) >= (idle == 0xffffffffu ? 1 : LW_REFILL)) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&cnt->ext_next, __popc(idle));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + __popc(idle) >= n) more = false;
+      if (s < 0) {
+        int k = base + __popc(idle & lt);
+        if (k < n) {
+          s = P.q_ext[k];
+          double o[3], d[3];
+          load_ray(P, s, o, d);
+          lw_rayf_setup(r, bvh, o, d);
+          ht = INFINITY;
+          hu = hv = 0.0;
+          best_det = 1.0;
+          htri = -1;
+          best = INFINITY;
+          sp = 0;
+          ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, s < 0)) break;
+    if (s < 0) continue;
+    // descend to the next leaf
+    while (ref >= 0 && ref != LW_REF_NONE) {
+      float tn[4];
+      int cr[4];
+      unsigned m = lw_node_test<LW_NODES_GLOBAL>(bvh, r, ref, best, tn, cr);
+      if (COUNT) tc.nodes++;
+      int nh = __popc(m);
+      if (nh <= 1) {
+        ref = nh == 0 ? LW_REF_NONE : lw_pick(m, cr);
+        if (nh == 0) break;
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; c++)
+        if (!(m & (1u << c))) tn[c] = INFINITY;
+      lw_cswap(tn[0], cr[0], tn[1], cr[1]);
+      lw_cswap(tn[2], cr[2], tn[3], cr[3]);
+      lw_cswap(tn[0], cr[0], tn[2], cr[2]);
+      lw_cswap(tn[1], cr[1], tn[3], cr[3]);
+      lw_cswap(tn[1], cr[1], tn[2], cr[2]);
+      if (nh > 3) stk[sp++] = lw_stk_pack(cr[3], tn[3]);
+      if (nh > 2) stk[sp++] = lw_stk_pack(cr[2], tn[2]);
+      stk[sp++] = lw_stk_pack(cr[1], tn[1]);
+      ref = cr[0];
+    }
+    if (ref != LW_REF_NONE) {
+      int v = -ref - 1;
+      int start = v >> 3, count = v & 7;
+      for (int k = start; k < start + count; k++) {
+        if (COUNT) tc.tris++;
+        double t, bu, bv, det;
+        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv, det) || t <= 0.0 || t > ht) continue;
+        long long id = bvh.tris[k].id;
+        if (t == ht && htri >= 0 && id >= htri) continue;
+        ht = t;
+        htri = id;
+        hu = bu;
+        hv = bv;
+        best_det = det;
+        best = __double2float_ru(t);
+      }
+    }
+    ref = LW_REF_NONE;
+    while (sp > 0) {
+      unsigned long long e = stk[--sp];
+      if (__uint_as_float((unsigned)(e >> 32)) <= best) {
+        ref = (int)(unsigned)e;
+        break;
+      }
+    }
+    if (ref == LW_REF_NONE) {
+      P.hit0[s] = make_double2(ht, htri >= 0 ? hu / best_det : 0.0);
+      P.hit1[s] = make_double2(htri >= 0 ? hv / best_det : 0.0, __longlong_as_double(htri));
+      s = -1;
+    }
+  }
+  if (COUNT) {
+    warp_add(&cnt->ext_nodes, tc.nodes);
+    warp_add(&cnt->ext_tris, tc.tris);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    cnt->rays_ext += (unsigned long long)n;
+    cnt->waves += 1;
+  }
+}
+
 __device__ __forceinline__ void load_hit(const Pool& P, int s, LwHit& h) {
   double2 h0 = P.hit0[s], h1 = P.hit1[s];
   h.t = h0.x;
@@ -707,6 +829,103 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
   warp_add(&cnt->n_alive_ull, alive_count);
 }
 
+// an unoccluded shadow ray adds its NEE contribution (and routes its LPE split)
+template <bool LPE>
+__device__ __forceinline__ void shadow_unoccluded(const Pool& P, int s, double cx, const LwLpe& lpe) {
+  double2 f = P.sh4[s], t1 = P.tp1[s], t2 = P.tp2[s];
+  t1.y = t1.y + cx;
+  t2.x = t2.x + f.x;
+  t2.y = t2.y + f.y;
+  P.tp1[s] = t1;
+  P.tp2[s] = t2;
+  if (LPE) {
+    double2 a5 = P.sh5[s], a6 = P.sh6[s], a7 = P.sh7[s];
+    int sl = P.sh_lpe[s], st0 = sl & 0xffff, term = sl >> 16;
+    long long pix = P.pix[s];
+    lw_lpe_route(&lpe, lw_lpe_step(&lpe, lw_lpe_step(&lpe, st0, LW_EV_RD), term), pix, mk3(a5.x, a5.y, a6.x));
+    lw_lpe_route(&lpe, lw_lpe_step(&lpe, lw_lpe_step(&lpe, st0, LW_EV_RG), term), pix, mk3(a6.y, a7.x, a7.y));
+  }
+}
+
+// persistent any-hit trace over a global-memory BVH with lane refill (see k_trace_ext_p)
+template <bool COUNT, bool LPE>
+__global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene S, Pool P, Counters* __restrict__ cnt,
+                                                                        LwLpe lpe) {
+  const RenderBVH& bvh = S.bvh;
+  const int n = cnt->n_shadow;
+  const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+  LwTraceCount tc;
+  int s = -1;
+  LwRayF r;
+  double tmax = 0.0, cx = 0.0;
+  float best = 0.0f;
+  int ref = LW_REF_NONE, sp = 0;
+  int stk[LW_STACK];
+  bool more = true;
+  for (;;) {
+    unsigned idle = __ballot_sync(0xffffffffu, s < 0);
+    if (more && __popc(idle) >= (idle == 0xffffffffu ? 1 : LW_REFILL)) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&cnt->sh_next, __popc(idle));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + __popc(idle) >= n) more = false;
+      if (s < 0) {
+        int k = base + __popc(idle & lt);
+        if (k < n) {
+          s = P.q_shadow[k];
+          double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
+          double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
+          lw_rayf_setup(r, bvh, o, d);
+          tmax = e.x;
+          cx = e.y;
+          best = __double2float_ru(tmax);
+          sp = 0;
+          ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, s < 0)) break;
+    if (s < 0) continue;
+    bool occluded = false;
+    while (ref >= 0 && ref != LW_REF_NONE) {
+      float tn[4];
+      int cr[4];
+      unsigned m = lw_node_test<LW_NODES_GLOBAL>(bvh, r, ref, best, tn, cr);
+      if (COUNT) tc.nodes++;
+      if (m == 0) {
+        ref = LW_REF_NONE;
+        break;
+      }
+      ref = lw_pick(m, cr);
+      m &= m - 1;
+#pragma unroll
+      for (int c = 1; c < 4; c++)
+        if (m & (1u << c)) stk[sp++] = cr[c];
+    }
+    if (ref != LW_REF_NONE) {
+      int v = -ref - 1;
+      int start = v >> 3, count = v & 7;
+      for (int k = start; k < start + count; k++) {
+        if (COUNT) tc.tris++;
+        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) {
+          occluded = true;
+          break;
+        }
+      }
+    }
+    ref = sp > 0 && !occluded ? stk[--sp] : LW_REF_NONE;
+    if (ref == LW_REF_NONE) {
+      if (!occluded) shadow_unoccluded<LPE>(P, s, cx, lpe);
+      s = -1;
+    }
+  }
+  if (COUNT) {
+    warp_add(&cnt->sh_nodes, tc.nodes);
+    warp_add(&cnt->sh_tris, tc.tris);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt->rays_shadow += (unsigned long long)n;
+}
+
 template <bool COUNT, bool LPE, int NODES>
 __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem,
                                                                       LwLpe lpe) {
@@ -720,21 +939,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S
       int s = P.q_shadow[k];
       double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
       double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
-      if (!lw_trace_any<COUNT, NODES>(bvh, o, d, e.x, &tc)) {
-        double2 f = P.sh4[s], t1 = P.tp1[s], t2 = P.tp2[s];
-        t1.y = t1.y + e.y;
-        t2.x = t2.x + f.x;
-        t2.y = t2.y + f.y;
-        P.tp1[s] = t1;
-        P.tp2[s] = t2;
-        if (LPE) {
-          double2 a5 = P.sh5[s], a6 = P.sh6[s], a7 = P.sh7[s];
-          int sl = P.sh_lpe[s], st0 = sl & 0xffff, term = sl >> 16;
-          long long pix = P.pix[s];
-          lw_lpe_route(&lpe, lw_lpe_step(&lpe, lw_lpe_step(&lpe, st0, LW_EV_RD), term), pix, mk3(a5.x, a5.y, a6.x));
-          lw_lpe_route(&lpe, lw_lpe_step(&lpe, lw_lpe_step(&lpe, st0, LW_EV_RG), term), pix, mk3(a6.y, a7.x, a7.y));
-        }
-      }
+      if (!lw_trace_any<COUNT, NODES>(bvh, o, d, e.x, &tc)) shadow_unoccluded<LPE>(P, s, e.y, lpe);
     }
   }
   if (COUNT) {
@@ -932,6 +1137,15 @@ int alloc_pool(lw_ctx* c, int size) {
 template <int NODES>
 void launch_shadow(lw_ctx* c, int grid, size_t smem, int nr, bool lpe_on, bool count) {
   cudaStream_t st = c->stream;
+  if (NODES == LW_NODES_GLOBAL && c->persist_sh) {
+    if (lpe_on)
+      k_trace_shadow_p<false, true><<<grid, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+    else if (count)
+      k_trace_shadow_p<true, false><<<grid, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+    else
+      k_trace_shadow_p<false, false><<<grid, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+    return;
+  }
   int use_smem = NODES == LW_NODES_SMEM ? 1 : 0;
   if (lpe_on)
     k_trace_shadow<false, true, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
@@ -1012,7 +1226,11 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           else
             k_trace_ext<false, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         } else {
-          if (count)
+          if (c->persist && count)
+            k_trace_ext_p<true><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
+          else if (c->persist)
+            k_trace_ext_p<false><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
+          else if (count)
             k_trace_ext<true, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
           else
             k_trace_ext<false, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);

@@ -358,8 +358,8 @@ __device__ __forceinline__ void lw_cswap(float& ta, int& ra, float& tb, int& rb)
 // (Written as a resumable object with init()/step() the whole object -- ray constants, hit
 // record, stack pointer -- lived in local memory and was re-read on every node visit, and a
 // dynamically indexed child array forced a local store per node: ~3x the L1TEX requests of the
-// node fetches themselves.  A persistent dynamic-fetch variant that refilled finished lanes between
-// leaves measured 4% faster on C3 and 25% slower on C2; not kept.)
+// node fetches themselves.)  The wavefront engine's persistent lane-refill kernels
+// (lw_render.cu k_trace_ext_p / k_trace_shadow_p) run the same loops with a yield after every leaf.
 
 // node placement of the trace: LW_NODES_ANY decides per node fetch (stateless / megakernel paths),
 // the wavefront trace kernels are instantiated for one placement so only that path is compiled

@@ -259,6 +259,30 @@ def test_full_frame_pass_split_and_pool_invariance(gpu, cfg):
         assert np.array_equal(outs[0], o)
 
 
+@pytest.mark.parametrize("cfg", ["C3", "C5"])
+def test_persistent_refill_trace_invariance(gpu, cfg, monkeypatch):
+    """The persistent lane-refill trace kernels (default for global-memory BVHs) and the one-ray-
+    per-thread kernels give the same full-frame framebuffer (same traversal, same hits), with
+    and without LPE layers (the LPE shadow instantiation)."""
+    c = scenes.CONFIGS[cfg]
+    packed = pack_scene(c.builder())
+    outs = []
+    for mask in ("0", "1", "3"):
+        monkeypatch.setenv("LW_TRACE_PERSIST", mask)
+        with _renderer(packed, c.width, c.height, c.max_depth) as r:
+            r.render_pass(0, 2)
+            fb = r.framebuffer()
+            r.clear()
+            r.set_lpe_layers({"direct": "C.?L", "all": "C.*[LE]"})
+            r.render_pass(0, 1)
+            outs.append((fb, r.layer_framebuffers()))
+    for fb, layers in outs[1:]:
+        assert np.array_equal(outs[0][0], fb)
+        for k in layers:
+            assert np.array_equal(outs[0][1][k], layers[k]), k
+    assert outs[0][0].sum() > 0
+
+
 def test_degenerate_deep_sah_tree_falls_back_to_median(gpu, oracle):
     """A SAH tree deeper than the traversal stack (exponentially spaced triangles) is replaced by the
     median tree at upload; hits do not depend on the tree, so the image still matches the oracle."""
