@@ -100,7 +100,8 @@ struct lw_ctx {
   double last_total_ms = 0.0, last_trace_ms = 0.0;
   int64_t last_launches = 0;
   size_t smem_bytes = 0;  // scene bytes staged in shared memory (0 = use global/L1)
-  // persistent lane-refill trace kernels for global-memory BVHs (bit 0: extension, bit 1: shadow);
+  // persistent lane-refill trace kernels: bits 0 / 1 extension / shadow rays on global-memory BVHs
+  // (default on), bits 2 / 3 the same on shared-memory BVHs (default off: C2 ±0 / -1.6 %);
   // LW_TRACE_PERSIST=<mask> overrides (A/B measurements)
   int persist_mask = getenv("LW_TRACE_PERSIST") ? atoi(getenv("LW_TRACE_PERSIST")) : 3;
   bool persist = (persist_mask & 1) != 0;
@@ -626,9 +627,11 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
 // of idling until the slowest lane of its warp is done, so the warp's SIMT efficiency does not
 // collapse on incoherent rays.  The traversal is the same as lw_trace_closest (same visit order,
 // same hits); the loop yields after every leaf so that refills can happen.
-template <bool COUNT>
-__global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, Pool P, Counters* __restrict__ cnt) {
-  const RenderBVH& bvh = S.bvh;
+template <bool COUNT, int NODES>
+__global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, Pool P, Counters* __restrict__ cnt,
+                                                                    int nrnodes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, NODES == LW_NODES_SMEM);
   const int n = cnt->n_ext;
   const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
   LwTraceCount tc;
@@ -670,7 +673,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_test<LW_NODES_GLOBAL>(bvh, r, ref, best, tn, cr);
+      unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
       if (COUNT) tc.nodes++;
       int nh = __popc(m);
       if (nh <= 1) {
@@ -848,10 +851,11 @@ __device__ __forceinline__ void shadow_unoccluded(const Pool& P, int s, double c
 }
 
 // persistent any-hit trace over a global-memory BVH with lane refill (see k_trace_ext_p)
-template <bool COUNT, bool LPE>
+template <bool COUNT, bool LPE, int NODES>
 __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene S, Pool P, Counters* __restrict__ cnt,
-                                                                        LwLpe lpe) {
-  const RenderBVH& bvh = S.bvh;
+                                                                        int nrnodes, LwLpe lpe) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, NODES == LW_NODES_SMEM);
   const int n = cnt->n_shadow;
   const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
   LwTraceCount tc;
@@ -890,7 +894,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
-      unsigned m = lw_node_test<LW_NODES_GLOBAL>(bvh, r, ref, best, tn, cr);
+      unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
       if (COUNT) tc.nodes++;
       if (m == 0) {
         ref = LW_REF_NONE;
@@ -1137,13 +1141,13 @@ int alloc_pool(lw_ctx* c, int size) {
 template <int NODES>
 void launch_shadow(lw_ctx* c, int grid, size_t smem, int nr, bool lpe_on, bool count) {
   cudaStream_t st = c->stream;
-  if (NODES == LW_NODES_GLOBAL && c->persist_sh) {
+  if (NODES == LW_NODES_GLOBAL ? c->persist_sh : (c->persist_mask & 8) != 0) {
     if (lpe_on)
-      k_trace_shadow_p<false, true><<<grid, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+      k_trace_shadow_p<false, true, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
     else if (count)
-      k_trace_shadow_p<true, false><<<grid, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+      k_trace_shadow_p<true, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
     else
-      k_trace_shadow_p<false, false><<<grid, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+      k_trace_shadow_p<false, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
     return;
   }
   int use_smem = NODES == LW_NODES_SMEM ? 1 : 0;
@@ -1220,16 +1224,21 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           marks.push_back({ev, 0});
           cudaEventRecord(event(), st);
         }
-        if (use_smem) {
+        if (use_smem && (c->persist_mask & 4)) {
+          if (count)
+            k_trace_ext_p<true, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
+          else
+            k_trace_ext_p<false, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
+        } else if (use_smem) {
           if (count)
             k_trace_ext<true, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
           else
             k_trace_ext<false, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         } else {
           if (c->persist && count)
-            k_trace_ext_p<true><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
+            k_trace_ext_p<true, LW_NODES_GLOBAL><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
           else if (c->persist)
-            k_trace_ext_p<false><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt);
+            k_trace_ext_p<false, LW_NODES_GLOBAL><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
           else if (count)
             k_trace_ext<true, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
           else
