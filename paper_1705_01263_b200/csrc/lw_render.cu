@@ -622,6 +622,17 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
 #ifndef LW_REFILL
 #define LW_REFILL 8
 #endif
+#ifndef LW_SPEC
+#define LW_SPEC 1
+#endif
+// next stack entry whose entry distance is within the current best (LW_REF_NONE when exhausted)
+__device__ __forceinline__ int lw_pop_cull(const unsigned long long* stk, int& sp, float best) {
+  while (sp > 0) {
+    unsigned long long e = stk[--sp];
+    if (__uint_as_float((unsigned)(e >> 32)) <= best) return (int)(unsigned)e;
+  }
+  return LW_REF_NONE;
+}
 // Persistent extension trace over a global-memory BVH with lane refill (Aila & Laine 2009): a lane
 // whose ray is finished takes the next queue entry (one warp-aggregated atomic per refill) instead
 // of idling until the slowest lane of its warp is done, so the warp's SIMT efficiency does not
@@ -669,6 +680,71 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
     }
     if (__all_sync(0xffffffffu, s < 0)) break;
     if (s < 0) continue;
+#if LW_SPEC
+    // speculative traversal (Aila & Laine 2009): a lane that reaches a leaf postpones it and keeps
+    // descending until every lane of the warp holds a leaf, so the node loop and the leaf loop
+    // each run with more lanes active.  Visit order changes, the closest hit does not.
+    int leaf = LW_REF_NONE;
+    if (ref < 0) {
+      leaf = ref;
+      ref = lw_pop_cull(stk, sp, best);
+    }
+    while (ref >= 0 && ref != LW_REF_NONE) {
+      float tn[4];
+      int cr[4];
+      unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
+      if (COUNT) tc.nodes++;
+      int nh = __popc(m);
+      if (nh <= 1) {
+        ref = nh == 0 ? lw_pop_cull(stk, sp, best) : lw_pick(m, cr);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          if (!(m & (1u << c))) tn[c] = INFINITY;
+        lw_cswap(tn[0], cr[0], tn[1], cr[1]);
+        lw_cswap(tn[2], cr[2], tn[3], cr[3]);
+        lw_cswap(tn[0], cr[0], tn[2], cr[2]);
+        lw_cswap(tn[1], cr[1], tn[3], cr[3]);
+        lw_cswap(tn[1], cr[1], tn[2], cr[2]);
+        if (nh > 3) stk[sp++] = lw_stk_pack(cr[3], tn[3]);
+        if (nh > 2) stk[sp++] = lw_stk_pack(cr[2], tn[2]);
+        stk[sp++] = lw_stk_pack(cr[1], tn[1]);
+        ref = cr[0];
+      }
+      if (ref < 0 && leaf == LW_REF_NONE) {
+        leaf = ref;
+        ref = lw_pop_cull(stk, sp, best);
+      }
+      if (!__any_sync(__activemask(), leaf == LW_REF_NONE)) break;
+    }
+    if (leaf == LW_REF_NONE && ref < 0) {
+      leaf = ref;
+      ref = lw_pop_cull(stk, sp, best);
+    }
+    if (leaf != LW_REF_NONE) {
+      int v = -leaf - 1;
+      int start = v >> 3, count = v & 7;
+      for (int k = start; k < start + count; k++) {
+        if (COUNT) tc.tris++;
+        double t, bu, bv, det;
+        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv, det) || t <= 0.0 || t > ht) continue;
+        long long id = bvh.tris[k].id;
+        if (t == ht && htri >= 0 && id >= htri) continue;
+        ht = t;
+        htri = id;
+        hu = bu;
+        hv = bv;
+        best_det = det;
+        best = __double2float_ru(t);
+      }
+    }
+    if (ref == LW_REF_NONE) {
+      P.hit0[s] = make_double2(ht, htri >= 0 ? hu / best_det : 0.0);
+      P.hit1[s] = make_double2(htri >= 0 ? hv / best_det : 0.0, __longlong_as_double(htri));
+      s = -1;
+    }
+  }
+#else
     // descend to the next leaf
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
@@ -725,6 +801,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
       s = -1;
     }
   }
+#endif
   if (COUNT) {
     warp_add(&cnt->ext_nodes, tc.nodes);
     warp_add(&cnt->ext_tris, tc.tris);
@@ -891,6 +968,53 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
     if (__all_sync(0xffffffffu, s < 0)) break;
     if (s < 0) continue;
     bool occluded = false;
+#if LW_SPEC
+    int leaf = LW_REF_NONE;
+    if (ref < 0) {
+      leaf = ref;
+      ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+    }
+    while (ref >= 0 && ref != LW_REF_NONE) {
+      float tn[4];
+      int cr[4];
+      unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
+      if (COUNT) tc.nodes++;
+      if (m == 0) {
+        ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+      } else {
+        ref = lw_pick(m, cr);
+        m &= m - 1;
+#pragma unroll
+        for (int c = 1; c < 4; c++)
+          if (m & (1u << c)) stk[sp++] = cr[c];
+      }
+      if (ref < 0 && leaf == LW_REF_NONE) {
+        leaf = ref;
+        ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+      }
+      if (!__any_sync(__activemask(), leaf == LW_REF_NONE)) break;
+    }
+    if (leaf == LW_REF_NONE && ref < 0) {
+      leaf = ref;
+      ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+    }
+    if (leaf != LW_REF_NONE) {
+      int v = -leaf - 1;
+      int start = v >> 3, count = v & 7;
+      for (int k = start; k < start + count; k++) {
+        if (COUNT) tc.tris++;
+        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) {
+          occluded = true;
+          break;
+        }
+      }
+    }
+    if (occluded || ref == LW_REF_NONE) {
+      if (!occluded) shadow_unoccluded<LPE>(P, s, cx, lpe);
+      s = -1;
+    }
+  }
+#else
     while (ref >= 0 && ref != LW_REF_NONE) {
       float tn[4];
       int cr[4];
@@ -923,6 +1047,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
       s = -1;
     }
   }
+#endif
   if (COUNT) {
     warp_add(&cnt->sh_nodes, tc.nodes);
     warp_add(&cnt->sh_tris, tc.tris);

@@ -1,0 +1,7 @@
+S="${S:-C3:;C4:;C5:}"
+for v in ${VARIANTS:-old spec new}; do
+  if [ $v = new ]; then unset LIB; else export LIB=variants/liblw_$v.so; fi
+  SWEEP="$S" bash tools/gpu_sweep.sh > /dev/null; cp gpurun_out/sweep.log gpurun_out/sweep_$v.log
+done
+unset LIB
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2 > gpurun_out/gpu_tests.txt
