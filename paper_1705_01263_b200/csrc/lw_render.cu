@@ -25,6 +25,17 @@
 using namespace lw;
 
 // occupancy knobs (min resident blocks of 128 threads per SM) for the FP64-heavy stage kernels
+// persistent trace kernels: refill when >= LW_REFILL lanes of a warp are idle; speculative
+// traversal in the persistent kernels (LW_SPEC) and in the one-ray-per-thread kernels (LW_SPEC_SMEM)
+#ifndef LW_REFILL
+#define LW_REFILL 8
+#endif
+#ifndef LW_SPEC
+#define LW_SPEC 1
+#endif
+#ifndef LW_SPEC_SMEM
+#define LW_SPEC_SMEM 2  // bit 0: extension rays (C2 trace +2 %: off), bit 1: shadow rays
+#endif
 #ifndef LW_TRACE_MINB
 #define LW_TRACE_MINB 8
 #endif
@@ -604,7 +615,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
       double o[3], d[3];
       load_ray(P, s, o, d);
       LwHit h;
-      lw_trace_closest<COUNT, NODES>(bvh, o, d, INFINITY, h, &tc);
+      lw_trace_closest<COUNT, NODES, (LW_SPEC_SMEM & 1) != 0>(bvh, o, d, INFINITY, h, &tc);
       P.hit0[s] = make_double2(h.t, h.bu);
       P.hit1[s] = make_double2(h.bv, __longlong_as_double(h.tri));
     }
@@ -619,20 +630,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
   }
 }
 
-#ifndef LW_REFILL
-#define LW_REFILL 8
-#endif
-#ifndef LW_SPEC
-#define LW_SPEC 1
-#endif
-// next stack entry whose entry distance is within the current best (LW_REF_NONE when exhausted)
-__device__ __forceinline__ int lw_pop_cull(const unsigned long long* stk, int& sp, float best) {
-  while (sp > 0) {
-    unsigned long long e = stk[--sp];
-    if (__uint_as_float((unsigned)(e >> 32)) <= best) return (int)(unsigned)e;
-  }
-  return LW_REF_NONE;
-}
+
 // Persistent extension trace over a global-memory BVH with lane refill (Aila & Laine 2009): a lane
 // whose ray is finished takes the next queue entry (one warp-aggregated atomic per refill) instead
 // of idling until the slowest lane of its warp is done, so the warp's SIMT efficiency does not
@@ -1068,7 +1066,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S
       int s = P.q_shadow[k];
       double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
       double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
-      if (!lw_trace_any<COUNT, NODES>(bvh, o, d, e.x, &tc)) shadow_unoccluded<LPE>(P, s, e.y, lpe);
+      if (!lw_trace_any<COUNT, NODES, (LW_SPEC_SMEM & 2) != 0>(bvh, o, d, e.x, &tc)) shadow_unoccluded<LPE>(P, s, e.y, lpe);
     }
   }
   if (COUNT) {

@@ -380,8 +380,19 @@ __device__ __forceinline__ int lw_pick(unsigned m, const int cr[4]) {
   return (m & 1u) ? cr[0] : (m & 2u) ? cr[1] : (m & 4u) ? cr[2] : cr[3];
 }
 
+// next stack entry whose entry distance is within the current best (LW_REF_NONE when exhausted)
+__device__ __forceinline__ int lw_pop_cull(const unsigned long long* stk, int& sp, float best) {
+  while (sp > 0) {
+    unsigned long long e = stk[--sp];
+    if (__uint_as_float((unsigned)(e >> 32)) <= best) return (int)(unsigned)e;
+  }
+  return LW_REF_NONE;
+}
+
 // closest hit, t in (0, tmax], nearest child first
-template <bool COUNT = false, int NODES = LW_NODES_ANY>
+// SPEC: speculative traversal (Aila & Laine 2009) -- a lane that reaches a leaf postpones it and
+// keeps descending until every active lane of the warp holds a leaf; same hit, fuller warps.
+template <bool COUNT = false, int NODES = LW_NODES_ANY, bool SPEC = false>
 __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const double o[3], const double d[3],
                                                  double tmax, LwHit& h, LwTraceCount* cnt = nullptr) {
   LwRayF r;
@@ -392,7 +403,64 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
   int ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
   int sp = 0;
   unsigned long long stk[LW_STACK];
-  while (ref != LW_REF_NONE) {
+  if (SPEC) {
+    while (ref != LW_REF_NONE) {
+      int leaf = LW_REF_NONE;
+      if (ref < 0) {
+        leaf = ref;
+        ref = lw_pop_cull(stk, sp, best);
+      }
+      while (ref >= 0 && ref != LW_REF_NONE) {
+        float tn[4];
+        int cr[4];
+        unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
+        if (COUNT) cnt->nodes++;
+        int nh = __popc(m);
+        if (nh <= 1) {
+          ref = nh == 0 ? lw_pop_cull(stk, sp, best) : lw_pick(m, cr);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; c++)
+            if (!(m & (1u << c))) tn[c] = INFINITY;
+          lw_cswap(tn[0], cr[0], tn[1], cr[1]);
+          lw_cswap(tn[2], cr[2], tn[3], cr[3]);
+          lw_cswap(tn[0], cr[0], tn[2], cr[2]);
+          lw_cswap(tn[1], cr[1], tn[3], cr[3]);
+          lw_cswap(tn[1], cr[1], tn[2], cr[2]);
+          if (nh > 3) stk[sp++] = lw_stk_pack(cr[3], tn[3]);
+          if (nh > 2) stk[sp++] = lw_stk_pack(cr[2], tn[2]);
+          stk[sp++] = lw_stk_pack(cr[1], tn[1]);
+          ref = cr[0];
+        }
+        if (ref < 0 && leaf == LW_REF_NONE) {
+          leaf = ref;
+          ref = lw_pop_cull(stk, sp, best);
+        }
+        if (!__any_sync(__activemask(), leaf == LW_REF_NONE)) break;
+      }
+      if (leaf == LW_REF_NONE && ref < 0) {
+        leaf = ref;
+        ref = lw_pop_cull(stk, sp, best);
+      }
+      if (leaf == LW_REF_NONE) continue;
+      int v = -leaf - 1;
+      int start = v >> 3, count = v & 7;
+      for (int k = start; k < start + count; k++) {
+        if (COUNT) cnt->tris++;
+        double t, bu, bv, det;
+        if (!lw_tri_eval(bvh.tris[k].v, r.sh, t, bu, bv, det) || t <= 0.0 || t > ht) continue;
+        long long id = bvh.tris[k].id;
+        if (t == ht && htri >= 0 && id >= htri) continue;
+        ht = t;
+        htri = id;
+        hu = bu;
+        hv = bv;
+        best_det = det;
+        best = __double2float_ru(t);
+      }
+    }
+  }
+  while (!SPEC && ref != LW_REF_NONE) {
     while (ref >= 0) {
       float tn[4];
       int cr[4];
@@ -450,7 +518,7 @@ __device__ __forceinline__ void lw_trace_closest(const RenderBVH& bvh, const dou
 }
 
 // any hit with 0 < t < tmax
-template <bool COUNT = false, int NODES = LW_NODES_ANY>
+template <bool COUNT = false, int NODES = LW_NODES_ANY, bool SPEC = false>
 __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double o[3], const double d[3], double tmax,
                                              LwTraceCount* cnt = nullptr) {
   LwRayF r;
@@ -459,6 +527,47 @@ __device__ __forceinline__ bool lw_trace_any(const RenderBVH& bvh, const double 
   int ref = bvh.ntris == 0 ? LW_REF_NONE : bvh.root_ref;
   int sp = 0;
   int stk[LW_STACK];
+  if (SPEC) {
+    while (ref != LW_REF_NONE) {
+      int leaf = LW_REF_NONE;
+      if (ref < 0) {
+        leaf = ref;
+        ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+      }
+      while (ref >= 0 && ref != LW_REF_NONE) {
+        float tn[4];
+        int cr[4];
+        unsigned m = lw_node_test<NODES>(bvh, r, ref, best, tn, cr);
+        if (COUNT) cnt->nodes++;
+        if (m == 0) {
+          ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+        } else {
+          ref = lw_pick(m, cr);
+          m &= m - 1;
+#pragma unroll
+          for (int c = 1; c < 4; c++)
+            if (m & (1u << c)) stk[sp++] = cr[c];
+        }
+        if (ref < 0 && leaf == LW_REF_NONE) {
+          leaf = ref;
+          ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+        }
+        if (!__any_sync(__activemask(), leaf == LW_REF_NONE)) break;
+      }
+      if (leaf == LW_REF_NONE && ref < 0) {
+        leaf = ref;
+        ref = sp > 0 ? stk[--sp] : LW_REF_NONE;
+      }
+      if (leaf == LW_REF_NONE) continue;
+      int v = -leaf - 1;
+      int start = v >> 3, count = v & 7;
+      for (int k = start; k < start + count; k++) {
+        if (COUNT) cnt->tris++;
+        if (lw_tri_occludes(bvh.tris[k].v, r.sh, tmax)) return true;
+      }
+    }
+    return false;
+  }
   while (ref != LW_REF_NONE) {
     while (ref >= 0) {
       float tn[4];
