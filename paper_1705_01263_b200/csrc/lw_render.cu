@@ -28,10 +28,10 @@ using namespace lw;
 // persistent trace kernels: refill when >= LW_REFILL lanes of a warp are idle; speculative
 // traversal in the persistent kernels (LW_SPEC) and in the one-ray-per-thread kernels (LW_SPEC_SMEM)
 #ifndef LW_REFILL
-#define LW_REFILL 8
+#define LW_REFILL 16
 #endif
 #ifndef LW_SPEC
-#define LW_SPEC 1
+#define LW_SPEC 3  // bit 0: extension rays, bit 1: shadow rays
 #endif
 #ifndef LW_SPEC_SMEM
 #define LW_SPEC_SMEM 2  // bit 0: extension rays (C2 trace +2 %: off), bit 1: shadow rays
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
     }
     if (__all_sync(0xffffffffu, s < 0)) break;
     if (s < 0) continue;
-#if LW_SPEC
+#if LW_SPEC & 1
     // speculative traversal (Aila & Laine 2009): a lane that reaches a leaf postpones it and keeps
     // descending until every lane of the warp holds a leaf, so the node loop and the leaf loop
     // each run with more lanes active.  Visit order changes, the closest hit does not.
@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
     if (__all_sync(0xffffffffu, s < 0)) break;
     if (s < 0) continue;
     bool occluded = false;
-#if LW_SPEC
+#if LW_SPEC & 2
     int leaf = LW_REF_NONE;
     if (ref < 0) {
       leaf = ref;
