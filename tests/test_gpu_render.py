@@ -259,15 +259,15 @@ def test_full_frame_pass_split_and_pool_invariance(gpu, cfg):
         assert np.array_equal(outs[0], o)
 
 
-@pytest.mark.parametrize("cfg", ["C3", "C5"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
 def test_persistent_refill_trace_invariance(gpu, cfg, monkeypatch):
-    """The persistent lane-refill trace kernels (default for global-memory BVHs) and the one-ray-
-    per-thread kernels give the same full-frame framebuffer (same traversal, same hits), with
-    and without LPE layers (the LPE shadow instantiation)."""
+    """The persistent lane-refill trace kernels with speculative traversal (the default, for
+    shared- and global-memory BVHs) and the one-ray-per-thread kernels give the same full-frame
+    framebuffer (same hits), with and without LPE layers (the LPE shadow instantiation)."""
     c = scenes.CONFIGS[cfg]
     packed = pack_scene(c.builder())
     outs = []
-    for mask in ("0", "1", "3"):
+    for mask in ("0", "5", "10", "15"):
         monkeypatch.setenv("LW_TRACE_PERSIST", mask)
         with _renderer(packed, c.width, c.height, c.max_depth) as r:
             r.render_pass(0, 2)
