@@ -383,7 +383,7 @@ def run_ours(a):
     # triangle record per test, plus the SoA ray read (48 B), queue index (4 B) and hit write (28 B)
     bytes_per_ray = 128.0 * nodes_per_ray + 80.0 * tris_per_ray + 80.0
     if prof_launches > 0:  # wavefront: the extension-ray trace kernel, timed per launch with CUDA events
-        kernel = "k_trace_ext (closest-hit traversal, wavefront stage)"
+        kernel = "k_trace_ext_p (persistent closest-hit traversal, wavefront stage)"
         avg_ms = prof_ms / prof_launches
         achieved = bytes_per_ray * rays_ext / prof_ms / 1e6  # GB/s
     else:  # megakernel: the whole pass is one launch; count extension + shadow traversal bytes
