@@ -7,14 +7,17 @@
 // partition.  Per level:
 //   1. bins of large segments (n > 32): ordered-u64 min/max + count atomics, privatised in
 //      shared memory when a 1024-position chunk lies inside one segment;
-//   2. one thread per segment: small segments bin their triangles sequentially, every segment
-//      sweeps its planes and decides leaf / split (identical FP64 formulas on both paths);
+//   2. one warp per segment (k_sah_decide_w; the per-thread k_sah_decide with LW_SAH_SERIAL=1,
+//      LW_SAH_CHECK=1 runs both and reports differing decisions): lanes own bins, small segments
+//      bin their triangles, prefix / suffix boxes by shuffles, first strict minimum of the plane
+//      costs by a warp argmin, leaf / split decision (identical FP64 formulas on every path);
 //   3. node ids = level base + rank among splitting segments (scan), child segments at 2r, 2r+1;
 //   4. stable partition of the position list (scan + scatter) and the next position->segment map.
 // Bounds are exact (min/max), so every path reproduces the sequential specification bit for bit.
 #include <string.h>
 
 #include <algorithm>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -352,6 +355,170 @@ __global__ void k_sah_decide(const SSeg* __restrict__ seg, int nseg, const int* 
   split_flag[s] = r.split;
 }
 
+// k_sah_decide with one warp per segment (the per-thread version serialises 48 bins and two
+// 16-bin sweeps through local memory: ~60 us per level even for a 36-triangle scene).  Lane
+// b & 15 owns bin b of the current axis (both half-warps compute the same axis); prefix / suffix
+// boxes come from shuffles.  min / max and integer counts are exact and order-free, and every
+// cost is the same FP64 expression of the same boxes, so the first strict minimum over
+// (axis, plane) -- taken as the lexicographic minimum of (cost, 15 * axis + plane) -- and the
+// split are those of the sequential specification, bit for bit.
+__device__ __forceinline__ double shfl_up_d(double v, int off) { return __shfl_up_sync(0xffffffffu, v, off, 16); }
+__device__ __forceinline__ double shfl_down_d(double v, int off) { return __shfl_down_sync(0xffffffffu, v, off, 16); }
+
+__global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int* __restrict__ large_rank,
+                               const BinAcc* __restrict__ bins, const int* __restrict__ ids,
+                               const double* __restrict__ tb, const double* __restrict__ cen,
+                               SSplit* __restrict__ out, int* __restrict__ split_flag) {
+  const int s = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31, bin = lane & 15;
+  if (s >= nseg) return;  // uniform per warp
+  const SSeg g = seg[s];
+  const int lr = large_rank[s];
+  double best = INFINITY;
+  int bkey = 1 << 30, bnl = 0;
+  double L[6], R[6], CL[6], CR[6];
+  if (g.n > 1) {
+    for (int a = 0; a < 3; a++) {
+      double ext = g.C[3 + a] - g.C[a];
+      if (!(ext > 0.0)) continue;
+      double scale = (double)kBins / ext;
+      int cnt = 0;
+      double bb[6], cb[6];
+      box_reset(bb);
+      box_reset(cb);
+      if (lr >= 0) {
+        const BinAcc& src = bins[(size_t)lr * 3 * kBins + a * kBins + bin];
+        cnt = (int)src.v[0];
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          bb[k] = unordd(src.v[1 + k]);
+          cb[k] = unordd(src.v[7 + k]);
+        }
+      } else {
+        for (int k = 0; k < g.n; k++) {
+          int t = ids[g.start + k];
+          const double* ct = cen + 3 * (size_t)t;
+          if (bin_of(ct[a], g.C[a], scale) != bin) continue;
+          cnt++;
+          box_grow(bb, tb + 6 * (size_t)t, tb + 6 * (size_t)t + 3);
+          box_grow(cb, ct, ct);
+        }
+      }
+      // inclusive prefix (bins 0..bin) and suffix (bins bin..15)
+      // scans start from the empty box grown by the bin's box, as the sequential sweep does: an
+      // empty large-segment bin decodes to NaN bounds, which box_grow ignores
+      int pn = cnt, sn = cnt;
+      double pb[6], pc[6], sb[6], sc[6];
+      box_reset(pb);
+      box_reset(pc);
+      box_grow(pb, bb, bb + 3);
+      box_grow(pc, cb, cb + 3);
+#pragma unroll
+      for (int k = 0; k < 6; k++) {
+        sb[k] = pb[k];
+        sc[k] = pc[k];
+      }
+#pragma unroll
+      for (int off = 1; off < kBins; off <<= 1) {
+        int un = __shfl_up_sync(0xffffffffu, pn, off, 16), dn = __shfl_down_sync(0xffffffffu, sn, off, 16);
+        double ub[6], uc[6], db[6], dc[6];
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          ub[k] = shfl_up_d(pb[k], off);
+          uc[k] = shfl_up_d(pc[k], off);
+          db[k] = shfl_down_d(sb[k], off);
+          dc[k] = shfl_down_d(sc[k], off);
+        }
+        if (bin >= off) {
+          pn += un;
+          box_grow(pb, ub, ub + 3);
+          box_grow(pc, uc, uc + 3);
+        }
+        if (bin + off < kBins) {
+          sn += dn;
+          box_grow(sb, db, db + 3);
+          box_grow(sc, dc, dc + 3);
+        }
+      }
+      // right side of plane p = bin: the suffix of bin + 1
+      int rn = __shfl_down_sync(0xffffffffu, sn, 1, 16);
+      double rb[6], rc[6];
+#pragma unroll
+      for (int k = 0; k < 6; k++) {
+        rb[k] = shfl_down_d(sb[k], 1);
+        rc[k] = shfl_down_d(sc[k], 1);
+      }
+      if (bin < kBins - 1 && pn != 0 && rn != 0) {
+        double cost = area6(pb) * (double)pn + area6(rb) * (double)rn;
+        if (cost < best) {
+          best = cost;
+          bkey = a * (kBins - 1) + bin;
+          bnl = pn;
+#pragma unroll
+          for (int k = 0; k < 6; k++) {
+            L[k] = pb[k];
+            CL[k] = pc[k];
+            R[k] = rb[k];
+            CR[k] = rc[k];
+          }
+        }
+      }
+    }
+  }
+  // warp argmin of (cost, key)
+  double wc = best;
+  int wk = bkey;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    double oc = __shfl_xor_sync(0xffffffffu, wc, off);
+    int ok = __shfl_xor_sync(0xffffffffu, wk, off);
+    if (oc < wc || (oc == wc && ok < wk)) {
+      wc = oc;
+      wk = ok;
+    }
+  }
+  SSplit r;
+  r.split = 0;
+  r.axis = -1;
+  r.plane = -1;
+  r.nl = 0;
+  if (wk < (1 << 30)) {
+    if (lane != (wk % (kBins - 1))) return;  // the owning lane of group 0 writes the split
+    r.axis = wk / (kBins - 1);
+    r.plane = wk % (kBins - 1);
+    r.nl = bnl;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      r.L[k] = L[k];
+      r.CL[k] = CL[k];
+      r.R[k] = R[k];
+      r.CR[k] = CR[k];
+    }
+    double aB = area6(g.B);
+    r.split = (g.n > kMaxLeaf || (aB + wc) < (double)g.n * aB) ? 1 : 0;
+  } else {
+    if (lane != 0) return;
+    if (g.n > kMaxLeaf) {
+      r.split = 1;  // coincident centroids: halve in the current order
+      r.axis = -1;
+      r.nl = g.n / 2;
+      box_reset(r.L);
+      box_reset(r.R);
+      box_reset(r.CL);
+      box_reset(r.CR);
+      for (int k = 0; k < g.n; k++) {
+        int t = ids[g.start + k];
+        double* B = k < r.nl ? r.L : r.R;
+        double* Cc = k < r.nl ? r.CL : r.CR;
+        box_grow(B, tb + 6 * (size_t)t, tb + 6 * (size_t)t + 3);
+        box_grow(Cc, cen + 3 * (size_t)t, cen + 3 * (size_t)t);
+      }
+    }
+  }
+  out[s] = r;
+  split_flag[s] = r.split;
+}
+
 __device__ __forceinline__ int leaf_ref32(long long start, long long count) {
   return (int)(-(1 + ((start << 3) | count)));
 }
@@ -524,9 +691,37 @@ int sah_build_device(const double* d_verts, int64_t n64, cudaStream_t st, Device
       k_sah_bin_large<<<(n + kChunk - 1) / kChunk, B, 0, st>>>(pos, ids, n, seg, b_lrank.as<int>(), b_tb.as<double>(),
                                                               b_cen.as<double>(), b_bins.as<BinAcc>());
     }
-    k_sah_decide<<<(nseg + 63) / 64, 64, 0, st>>>(seg, nseg, b_lrank.as<int>(), b_bins.as<BinAcc>(), ids,
-                                                  b_tb.as<double>(), b_cen.as<double>(), b_split.as<SSplit>(),
-                                                  b_sflag.as<int>());
+    if (getenv("LW_SAH_CHECK")) {
+      std::vector<SSplit> h1(nseg), h2(nseg);
+      k_sah_decide<<<(nseg + 63) / 64, 64, 0, st>>>(seg, nseg, b_lrank.as<int>(), b_bins.as<BinAcc>(), ids,
+                                                    b_tb.as<double>(), b_cen.as<double>(), b_split.as<SSplit>(),
+                                                    b_sflag.as<int>());
+      cudaMemcpyAsync(h1.data(), b_split.p, sizeof(SSplit) * nseg, cudaMemcpyDeviceToHost, st);
+      k_sah_decide_w<<<(nseg + 3) / 4, 128, 0, st>>>(seg, nseg, b_lrank.as<int>(), b_bins.as<BinAcc>(), ids,
+                                                     b_tb.as<double>(), b_cen.as<double>(), b_split.as<SSplit>(),
+                                                     b_sflag.as<int>());
+      cudaMemcpyAsync(h2.data(), b_split.p, sizeof(SSplit) * nseg, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      int bad = 0;
+      for (int q = 0; q < nseg && bad < 5; q++) {
+        const SSplit &x = h1[q], &y = h2[q];
+        bool same = x.split == y.split && x.axis == y.axis && x.plane == y.plane && x.nl == y.nl;
+        if (same && x.split) same = memcmp(x.L, y.L, sizeof(x.L)) == 0 && memcmp(x.R, y.R, sizeof(x.R)) == 0;
+        if (!same) {
+          bad++;
+          fprintf(stderr, "seg %d/%d: serial split %d axis %d plane %d nl %d | warp split %d axis %d plane %d nl %d\n", q,
+                  nseg, x.split, x.axis, x.plane, x.nl, y.split, y.axis, y.plane, y.nl);
+        }
+      }
+    }
+    if (getenv("LW_SAH_SERIAL"))
+      k_sah_decide<<<(nseg + 63) / 64, 64, 0, st>>>(seg, nseg, b_lrank.as<int>(), b_bins.as<BinAcc>(), ids,
+                                                    b_tb.as<double>(), b_cen.as<double>(), b_split.as<SSplit>(),
+                                                    b_sflag.as<int>());
+    else
+      k_sah_decide_w<<<(nseg + 3) / 4, 128, 0, st>>>(seg, nseg, b_lrank.as<int>(), b_bins.as<BinAcc>(), ids,
+                                                     b_tb.as<double>(), b_cen.as<double>(), b_split.as<SSplit>(),
+                                                     b_sflag.as<int>());
     t = b_tmp.bytes;
     TRY(cub::DeviceScan::ExclusiveSum(b_tmp.p, t, b_sflag.as<int>(), b_srank.as<int>(), nseg + 1, st));
     k_sah_emit<<<gs, B, 0, st>>>(seg, nseg, b_split.as<SSplit>(), b_srank.as<int>(), node_base, out.nodes,

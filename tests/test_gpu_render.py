@@ -283,6 +283,32 @@ def test_persistent_refill_trace_invariance(gpu, cfg, monkeypatch):
     assert outs[0][0].sum() > 0
 
 
+@pytest.mark.parametrize("name", ["cornell", "soup65k", "many_lights", "soup1M"])
+def test_warp_sah_decide_builds_the_serial_tree(gpu, name, monkeypatch):
+    """The warp-per-segment SAH split decision builds the same render tree as the per-thread one
+    (LW_SAH_SERIAL=1): the extension-ray work counters of the one-ray-per-thread trace kernels (a
+    function of the tree) agree exactly on a full pass."""
+    sc = {"cornell": lambda: scenes.cornell(), "soup65k": lambda: scenes.soup(1 << 16),
+          "many_lights": lambda: scenes.many_lights(), "soup1M": lambda: scenes.soup()}[name]()
+    packed = pack_scene(sc, bvh="sah")
+    monkeypatch.setenv("LW_TRACE_PERSIST", "0")
+    prof = []
+    for serial in (True, False):
+        if serial:
+            monkeypatch.setenv("LW_SAH_SERIAL", "1")
+        else:
+            monkeypatch.delenv("LW_SAH_SERIAL", raising=False)
+        with _renderer(packed, 256, 256, 6) as r:
+            r.set_instrumentation(count_work=True)
+            r.render_pass(0, 1)
+            p = r.kernel_profile()
+            # extension rays only: the shadow kernels traverse speculatively, and which lanes are
+            # converged at a speculation vote is up to the warp scheduler (counts vary, hits do not)
+            prof.append({k: p[k] for k in ("ext_nodes", "ext_tris")})
+    assert prof[0] == prof[1]
+    assert prof[0]["ext_nodes"] > 0
+
+
 def test_degenerate_deep_sah_tree_falls_back_to_median(gpu, oracle):
     """A SAH tree deeper than the traversal stack (exponentially spaced triangles) is replaced by the
     median tree at upload; hits do not depend on the tree, so the image still matches the oracle."""
