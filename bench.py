@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--pass-iterations", type=int, default=0, help="QMC iterations per GPU per step (0: ~16M paths)")
     ap.add_argument("--engine", default="wavefront", choices=["wavefront", "megakernel"])
-    ap.add_argument("--pool-log2", type=int, default=23)
+    ap.add_argument("--pool-log2", type=int, default=24)
     ap.add_argument("--regen-fraction", type=float, default=0.5)
     ap.add_argument("--megakernel-tail", type=int, default=0)
     ap.add_argument("--env-sampling", default="alias", choices=["alias", "pyramid"],

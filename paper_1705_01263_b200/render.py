@@ -24,7 +24,7 @@ FB_SCALE = float(1 << _abi.LW_FB_FRAC_BITS)
 class RenderParams:
     """Resolution, depth, QMC dimension table and engine knobs (LwRenderParams + owned arrays)."""
 
-    def __init__(self, width, height, max_depth=8, rr_start=4, engine="wavefront", pool_log2=23,
+    def __init__(self, width, height, max_depth=8, rr_start=4, engine="wavefront", pool_log2=24,
                  regen_fraction=0.5, megakernel_tail=0):
         if engine not in ENGINES:
             raise ValueError(f"unknown engine '{engine}'")
@@ -56,7 +56,7 @@ class Renderer:
     """Progressive renderer on one GPU."""
 
     def __init__(self, scene, width, height, max_depth=8, device=0, engine="wavefront", p_env=0.5, rr_start=4,
-                 pool_log2=23, regen_fraction=0.5, megakernel_tail=0, packed=None):
+                 pool_log2=24, regen_fraction=0.5, megakernel_tail=0, packed=None):
         self.lib = _abi.lib()
         self.packed = packed if packed is not None else pack_scene(scene, p_env=p_env)
         self.params = RenderParams(width, height, max_depth, rr_start, engine, pool_log2, regen_fraction,
