@@ -111,6 +111,7 @@ struct lw_ctx {
   double last_total_ms = 0.0, last_trace_ms = 0.0;
   int64_t last_launches = 0;
   size_t smem_bytes = 0;  // scene bytes staged in shared memory (0 = use global/L1)
+  size_t pool_bytes = 0;  // bytes of pool.block
   // persistent lane-refill trace kernels (with speculative traversal): bits 0 / 1 extension /
   // shadow rays on global-memory BVHs, bits 2 / 3 the same on shared-memory BVHs; all on by
   // default (C2 +4 %, C3 +13 %); LW_TRACE_PERSIST=<mask> overrides (A/B measurements)
@@ -160,9 +161,46 @@ void free_scene(lw_ctx* c) {
   c->has_scene = false;
 }
 
+// Per-device cache of wavefront-pool blocks (several GB): a destroyed context hands its block to
+// the next one instead of returning it to the stream-ordered allocator, where interleaved scene
+// and BVH-build allocations fragment the address range and force a fresh multi-GB mapping
+// (measured: C3 end-to-end 79 vs 198 Mpaths/s with a 2^24-slot pool).
+struct PoolBlock {
+  int device;
+  size_t bytes;
+  void* p;
+};
+std::mutex g_pool_mu;
+std::vector<PoolBlock> g_pool_free;
+constexpr size_t kPoolCache = 2;
+
 void free_pool(lw_ctx* c) {
-  if (c->pool.block) cudaFreeAsync(c->pool.block, c->stream);
+  if (c->pool.block) {
+    cudaStreamSynchronize(c->stream);  // the block may still be in use by queued kernels
+    bool kept = false;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      if (g_pool_free.size() < kPoolCache) {
+        g_pool_free.push_back({c->device, c->pool_bytes, c->pool.block});
+        kept = true;
+      }
+    }
+    if (!kept) cudaFree(c->pool.block);
+  }
   c->pool = Pool();
+  c->pool_bytes = 0;
+}
+
+void* take_pool_block(int device, size_t bytes, size_t& got) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (size_t k = 0; k < g_pool_free.size(); k++)
+    if (g_pool_free[k].device == device && g_pool_free[k].bytes >= bytes && g_pool_free[k].bytes <= 2 * bytes) {
+      void* p = g_pool_free[k].p;
+      got = g_pool_free[k].bytes;
+      g_pool_free.erase(g_pool_free.begin() + k);
+      return p;
+    }
+  return nullptr;
 }
 
 // ---- warp-aggregated queue append ---------------------------------------------------------
@@ -1237,7 +1275,10 @@ int alloc_pool(lw_ctx* c, int size) {
   Pool& P = c->pool;
   const size_t nvec = 17;  // double2 arrays
   size_t bytes = (size_t)size * (nvec * 16 + 7 * 4 + 1) + 8192;
-  LW_CUDA_TRY(cudaMallocAsync(&P.block, bytes, c->stream));
+  size_t got = bytes;
+  P.block = take_pool_block(c->device, bytes, got);
+  if (!P.block) LW_CUDA_TRY(cudaMalloc(&P.block, bytes));
+  c->pool_bytes = got;
   char* p = (char*)P.block;
   auto v2 = [&](double2*& x) {
     x = (double2*)p;
