@@ -250,8 +250,9 @@ def load_stage_profile(config):
     return {"l1tex_throughput_pct": k.get("l1tex_throughput_pct"), "issue_active_pct": k.get("issue_active_pct"),
             "dram_throughput_gbs": round((k["dram_read_bytes"] + k["dram_write_bytes"]) / k["duration_us"] / 1e3, 1),
             "threads_per_warp_inst": k.get("threads_per_warp_inst"),
-            "note": "measured limiter of this kernel: L1TEX throughput (local-memory stack, shared/global node "
-                    "loads of divergent lanes), not HBM; source profiles/r01_ncu_stage_kernels.json"}
+            "note": "measured limiter of this kernel: latency and SIMT efficiency (long-scoreboard stalls on node "
+                    "fetches, threads_per_warp_inst of 32 lanes active; L1TEX at l1tex_throughput_pct), not HBM; "
+                    "source profiles/r01_ncu_stage_kernels.json"}
 
 
 def load_traffic():
