@@ -75,7 +75,9 @@ __device__ __forceinline__ void lw_lt_importance(const LwLightNode& N, float x0,
 // visited by every walk -- are one contiguous prefix that the shading kernels stage in shared
 // memory; only the deepest levels come from L2.  Same values, same operation order as the
 // oracle's depth-first layout, so samples and probabilities are unchanged.
+#ifndef LW_LT_SMEM_NODES
 #define LW_LT_SMEM_NODES 511
+#endif
 
 struct LwLightTree {
   const LwLightNode* nodes;  // heap order, global memory
