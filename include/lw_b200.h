@@ -149,7 +149,16 @@ typedef struct lw_render_params {
   int32_t pool_log2;         /* wavefront state pool = 2^pool_log2 slots */
   double regen_fraction;     /* regenerate when free slots exceed this fraction of the pool (paper: 0.5) */
   int64_t megakernel_tail;   /* switch to the megakernel once active paths drop below this (0 = never) */
+  int32_t estimator;         /* LW_EST_*: how emitter / environment radiance is estimated */
 } lw_render_params;
+
+/* estimators (SPEC.md:400-402 estimator equivalence): balance-heuristic MIS of light sampling and
+ * BSDF sampling (the renderer), light sampling only (NEE weight 1; emitters / environment reached by
+ * BSDF sampling after a non-specular vertex count 0), BSDF sampling only (no NEE; every emitter /
+ * environment hit counts with weight 1).  All three are unbiased estimators of the same image. */
+#define LW_EST_MIS 0
+#define LW_EST_NEE 1
+#define LW_EST_BSDF 2
 
 typedef struct lw_render_stats {
   int64_t paths;          /* (pixel, iteration) samples completed */
@@ -170,7 +179,22 @@ typedef struct lw_kernel_profile {
   int64_t kernel_launches;   /* every kernel this library launched in the pass */
   int64_t ext_rays, ext_nodes, ext_tris;        /* traversal work (LW_INSTR_COUNT) */
   int64_t shadow_rays, shadow_nodes, shadow_tris;
+  /* per wavefront stage (LW_INSTR_TIME): summed CUDA-event time and launches, index LW_PROF_* */
+  double stage_ms[6];
+  int64_t stage_launches[6];
+  int64_t pool_slots;        /* wavefront pool of the pass */
+  int64_t waves;             /* stage rounds */
+  int64_t paths;             /* paths generated and flushed */
+  int64_t shadow_unoccluded; /* shadow rays that added their NEE contribution */
 } lw_kernel_profile;
+
+#define LW_PROF_GENERATE 0     /* k_generate: flush + regenerate + extension queue */
+#define LW_PROF_TRACE_EXT 1    /* k_trace_ext(_p): closest hit */
+#define LW_PROF_SHADE_NEE 2    /* k_shade_nee: light sample, BSDF eval, shadow-ray setup */
+#define LW_PROF_SHADE 3        /* k_shade: emission/MIS, BSDF sampling, roulette, next ray */
+#define LW_PROF_TRACE_SHADOW 4 /* k_trace_shadow(_p): any hit + NEE accumulation */
+#define LW_PROF_OTHER 5        /* wave bookkeeping (k_wave_begin / k_wave_end, tail) */
+#define LW_PROF_END 6
 
 #define LW_INSTR_TIME 1  /* bracket trace launches with CUDA events */
 #define LW_INSTR_COUNT 2 /* count node visits / triangle tests (separate kernel instantiation) */
@@ -243,6 +267,22 @@ int lw_framebuffer_resolve(lw_ctx* ctx, double inv_samples, float* host_rgb); /*
 int lw_framebuffer_copy_device(lw_ctx* ctx, void* dst_device);         /* D2D copy for NCCL reduction */
 int lw_framebuffer_load_device(lw_ctx* ctx, const void* src_device);   /* D2D copy back after reduction */
 int lw_framebuffer_upload(lw_ctx* ctx, const int64_t* host_fb);       /* H2D: resume from a checkpoint */
+/* Progressive accumulation on the context's stream (asynchronous): dst_device (W*H*3 int64,
+ * 16-byte aligned, caller-owned) += framebuffer; clear != 0 also zeroes the framebuffer for the
+ * next pass.  One kernel instead of copy + add + clear. */
+int lw_framebuffer_accumulate(lw_ctx* ctx, void* dst_device, int clear);
+
+/* Sample-space partition across GPUs: one context per GPU and
+ * process; every rank renders a disjoint block of iterations, then the pass framebuffers are
+ * sum-reduced in place with an NCCL all-reduce on the context's stream (int64 addition is
+ * associative: the image is bit-identical for any rank count).  NCCL is loaded at first use
+ * (libnccl.so.2).  lw_comm_unique_id: rank 0 creates the id, the caller broadcasts it (e.g. over
+ * torch.distributed); lw_ctx_comm_init: every rank joins; lw_framebuffer_reduce: asynchronous
+ * all-reduce of the framebuffer (and LPE layer framebuffers). */
+#define LW_COMM_ID_BYTES 128
+int lw_comm_unique_id(uint8_t* id_out);
+int lw_ctx_comm_init(lw_ctx* ctx, const uint8_t* id, int rank, int world);
+int lw_framebuffer_reduce(lw_ctx* ctx);
 int lw_get_stats(lw_ctx* ctx, lw_render_stats* stats);
 /* debug/parity surface of the render traversal (near-first, conservative cull) */
 int lw_ctx_trace_closest(lw_ctx* ctx, const double* origins, const double* dirs, const double* tmaxs, int64_t n,
@@ -274,10 +314,36 @@ int lw_ctx_light_pdf(lw_ctx* ctx, const int64_t* e, const double* x, const doubl
 int lw_ctx_set_lpe(lw_ctx* ctx, int32_t nlayers, int32_t nstates, const int16_t* trans, const uint8_t* accept,
                    int32_t start);
 int lw_ctx_lpe_download(lw_ctx* ctx, int32_t layer, int64_t* fb);
+/* H2D copy of one layer framebuffer (checkpoint resume of a render with layers) */
+int lw_ctx_lpe_upload(lw_ctx* ctx, int32_t layer, const int64_t* fb);
 int lw_ctx_env_pyramid_info(lw_ctx* ctx, int32_t* nlevels);
 int lw_ctx_env_sample(lw_ctx* ctx, const int64_t* packed_normal, const double* uv, int64_t n, int64_t* out_texel,
                       double* out_p, double* out_uv);
 int lw_ctx_env_pdf(lw_ctx* ctx, const int64_t* packed_normal, const int64_t* texel, int64_t n, double* out_p);
+/* Known-answer surface of the render math (SPEC.md:309-317 bsdf_evaluate / bsdf_sample,
+ * 394-402 next_event + MIS, 204-230 sample_light / light_pdf / sample_env / env_pdf), the same
+ * device functions the engines run.
+ * lw_bsdf_eval_batch: f (RGB) and pdf (solid angle, non-delta lobes) for local-frame directions
+ *   (z = shading normal), layer weights from wo.z.
+ * lw_bsdf_sample_batch: sampled wi, weight f*cos/pdf (delta lobes: the lobe's throughput), pdf
+ *   (0 for delta lobes) and flags: bit 0 sampled, bit 1 delta, bit 2 transmission, bits 8+ the
+ *   LPE event (LW_EV_*).  front: the ray arrived on the front side (transmission eta).
+ * lw_mis_weight_batch: the balance heuristic a / (a + b) of the engines.
+ * lw_ctx_nee_light_sample: the light half of NEE at points p with facing normals ngf for NEE
+ *   uniforms uv: direction, radiance, solid-angle pdf (0: no light), shadow-ray tmax, emitter
+ *   (-1 = environment).
+ * lw_ctx_emission_pdf: what BSDF sampling meets along (o, d): radiance and the light-sampling pdf
+ *   MIS weighs it against (nprev: packed facing normal of the vertex the ray leaves), emitter
+ *   (-1 environment, -2 non-emissive surface). */
+int lw_bsdf_eval_batch(const lw_material* m, const double* wo, const double* wi, int64_t n, double* out_f,
+                       double* out_pdf);
+int lw_bsdf_sample_batch(const lw_material* m, const double* wo, const int32_t* front, const double* uv, int64_t n,
+                         double* out_wi, double* out_weight, double* out_pdf, int32_t* out_flags);
+int lw_mis_weight_batch(const double* pdf_a, const double* pdf_b, int64_t n, double* out);
+int lw_ctx_nee_light_sample(lw_ctx* ctx, const double* p, const double* ngf, const double* uv, int64_t n,
+                            double* out_wi, double* out_le, double* out_pdf, double* out_tmax, int64_t* out_emitter);
+int lw_ctx_emission_pdf(lw_ctx* ctx, const double* o, const double* d, const int32_t* nprev, int64_t n,
+                        double* out_le, double* out_pdf, int64_t* out_emitter);
 /* BVH arrays the context built (reference layout), for parity checks */
 int lw_ctx_bvh_info(lw_ctx* ctx, int64_t* nnodes);
 int lw_ctx_bvh_download(lw_ctx* ctx, double* bounds, int64_t* children, int64_t* order);

@@ -2007,7 +2007,109 @@ static void lpe_route(const lpe_ctx* x, int state, int64_t pix, v3 c) {
       for (int k = 0; k < 3; k++) x->fb[(int64_t)l * x->npix * 3 + 3 * pix + k] += q[k];
 }
 
+/* light half of next-event estimation (device: lw_nee_light_sample): from p with
+ * facing normal ngf and the NEE uniforms, the environment (p_env) or an emitter, the direction wi,
+ * its radiance, solid-angle pdf (selection included) and the shadow-ray length; e_out the emitter
+ * (-1 = environment).  Returns 0 when the sample carries no light. */
+static int nee_light_sample(const lwo_scene* s, v3 p, v3 ngf, double ul, double vl, v3* wi, v3* Le, double* pl,
+                            double* tmax_sh, int64_t* e_out) {
+  *wi = mk(0, 0, 0);
+  *Le = mk(0, 0, 0);
+  *pl = 0.0;
+  *tmax_sh = INFINITY;
+  *e_out = -1;
+  int ok = 0;
+  if (s->env_kind != LW_ENV_NONE && ul < s->p_env) {
+    double ue = s->nemit > 0 ? ul / s->p_env : ul;
+    if (s->env_kind == LW_ENV_CONSTANT) {
+      double z = 1.0 - 2.0 * ue;
+      double r2 = 1.0 - z * z;
+      double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
+      lwo_sincos2pi(vl, &sp, &cp);
+      *wi = mk(r * cp, z, r * sp);
+      *pl = s->p_env * LW_INV_FOUR_PI;
+      *Le = scl(ld3(s->d.env_constant), s->d.env_scale);
+      ok = 1;
+    } else {
+      double ur, vr, pt;
+      int64_t j, row, col;
+      if (s->ep_on) {
+        ep_sample(s, ep_bin(lwo_oct_encode(ngf.x, ngf.y, ngf.z)), ue, vl, &row, &col, &pt, &ur, &vr);
+        j = row * s->env_w + col;
+      } else {
+        j = alias_sample(s->env_prob, s->env_alias, (int64_t)s->env_w * s->env_h, ue, &ur);
+        row = j / s->env_w;
+        col = j % s->env_w;
+        vr = vl;
+        pt = s->env_pdf[j];
+      }
+      double uu = ((double)col + ur) / (double)s->env_w;
+      double vv2 = ((double)row + vr) / (double)s->env_h;
+      double st_, ct, sp, cp;
+      lwo_sincos2pi(vv2 * 0.5, &st_, &ct);
+      lwo_sincos2pi(uu, &sp, &cp);
+      *wi = mk(st_ * cp, ct, st_ * sp);
+      if (st_ > 0.0) {
+        *pl = s->p_env * pt * (double)((int64_t)s->env_w * s->env_h) / (LW_TWO_PI_SQ * st_);
+        const float* px = s->env_img + 3 * j;
+        *Le = mk((double)px[0] * s->d.env_scale, (double)px[1] * s->d.env_scale, (double)px[2] * s->d.env_scale);
+        ok = 1;
+      }
+    }
+  } else if (s->nemit > 0) {
+    double ut = s->env_kind != LW_ENV_NONE ? (ul - s->p_env) / (1.0 - s->p_env) : ul;
+    double ur, psel;
+    int64_t le;
+    if (s->lt) {
+      v3 xr = offset_origin(p, ngf, ngf);
+      v3 nr = lt_ref_normal(lwo_oct_encode(ngf.x, ngf.y, ngf.z));
+      le = lt_sample(s, xr, nr, ut, &psel, &ur);
+    } else {
+      le = alias_sample(s->emit_prob, s->emit_alias, s->nemit, ut, &ur);
+      psel = s->emit_pdf[le];
+    }
+    *e_out = le;
+    const double* lv = s->verts + 9 * s->emit_tri[le];
+    v3 l0 = ld3(lv), l1 = ld3(lv + 3), l2 = ld3(lv + 6);
+    double su = sqrt(ur);
+    double b0 = 1.0 - su, b1 = vl * su;
+    double b2 = (1.0 - b0) - b1;
+    v3 q = bary3(l0, l1, l2, b0, b1, b2);
+    v3 dl = sub(q, p);
+    double dist2 = dot(dl, dl);
+    double dist = sqrt(dist2);
+    double inv_dist = 1.0 / dist;
+    *wi = mk(dl.x * inv_dist, dl.y * inv_dist, dl.z * inv_dist);
+    v3 ngl = normalize(cross(sub(l1, l0), sub(l2, l0)));
+    double cos_l = -dot(ngl, *wi);
+    if (s->emit_two[le]) cos_l = fabs(cos_l);
+    if (cos_l > 0.0 && dist > 0.0) {
+      *pl = (s->p_tri * psel / s->emit_area[le]) * dist2 / cos_l;
+      *Le = ld3(s->emit_rad + 3 * le);
+      *tmax_sh = dist * (1.0 - 1e-7);
+      ok = 1;
+    }
+  }
+  return ok;
+}
+
+/* solid-angle light-sampling pdf of emitter e hit at distance t from o along d (geometric normal ng;
+ * nprev: packed facing normal of the vertex the ray left) -- device lw_emitter_hit_pdf */
+static double emitter_hit_pdf(const lwo_scene* s, int64_t e, v3 o, int64_t nprev, v3 ng, v3 d, double t) {
+  double cos_l = fabs(dot(ng, d));
+  double psel = s->lt ? lt_pdf(s, e, o, lt_ref_normal(nprev)) : s->emit_pdf[e];
+  double pdf_area = s->p_tri * psel / s->emit_area[e];
+  return pdf_area * (t * t) / cos_l;
+}
+
 static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, const lpe_ctx* lpe, int64_t pix);
+
+/* balance heuristic and the estimator switch of lw_render_params.estimator
+ * (SPEC.md:400-402): weight of emission reached by BSDF sampling after a non-specular vertex */
+static double mis_balance(double a, double b) { return a / (a + b); }
+static double bsdf_hit_weight(int est, double pdf_bsdf, double pdf_light) {
+  return est == LW_EST_MIS ? mis_balance(pdf_bsdf, pdf_light) : (est == LW_EST_BSDF ? 1.0 : 0.0);
+}
 
 static v3 trace_path(const rctx* c, int64_t index, lw_render_stats* st) { return trace_path_lpe(c, index, st, NULL, 0); }
 
@@ -2029,7 +2131,7 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
       if (s->env_kind != LW_ENV_NONE) {
         double pe;
         v3 Le = env_eval(s, d, nprev, &pe);
-        double w = spec_prev ? 1.0 : pdf_prev / (pdf_prev + pe);
+        double w = spec_prev ? 1.0 : bsdf_hit_weight(c->p->estimator, pdf_prev, pe);
         v3 cc = mk(beta.x * Le.x * w, beta.y * Le.y * w, beta.z * Le.z * w);
         L = add(L, cc);
         if (lpe) lpe_route(lpe, lpe_step(lpe, lst, LW_EV_E), pix, cc);
@@ -2048,13 +2150,7 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
     if (e >= 0 && s->nemit > 0 && (front || s->emit_two[e])) {
       v3 Le = ld3(s->emit_rad + 3 * e);
       double wm = 1.0;
-      if (!spec_prev) {
-        double cos_l = fabs(dot(ng, d));
-        double psel = s->lt ? lt_pdf(s, e, o, lt_ref_normal(nprev)) : s->emit_pdf[e];
-        double pdf_area = s->p_tri * psel / s->emit_area[e];
-        double pl = pdf_area * (h.t * h.t) / cos_l;
-        wm = pdf_prev / (pdf_prev + pl);
-      }
+      if (!spec_prev) wm = bsdf_hit_weight(c->p->estimator, pdf_prev, emitter_hit_pdf(s, e, o, nprev, ng, d, h.t));
       v3 cc = mk(beta.x * Le.x * wm, beta.y * Le.y * wm, beta.z * Le.z * wm);
       L = add(L, cc);
       if (lpe) lpe_route(lpe, lpe_step(lpe, lst, LW_EV_L), pix, cc);
@@ -2076,87 +2172,18 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
     layer_weights(m, wol.z, &lw);
     int64_t bd = 4 + 8 * (int64_t)b;
     /* next-event estimation */
-    if (lw.nonspec && has_light(s)) {
+    if (lw.nonspec && has_light(s) && c->p->estimator != LW_EST_BSDF) {
       double ul = qmc(c, bd + 2, index), vl = qmc(c, bd + 3, index);
-      v3 wi, Le = mk(0, 0, 0);
-      double pl = 0.0, tmax_sh = INFINITY;
-      int ok = 0;
-      if (s->env_kind != LW_ENV_NONE && ul < s->p_env) {
-        double ue = s->nemit > 0 ? ul / s->p_env : ul;
-        if (s->env_kind == LW_ENV_CONSTANT) {
-          double z = 1.0 - 2.0 * ue;
-          double r2 = 1.0 - z * z;
-          double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
-          lwo_sincos2pi(vl, &sp, &cp);
-          wi = mk(r * cp, z, r * sp);
-          pl = s->p_env * LW_INV_FOUR_PI;
-          Le = scl(ld3(s->d.env_constant), s->d.env_scale);
-          ok = 1;
-        } else {
-          double ur, vr, pt;
-          int64_t j, row, col;
-          if (s->ep_on) {
-            ep_sample(s, ep_bin(lwo_oct_encode(ngf.x, ngf.y, ngf.z)), ue, vl, &row, &col, &pt, &ur, &vr);
-            j = row * s->env_w + col;
-          } else {
-            j = alias_sample(s->env_prob, s->env_alias, (int64_t)s->env_w * s->env_h, ue, &ur);
-            row = j / s->env_w;
-            col = j % s->env_w;
-            vr = vl;
-            pt = s->env_pdf[j];
-          }
-          double uu = ((double)col + ur) / (double)s->env_w;
-          double vv2 = ((double)row + vr) / (double)s->env_h;
-          double st_, ct, sp, cp;
-          lwo_sincos2pi(vv2 * 0.5, &st_, &ct);
-          lwo_sincos2pi(uu, &sp, &cp);
-          wi = mk(st_ * cp, ct, st_ * sp);
-          if (st_ > 0.0) {
-            pl = s->p_env * pt * (double)((int64_t)s->env_w * s->env_h) / (LW_TWO_PI_SQ * st_);
-            const float* px = s->env_img + 3 * j;
-            Le = mk((double)px[0] * s->d.env_scale, (double)px[1] * s->d.env_scale, (double)px[2] * s->d.env_scale);
-            ok = 1;
-          }
-        }
-      } else if (s->nemit > 0) {
-        double ut = s->env_kind != LW_ENV_NONE ? (ul - s->p_env) / (1.0 - s->p_env) : ul;
-        double ur, psel;
-        int64_t le;
-        if (s->lt) {
-          v3 xr = offset_origin(p, ngf, ngf);
-          v3 nr = lt_ref_normal(lwo_oct_encode(ngf.x, ngf.y, ngf.z));
-          le = lt_sample(s, xr, nr, ut, &psel, &ur);
-        } else {
-          le = alias_sample(s->emit_prob, s->emit_alias, s->nemit, ut, &ur);
-          psel = s->emit_pdf[le];
-        }
-        const double* lv = s->verts + 9 * s->emit_tri[le];
-        v3 l0 = ld3(lv), l1 = ld3(lv + 3), l2 = ld3(lv + 6);
-        double su = sqrt(ur);
-        double b0 = 1.0 - su, b1 = vl * su;
-        double b2 = (1.0 - b0) - b1;
-        v3 q = bary3(l0, l1, l2, b0, b1, b2);
-        v3 dl = sub(q, p);
-        double dist2 = dot(dl, dl);
-        double dist = sqrt(dist2);
-        double inv_dist = 1.0 / dist;
-        wi = mk(dl.x * inv_dist, dl.y * inv_dist, dl.z * inv_dist);
-        v3 ngl = normalize(cross(sub(l1, l0), sub(l2, l0)));
-        double cos_l = -dot(ngl, wi);
-        if (s->emit_two[le]) cos_l = fabs(cos_l);
-        if (cos_l > 0.0 && dist > 0.0) {
-          pl = (s->p_tri * psel / s->emit_area[le]) * dist2 / cos_l;
-          Le = ld3(s->emit_rad + 3 * le);
-          tmax_sh = dist * (1.0 - 1e-7);
-          ok = 1;
-        }
-      }
+      v3 wi, Le;
+      double pl, tmax_sh;
+      int64_t le_;
+      int ok = nee_light_sample(s, p, ngf, ul, vl, &wi, &Le, &pl, &tmax_sh, &le_);
       if (ok && pl > 0.0 && dot(ngf, wi) > 0.0) {
         v3 wil = to_local(&fr, wi);
         double pb;
         v3 f = bsdf_eval(m, &lw, wol, wil, &pb);
         if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
-          double wm = pl / (pl + pb);
+          double wm = c->p->estimator == LW_EST_NEE ? 1.0 : mis_balance(pl, pb);
           double k = (wil.z * wm) / pl;
           v3 contrib = mk(beta.x * f.x * Le.x * k, beta.y * f.y * Le.y * k, beta.z * f.z * Le.z * k);
           v3 so = offset_origin(p, ngf, wi);
@@ -2265,3 +2292,90 @@ void lwo_render(const lwo_scene* s, const lw_render_params* p, int64_t pix_begin
   }
 }
 
+/* ---- known-answer surface of the render math (device: lw_bsdf_eval_batch, ...) ---------------- */
+
+void lwo_bsdf_eval_batch(const lw_material* m, const double* wo, const double* wi, int64_t n, double* out_f,
+                         double* out_pdf) {
+  for (int64_t i = 0; i < n; i++) {
+    v3 a = ld3(wo + 3 * i), b = ld3(wi + 3 * i);
+    layerw lw;
+    layer_weights(m, a.z, &lw);
+    double pdf;
+    v3 f = bsdf_eval(m, &lw, a, b, &pdf);
+    out_f[3 * i] = f.x;
+    out_f[3 * i + 1] = f.y;
+    out_f[3 * i + 2] = f.z;
+    out_pdf[i] = pdf;
+  }
+}
+
+void lwo_bsdf_sample_batch(const lw_material* m, const double* wo, const int32_t* front, const double* uv, int64_t n,
+                           double* out_wi, double* out_weight, double* out_pdf, int32_t* out_flags) {
+  for (int64_t i = 0; i < n; i++) {
+    v3 a = ld3(wo + 3 * i);
+    layerw lw;
+    layer_weights(m, a.z, &lw);
+    bsample bs;
+    memset(&bs, 0, sizeof(bs));
+    int ok = bsdf_sample(m, &lw, a, front[i] != 0, uv[2 * i], uv[2 * i + 1], &bs);
+    out_wi[3 * i] = bs.wi.x;
+    out_wi[3 * i + 1] = bs.wi.y;
+    out_wi[3 * i + 2] = bs.wi.z;
+    out_weight[3 * i] = bs.weight.x;
+    out_weight[3 * i + 1] = bs.weight.y;
+    out_weight[3 * i + 2] = bs.weight.z;
+    out_pdf[i] = bs.pdf;
+    out_flags[i] = (ok ? 1 : 0) | (bs.delta ? 2 : 0) | (bs.transmit ? 4 : 0) | (bs.event << 8);
+  }
+}
+
+void lwo_nee_light_sample_batch(const lwo_scene* s, const double* p, const double* ngf, const double* uv, int64_t n,
+                                double* out_wi, double* out_le, double* out_pdf, double* out_tmax, int64_t* out_e) {
+  for (int64_t i = 0; i < n; i++) {
+    v3 wi, Le;
+    double pl, tm;
+    int64_t e;
+    int ok = nee_light_sample(s, ld3(p + 3 * i), ld3(ngf + 3 * i), uv[2 * i], uv[2 * i + 1], &wi, &Le, &pl, &tm, &e);
+    out_wi[3 * i] = wi.x;
+    out_wi[3 * i + 1] = wi.y;
+    out_wi[3 * i + 2] = wi.z;
+    out_le[3 * i] = Le.x;
+    out_le[3 * i + 1] = Le.y;
+    out_le[3 * i + 2] = Le.z;
+    out_pdf[i] = ok ? pl : 0.0;
+    out_tmax[i] = tm;
+    out_e[i] = e;
+  }
+}
+
+void lwo_emission_pdf_batch(const lwo_scene* s, const double* o, const double* d, const int32_t* nprev, int64_t n,
+                            double* out_le, double* out_pdf, int64_t* out_e) {
+  for (int64_t i = 0; i < n; i++) {
+    v3 oo = ld3(o + 3 * i), dd = ld3(d + 3 * i);
+    hitrec h;
+    trace_closest(s, &oo.x, &dd.x, INFINITY, &h);
+    v3 Le = mk(0, 0, 0);
+    double pdf = 0.0;
+    int64_t e = -2;
+    if (h.tri < 0) {
+      e = -1;
+      Le = env_eval(s, dd, nprev[i], &pdf);
+    } else {
+      const double* vv = s->verts + 9 * h.tri;
+      v3 v0 = ld3(vv), v1 = ld3(vv + 3), v2 = ld3(vv + 6);
+      v3 ng = normalize(cross(sub(v1, v0), sub(v2, v0)));
+      int front = dot(ng, dd) < 0.0;
+      int64_t k = s->emit_of_tri[h.tri];
+      if (k >= 0 && s->nemit > 0 && (front || s->emit_two[k])) {
+        e = k;
+        Le = ld3(s->emit_rad + 3 * k);
+        pdf = emitter_hit_pdf(s, k, oo, nprev[i], ng, dd, h.t);
+      }
+    }
+    out_le[3 * i] = Le.x;
+    out_le[3 * i + 1] = Le.y;
+    out_le[3 * i + 2] = Le.z;
+    out_pdf[i] = pdf;
+    out_e[i] = e;
+  }
+}

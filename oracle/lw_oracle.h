@@ -87,6 +87,17 @@ void lwo_render_lpe(const lwo_scene* s, const lw_render_params* p, int64_t pix_b
                     int64_t it_begin, int64_t it_end, int64_t* fb, int nlayers, int nstates, const int16_t* trans,
                     const uint8_t* accept, int start, int64_t* layer_fb, int nthreads, lw_render_stats* stats);
 
+/* Known-answer surface of the render math (same semantics as the lw_bsdf_eval_batch /
+ * lw_bsdf_sample_batch / lw_ctx_nee_light_sample / lw_ctx_emission_pdf entries of the library). */
+void lwo_bsdf_eval_batch(const lw_material* m, const double* wo, const double* wi, int64_t n, double* out_f,
+                         double* out_pdf);
+void lwo_bsdf_sample_batch(const lw_material* m, const double* wo, const int32_t* front, const double* uv, int64_t n,
+                           double* out_wi, double* out_weight, double* out_pdf, int32_t* out_flags);
+void lwo_nee_light_sample_batch(const lwo_scene* s, const double* p, const double* ngf, const double* uv, int64_t n,
+                                double* out_wi, double* out_le, double* out_pdf, double* out_tmax, int64_t* out_e);
+void lwo_emission_pdf_batch(const lwo_scene* s, const double* o, const double* d, const int32_t* nprev, int64_t n,
+                            double* out_le, double* out_pdf, int64_t* out_e);
+
 /* Deterministic math shared by oracle and device (restated independently in lw_detmath.cuh). */
 void lwo_sincos2pi(double u, double* s, double* c);
 double lwo_atan2(double y, double x);

@@ -56,6 +56,10 @@ _SIG = {
                                C.c_int, C.c_int, C.POINTER(C.c_int16), C.POINTER(C.c_uint8), C.c_int, _pi64, C.c_int,
                                C.POINTER(LwRenderStats)]),
     "lwo_sincos2pi": (None, [C.c_double, _pd, _pd]),
+    "lwo_bsdf_eval_batch": (None, [C.POINTER(_abi.LwMaterial), _pd, _pd, C.c_int64, _pd, _pd]),
+    "lwo_bsdf_sample_batch": (None, [C.POINTER(_abi.LwMaterial), _pd, _pi32, _pd, C.c_int64, _pd, _pd, _pd, _pi32]),
+    "lwo_nee_light_sample_batch": (None, [_V, _pd, _pd, _pd, C.c_int64, _pd, _pd, _pd, _pd, _pi64]),
+    "lwo_emission_pdf_batch": (None, [_V, _pd, _pd, _pi32, C.c_int64, _pd, _pd, _pi64]),
     "lwo_atan2": (C.c_double, [C.c_double, C.c_double]),
 }
 
@@ -175,6 +179,31 @@ def atan2(y, x):
     return lib().lwo_atan2(float(y), float(x))
 
 
+def bsdf_evaluate(m, wo, wi):
+    """Oracle bsdf_eval (lw_oracle.c) with the semantics of paper_1705_01263_b200.bsdf.bsdf_evaluate."""
+    wo = np.ascontiguousarray(wo, np.float64).reshape(-1, 3)
+    wi = np.ascontiguousarray(wi, np.float64).reshape(-1, 3)
+    n = max(len(wo), len(wi))
+    wo = np.ascontiguousarray(np.broadcast_to(wo, (n, 3)))
+    wi = np.ascontiguousarray(np.broadcast_to(wi, (n, 3)))
+    f, pdf = np.empty((n, 3)), np.empty(n)
+    lib().lwo_bsdf_eval_batch(C.byref(m), ptr(wo, C.c_double), ptr(wi, C.c_double), n, ptr(f, C.c_double),
+                              ptr(pdf, C.c_double))
+    return f, pdf
+
+
+def bsdf_sample(m, wo, uv, front=True):
+    uv = np.ascontiguousarray(uv, np.float64).reshape(-1, 2)
+    n = len(uv)
+    wo = np.ascontiguousarray(np.broadcast_to(np.asarray(wo, np.float64).reshape(-1, 3), (n, 3)))
+    fr = np.ascontiguousarray(np.broadcast_to(np.asarray(front, np.int32), (n,)))
+    wi, w, pdf, fl = np.empty((n, 3)), np.empty((n, 3)), np.empty(n), np.empty(n, np.int32)
+    lib().lwo_bsdf_sample_batch(C.byref(m), ptr(wo, C.c_double), ptr(fr, C.c_int32), ptr(uv, C.c_double), n,
+                                ptr(wi, C.c_double), ptr(w, C.c_double), ptr(pdf, C.c_double), ptr(fl, C.c_int32))
+    return {"wi": wi, "weight": w, "pdf": pdf, "sampled": (fl & 1) != 0, "delta": (fl & 2) != 0,
+            "transmit": (fl & 4) != 0, "event": fl >> 8}
+
+
 class OracleScene:
     """Oracle-side scene built from the same packed description the GPU receives."""
 
@@ -265,6 +294,28 @@ class OracleScene:
         p = np.empty(len(pk))
         lib().lwo_env_pdf_batch(self.h, ptr(pk, C.c_int64), ptr(tx, C.c_int64), len(pk), ptr(p, C.c_double))
         return p
+
+    def nee_light_sample(self, points, facing_normals, uv):
+        uv = np.ascontiguousarray(uv, np.float64).reshape(-1, 2)
+        n = len(uv)
+        p = np.ascontiguousarray(np.broadcast_to(np.asarray(points, np.float64).reshape(-1, 3), (n, 3)))
+        nrm = np.ascontiguousarray(np.broadcast_to(np.asarray(facing_normals, np.float64).reshape(-1, 3), (n, 3)))
+        wi, le, pdf, tm, e = np.empty((n, 3)), np.empty((n, 3)), np.empty(n), np.empty(n), np.empty(n, np.int64)
+        lib().lwo_nee_light_sample_batch(self.h, ptr(p, C.c_double), ptr(nrm, C.c_double), ptr(uv, C.c_double), n,
+                                         ptr(wi, C.c_double), ptr(le, C.c_double), ptr(pdf, C.c_double),
+                                         ptr(tm, C.c_double), ptr(e, C.c_int64))
+        return {"wi": wi, "radiance": le, "pdf": pdf, "tmax": tm, "emitter": e}
+
+    def emission_pdf(self, origins, dirs, nprev=None):
+        d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+        n = len(d)
+        o = np.ascontiguousarray(np.broadcast_to(np.asarray(origins, np.float64).reshape(-1, 3), (n, 3)))
+        npv = np.zeros(n, np.int32) if nprev is None else np.ascontiguousarray(  # packed normals are 32-bit patterns
+            np.broadcast_to((np.asarray(nprev, np.int64) & 0xFFFFFFFF).astype(np.uint32).view(np.int32), (n,)))
+        le, pdf, e = np.empty((n, 3)), np.empty(n), np.empty(n, np.int64)
+        lib().lwo_emission_pdf_batch(self.h, ptr(o, C.c_double), ptr(d, C.c_double), ptr(npv, C.c_int32), n,
+                                     ptr(le, C.c_double), ptr(pdf, C.c_double), ptr(e, C.c_int64))
+        return {"radiance": le, "pdf": pdf, "emitter": e}
 
     def camera_rays(self, params, sample_index):
         idx = np.ascontiguousarray(sample_index, np.int64)

@@ -37,8 +37,14 @@ LW_ENV_NONE = 0
 LW_ENV_CONSTANT = 1
 LW_ENV_IMAGE = 2
 
+LW_EST_MIS = 0
+LW_EST_NEE = 1
+LW_EST_BSDF = 2
+
 LW_ENGINE_WAVEFRONT = 0
 LW_ENGINE_MEGAKERNEL = 1
+
+LW_COMM_ID_BYTES = 128
 
 LW_FB_FRAC_BITS = 20
 LW_FB_SAMPLE_CLAMP = 4294967296.0
@@ -121,6 +127,7 @@ class LwRenderParams(C.Structure):
         ("pool_log2", C.c_int32),
         ("regen_fraction", C.c_double),
         ("megakernel_tail", C.c_int64),
+        ("estimator", C.c_int32),
     ]
 
 
@@ -152,14 +159,31 @@ class LwKernelProfile(C.Structure):
         ("shadow_rays", C.c_int64),
         ("shadow_nodes", C.c_int64),
         ("shadow_tris", C.c_int64),
+        ("stage_ms", C.c_double * 6),
+        ("stage_launches", C.c_int64 * 6),
+        ("pool_slots", C.c_int64),
+        ("waves", C.c_int64),
+        ("paths", C.c_int64),
+        ("shadow_unoccluded", C.c_int64),
     ]
 
     def as_dict(self):
-        return {k: (float(getattr(self, k)) if t is C.c_double else int(getattr(self, k))) for k, t in self._fields_}
+        out = {}
+        for k, t in self._fields_:
+            v = getattr(self, k)
+            if k == "stage_ms":
+                out[k] = {n: float(v[i]) for i, n in enumerate(PROF_STAGES)}
+            elif k == "stage_launches":
+                out[k] = {n: int(v[i]) for i, n in enumerate(PROF_STAGES)}
+            else:
+                out[k] = float(v) if t is C.c_double else int(v)
+        return out
 
 
 LW_INSTR_TIME = 1
 LW_INSTR_COUNT = 2
+
+PROF_STAGES = ("generate", "trace_ext", "shade_nee", "shade", "trace_shadow", "other")  # LW_PROF_*
 
 
 def ptr(a: np.ndarray | None, ctype):
@@ -220,6 +244,16 @@ SIGNATURES = {
     "lw_framebuffer_upload": (C.c_int, [_V, _pi64]),
     "lw_ctx_set_lpe": (C.c_int, [_V, C.c_int32, C.c_int32, C.POINTER(C.c_int16), C.POINTER(C.c_uint8), C.c_int32]),
     "lw_ctx_lpe_download": (C.c_int, [_V, C.c_int32, _pi64]),
+    "lw_ctx_lpe_upload": (C.c_int, [_V, C.c_int32, _pi64]),
+    "lw_framebuffer_accumulate": (C.c_int, [_V, _V, C.c_int]),
+    "lw_bsdf_eval_batch": (C.c_int, [C.POINTER(LwMaterial), _pd, _pd, C.c_int64, _pd, _pd]),
+    "lw_bsdf_sample_batch": (C.c_int, [C.POINTER(LwMaterial), _pd, _pi32, _pd, C.c_int64, _pd, _pd, _pd, _pi32]),
+    "lw_mis_weight_batch": (C.c_int, [_pd, _pd, C.c_int64, _pd]),
+    "lw_ctx_nee_light_sample": (C.c_int, [_V, _pd, _pd, _pd, C.c_int64, _pd, _pd, _pd, _pd, _pi64]),
+    "lw_ctx_emission_pdf": (C.c_int, [_V, _pd, _pd, _pi32, C.c_int64, _pd, _pd, _pi64]),
+    "lw_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "lw_ctx_comm_init": (C.c_int, [_V, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
+    "lw_framebuffer_reduce": (C.c_int, [_V]),
     "lw_ctx_env_pyramid_info": (C.c_int, [_V, _pi32]),
     "lw_ctx_env_sample": (C.c_int, [_V, _pi64, _pd, C.c_int64, _pi64, _pd, _pd]),
     "lw_ctx_env_pdf": (C.c_int, [_V, _pi64, _pi64, C.c_int64, _pd]),

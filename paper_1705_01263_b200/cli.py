@@ -76,14 +76,6 @@ def cmd_render(args) -> int:
     step = args.snapshot_every or spp
     t0 = time.perf_counter()
     with Renderer(None, w, h, depth, device=args.device, engine=engine, packed=packed) as r:
-        done0 = 0
-        if args.resume:
-            try:
-                r.load_checkpoint(args.resume)
-            except (OSError, ValueError, KeyError) as e:
-                print(f"error: cannot resume from '{args.resume}': {e}", file=sys.stderr)
-                return 2
-            done0 = r.iterations
         if layers:
             from paper_1705_01263_b200.lpe import LpeError
 
@@ -92,6 +84,14 @@ def cmd_render(args) -> int:
             except LpeError as e:
                 print(f"error: --layer: {e}", file=sys.stderr)
                 return 2
+        done0 = 0
+        if args.resume:
+            try:
+                r.load_checkpoint(args.resume)
+            except (OSError, ValueError, KeyError) as e:
+                print(f"error: cannot resume from '{args.resume}': {e}", file=sys.stderr)
+                return 2
+            done0 = r.iterations
         done = done0
         while done < spp:
             k = min(step, spp - done)

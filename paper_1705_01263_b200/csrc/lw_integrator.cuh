@@ -48,6 +48,7 @@ struct DevScene {
   double cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3];
   double tan_half;
   int W, H, max_depth, rr_start;
+  int estimator;  // LW_EST_* (MIS in the renderer; NEE-only / BSDF-only for estimator-equivalence checks)
   const QmcDim* qdims;
   const uint16_t* qperm;
 };
@@ -172,6 +173,15 @@ __device__ __forceinline__ v3 lw_env_eval(const DevScene& S, v3 d, int nprev, do
   }
   pdf = 0.0;
   return mk3(0.0, 0.0, 0.0);
+}
+
+// balance heuristic: weight of the strategy with pdf `a` against the one with `b`
+__host__ __device__ __forceinline__ double lw_mis_balance(double a, double b) { return a / (a + b); }
+
+// weight of radiance reached by BSDF sampling after a non-specular vertex (pdf_bsdf) whose
+// light-sampling pdf is pdf_light
+__device__ __forceinline__ double lw_bsdf_hit_weight(const DevScene& S, double pdf_bsdf, double pdf_light) {
+  return S.estimator == LW_EST_MIS ? lw_mis_balance(pdf_bsdf, pdf_light) : (S.estimator == LW_EST_BSDF ? 1.0 : 0.0);
 }
 
 // ---- BSDF (oracle: make_frame .. bsdf_sample) --------------------------------------------
@@ -465,19 +475,19 @@ __device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const Lw
   lw_layer_weights(*g.m, g.wol.z, g.lw);
 }
 
-// next-event estimation: fills sh (valid = 0 if no contribution)
-// lt: the light hierarchy with its top staged in shared memory (nullptr: S.lt, global memory)
-__device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh,
-                                             const LwLpe* lpe = nullptr, const LwLightTree* lt = nullptr) {
-  sh.valid = 0;
-  const lw_material& m = *g.m;
-  const LayerW& lw = g.lw;
-  if (!(lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE))) return;
-  const int bd = 4 + 8 * ps.bounce;
-  double ul, vl;
-  lw_halton2(S.qdims, S.qperm, bd + 2, bd + 3, ps.index, ul, vl);
-  v3 wi = mk3(0.0, 0.0, 0.0), Le = mk3(0.0, 0.0, 0.0);
-  double pl = 0.0, tmax_sh = INFINITY;
+// light half of next-event estimation (SPEC.md:204-230 sample_light / sample_env): from the point p
+// with facing geometric normal ngf and the NEE uniforms (ul, vl), choose the environment (p_env) or
+// an emitter and a direction wi towards it; Le its radiance, pl the solid-angle pdf of wi (selection
+// probabilities included), tmax the shadow-ray length (INFINITY for the environment), e the emitter
+// (-1: environment).  Returns false when the sample carries no light (back side, sin(theta) = 0).
+__device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 ngf, double ul, double vl,
+                                                    const LwLightTree* lt, v3& wi, v3& Le, double& pl,
+                                                    double& tmax_sh, long long& e_out) {
+  wi = mk3(0.0, 0.0, 0.0);
+  Le = mk3(0.0, 0.0, 0.0);
+  pl = 0.0;
+  tmax_sh = INFINITY;
+  e_out = -1;
   bool ok = false;
   if (S.env_kind != LW_ENV_NONE && ul < S.p_env) {
     double ue = S.nemit > 0 ? ul / S.p_env : ul;
@@ -495,7 +505,7 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
       long long nt = (long long)S.env_w * S.env_h;
       long long j, row, col;
       if (S.env_mode == LW_LIGHTS_ENV_PYRAMID) {
-        lw_ep_sample(S.env_pyr, lw_ep_bin(lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z)), ue, vl, row, col, pt, ur, vr);
+        lw_ep_sample(S.env_pyr, lw_ep_bin(lw_oct_encode(ngf.x, ngf.y, ngf.z)), ue, vl, row, col, pt, ur, vr);
         j = row * S.env_w + col;
       } else {
         j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
@@ -523,20 +533,21 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
     double ur, psel;
     long long le;
     if (S.light_mode == LW_LIGHTS_TREE) {
-      v3 xr = lw_offset_origin(g.p, g.ngf, g.ngf);
-      v3 nr = lw_lt_ref_normal((int)lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z));
+      v3 xr = lw_offset_origin(p, ngf, ngf);
+      v3 nr = lw_lt_ref_normal((int)lw_oct_encode(ngf.x, ngf.y, ngf.z));
       le = lw_lt_sample(lt ? *lt : S.lt, xr, nr, ut, psel, ur);
     } else {
       le = lw_alias_sample(S.emit_prob, S.emit_alias, S.nemit, ut, ur);
       psel = S.emit_pdf[le];
     }
+    e_out = le;
     const double* lv = S.verts + 9 * S.emit_tri[le];
     v3 l0 = lw_ld3(lv), l1 = lw_ld3(lv + 3), l2 = lw_ld3(lv + 6);
     double su = sqrt(ur);
     double b0 = 1.0 - su, b1 = vl * su;
     double b2 = (1.0 - b0) - b1;
     v3 q = bary3(l0, l1, l2, b0, b1, b2);
-    v3 dl = q - g.p;
+    v3 dl = q - p;
     double dist2 = dot3(dl, dl);
     double dist = sqrt(dist2);
     double inv_dist = 1.0 / dist;
@@ -551,12 +562,42 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
       ok = true;
     }
   }
+  return ok;
+}
+
+// solid-angle light-sampling pdf of emitter e reached by a ray from `o` (leaving a vertex whose
+// packed facing normal is nprev) that hits it at distance t with geometric normal ng along d: the
+// MIS counterpart of lw_nee_light_sample for BSDF-sampled emitter hits (SPEC.md:213-221 light_pdf)
+__device__ __forceinline__ double lw_emitter_hit_pdf(const DevScene& S, long long e, v3 o, int nprev, v3 ng, v3 d,
+                                                     double t, const LwLightTree* lt) {
+  double cos_l = fabs(dot3(ng, d));
+  double psel = S.light_mode == LW_LIGHTS_TREE ? lw_lt_pdf(lt ? *lt : S.lt, e, o, lw_lt_ref_normal(nprev))
+                                               : S.emit_pdf[e];
+  double pdf_area = S.p_tri * psel / S.emit_area[e];
+  return pdf_area * (t * t) / cos_l;
+}
+
+// next-event estimation: fills sh (valid = 0 if no contribution)
+// lt: the light hierarchy with its top staged in shared memory (nullptr: S.lt, global memory)
+__device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh,
+                                             const LwLpe* lpe = nullptr, const LwLightTree* lt = nullptr) {
+  sh.valid = 0;
+  const lw_material& m = *g.m;
+  const LayerW& lw = g.lw;
+  if (!(lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE)) || S.estimator == LW_EST_BSDF) return;
+  const int bd = 4 + 8 * ps.bounce;
+  double ul, vl;
+  lw_halton2(S.qdims, S.qperm, bd + 2, bd + 3, ps.index, ul, vl);
+  v3 wi, Le;
+  double pl, tmax_sh;
+  long long le;
+  bool ok = lw_nee_light_sample(S, g.p, g.ngf, ul, vl, lt, wi, Le, pl, tmax_sh, le);
   if (ok && pl > 0.0 && dot3(g.ngf, wi) > 0.0) {
     v3 wil = lw_to_local(g.fr, wi);
     double pb;
     v3 f = lw_bsdf_eval(m, lw, g.wol, wil, pb);
     if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
-      double wm = pl / (pl + pb);
+      double wm = S.estimator == LW_EST_NEE ? 1.0 : lw_mis_balance(pl, pb);
       double k = (wil.z * wm) / pl;
       sh.contrib = mk3(ps.beta.x * f.x * Le.x * k, ps.beta.y * f.y * Le.y * k, ps.beta.z * f.z * Le.z * k);
       sh.o = lw_offset_origin(g.p, g.ngf, wi);
@@ -585,7 +626,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
     if (S.env_kind != LW_ENV_NONE) {
       double pe;
       v3 Le = lw_env_eval(S, d, ps.nprev, pe);
-      double wm = ps.spec_prev ? 1.0 : ps.pdf_prev / (ps.pdf_prev + pe);
+      double wm = ps.spec_prev ? 1.0 : lw_bsdf_hit_weight(S, ps.pdf_prev, pe);
       v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
       ps.L = ps.L + c;
       if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_E), pix, c);
@@ -597,15 +638,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
   if (e >= 0 && S.nemit > 0 && (g.front || S.emit_two[e])) {
     v3 Le = lw_ld3(S.emit_rad + 3 * e);
     double wm = 1.0;
-    if (!ps.spec_prev) {
-      double cos_l = fabs(dot3(g.ng, d));
-      double psel = S.light_mode == LW_LIGHTS_TREE
-                        ? lw_lt_pdf(lt ? *lt : S.lt, e, ps.o, lw_lt_ref_normal(ps.nprev))
-                        : S.emit_pdf[e];
-      double pdf_area = S.p_tri * psel / S.emit_area[e];
-      double pl = pdf_area * (h.t * h.t) / cos_l;
-      wm = ps.pdf_prev / (ps.pdf_prev + pl);
-    }
+    if (!ps.spec_prev) wm = lw_bsdf_hit_weight(S, ps.pdf_prev, lw_emitter_hit_pdf(S, e, ps.o, ps.nprev, g.ng, d, h.t, lt));
     v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
     ps.L = ps.L + c;
     if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_L), pix, c);

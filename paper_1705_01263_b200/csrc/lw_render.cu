@@ -10,6 +10,8 @@
 //  * the tail of a pass can switch to the megakernel.
 // Radiance is accumulated per path into an int64 fixed-point framebuffer, so the image is
 // independent of execution strategy, pool size, switch threshold and GPU count.
+#include <dlfcn.h>
+#include <nccl.h>
 #include <string.h>
 
 #include <algorithm>
@@ -58,6 +60,7 @@ struct Counters {
   unsigned long long n_alive_ull;
   unsigned long long rays_ext, rays_shadow, paths, nonfinite, regens, waves;
   unsigned long long ext_nodes, ext_tris, sh_nodes, sh_tris;
+  unsigned long long sh_unocc;  // shadow rays that reached their light (NEE contribution added)
   int ext_next, sh_next;  // queue heads of the persistent trace kernels
 };
 
@@ -123,6 +126,8 @@ struct lw_ctx {
   int instr = 0;
   std::vector<cudaEvent_t> evpool;  // pairs bracketing trace launches
   lw_kernel_profile prof;
+  ncclComm_t comm = nullptr;  // sample-space partition: per-pass framebuffer sum over the ranks
+  int comm_rank = 0, comm_world = 1;
 };
 
 void free_lpe(lw_ctx* c) {
@@ -1046,7 +1051,10 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
       }
     }
     if (occluded || ref == LW_REF_NONE) {
-      if (!occluded) shadow_unoccluded<LPE>(P, s, cx, lpe);
+      if (!occluded) {
+        shadow_unoccluded<LPE>(P, s, cx, lpe);
+        if (COUNT) tc.lit++;
+      }
       s = -1;
     }
   }
@@ -1079,7 +1087,10 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
     }
     ref = sp > 0 && !occluded ? stk[--sp] : LW_REF_NONE;
     if (ref == LW_REF_NONE) {
-      if (!occluded) shadow_unoccluded<LPE>(P, s, cx, lpe);
+      if (!occluded) {
+        shadow_unoccluded<LPE>(P, s, cx, lpe);
+        if (COUNT) tc.lit++;
+      }
       s = -1;
     }
   }
@@ -1087,6 +1098,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
   if (COUNT) {
     warp_add(&cnt->sh_nodes, tc.nodes);
     warp_add(&cnt->sh_tris, tc.tris);
+    warp_add(&cnt->sh_unocc, tc.lit);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->rays_shadow += (unsigned long long)n;
 }
@@ -1104,12 +1116,16 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S
       int s = P.q_shadow[k];
       double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
       double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
-      if (!lw_trace_any<COUNT, NODES, (LW_SPEC_SMEM & 2) != 0>(bvh, o, d, e.x, &tc)) shadow_unoccluded<LPE>(P, s, e.y, lpe);
+      if (!lw_trace_any<COUNT, NODES, (LW_SPEC_SMEM & 2) != 0>(bvh, o, d, e.x, &tc)) {
+        shadow_unoccluded<LPE>(P, s, e.y, lpe);
+        if (COUNT) tc.lit++;
+      }
     }
   }
   if (COUNT) {
     warp_add(&cnt->sh_nodes, tc.nodes);
     warp_add(&cnt->sh_tris, tc.tris);
+    warp_add(&cnt->sh_unocc, tc.lit);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->rays_shadow += (unsigned long long)n;
 }
@@ -1161,6 +1177,105 @@ __global__ void k_trace_closest_dbg(DevScene S, const double* o, const double* d
   otri[i] = hit ? h.tri : -1;
   ob[2 * i] = hit ? h.bu : 0.0;
   ob[2 * i + 1] = hit ? h.bv : 0.0;
+}
+
+// ---- known-answer surface of the render math ----------------
+// BSDF evaluate / sample in the local shading frame (z = shading normal), layer weights from wo.z
+__global__ void k_bsdf_eval_dbg(lw_material m, const double* wo, const double* wi, long long n, double* of,
+                                double* op) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  v3 a = lw_ld3(wo + 3 * i), b = lw_ld3(wi + 3 * i);
+  LayerW lw;
+  lw_layer_weights(m, a.z, lw);
+  double pdf;
+  v3 f = lw_bsdf_eval(m, lw, a, b, pdf);
+  of[3 * i] = f.x;
+  of[3 * i + 1] = f.y;
+  of[3 * i + 2] = f.z;
+  op[i] = pdf;
+}
+
+__global__ void k_bsdf_sample_dbg(lw_material m, const double* wo, const int* front, const double* uv, long long n,
+                                  double* owi, double* ow, double* op, int* oflags) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  v3 a = lw_ld3(wo + 3 * i);
+  LayerW lw;
+  lw_layer_weights(m, a.z, lw);
+  BSample bs;
+  bs.wi = bs.weight = mk3(0.0, 0.0, 0.0);
+  bs.pdf = 0.0;
+  bs.delta = bs.transmit = bs.event = 0;
+  bool ok = lw_bsdf_sample(m, lw, a, front[i] != 0, uv[2 * i], uv[2 * i + 1], bs);
+  owi[3 * i] = bs.wi.x;
+  owi[3 * i + 1] = bs.wi.y;
+  owi[3 * i + 2] = bs.wi.z;
+  ow[3 * i] = bs.weight.x;
+  ow[3 * i + 1] = bs.weight.y;
+  ow[3 * i + 2] = bs.weight.z;
+  op[i] = bs.pdf;
+  oflags[i] = (ok ? 1 : 0) | (bs.delta ? 2 : 0) | (bs.transmit ? 4 : 0) | (bs.event << 8);
+}
+
+__global__ void k_mis_dbg(const double* a, const double* b, long long n, double* o) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) o[i] = lw_mis_balance(a[i], b[i]);
+}
+
+__global__ void k_nee_light_dbg(DevScene S, const double* p, const double* ngf, const double* uv, long long n,
+                                double* owi, double* oLe, double* opdf, double* otmax, long long* oe) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  v3 wi, Le;
+  double pl, tm;
+  long long e;
+  bool ok = lw_nee_light_sample(S, lw_ld3(p + 3 * i), lw_ld3(ngf + 3 * i), uv[2 * i], uv[2 * i + 1], nullptr, wi, Le,
+                                pl, tm, e);
+  owi[3 * i] = wi.x;
+  owi[3 * i + 1] = wi.y;
+  owi[3 * i + 2] = wi.z;
+  oLe[3 * i] = Le.x;
+  oLe[3 * i + 1] = Le.y;
+  oLe[3 * i + 2] = Le.z;
+  opdf[i] = ok ? pl : 0.0;
+  otmax[i] = tm;
+  oe[i] = e;
+}
+
+// what BSDF sampling sees along (o, d): emitted radiance and the light-sampling pdf MIS weighs it
+// against (emitter hit: lw_emitter_hit_pdf; miss: the environment's lw_env_eval); e = emitter,
+// -1 environment, -2 a non-emissive surface (pdf 0)
+__global__ void k_emission_pdf_dbg(DevScene S, const double* o, const double* d, const int* nprev, long long n,
+                                   double* oLe, double* opdf, long long* oe) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]}, dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  LwHit h;
+  lw_trace_closest(S.bvh, oo, dd, INFINITY, h);
+  v3 dv = mk3(dd[0], dd[1], dd[2]);
+  v3 Le = mk3(0.0, 0.0, 0.0);
+  double pdf = 0.0;
+  long long e = -2;
+  if (h.tri < 0) {
+    e = -1;
+    Le = lw_env_eval(S, dv, nprev[i], pdf);
+  } else {
+    ShadeGeom g;
+    double w;
+    lw_shade_hit(S, dv, h, g, w);
+    int k = S.emit_of_tri[h.tri];
+    if (k >= 0 && S.nemit > 0 && (g.front || S.emit_two[k])) {
+      e = k;
+      Le = lw_ld3(S.emit_rad + 3 * k);
+      pdf = lw_emitter_hit_pdf(S, k, mk3(oo[0], oo[1], oo[2]), nprev[i], g.ng, dv, h.t, nullptr);
+    }
+  }
+  oLe[3 * i] = Le.x;
+  oLe[3 * i + 1] = Le.y;
+  oLe[3 * i + 2] = Le.z;
+  opdf[i] = pdf;
+  oe[i] = e;
 }
 
 __global__ void k_trace_any_dbg(DevScene S, const double* o, const double* d, const double* tm, long long n, int* occ) {
@@ -1376,18 +1491,22 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       }
       return c->evpool[ev++];
     };
-    marks.clear();  // (event index of the start, 0 = ext / 1 = shadow)
+    marks.clear();  // (event index, stage starting there: LW_PROF_*)
+    auto mark = [&](int stage) {
+      if (!timed) return;
+      marks.push_back({ev, stage});
+      cudaEventRecord(event(), st);
+    };
     for (;;) {
       for (int k = 0; k < check_every; k++) {
+        mark(LW_PROF_OTHER);
         k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0);
+        mark(LW_PROF_GENERATE);
         if (lpe_on)
           k_generate<true><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
         else
           k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
-        if (timed) {
-          marks.push_back({ev, 0});
-          cudaEventRecord(event(), st);
-        }
+        mark(LW_PROF_TRACE_EXT);
         if (use_smem && (c->persist_mask & 4)) {
           if (count)
             k_trace_ext_p<true, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
@@ -1408,29 +1527,30 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
           else
             k_trace_ext<false, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         }
-        if (timed) cudaEventRecord(event(), st);
-        if (lpe_on && ltm) {
+        mark(LW_PROF_SHADE_NEE);
+        if (lpe_on && ltm)
           k_shade_nee<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-          k_shade<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        } else if (lpe_on) {
+        else if (lpe_on)
           k_shade_nee<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-          k_shade<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        } else if (ltm) {
+        else if (ltm)
           k_shade_nee<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-          k_shade<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        } else {
+        else
           k_shade_nee<false, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        mark(LW_PROF_SHADE);
+        if (lpe_on && ltm)
+          k_shade<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        else if (lpe_on)
+          k_shade<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        else if (ltm)
+          k_shade<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+        else
           k_shade<false, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        }
-        if (timed) {
-          marks.push_back({ev, 1});
-          cudaEventRecord(event(), st);
-        }
+        mark(LW_PROF_TRACE_SHADOW);
         if (use_smem)
           launch_shadow<LW_NODES_SMEM>(c, gT, smem, nr, lpe_on, count);
         else
           launch_shadow<LW_NODES_GLOBAL>(c, gT, smem, nr, lpe_on, count);
-        if (timed) cudaEventRecord(event(), st);
+        mark(LW_PROF_OTHER);
         k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 7;
         waves++;
@@ -1456,8 +1576,11 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       }
     }
     // flush the remaining finished paths
+    mark(LW_PROF_OTHER);
     k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1);
+    mark(LW_PROF_GENERATE);
     k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
+    mark(LW_PROF_END);
     launches += 2;
   }
   LW_CUDA_TRY(cudaGetLastError());
@@ -1472,17 +1595,22 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
   memset(&c->prof, 0, sizeof(c->prof));
   c->prof.total_ms = ms;
   c->prof.kernel_launches = launches;
-  for (auto& m : marks) {
+  // consecutive marks bracket one stage each; a stage's launch count is the number of its marks
+  for (size_t k = 0; k + 1 < marks.size(); k++) {
+    int sg = marks[k].second;
+    if (sg == LW_PROF_END) continue;
     float e = 0.f;
-    cudaEventElapsedTime(&e, c->evpool[m.first], c->evpool[m.first + 1]);
-    if (m.second == 0) {
-      c->prof.trace_ext_ms += e;
-      c->prof.trace_ext_launches++;
-    } else {
-      c->prof.trace_shadow_ms += e;
-      c->prof.trace_shadow_launches++;
-    }
+    cudaEventElapsedTime(&e, c->evpool[marks[k].first], c->evpool[marks[k + 1].first]);
+    c->prof.stage_ms[sg] += e;
+    if (sg != LW_PROF_OTHER) c->prof.stage_launches[sg]++;
   }
+  c->prof.trace_ext_ms = c->prof.stage_ms[LW_PROF_TRACE_EXT];
+  c->prof.trace_shadow_ms = c->prof.stage_ms[LW_PROF_TRACE_SHADOW];
+  c->prof.trace_ext_launches = c->prof.stage_launches[LW_PROF_TRACE_EXT];
+  c->prof.trace_shadow_launches = c->prof.stage_launches[LW_PROF_TRACE_SHADOW];
+  c->prof.pool_slots = c->pool.size;
+  c->prof.waves = (int64_t)h.waves;
+  c->prof.paths = (int64_t)h.paths;
   c->last_trace_ms = c->prof.trace_ext_ms + c->prof.trace_shadow_ms;
   c->prof.ext_rays = (int64_t)h.rays_ext;
   c->prof.shadow_rays = (int64_t)h.rays_shadow;
@@ -1490,6 +1618,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
   c->prof.ext_tris = (int64_t)h.ext_tris;
   c->prof.shadow_nodes = (int64_t)h.sh_nodes;
   c->prof.shadow_tris = (int64_t)h.sh_tris;
+  c->prof.shadow_unoccluded = (int64_t)h.sh_unocc;
   c->stats.paths += (int64_t)h.paths;
   c->stats.rays_extension += (int64_t)h.rays_ext;
   c->stats.rays_shadow += (int64_t)h.rays_shadow;
@@ -1552,9 +1681,128 @@ void give_res(const CtxRes& r) {
   if (r.ev1) cudaEventDestroy(r.ev1);
   if (r.stream) cudaStreamDestroy(r.stream);
 }
+// NCCL, resolved at first use with dlopen("libnccl.so.2"): in a PyTorch process this is the
+// library torch.distributed already loaded; the render library itself has no link-time NCCL
+// dependency (stateless kernels and single-GPU rendering never need it).
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*get_id)(ncclUniqueId*);
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*destroy)(ncclComm_t);
+  const char* (*err)(ncclResult_t);
+};
+
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.get_id = (ncclResult_t(*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+    api.init_rank = (ncclResult_t(*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+    api.all_reduce = (ncclResult_t(*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                      cudaStream_t))dlsym(h, "ncclAllReduce");
+    api.destroy = (ncclResult_t(*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+    api.err = (const char* (*)(ncclResult_t))dlsym(h, "ncclGetErrorString");
+    api.ok = api.get_id && api.init_rank && api.all_reduce && api.destroy && api.err;
+  });
+  return &api;
+}
+
+#define LW_NCCL_TRY(expr)                                                     \
+  do {                                                                        \
+    ncclResult_t _r = (expr);                                                 \
+    if (_r != ncclSuccess) {                                                  \
+      set_error("NCCL: %s (%s)", nccl_api()->err(_r), #expr);                 \
+      return LW_ERR_CUDA;                                                     \
+    }                                                                         \
+  } while (0)
+
+// progressive accumulation of a pass: dst += fb, fb = 0 (one read of each, one write of each)
+__global__ void k_fb_accumulate(unsigned long long* __restrict__ fb, unsigned long long* __restrict__ dst, long long n,
+                                int clear) {
+  long long n2 = n >> 1;
+  ulonglong2* f2 = reinterpret_cast<ulonglong2*>(fb);
+  ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n2; k += (long long)gridDim.x * blockDim.x) {
+    ulonglong2 a = f2[k], b = d2[k];
+    d2[k] = make_ulonglong2(a.x + b.x, a.y + b.y);
+    if (clear) f2[k] = make_ulonglong2(0ull, 0ull);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    dst[n - 1] += fb[n - 1];
+    if (clear) fb[n - 1] = 0ull;
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int lw_comm_unique_id(uint8_t* out) {
+  LW_CHECK_ARG(out, "null out");
+  NcclApi* api = nccl_api();
+  if (!api->ok) {
+    set_error("NCCL (libnccl.so.2) is not available");
+    return LW_ERR_STATE;
+  }
+  ncclUniqueId id;
+  LW_NCCL_TRY(api->get_id(&id));
+  static_assert(sizeof(ncclUniqueId) == LW_COMM_ID_BYTES, "ncclUniqueId size");
+  memcpy(out, &id, sizeof(id));
+  return LW_OK;
+}
+
+int lw_ctx_comm_init(lw_ctx* c, const uint8_t* id, int rank, int world) {
+  LW_CHECK_ARG(c && id && world >= 1 && rank >= 0 && rank < world, "bad communicator arguments");
+  NcclApi* api = nccl_api();
+  if (!api->ok) {
+    set_error("NCCL (libnccl.so.2) is not available");
+    return LW_ERR_STATE;
+  }
+  cudaSetDevice(c->device);
+  if (c->comm) {
+    api->destroy(c->comm);
+    c->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  LW_NCCL_TRY(api->init_rank(&c->comm, world, uid, rank));
+  c->comm_rank = rank;
+  c->comm_world = world;
+  return LW_OK;
+}
+
+int lw_framebuffer_reduce(lw_ctx* c) {
+  LW_CHECK_ARG(c && c->configured, "not configured");
+  if (!c->comm) {
+    set_error("lw_framebuffer_reduce: no communicator (lw_ctx_comm_init)");
+    return LW_ERR_STATE;
+  }
+  cudaSetDevice(c->device);
+  NcclApi* api = nccl_api();
+  LW_NCCL_TRY(api->all_reduce(c->d_fb, c->d_fb, (size_t)(3 * c->fb_pixels), ncclUint64, ncclSum, c->comm, c->stream));
+  if (c->lpe.nlayers > 0)
+    LW_NCCL_TRY(api->all_reduce(c->lpe.fb, c->lpe.fb, (size_t)(3 * c->lpe.npix * c->lpe.nlayers), ncclUint64, ncclSum,
+                                c->comm, c->stream));
+  return LW_OK;
+}
+
+int lw_framebuffer_accumulate(lw_ctx* c, void* dst, int clear) {
+  LW_CHECK_ARG(c && c->configured && dst, "bad arguments");
+  LW_CHECK_ARG(((uintptr_t)dst & 15) == 0, "accumulation buffer must be 16-byte aligned");
+  cudaSetDevice(c->device);
+  long long n = 3 * c->fb_pixels;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  long long need = ((n >> 1) + 255) / 256;
+  int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)nsm * 8));
+  k_fb_accumulate<<<grid, 256, 0, c->stream>>>(c->d_fb, (unsigned long long*)dst, n, clear);
+  LW_CUDA_TRY(cudaGetLastError());
+  return LW_OK;
+}
 
 int lw_ctx_create(int device, lw_ctx** out) {
   LW_CHECK_ARG(out, "null out");
@@ -1621,6 +1869,7 @@ int lw_ctx_destroy(lw_ctx* c) {
   if (c->d_qdims) cudaFreeAsync(c->d_qdims, c->stream);
   if (c->d_qperm) cudaFreeAsync(c->d_qperm, c->stream);
   cudaStreamSynchronize(c->stream);
+  if (c->comm) nccl_api()->destroy(c->comm);
   CtxRes r{c->device, c->own_stream, c->d_cnt, c->h_cnt, c->ev0, c->ev1};
   give_res(r);
   delete c;
@@ -1891,6 +2140,7 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   LW_CHECK_ARG(p->max_depth >= 1 && p->max_depth <= 255, "max_depth must be in [1, 255]");
   LW_CHECK_ARG(p->engine == LW_ENGINE_WAVEFRONT || p->engine == LW_ENGINE_MEGAKERNEL, "unknown engine");
   LW_CHECK_ARG(p->pool_log2 >= 10 && p->pool_log2 <= 26, "pool_log2 must be in [10, 26]");
+  LW_CHECK_ARG(p->estimator >= LW_EST_MIS && p->estimator <= LW_EST_BSDF, "unknown estimator");
   LW_CHECK_ARG(p->ndims >= 4 + 8 * (int64_t)p->max_depth, "dimension table too small for max_depth");
   cudaSetDevice(c->device);
   std::vector<QmcDim> dims;
@@ -1915,6 +2165,7 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   c->S.H = p->height;
   c->S.max_depth = p->max_depth;
   c->S.rr_start = p->rr_start;
+  c->S.estimator = p->estimator;
   int64_t px = (int64_t)p->width * p->height;
   if (px != c->fb_pixels) {
     free_lpe(c);  // layer framebuffers have the old size
@@ -2272,6 +2523,165 @@ int lw_ctx_lpe_download(lw_ctx* c, int32_t layer, int64_t* fb) {
   LW_CHECK_ARG(c && fb && layer >= 0 && layer < c->lpe.nlayers, "no such LPE layer");
   LW_CUDA_TRY(cudaMemcpyAsync(fb, c->lpe.fb + (size_t)layer * 3 * c->lpe.npix,
                               sizeof(int64_t) * 3 * c->lpe.npix, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_lpe_upload(lw_ctx* c, int32_t layer, const int64_t* fb) {
+  LW_CHECK_ARG(c && fb && layer >= 0 && layer < c->lpe.nlayers, "no such LPE layer");
+  LW_CUDA_TRY(cudaMemcpyAsync(c->lpe.fb + (size_t)layer * 3 * c->lpe.npix, fb, sizeof(int64_t) * 3 * c->lpe.npix,
+                              cudaMemcpyHostToDevice, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+// ---- known-answer surface of the render math ----------------------------------------------------
+
+}  // extern "C"
+
+namespace {
+struct DbgIO {  // device copies of host inputs / outputs of one debug call, on one stream
+  cudaStream_t st;
+  std::vector<DevBuf*> bufs;
+  explicit DbgIO(cudaStream_t s) : st(s) {}
+  ~DbgIO() {
+    for (DevBuf* b : bufs) delete b;
+  }
+  template <class T>
+  T* in(const void* host, size_t bytes) {
+    DevBuf* b = new DevBuf();
+    bufs.push_back(b);
+    if (b->alloc(bytes, st) != cudaSuccess) return nullptr;
+    if (cudaMemcpyAsync(b->p, host, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) return nullptr;
+    return (T*)b->p;
+  }
+  template <class T>
+  T* out(size_t bytes) {
+    DevBuf* b = new DevBuf();
+    bufs.push_back(b);
+    if (b->alloc(bytes, st) != cudaSuccess) return nullptr;
+    return (T*)b->p;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+#define LW_DBG_PTR(p)                                \
+  do {                                               \
+    if (!(p)) {                                      \
+      set_error("debug call: device buffer failed"); \
+      return LW_ERR_NOMEM;                           \
+    }                                                \
+  } while (0)
+
+int lw_bsdf_eval_batch(const lw_material* m, const double* wo, const double* wi, int64_t n, double* out_f,
+                       double* out_pdf) {
+  LW_CHECK_ARG(m && wo && wi && out_f && out_pdf && n >= 0, "bad arguments");
+  LW_CHECK_ARG(m->nlayers >= 0 && m->nlayers <= LW_MAX_LAYERS, "bad material");
+  if (n == 0) return LW_OK;
+  cudaStream_t st = cudaStreamPerThread;
+  DbgIO io(st);
+  const double* a = io.in<double>(wo, sizeof(double) * 3 * n);
+  const double* b = io.in<double>(wi, sizeof(double) * 3 * n);
+  double* f = io.out<double>(sizeof(double) * 3 * n);
+  double* p = io.out<double>(sizeof(double) * n);
+  LW_DBG_PTR(a && b && f && p);
+  k_bsdf_eval_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(*m, a, b, n, f, p);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_f, f, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_pdf, p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_bsdf_sample_batch(const lw_material* m, const double* wo, const int32_t* front, const double* uv, int64_t n,
+                         double* out_wi, double* out_weight, double* out_pdf, int32_t* out_flags) {
+  LW_CHECK_ARG(m && wo && front && uv && out_wi && out_weight && out_pdf && out_flags && n >= 0, "bad arguments");
+  LW_CHECK_ARG(m->nlayers >= 0 && m->nlayers <= LW_MAX_LAYERS, "bad material");
+  if (n == 0) return LW_OK;
+  cudaStream_t st = cudaStreamPerThread;
+  DbgIO io(st);
+  const double* a = io.in<double>(wo, sizeof(double) * 3 * n);
+  const int* fr = io.in<int>(front, sizeof(int32_t) * n);
+  const double* u = io.in<double>(uv, sizeof(double) * 2 * n);
+  double* wi = io.out<double>(sizeof(double) * 3 * n);
+  double* w = io.out<double>(sizeof(double) * 3 * n);
+  double* p = io.out<double>(sizeof(double) * n);
+  int* fl = io.out<int>(sizeof(int32_t) * n);
+  LW_DBG_PTR(a && fr && u && wi && w && p && fl);
+  k_bsdf_sample_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(*m, a, fr, u, n, wi, w, p, fl);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_wi, wi, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_weight, w, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_pdf, p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_flags, fl, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_mis_weight_batch(const double* pdf_a, const double* pdf_b, int64_t n, double* out) {
+  LW_CHECK_ARG(pdf_a && pdf_b && out && n >= 0, "bad arguments");
+  if (n == 0) return LW_OK;
+  cudaStream_t st = cudaStreamPerThread;
+  DbgIO io(st);
+  const double* a = io.in<double>(pdf_a, sizeof(double) * n);
+  const double* b = io.in<double>(pdf_b, sizeof(double) * n);
+  double* o = io.out<double>(sizeof(double) * n);
+  LW_DBG_PTR(a && b && o);
+  k_mis_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(a, b, n, o);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out, o, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  return LW_OK;
+}
+
+int lw_ctx_nee_light_sample(lw_ctx* c, const double* p, const double* ngf, const double* uv, int64_t n, double* out_wi,
+                            double* out_le, double* out_pdf, double* out_tmax, int64_t* out_emitter) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  LW_CHECK_ARG(p && ngf && uv && out_wi && out_le && out_pdf && out_tmax && out_emitter && n >= 0, "bad arguments");
+  if (n == 0) return LW_OK;
+  cudaSetDevice(c->device);
+  DbgIO io(c->stream);
+  const double* dp = io.in<double>(p, sizeof(double) * 3 * n);
+  const double* dn = io.in<double>(ngf, sizeof(double) * 3 * n);
+  const double* du = io.in<double>(uv, sizeof(double) * 2 * n);
+  double* wi = io.out<double>(sizeof(double) * 3 * n);
+  double* le = io.out<double>(sizeof(double) * 3 * n);
+  double* pd = io.out<double>(sizeof(double) * n);
+  double* tm = io.out<double>(sizeof(double) * n);
+  long long* em = io.out<long long>(sizeof(int64_t) * n);
+  LW_DBG_PTR(dp && dn && du && wi && le && pd && tm && em);
+  k_nee_light_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, c->stream>>>(c->S, dp, dn, du, n, wi, le, pd, tm, em);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_wi, wi, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_le, le, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_pdf, pd, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_tmax, tm, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_emitter, em, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LW_OK;
+}
+
+int lw_ctx_emission_pdf(lw_ctx* c, const double* o, const double* d, const int32_t* nprev, int64_t n, double* out_le,
+                        double* out_pdf, int64_t* out_emitter) {
+  LW_CHECK_ARG(c && c->has_scene, "no scene");
+  LW_CHECK_ARG(o && d && nprev && out_le && out_pdf && out_emitter && n >= 0, "bad arguments");
+  if (n == 0) return LW_OK;
+  cudaSetDevice(c->device);
+  DbgIO io(c->stream);
+  const double* dO = io.in<double>(o, sizeof(double) * 3 * n);
+  const double* dD = io.in<double>(d, sizeof(double) * 3 * n);
+  const int* dN = io.in<int>(nprev, sizeof(int32_t) * n);
+  double* le = io.out<double>(sizeof(double) * 3 * n);
+  double* pd = io.out<double>(sizeof(double) * n);
+  long long* em = io.out<long long>(sizeof(int64_t) * n);
+  LW_DBG_PTR(dO && dD && dN && le && pd && em);
+  k_emission_pdf_dbg<<<grid_for(n, 128, 1 << 30), 128, 0, c->stream>>>(c->S, dO, dD, dN, n, le, pd, em);
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaMemcpyAsync(out_le, le, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_pdf, pd, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  LW_CUDA_TRY(cudaMemcpyAsync(out_emitter, em, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
   LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return LW_OK;
 }

@@ -336,7 +336,7 @@ __device__ __forceinline__ void lw_load_tri(const LTri* __restrict__ p, double v
 // work counters of the instrumented instantiation (node = one 128-byte node fetch,
 // tri = one 80-byte triangle test)
 struct LwTraceCount {
-  unsigned nodes = 0, tris = 0;
+  unsigned nodes = 0, tris = 0, lit = 0;  // lit: shadow rays that reached their light
 };
 
 __device__ __forceinline__ unsigned long long lw_stk_pack(int ref, float tn) {

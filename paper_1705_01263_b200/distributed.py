@@ -14,6 +14,8 @@ import os
 
 import numpy as np
 
+LW_COMM_ID_BYTES = 128  # include/lw_b200.h (the NCCL unique id)
+
 
 def partition_iterations(it_begin: int, it_end: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous block of [it_begin, it_end) for `rank` of `world` (sizes differ by at most one)."""
@@ -57,9 +59,10 @@ class DistributedRenderer:
     The GPU path wires these to `render.Renderer`; the CPU tests wire them to the oracle.
     """
 
-    def __init__(self, render_fn, fetch_fb, rank: int, world: int, group=None):
+    def __init__(self, render_fn, fetch_fb, rank: int, world: int, group=None, reduce: bool = True):
         self.render_fn, self.fetch_fb = render_fn, fetch_fb
         self.rank, self.world, self.group = rank, world, group
+        self.reduce = reduce  # False: fetch_fb already returns the reduced framebuffer
 
     def run_pass(self, it_begin: int, it_end: int):
         a, b = partition_iterations(it_begin, it_end, self.rank, self.world)
@@ -69,21 +72,49 @@ class DistributedRenderer:
 
     def reduced(self):
         fb = self.fetch_fb()
+        if not self.reduce:
+            return fb
         return reduce_framebuffer(fb, self.group)
 
 
-def gpu_distributed_renderer(renderer, rank, world, group=None):
-    """DistributedRenderer over a GPU `render.Renderer` (framebuffer copied D2D into a torch tensor)."""
+def gpu_distributed_renderer(renderer, rank, world, group=None, backend="nccl"):
+    """DistributedRenderer over a GPU `render.Renderer`; `reduced()` returns the summed int64
+    framebuffer (H*W, 3) as a host numpy array.
+
+    backend="nccl": the library's own communicator (lw_ctx_comm_init; the unique id is broadcast
+    over `group`), an in-place all-reduce of the device framebuffer on the context's stream
+    (lw_framebuffer_reduce) -- the path for one process per GPU.
+    backend="gloo": framebuffer downloaded and summed over a gloo group on the host -- for several
+    processes sharing one GPU (NCCL cannot put two ranks on one device) and CPU-only tests."""
     import torch
+    import torch.distributed as dist
 
-    dev = torch.device("cuda", renderer.device)
-    buf = torch.empty((renderer.params.pixels, 3), dtype=torch.int64, device=dev)
+    if backend == "nccl":
+        if world > 1:
+            uid = torch.zeros(LW_COMM_ID_BYTES, dtype=torch.uint8)
+            if rank == 0:
+                uid[:] = torch.frombuffer(bytearray(renderer.comm_unique_id()), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                uid = uid.to(torch.device("cuda", renderer.device))
+            dist.broadcast(uid, src=0, group=group)
+            renderer.comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
 
-    def fetch():
-        renderer.copy_framebuffer_to(buf.data_ptr())
-        return buf
+        def fetch():
+            if world > 1:
+                renderer.reduce_framebuffer()
+            return renderer.framebuffer()  # synchronises the context stream
 
-    return DistributedRenderer(lambda a, b: renderer.render_pass(a, b), fetch, rank, world, group)
+        return DistributedRenderer(lambda a, b: renderer.render_pass(a, b), fetch, rank, world, group,
+                                   reduce=False)
+    if backend == "gloo":
+        def fetch_host():
+            t = torch.from_numpy(renderer.framebuffer())
+            reduce_framebuffer(t, group)
+            return t.numpy()
+
+        return DistributedRenderer(lambda a, b: renderer.render_pass(a, b), fetch_host, rank, world, group,
+                                   reduce=False)
+    raise ValueError("backend must be 'nccl' or 'gloo'")
 
 
 def fb_to_image(fb: np.ndarray, width: int, height: int, samples: int) -> np.ndarray:

@@ -18,6 +18,7 @@ from paper_1705_01263_b200.qmc import DimensionTable
 from paper_1705_01263_b200.scene import pack_scene
 
 ENGINES = {"wavefront": _abi.LW_ENGINE_WAVEFRONT, "megakernel": _abi.LW_ENGINE_MEGAKERNEL}
+ESTIMATORS = {"mis": _abi.LW_EST_MIS, "nee": _abi.LW_EST_NEE, "bsdf": _abi.LW_EST_BSDF}
 FB_SCALE = float(1 << _abi.LW_FB_FRAC_BITS)
 
 
@@ -25,9 +26,11 @@ class RenderParams:
     """Resolution, depth, QMC dimension table and engine knobs (LwRenderParams + owned arrays)."""
 
     def __init__(self, width, height, max_depth=8, rr_start=4, engine="wavefront", pool_log2=24,
-                 regen_fraction=0.5, megakernel_tail=0):
+                 regen_fraction=0.5, megakernel_tail=0, estimator="mis"):
         if engine not in ENGINES:
             raise ValueError(f"unknown engine '{engine}'")
+        if estimator not in ESTIMATORS:
+            raise ValueError(f"unknown estimator '{estimator}' (mis, nee, bsdf)")
         self.width, self.height, self.max_depth = int(width), int(height), int(max_depth)
         self.table = DimensionTable(max(self.max_depth, 1))
         self.bases = np.ascontiguousarray(self.table.bases, dtype=np.int64)
@@ -44,6 +47,7 @@ class RenderParams:
         s.pool_log2 = int(pool_log2)
         s.regen_fraction = float(regen_fraction)
         s.megakernel_tail = int(megakernel_tail)
+        s.estimator = ESTIMATORS[estimator]
         self.struct = s
         self.engine = engine
 
@@ -56,11 +60,11 @@ class Renderer:
     """Progressive renderer on one GPU."""
 
     def __init__(self, scene, width, height, max_depth=8, device=0, engine="wavefront", p_env=0.5, rr_start=4,
-                 pool_log2=24, regen_fraction=0.5, megakernel_tail=0, packed=None):
+                 pool_log2=24, regen_fraction=0.5, megakernel_tail=0, packed=None, estimator="mis"):
         self.lib = _abi.lib()
         self.packed = packed if packed is not None else pack_scene(scene, p_env=p_env)
         self.params = RenderParams(width, height, max_depth, rr_start, engine, pool_log2, regen_fraction,
-                                   megakernel_tail)
+                                   megakernel_tail, estimator)
         self.device = int(device)
         h = C.c_void_p()
         check(self.lib.lw_ctx_create(self.device, C.byref(h)))
@@ -124,29 +128,91 @@ class Renderer:
 
     # -- checkpoint / resume (progressive state = int64 framebuffer + iteration count)
     def _fingerprint(self) -> str:
+        """Hash of everything that determines the image: every scene array (geometry, materials,
+        emitters, environment), every scalar of the scene description (camera, environment
+        constants and scale, p_env, BVH and sampler choices) and the render parameters that change
+        samples (resolution, depth, Russian-roulette start, QMC tables).  Engine knobs (engine,
+        pool size, regeneration, megakernel tail) are left out: the image does not depend on them."""
         import hashlib
 
         h = hashlib.sha256()
-        for k in ("verts", "normals", "material", "emit_tri", "emit_rad"):
-            a = self.packed.arrays.get(k)
+        for k in sorted(self.packed.arrays):
+            a = self.packed.arrays[k]
             if isinstance(a, np.ndarray):
-                h.update(np.ascontiguousarray(a).tobytes())
+                h.update(k.encode() + np.ascontiguousarray(a).tobytes())
+            elif isinstance(a, C.Array):  # packed lw_material records
+                h.update(k.encode() + bytes(a))
+        d = self.packed.desc
+        for name, ctype in d._fields_:
+            if issubclass(ctype, (C._Pointer, C.c_void_p)):
+                continue
+            v = getattr(d, name)
+            h.update(f"{name}={list(v) if isinstance(v, C.Array) else v!r};".encode())
         p = self.params
-        h.update(f"{p.width}x{p.height}d{p.max_depth}".encode())
+        s = p.struct
+        h.update(f"{s.width}x{s.height}d{s.max_depth}rr{s.rr_start}e{s.estimator}".encode())
+        for a in (p.bases, p.perm_flat, p.perm_offset):
+            h.update(a.tobytes())
         return h.hexdigest()
 
     def save_checkpoint(self, path):
-        """Framebuffer + progressive state; load_checkpoint on a renderer of the same scene and
-        parameters continues the render bit-identically (int64 accumulation)."""
-        np.savez(path, fb=self.framebuffer(), iterations=self.iterations, fingerprint=self._fingerprint())
+        """Framebuffer + progressive state (+ the LPE layer framebuffers and their expressions);
+        load_checkpoint on a renderer of the same scene and parameters continues the render
+        bit-identically (int64 accumulation)."""
+        extra = {}
+        if getattr(self, "lpe", None):
+            extra["layer_names"] = np.array(self.lpe.names)
+            extra["layer_exprs"] = np.array([self.lpe_exprs[n] for n in self.lpe.names])
+            for k, fb in enumerate(self.layer_framebuffers().values()):
+                extra[f"layer_fb_{k}"] = fb
+        np.savez(path, fb=self.framebuffer(), iterations=self.iterations, fingerprint=self._fingerprint(), **extra)
 
     def load_checkpoint(self, path):
+        """Restore a checkpoint.  A checkpoint with LPE layers restores them too (the expressions
+        must equal the layers already set on this renderer, if any); one without layers is refused
+        by a renderer that has layers (their framebuffers would start from zero while the beauty
+        does not)."""
         z = np.load(path)
         if str(z["fingerprint"]) != self._fingerprint():
-            raise ValueError("checkpoint belongs to a different scene or resolution/depth")
+            raise ValueError("checkpoint belongs to a different scene, camera, material set, environment or "
+                             "resolution/depth")
+        saved = dict(zip([str(x) for x in z["layer_names"]], [str(x) for x in z["layer_exprs"]])) \
+            if "layer_names" in z.files else {}
+        have = dict(getattr(self, "lpe_exprs", None) or {}) if getattr(self, "lpe", None) else {}
+        if have and have != saved:
+            raise ValueError("checkpoint LPE layers differ from this renderer's layers")
+        if saved and not have:
+            self.set_lpe_layers(saved)
         fb = np.ascontiguousarray(z["fb"], np.int64)
         check(self.lib.lw_framebuffer_upload(self.ctx, ptr(fb, C.c_int64)))
+        for k in range(len(saved)):
+            lf = np.ascontiguousarray(z[f"layer_fb_{k}"], np.int64)
+            check(self.lib.lw_ctx_lpe_upload(self.ctx, k, ptr(lf, C.c_int64)))
         self.iterations = int(z["iterations"])
+
+    def accumulate_into(self, device_ptr: int, clear: bool = True):
+        """dst (caller-owned device int64 (H*W, 3), 16-byte aligned) += framebuffer, and zero the
+        framebuffer for the next pass (clear=True): one asynchronous kernel on the context stream."""
+        check(self.lib.lw_framebuffer_accumulate(self.ctx, C.c_void_p(device_ptr), int(bool(clear))))
+
+    # -- sample-space partition across GPUs (PAPER.md:779-817): NCCL inside the library
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """New NCCL unique id (create on rank 0, broadcast to the others)."""
+        buf = (C.c_uint8 * _abi.LW_COMM_ID_BYTES)()
+        check(_abi.lib().lw_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, rank: int, world: int):
+        """Join the communicator `uid` as `rank` of `world` (one context per GPU and process)."""
+        if len(uid) != _abi.LW_COMM_ID_BYTES:
+            raise ValueError(f"communicator id must be {_abi.LW_COMM_ID_BYTES} bytes")
+        buf = (C.c_uint8 * _abi.LW_COMM_ID_BYTES).from_buffer_copy(uid)
+        check(self.lib.lw_ctx_comm_init(self.ctx, buf, int(rank), int(world)))
+
+    def reduce_framebuffer(self):
+        """Sum the pass framebuffers of all ranks in place (NCCL all-reduce on the context stream)."""
+        check(self.lib.lw_framebuffer_reduce(self.ctx))
 
     def copy_framebuffer_to(self, device_ptr: int):
         check(self.lib.lw_framebuffer_copy_device(self.ctx, C.c_void_p(device_ptr)))
@@ -210,6 +276,7 @@ class Renderer:
         if not layers:
             check(self.lib.lw_ctx_set_lpe(self.ctx, 0, 0, None, None, 0))
             self.lpe = None
+            self.lpe_exprs = None
             return None
         t = compile_layers(layers)
         tr = np.ascontiguousarray(t.trans, np.int16)
@@ -217,6 +284,7 @@ class Renderer:
         check(self.lib.lw_ctx_set_lpe(self.ctx, len(t.names), len(tr), ptr(tr, C.c_int16), ptr(ac, C.c_uint8),
                                       int(t.start)))
         self.lpe = t
+        self.lpe_exprs = dict(layers)
         return t
 
     def layer_framebuffers(self) -> dict:
@@ -293,6 +361,41 @@ class Renderer:
         p = np.empty(len(pk))
         check(self.lib.lw_ctx_env_pdf(self.ctx, ptr(pk, C.c_int64), ptr(tx, C.c_int64), len(pk), ptr(p, C.c_double)))
         return p
+
+    # -- known-answer surface of the light sampling
+    def nee_light_sample(self, points, facing_normals, uv):
+        """Light half of NEE at points with facing geometric normals for NEE uniforms uv [n,2]:
+        dict of wi, radiance, pdf (solid angle, selection included; 0 = no light), shadow tmax,
+        emitter (-1 = environment)."""
+        p = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        nrm = np.ascontiguousarray(facing_normals, np.float64).reshape(-1, 3)
+        uv = np.ascontiguousarray(uv, np.float64).reshape(-1, 2)
+        n = len(uv)
+        if len(p) == 1 and n > 1:
+            p = np.ascontiguousarray(np.repeat(p, n, axis=0))
+        if len(nrm) == 1 and n > 1:
+            nrm = np.ascontiguousarray(np.repeat(nrm, n, axis=0))
+        wi, le, pdf, tm, e = np.empty((n, 3)), np.empty((n, 3)), np.empty(n), np.empty(n), np.empty(n, np.int64)
+        check(self.lib.lw_ctx_nee_light_sample(self.ctx, ptr(p, C.c_double), ptr(nrm, C.c_double),
+                                               ptr(uv, C.c_double), n, ptr(wi, C.c_double), ptr(le, C.c_double),
+                                               ptr(pdf, C.c_double), ptr(tm, C.c_double), ptr(e, C.c_int64)))
+        return {"wi": wi, "radiance": le, "pdf": pdf, "tmax": tm, "emitter": e}
+
+    def emission_pdf(self, origins, dirs, nprev=None):
+        """What BSDF sampling meets along (o, d): radiance, the light-sampling pdf MIS weighs it
+        against (nprev: packed facing normal of the vertex the ray leaves) and the emitter
+        (-1 = environment, -2 = non-emissive surface)."""
+        o = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
+        d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+        n = len(d)
+        if len(o) == 1 and n > 1:
+            o = np.ascontiguousarray(np.repeat(o, n, axis=0))
+        npv = np.zeros(n, np.int32) if nprev is None else np.ascontiguousarray(  # packed normals are 32-bit patterns
+            np.broadcast_to((np.asarray(nprev, np.int64) & 0xFFFFFFFF).astype(np.uint32).view(np.int32), (n,)))
+        le, pdf, e = np.empty((n, 3)), np.empty(n), np.empty(n, np.int64)
+        check(self.lib.lw_ctx_emission_pdf(self.ctx, ptr(o, C.c_double), ptr(d, C.c_double), ptr(npv, C.c_int32), n,
+                                           ptr(le, C.c_double), ptr(pdf, C.c_double), ptr(e, C.c_int64)))
+        return {"radiance": le, "pdf": pdf, "emitter": e}
 
     def camera_rays(self, sample_index):
         idx = np.ascontiguousarray(sample_index, np.int64)

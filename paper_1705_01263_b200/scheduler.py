@@ -160,14 +160,16 @@ class IterationLedger:
             d.merges += 1
             d.merging = False
 
-    def fail(self, w: int) -> list[int]:
-        """Device failure: its unmerged iterations are lost and re-queued exactly once."""
+    def fail(self, w: int, in_flight: list[int] | None = None) -> list[int]:
+        """Device failure: its unmerged iterations -- and `in_flight`, iterations it was assigned
+        but had not reported rendered (a device that raised mid-pass) -- are lost and re-queued
+        exactly once."""
         with self.lock:
             p = self.profiles[w]
             if not p.alive:
                 return []
             p.alive = False
-            lost = sorted(self.dev[w].unmerged)
+            lost = sorted(set(self.dev[w].unmerged) | set(in_flight or []))
             self.dev[w].unmerged = []
             self.requeue.extend(lost)
             self.requeue.sort()
@@ -198,6 +200,7 @@ class BatchScheduler:
         self.master_lock = threading.Lock()
         self.ledger = None
         self.errors: list[BaseException] = []
+        self.abort = threading.Event()  # set when the run cannot finish (every device failed)
 
     @staticmethod
     def _runs(its: list[int]):
@@ -217,15 +220,18 @@ class BatchScheduler:
             if self.master is None:
                 self.master = np.zeros_like(fb)
             self.master += fb
+            # recorded as merged before the local clear: if clear() raises, the failure path
+            # must not re-queue iterations the master already holds
+            self.ledger.end_merge(w, its)
         dev.clear()
-        self.ledger.end_merge(w, its)
 
     def _worker(self, prof: WorkerProfile):
         w = prof.worker
+        in_flight: list[int] = []  # assigned, not yet reported rendered
         try:
             dev = self.make_device(w)
             try:
-                while not self.ledger.done():
+                while not self.ledger.done() and not self.abort.is_set():
                     if not self.ledger.profiles[w].alive:
                         return
                     its = self.ledger.assign_iteration_set(w)
@@ -235,6 +241,7 @@ class BatchScheduler:
                             continue
                         time.sleep(0.001)  # others still merging / may fail and re-queue
                         continue
+                    in_flight = its
                     t = time.perf_counter()
                     for a, b in self._runs(its):
                         dev.render_pass(a, b)
@@ -243,20 +250,26 @@ class BatchScheduler:
                         time.sleep(dt * (1.0 / prof.speed - 1.0))
                         dt = dt / prof.speed
                     self.ledger.rendered(w, its, max(dt, 1e-9))
+                    in_flight = []
                     if prof.fail_after is not None and self.ledger.dev[w].rendered >= prof.fail_after:
                         self.ledger.fail(w)  # local framebuffer (unmerged work) is lost
                         dev.clear()
                         return
                     if self.ledger.should_merge(w):
                         self._merge(w, dev)
-                if self.ledger.dev[w].unmerged:
+                if self.ledger.dev[w].unmerged and not self.abort.is_set():
                     self._merge(w, dev)
             finally:
                 close = getattr(dev, "close", None)
                 if close:
                     close()
-        except BaseException as e:  # surfaced by run()
+        except BaseException as e:  # a real device error: fail the device, re-queue its work
             self.errors.append(e)
+            try:
+                self.ledger.fail(w, in_flight)
+            except SchedulerError as e2:  # no device left to finish the range
+                self.errors.append(e2)
+                self.abort.set()
 
     def run(self, it_begin: int, it_end: int) -> np.ndarray:
         """Master int64 framebuffer holding every iteration of the range exactly once."""
@@ -268,13 +281,14 @@ class BatchScheduler:
                                       cap=self.cap)
         self.master = None
         self.errors = []
+        self.abort.clear()
         threads = [threading.Thread(target=self._worker, args=(p,), daemon=True) for p in self.profiles]
         for t in threads:
             t.start()
         for t in threads:
             t.join()
-        if self.errors:
-            raise self.errors[0]
+        if self.abort.is_set() or (self.errors and not self.ledger.done()):
+            raise self.errors[-1] if self.errors else SchedulerError("render aborted")
         if not self.ledger.done():
             raise SchedulerError("not every iteration was merged")
         m = self.ledger

@@ -180,18 +180,6 @@ def test_white_furnace(gpu):
     assert abs(float(img.mean()) - 1.0) < 0.01
 
 
-def test_nee_and_bsdf_agree_single_light(gpu):
-    """Cornell image is stable between two disjoint sample sets (estimator sanity, 3 sigma)."""
-    packed = pack_scene(scenes.cornell())
-    with _renderer(packed, 32, 32, 4) as r:
-        r.render_pass(0, 64)
-        a = r.image().astype(np.float64)
-        r.clear()
-        r.render_pass(64, 128)
-        b = r.image().astype(np.float64)
-    assert abs(a.mean() - b.mean()) / a.mean() < 0.03
-
-
 @pytest.mark.parametrize("n", [1, 5, 8, 100, 4097, 70000])
 def test_gpu_sah_tree_traversal_matches_oracle(gpu, oracle, n):
     """The device-built SAH tree and the oracle's sequential restatement give identical hits on

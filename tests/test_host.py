@@ -193,7 +193,7 @@ def test_struct_layouts_match_header():
 
     assert C.sizeof(_abi.LwLayer) == 48
     assert C.sizeof(_abi.LwMaterial) == 8 + 4 * 48 + 8
-    assert C.sizeof(_abi.LwRenderParams) == 4 * 4 + 8 * 5 + 4 * 2 + 8 + 8
+    assert C.sizeof(_abi.LwRenderParams) == 4 * 4 + 8 * 5 + 4 * 2 + 8 + 8 + 8  # estimator (+4 padding)
 
 
 def test_product_never_imports_oracle():

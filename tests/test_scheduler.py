@@ -115,3 +115,46 @@ def test_cli_batch_with_failure_matches_single(gpu, tmp_path):
     assert cli.main(["render", "--config", "C1", "--res", "32x32", "--iterations", "12", "--out", b,
                      "--contexts-per-device", "3", "--fail", "1@2", "--metrics", str(tmp_path / "m.json")]) == 0
     assert (read_pfm(a + "_000012.pfm") == read_pfm(b + "_000012.pfm")).all()
+
+
+class RaisingDevice(FakeDevice):
+    """Raises inside render_pass after `after` iterations (a CUDA error / OOM mid-pass); the
+    iterations it half-rendered stay in its local framebuffer and must never reach the master."""
+
+    def __init__(self, after):
+        super().__init__()
+        self.after = after
+        self.count = 0
+
+    def render_pass(self, a, b):
+        for i in range(a, b):
+            if self.count >= self.after:
+                raise RuntimeError("simulated device error")
+            self.fb += _contrib(i)
+            self.count += 1
+
+
+@pytest.mark.timeout(60)
+def test_device_error_requeues_in_flight_work():
+    # worker 1 raises mid-pass: its assigned-but-unreported iterations are re-queued exactly once and
+    # the other workers finish the range; the image equals the single-device one bit for bit
+    class Slow(FakeDevice):  # keeps the healthy devices busy long enough for device 1 to fail
+        def render_pass(self, a, b):
+            import time
+
+            time.sleep(0.002)
+            super().render_pass(a, b)
+
+    devs = {0: lambda: Slow(), 1: lambda: RaisingDevice(2), 2: lambda: Slow()}
+    sch = BatchScheduler(lambda w: devs[w](), [WorkerProfile(k) for k in range(3)], cap=4)
+    fb = sch.run(0, 1500)
+    assert np.array_equal(fb, _expected(0, 1500))
+    assert any(isinstance(e, RuntimeError) for e in sch.errors)
+    assert not sch.ledger.profiles[1].alive
+
+
+@pytest.mark.timeout(60)
+def test_every_device_erroring_raises_instead_of_hanging():
+    sch = BatchScheduler(lambda w: RaisingDevice(3), [WorkerProfile(k) for k in range(2)], cap=4)
+    with pytest.raises((SchedulerError, RuntimeError)):
+        sch.run(0, 100)
