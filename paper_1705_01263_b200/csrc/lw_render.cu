@@ -536,91 +536,73 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
 }
 
 // pool order: flush TERMINATED slots, refill free slots with new (iteration, pixel) samples and
-// compact TRACE slots into the extension queue.  Each block owns a contiguous slot range: a
-// counting pass over the stage bytes sizes its claims, so the whole block takes its work items
-// and its queue segment with two global atomics, and the writing pass assigns items and queue
-// positions in slot order from block prefixes (one barrier per 256 slots).  The generated
-// samples form the first `granted` free slots of the range, so the queue prefix of a lane is
-// trace_prefix + min(want_prefix, granted_left).
+// compact TRACE slots into the extension queue.  Each WARP owns a contiguous slot range (no block
+// barriers): a counting pass reads the range's stage bytes 16 at a time (one 16-byte load per
+// lane) and sizes the warp's claims, which it takes with two atomics (work items, queue segment);
+// the writing pass walks the range 32 slots per round (lane = slot, coalesced), assigning items
+// and queue positions in slot order from ballot prefixes.  The generated samples are the first
+// `granted` free slots of the range, so a lane's queue offset is trace_prefix + min(want_prefix,
+// granted_left).  (Block-granular with a barrier per 256 slots, this scan cost ~170 us per wave on
+// C2 even when nothing was left to do; the per-warp form is bound by the stage-byte reads.)
 template <bool LPE>
 __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
                                                   Counters* __restrict__ cnt, LwLpe lpe) {
-  __shared__ int wc[2][8][2];  // per-warp (want, trace) counts, double-buffered by iteration parity
-  __shared__ long long s_wbase;
-  __shared__ int s_ebase, s_red[8][2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const bool regen = cnt->regen_now != 0;
   const long long total = w.nits * w.npix;
-  const int per = (int)(((long long)P.size + (long long)gridDim.x * 256 - 1) / ((long long)gridDim.x * 256)) * 256;
-  const int r0 = (int)min((long long)blockIdx.x * per, (long long)P.size);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int per = (int)((((long long)P.size + nwarps * 512 - 1) / (nwarps * 512)) * 512);
+  const int r0 = (int)min(gwarp * per, (long long)P.size);
   const int r1 = min(r0 + per, P.size);
-  // pass 1: sizes of the claims
+  if (r0 >= r1) return;  // warp-uniform
+  // pass 1: sizes of the claims (16 stage bytes per lane per load; ranges are multiples of 512)
   int c_want = 0, c_trace = 0;
-  for (int s = r0 + threadIdx.x; s < r1; s += 256) {
-    int st = P.stage[s];
-    if (regen && st != LW_STAGE_TRACE) c_want++;
-    else if (st == LW_STAGE_TRACE) c_trace++;
+  for (int s = r0 + 16 * lane; s < r1; s += 512) {
+    uint4 v = *reinterpret_cast<const uint4*>(P.stage + s);
+    unsigned wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      unsigned b = (wd[k >> 2] >> (8 * (k & 3))) & 0xffu;
+      c_trace += b == LW_STAGE_TRACE ? 1 : 0;
+      c_want += (regen && b != LW_STAGE_TRACE) ? 1 : 0;
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    c_want += __shfl_down_sync(0xffffffffu, c_want, off);
-    c_trace += __shfl_down_sync(0xffffffffu, c_trace, off);
+    c_want += __shfl_xor_sync(0xffffffffu, c_want, off);
+    c_trace += __shfl_xor_sync(0xffffffffu, c_trace, off);
   }
+  long long wb = 0;
+  int eb = 0, granted = 0;
   if (lane == 0) {
-    s_red[warp][0] = c_want;
-    s_red[warp][1] = c_trace;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int want = 0, trace = 0;
-    for (int k = 0; k < 8; k++) {
-      want += s_red[k][0];
-      trace += s_red[k][1];
-    }
-    long long wb = want ? (long long)atomicAdd(&cnt->work_next, (unsigned long long)want) : 0;
+    wb = c_want ? (long long)atomicAdd(&cnt->work_next, (unsigned long long)c_want) : 0;
     long long left = total - wb;
-    int granted = left <= 0 ? 0 : (int)min(left, (long long)want);
-    s_wbase = wb;
-    s_ebase = (trace + granted) ? atomicAdd(&cnt->n_ext, trace + granted) : 0;
+    granted = left <= 0 ? 0 : (int)min(left, (long long)c_want);
+    eb = (c_trace + granted) ? atomicAdd(&cnt->n_ext, c_trace + granted) : 0;
   }
-  __syncthreads();
-  long long wnext = s_wbase;  // next work item of this block
-  int enext = s_ebase;        // next queue position of this block
+  long long wnext = __shfl_sync(0xffffffffu, wb, 0);  // next work item of this warp
+  int gleft = __shfl_sync(0xffffffffu, granted, 0);  // work items left to place
+  int enext = __shfl_sync(0xffffffffu, eb, 0);       // next queue position of this warp
   unsigned long long bad = 0, paths = 0;
-  int it = 0;
-  for (int base = r0; base < r1; base += 256, it ^= 1) {
-    int s = base + threadIdx.x;
-    bool valid = s < r1;
-    int stage = valid ? P.stage[s] : LW_STAGE_GENERATE;
+  if (c_trace == 0 && (!regen || c_want == 0)) return;  // nothing to flush, generate or queue here
+  for (int base = r0; base < r1; base += 32) {
+    int s = base + lane;
+    int stage = P.stage[s];
     bool flushed = false;
-    if (regen && valid && stage == LW_STAGE_TERMINATED) {
+    if (regen && stage == LW_STAGE_TERMINATED) {
       bad += lw_accumulate(fb, P.pix[s], load_L(P, s));
       paths++;
       stage = LW_STAGE_GENERATE;
       flushed = true;
     }
-    bool want = regen && valid && stage == LW_STAGE_GENERATE;
-    bool trace = valid && stage == LW_STAGE_TRACE;
+    bool want = regen && stage == LW_STAGE_GENERATE;
+    bool trace = stage == LW_STAGE_TRACE;
     unsigned mw = __ballot_sync(0xffffffffu, want), mt = __ballot_sync(0xffffffffu, trace);
-    if (lane == 0) {
-      wc[it][warp][0] = __popc(mw);
-      wc[it][warp][1] = __popc(mt);
-    }
-    __syncthreads();
-    int pw = __popc(mw & lt), pt = __popc(mt & lt), tw = 0, tt = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      int a = wc[it][k][0], b = wc[it][k][1];
-      if (k < warp) {
-        pw += a;
-        pt += b;
-      }
-      tw += a;
-      tt += b;
-    }
-    long long left = total - wnext;
-    int avail = left <= 0 ? 0 : (int)min(left, (long long)tw);
+    if (!(mw | mt)) continue;
+    int pw = __popc(mw & lt), pt = __popc(mt & lt);
+    int avail = min(gleft, __popc(mw));
     if (want) {
       if (pw < avail) {
         long long item = wnext + pw;
@@ -638,8 +620,9 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
       }
     }
     if (trace) P.q_ext[enext + pt + min(pw, avail)] = s;
-    wnext += tw;
-    enext += tt + avail;
+    wnext += avail;
+    gleft -= avail;
+    enext += __popc(mt) + avail;
   }
   warp_add(&cnt->nonfinite, bad);
   warp_add(&cnt->paths, paths);

@@ -10,5 +10,5 @@ for c in ${CONFIGS:-C1 C2 C3 C4 C5}; do
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/launches_C2.csv $B --config C2 > /dev/null 2>&1
-python tools/kernel_traffic_json.py > profiles/r02_kernel_traffic.json
+python tools/kernel_traffic_json.py > gpurun_out/r02_kernel_traffic.json  # copy to profiles/ after the call
 ls gpurun_out
