@@ -62,6 +62,9 @@ struct Counters {
   unsigned long long ext_nodes, ext_tris, sh_nodes, sh_tris;
   unsigned long long sh_unocc;  // shadow rays that reached their light (NEE contribution added)
   int ext_next, sh_next;  // queue heads of the persistent trace kernels
+  // tail queue: once the pool is mostly empty the last compacted extension queue is
+  // kept for the rest of the pass (no more compaction); stage kernels skip its finished entries
+  int tail, tail_armed, n_trace;
 };
 
 // SoA of 16-byte vectors: slot s of every array is one LDG.128/STG.128, and a warp's 32
@@ -121,6 +124,9 @@ struct lw_ctx {
   int persist_mask = getenv("LW_TRACE_PERSIST") ? atoi(getenv("LW_TRACE_PERSIST")) : 15;
   bool persist = (persist_mask & 1) != 0;
   bool persist_sh = (persist_mask & 2) != 0;
+  // tail queue: keep the compacted queue once fewer than pool / tail_div paths are
+  // alive and nothing is left to regenerate (0 = compact every wave); LW_TAIL_QUEUE overrides
+  int tail_div = getenv("LW_TAIL_QUEUE") ? atoi(getenv("LW_TAIL_QUEUE")) : 16;
   int nrnodes = 0;        // internal nodes of the render BVH
   cudaStream_t own_stream = nullptr;
   int instr = 0;
@@ -523,16 +529,31 @@ __device__ __forceinline__ v3 load_L(const Pool& P, int s) {
 
 // paper §3.1.3: regenerate only once more than regen_fraction of the pool is free (or nothing
 // is in flight); one thread decides so every block of k_generate sees the same choice
-__global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int force) {
+//
+// Tail queue ("when the runtime of the compaction kernel exceeds the runtime of the
+// state kernel, we generate a single tail queue once"): once no work is left to regenerate and
+// fewer than pool / tail_div paths are alive, the next compaction is the last; later waves reuse
+// that queue (n_ext unchanged), k_generate returns at once and the stage kernels skip entries whose
+// path has finished.  `force` (the final flush) leaves tail mode.
+__global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int force, long long total, int tail_div) {
+  if (force) cnt->tail = cnt->tail_armed = 0;
+  if (cnt->tail_armed) cnt->tail = 1;
   int alive = cnt->n_alive;
-  bool regen = force || (pool - alive) > (int)(regen_fraction * (double)pool) || alive == 0;
-  cnt->regen_now = regen ? 1 : 0;
-  if (regen) cnt->regens += 1;
-  cnt->n_ext = 0;
   cnt->n_shadow = 0;
   cnt->n_alive = 0;
   cnt->ext_next = 0;
   cnt->sh_next = 0;
+  if (cnt->tail) {
+    cnt->regen_now = 0;
+    cnt->n_trace = alive;  // rays this wave (the queue also holds finished entries)
+    return;
+  }
+  bool regen = force || (pool - alive) > (int)(regen_fraction * (double)pool) || alive == 0;
+  cnt->regen_now = regen ? 1 : 0;
+  if (regen) cnt->regens += 1;
+  if (!force && !regen && tail_div > 0 && (long long)cnt->work_next >= total && alive < pool / tail_div)
+    cnt->tail_armed = 1;  // this wave's compaction builds the tail queue
+  cnt->n_ext = 0;
 }
 
 // pool order: flush TERMINATED slots, refill free slots with new (iteration, pixel) samples and
@@ -547,6 +568,7 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
 template <bool LPE>
 __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
                                                   Counters* __restrict__ cnt, LwLpe lpe) {
+  if (cnt->tail) return;  // tail queue: no compaction, nothing to regenerate
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const bool regen = cnt->regen_now != 0;
@@ -633,11 +655,13 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
   int n = cnt->n_ext;
+  const bool tail = cnt->tail != 0;
   LwTraceCount tc;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
     if (k < n) {
       int s = P.q_ext[k];
+      if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       double o[3], d[3];
       load_ray(P, s, o, d);
       LwHit h;
@@ -651,7 +675,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
     warp_add(&cnt->ext_tris, tc.tris);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    cnt->rays_ext += (unsigned long long)n;
+    cnt->rays_ext += (unsigned long long)(cnt->tail ? cnt->n_trace : n);
     cnt->waves += 1;
   }
 }
@@ -668,6 +692,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, NODES == LW_NODES_SMEM);
   const int n = cnt->n_ext;
+  const bool tail = cnt->tail != 0;
   const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
   LwTraceCount tc;
   int s = -1;
@@ -687,7 +712,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
       if (base + __popc(idle) >= n) more = false;
       if (s < 0) {
         int k = base + __popc(idle & lt);
-        if (k < n) {
+        if (k < n && (!tail || P.stage[P.q_ext[k]] == LW_STAGE_TRACE)) {
           s = P.q_ext[k];
           double o[3], d[3];
           load_ray(P, s, o, d);
@@ -702,7 +727,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
         }
       }
     }
-    if (__all_sync(0xffffffffu, s < 0)) break;
+    if (__all_sync(0xffffffffu, s < 0) && !more) break;  // (tail queue: a refill may hit only finished entries)
     if (s < 0) continue;
 #if LW_SPEC & 1
     // speculative traversal (Aila & Laine 2009): a lane that reaches a leaf postpones it and keeps
@@ -831,7 +856,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
     warp_add(&cnt->ext_tris, tc.tris);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    cnt->rays_ext += (unsigned long long)n;
+    cnt->rays_ext += (unsigned long long)(cnt->tail ? cnt->n_trace : n);
     cnt->waves += 1;
   }
 }
@@ -853,6 +878,7 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
   LwLightTree lt;
   if (LT) lt = lw_lt_stage(S.lt, S.lt_nheap, smem);
   int n = cnt->n_ext;
+  const bool tail = cnt->tail != 0;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
     bool valid = k < n;
@@ -864,7 +890,7 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
       load_hit(P, s, h);
       int f = P.flags[s];
       int bounce = f & F_BOUNCE;
-      if (h.tri >= 0 && bounce != S.max_depth - 1) {
+      if (h.tri >= 0 && bounce != S.max_depth - 1 && (!tail || P.stage[s] == LW_STAGE_TRACE)) {
         PathState ps;
         double2 a = P.ray1[s], c = P.ray2[s];
         ps.d = mk3(a.y, c.x, c.y);
@@ -907,11 +933,13 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
   LwLightTree lt;
   if (LT) lt = lw_lt_stage(S.lt, S.lt_nheap, smem);
   int n = cnt->n_ext;
+  const bool tail = cnt->tail != 0;
   unsigned long long alive_count = 0;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     int k = base + threadIdx.x;
     if (k < n) {
       int s = P.q_ext[k];
+      if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       PathState ps;
       load_state(P, s, ps, needs_nprev(S));
       LwHit h;
@@ -1483,7 +1511,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     for (;;) {
       for (int k = 0; k < check_every; k++) {
         mark(LW_PROF_OTHER);
-        k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0);
+        k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0, total, c->tail_div);
         mark(LW_PROF_GENERATE);
         if (lpe_on)
           k_generate<true><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
@@ -1560,7 +1588,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     }
     // flush the remaining finished paths
     mark(LW_PROF_OTHER);
-    k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1);
+    k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1, total, 0);
     mark(LW_PROF_GENERATE);
     k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
     mark(LW_PROF_END);
