@@ -88,6 +88,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-per-config", action="store_true", help="skip the C1-C5 table (N = 1 only)")
+    ap.add_argument("--state", default="fp64", choices=["fp64", "compact"],
+                    help="path state in the wavefront pool: FP64, or compact (oct-16 directions, FP32 "
+                         "throughput / radiance / pdf; PAPER.md:632-635)")
     a = ap.parse_args()
     a.width, a.height, a.depth, a.pass_iterations = resolve(a, a.config)
     return a
@@ -103,7 +106,8 @@ def workload(a, config=None):
 
 def config_dict(a, world):
     """The `config` object of the JSON line -- identical for both arms (same workload, same knobs)."""
-    return {"workload": workload(a), "engine": a.engine, "lights": a.lights, "env_sampling": a.env_sampling,
+    return {"workload": workload(a), "engine": a.engine, "state": a.state, "lights": a.lights,
+            "env_sampling": a.env_sampling,
             "pool_slots": 1 << a.pool_log2, "regen_fraction": a.regen_fraction,
             "parallelism": f"sample-space dp{world}",
             "l2": f"wavefront state pool (~{(1 << a.pool_log2) * 250 / 1e9:.1f} GB) exceeds the 126 MB L2 "
@@ -218,7 +222,7 @@ def cpu_render_sample(a, config, budget_s, threads=0, it0=3, gpu=None):
     W, H, D, _ = resolve(a, config)
     packed = pack_scene(build_scene(config), lights=a.lights, env_sampling=a.env_sampling)
     osc = O.OracleScene(packed)
-    params = RenderParams(W, H, D)
+    params = RenderParams(W, H, D, compact_state=a.state == "compact")
     threads = threads or os.cpu_count()
     # probe: 8 centre rows, one iteration (the centre is where the geometry is)
     r0 = max(0, H // 2 - 4)
@@ -487,7 +491,8 @@ class Measure:
         self.P = self.W * self.H
         self.packed = pack_scene(build_scene(config), lights=a.lights, env_sampling=a.env_sampling)
         self.r = Renderer(None, self.W, self.H, self.D, device=local, packed=self.packed, engine=a.engine,
-                          pool_log2=a.pool_log2, regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail)
+                          pool_log2=a.pool_log2, regen_fraction=a.regen_fraction, megakernel_tail=a.megakernel_tail,
+                          compact_state=a.state == "compact")
         self.r.set_stream(stream.cuda_stream)
         self.stream = stream
         self.local = local
@@ -585,7 +590,7 @@ class Measure:
         def one(s):
             with Renderer(None, self.W, self.H, self.D, device=self.local, packed=pscene, engine=a.engine,
                           pool_log2=a.pool_log2, regen_fraction=a.regen_fraction,
-                          megakernel_tail=a.megakernel_tail) as r2:
+                          megakernel_tail=a.megakernel_tail, compact_state=a.state == "compact") as r2:
                 r2.set_stream(self.stream.cuda_stream)
                 lo, hi = partition_iterations(s * self.world * self.its, (s + 1) * self.world * self.its, self.rank,
                                               self.world)

@@ -150,6 +150,10 @@ typedef struct lw_render_params {
   double regen_fraction;     /* regenerate when free slots exceed this fraction of the pool (paper: 0.5) */
   int64_t megakernel_tail;   /* switch to the megakernel once active paths drop below this (0 = never) */
   int32_t estimator;         /* LW_EST_*: how emitter / environment radiance is estimated */
+  int32_t compact_state;     /* 1: compressed path state: ray directions as 2x16-bit
+                                octahedral codes (the reference codec, _kernels.py:233-299), throughput,
+                                radiance and BSDF pdf in FP32 -- quantised where produced, identically in
+                                both engines and the oracle; 0: FP64 state */
 } lw_render_params;
 
 /* estimators (SPEC.md:400-402 estimator equivalence): balance-heuristic MIS of light sampling and

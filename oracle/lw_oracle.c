@@ -2104,6 +2104,17 @@ static double emitter_hit_pdf(const lwo_scene* s, int64_t e, v3 o, int64_t nprev
 
 static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, const lpe_ctx* lpe, int64_t pix);
 
+/* compressed path state (lw_render_params.compact_state; device: lw_q32 /
+ * lw_oct_dir in lw_integrator.cuh): FP32 throughput, radiance and pdf, directions through the
+ * reference's octahedral codec (_kernels.py:233-299), quantised where each value is produced */
+static double q32(double x) { return (double)(float)x; }
+static v3 q32v(v3 a) { return mk(q32(a.x), q32(a.y), q32(a.z)); }
+static v3 dir_q(v3 d) {
+  double o[3];
+  lwo_oct_decode(lwo_oct_encode(d.x, d.y, d.z), o);
+  return normalize(mk(o[0], o[1], o[2]));
+}
+
 /* balance heuristic and the estimator switch of lw_render_params.estimator
  * (SPEC.md:400-402): weight of emission reached by BSDF sampling after a non-specular vertex */
 static double mis_balance(double a, double b) { return a / (a + b); }
@@ -2118,6 +2129,8 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
   int depth = c->p->max_depth;
   v3 o, d;
   camera_ray(c, index, &o, &d);
+  const int compact = c->p->compact_state != 0;
+  if (compact) d = dir_q(d);
   v3 beta = mk(1, 1, 1), L = mk(0, 0, 0);
   int spec_prev = 1;
   double pdf_prev = 0.0;
@@ -2133,7 +2146,7 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
         v3 Le = env_eval(s, d, nprev, &pe);
         double w = spec_prev ? 1.0 : bsdf_hit_weight(c->p->estimator, pdf_prev, pe);
         v3 cc = mk(beta.x * Le.x * w, beta.y * Le.y * w, beta.z * Le.z * w);
-        L = add(L, cc);
+        L = compact ? q32v(add(L, cc)) : add(L, cc);
         if (lpe) lpe_route(lpe, lpe_step(lpe, lst, LW_EV_E), pix, cc);
       }
       break;
@@ -2152,7 +2165,7 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
       double wm = 1.0;
       if (!spec_prev) wm = bsdf_hit_weight(c->p->estimator, pdf_prev, emitter_hit_pdf(s, e, o, nprev, ng, d, h.t));
       v3 cc = mk(beta.x * Le.x * wm, beta.y * Le.y * wm, beta.z * Le.z * wm);
-      L = add(L, cc);
+      L = compact ? q32v(add(L, cc)) : add(L, cc);
       if (lpe) lpe_route(lpe, lpe_step(lpe, lst, LW_EV_L), pix, cc);
     }
     if (b == depth - 1) break;
@@ -2189,7 +2202,7 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
           v3 so = offset_origin(p, ngf, wi);
           if (st) st->rays_shadow++;
           if (!trace_any(s, &so.x, &wi.x, tmax_sh)) {
-            L = add(L, contrib);
+            L = compact ? q32v(add(L, contrib)) : add(L, contrib);
             if (lpe) { /* diffuse and glossy parts, terminal L (triangle) or E (environment) */
               v3 fd, fg;
               bsdf_eval_split(m, &lw, wol, wil, &fd, &fg);
@@ -2209,11 +2222,12 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
     if (!bsdf_sample(m, &lw, wol, front, ub, vb, &bs)) break;
     if (lpe) lst = lpe_step(lpe, lst, bs.event);
     v3 wi = to_world(&fr, bs.wi);
+    if (compact) wi = dir_q(wi);
     double gside = dot(ngf, wi);
     if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) break;
     beta = mk(beta.x * bs.weight.x, beta.y * bs.weight.y, beta.z * bs.weight.z);
     spec_prev = bs.delta;
-    pdf_prev = bs.pdf;
+    pdf_prev = compact ? q32(bs.pdf) : bs.pdf;
     if (b >= c->p->rr_start) {
       double q = beta.x;
       if (beta.y > q) q = beta.y;
@@ -2224,6 +2238,7 @@ static v3 trace_path_lpe(const rctx* c, int64_t index, lw_render_stats* st, cons
       double inv_q = 1.0 / q;
       beta = mk(beta.x * inv_q, beta.y * inv_q, beta.z * inv_q);
     }
+    if (compact) beta = q32v(beta);
     o = offset_origin(p, ngf, wi);
     d = wi;
     nprev = lwo_oct_encode(ngf.x, ngf.y, ngf.z);

@@ -128,6 +128,7 @@ class LwRenderParams(C.Structure):
         ("regen_fraction", C.c_double),
         ("megakernel_tail", C.c_int64),
         ("estimator", C.c_int32),
+        ("compact_state", C.c_int32),
     ]
 
 

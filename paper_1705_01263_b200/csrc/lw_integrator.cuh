@@ -49,6 +49,8 @@ struct DevScene {
   double tan_half;
   int W, H, max_depth, rr_start;
   int estimator;  // LW_EST_* (MIS in the renderer; NEE-only / BSDF-only for estimator-equivalence checks)
+  int compact;    // compressed path state: oct-16 ray directions, FP32 throughput,
+                  // radiance and pdf, quantised where the state is produced (both engines, the oracle)
   const QmcDim* qdims;
   const uint16_t* qperm;
 };
@@ -62,6 +64,7 @@ struct PathState {
   int spec_prev;
   int nprev;  // octahedral-packed facing geometric normal of the previous vertex (light-tree MIS)
   int lpe;    // light-path-expression automaton state (megakernel with layers)
+  unsigned doct;  // compact state: octahedral code of d (d == lw_oct_dir(doct))
 };
 
 struct ShadowRay {
@@ -115,6 +118,16 @@ __device__ __forceinline__ double lw_qmc_s(const DevScene& S, int dim, long long
 }
 
 __device__ __forceinline__ v3 lw_ld3(const double* p) { return mk3(p[0], p[1], p[2]); }
+
+// ---- compressed path state (oracle: q32 / dir_q) ----------------------------
+// Directions are stored as the 2x16-bit octahedral code of the reference's codec (_kernels.py:
+// 233-299) and used as its decoded, normalised vector; throughput, radiance and the BSDF pdf as
+// FP32.  Quantisation happens where a value is produced, identically in both engines and the
+// oracle, so the compact render is as deterministic (and bit-identical across engines) as the
+// FP64 one.
+__device__ __forceinline__ double lw_q32(double x) { return (double)__double2float_rn(x); }
+__device__ __forceinline__ v3 lw_q32v(v3 a) { return mk3(lw_q32(a.x), lw_q32(a.y), lw_q32(a.z)); }
+__device__ __forceinline__ v3 lw_oct_dir(unsigned code) { return normalize3(lw_oct_decode((long long)code)); }
 
 // DESIGN.md §4.1 (oracle camera_ray)
 __device__ __forceinline__ void lw_camera_ray(const DevScene& S, long long index, v3& o, v3& d) {
@@ -419,8 +432,15 @@ __device__ __forceinline__ long long lw_alias_sample(const double* __restrict__ 
 
 // ---- stages ---------------------------------------------------------------------------
 
+// CMP: compressed path state (S.compact), a compile-time choice of the calling kernel
+template <bool CMP = false>
 __device__ __forceinline__ void lw_path_init(const DevScene& S, long long index, PathState& ps) {
   lw_camera_ray(S, index, ps.o, ps.d);
+  ps.doct = 0;
+  if (CMP) {
+    ps.doct = (unsigned)lw_oct_encode(ps.d.x, ps.d.y, ps.d.z);
+    ps.d = lw_oct_dir(ps.doct);
+  }
   ps.beta = mk3(1.0, 1.0, 1.0);
   ps.L = mk3(0.0, 0.0, 0.0);
   ps.pdf_prev = 0.0;
@@ -618,6 +638,7 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
 
 // miss / emission part: returns false if the path ends before any scattering
 // lpe (megakernel with LPE layers): routes the emission to the layers accepting ... L / ... E
+template <bool CMP = false>
 __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& ps, const LwHit& h, ShadeGeom& g,
                                                   double& w, const LwLpe* lpe = nullptr, long long pix = 0,
                                                   const LwLightTree* lt = nullptr) {
@@ -628,7 +649,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
       v3 Le = lw_env_eval(S, d, ps.nprev, pe);
       double wm = ps.spec_prev ? 1.0 : lw_bsdf_hit_weight(S, ps.pdf_prev, pe);
       v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
-      ps.L = ps.L + c;
+      ps.L = CMP ? lw_q32v(ps.L + c) : ps.L + c;
       if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_E), pix, c);
     }
     return false;
@@ -640,13 +661,14 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
     double wm = 1.0;
     if (!ps.spec_prev) wm = lw_bsdf_hit_weight(S, ps.pdf_prev, lw_emitter_hit_pdf(S, e, ps.o, ps.nprev, g.ng, d, h.t, lt));
     v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
-    ps.L = ps.L + c;
+    ps.L = CMP ? lw_q32v(ps.L + c) : ps.L + c;
     if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_L), pix, c);
   }
   return ps.bounce != S.max_depth - 1;
 }
 
 // BSDF sampling, Russian roulette and the next ray; returns true if the path continues
+template <bool CMP = false>
 __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& ps, const ShadeGeom& g,
                                                   const LwLpe* lpe = nullptr) {
   const int b = ps.bounce;
@@ -657,11 +679,16 @@ __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& 
   if (!lw_bsdf_sample(*g.m, g.lw, g.wol, g.front, ub, vb, bs)) return false;
   if (lpe) ps.lpe = lw_lpe_step(lpe, ps.lpe, bs.event);
   v3 wi = lw_to_world(g.fr, bs.wi);
+  unsigned code = 0;
+  if (CMP) {  // the next ray runs along the stored (quantised) direction
+    code = (unsigned)lw_oct_encode(wi.x, wi.y, wi.z);
+    wi = lw_oct_dir(code);
+  }
   double gside = dot3(g.ngf, wi);
   if (bs.transmit ? !(gside < 0.0) : !(gside > 0.0)) return false;
   ps.beta = mk3(ps.beta.x * bs.weight.x, ps.beta.y * bs.weight.y, ps.beta.z * bs.weight.z);
   ps.spec_prev = bs.delta;
-  ps.pdf_prev = bs.pdf;
+  ps.pdf_prev = CMP ? lw_q32(bs.pdf) : bs.pdf;
   if (b >= S.rr_start) {
     double q = ps.beta.x;
     if (ps.beta.y > q) q = ps.beta.y;
@@ -672,23 +699,26 @@ __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& 
     double inv_q = 1.0 / q;
     ps.beta = mk3(ps.beta.x * inv_q, ps.beta.y * inv_q, ps.beta.z * inv_q);
   }
+  if (CMP) ps.beta = lw_q32v(ps.beta);
   ps.o = lw_offset_origin(g.p, g.ngf, wi);
   ps.d = wi;
+  ps.doct = code;
   ps.bounce = b + 1;
   ps.nprev = (int)lw_oct_encode(g.ngf.x, g.ngf.y, g.ngf.z);
   return true;
 }
 
 // whole stage in the oracle's order (megakernel): emission, NEE, BSDF sampling
+template <bool CMP = false>
 __device__ __forceinline__ bool lw_path_shade(const DevScene& S, PathState& ps, const LwHit& h, ShadowRay& sh,
                                               const LwLpe* lpe = nullptr, long long pix = 0) {
   sh.valid = 0;
   ShadeGeom g;
   double w;
-  if (!lw_shade_emission(S, ps, h, g, w, lpe, pix)) return false;
+  if (!lw_shade_emission<CMP>(S, ps, h, g, w, lpe, pix)) return false;
   lw_shade_frame(S, ps.d, h, w, g);
   lw_shade_nee(S, ps, g, sh, lpe);
-  return lw_shade_material(S, ps, g, lpe);
+  return lw_shade_material<CMP>(S, ps, g, lpe);
 }
 
 // fixed-point accumulation (oracle accumulate); returns 1 if a channel was non-finite

@@ -417,6 +417,7 @@ __device__ __forceinline__ long long work_index(const DevScene& S, const WorkRan
   return it * ((long long)S.W * S.H) + p;
 }
 
+template <bool CMP>
 __device__ __forceinline__ void run_to_completion(const DevScene& S, const RenderBVH& bvh, PathState& ps,
                                                   unsigned long long& next, unsigned long long& nsh,
                                                   const LwLpe* lpe = nullptr, long long pix = 0) {
@@ -426,12 +427,12 @@ __device__ __forceinline__ void run_to_completion(const DevScene& S, const Rende
     lw_trace_closest(bvh, o, d, INFINITY, h);
     next++;
     ShadowRay sh;
-    bool alive = lw_path_shade(S, ps, h, sh, lpe, pix);
+    bool alive = lw_path_shade<CMP>(S, ps, h, sh, lpe, pix);
     if (sh.valid) {
       double so[3] = {sh.o.x, sh.o.y, sh.o.z}, sd[3] = {sh.d.x, sh.d.y, sh.d.z};
       nsh++;
       if (!lw_trace_any(bvh, so, sd, sh.tmax)) {
-        ps.L = ps.L + sh.contrib;
+        ps.L = CMP ? lw_q32v(ps.L + sh.contrib) : ps.L + sh.contrib;
         if (lpe) {
           lw_lpe_route(lpe, lw_lpe_step(lpe, lw_lpe_step(lpe, sh.lpe, LW_EV_RD), sh.term), pix, sh.c_diffuse);
           lw_lpe_route(lpe, lw_lpe_step(lpe, lw_lpe_step(lpe, sh.lpe, LW_EV_RG), sh.term), pix, sh.c_glossy);
@@ -443,7 +444,7 @@ __device__ __forceinline__ void run_to_completion(const DevScene& S, const Rende
 }
 
 // LPE = true: every contribution is also routed to the light-path-expression layers
-template <bool LPE>
+template <bool LPE, bool CMP>
 __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, unsigned long long* __restrict__ fb,
                                                     Counters* __restrict__ cnt, int nrnodes, int use_smem, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -456,9 +457,9 @@ __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, uns
       int pix;
       long long index = work_index(S, w, item, pix);
       PathState ps;
-      lw_path_init(S, index, ps);
+      lw_path_init<CMP>(S, index, ps);
       if (LPE) ps.lpe = lw_lpe_step(&lpe, lpe.start, LW_EV_C);
-      run_to_completion(S, bvh, ps, next, nsh, LPE ? &lpe : nullptr, pix);
+      run_to_completion<CMP>(S, bvh, ps, next, nsh, LPE ? &lpe : nullptr, pix);
       bad += lw_accumulate(fb, pix, ps.L);
       paths++;
     }
@@ -481,11 +482,27 @@ __global__ void __launch_bounds__(128) k_megakernel(DevScene S, WorkRange w, uns
 #define F_BOUNCE 0xff
 #define F_SPEC (1 << 8)
 
-__device__ __forceinline__ void load_ray(const Pool& P, int s, double o[3], double d[3]) {
-  double2 a = P.ray0[s], b = P.ray1[s], c = P.ray2[s];
+// Pool layout of a path (16-byte vectors).  FP64 state: ray0 (o.x, o.y), ray1 (o.z, d.x), ray2
+// (d.y, d.z), tp0 (beta.x, beta.y), tp1 (beta.z, L.x), tp2 (L.y, L.z), misc (pdf_prev, index) --
+// 112 bytes.  Compact state (S.compact): ray0 (o.x, o.y), ray1 (o.z, oct(d) << 32
+// | fp32 pdf_prev), tp0 as float4 (beta.xyz, L.x), tp1 (fp32 L.y | L.z << 32, index) -- 64 bytes.
+__device__ __forceinline__ unsigned long long pack2f(double lo, double hi) {
+  return ((unsigned long long)__float_as_uint((float)hi) << 32) | __float_as_uint((float)lo);
+}
+
+__device__ __forceinline__ void load_ray(const Pool& P, int s, double o[3], double d[3], bool compact) {
+  double2 a = P.ray0[s], b = P.ray1[s];
   o[0] = a.x;
   o[1] = a.y;
   o[2] = b.x;
+  if (compact) {
+    v3 v = lw_oct_dir((unsigned)((unsigned long long)__double_as_longlong(b.y) >> 32));
+    d[0] = v.x;
+    d[1] = v.y;
+    d[2] = v.z;
+    return;
+  }
+  double2 c = P.ray2[s];
   d[0] = b.y;
   d[1] = c.x;
   d[2] = c.y;
@@ -494,35 +511,64 @@ __device__ __forceinline__ void load_ray(const Pool& P, int s, double o[3], doub
 // nprev (previous vertex normal) is only consumed by the light hierarchy / environment pyramid MIS
 __device__ __forceinline__ bool needs_nprev(const DevScene& S) { return S.light_mode != 0 || S.env_mode != 0; }
 
-__device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps, bool nprev) {
-  double2 a = P.ray0[s], b = P.ray1[s], c = P.ray2[s];
+__device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps, bool nprev, bool compact) {
+  double2 a = P.ray0[s], b = P.ray1[s];
   ps.o = mk3(a.x, a.y, b.x);
-  ps.d = mk3(b.y, c.x, c.y);
-  double2 t0 = P.tp0[s], t1 = P.tp1[s], t2 = P.tp2[s];
-  ps.beta = mk3(t0.x, t0.y, t1.x);
-  ps.L = mk3(t1.y, t2.x, t2.y);
-  double2 m = P.misc[s];
-  ps.pdf_prev = m.x;
-  ps.index = __double_as_longlong(m.y);
+  if (compact) {
+    unsigned long long bits = (unsigned long long)__double_as_longlong(b.y);
+    ps.doct = (unsigned)(bits >> 32);
+    ps.d = lw_oct_dir(ps.doct);
+    ps.pdf_prev = (double)__uint_as_float((unsigned)bits);
+    float4 t0 = reinterpret_cast<const float4*>(P.tp0)[s];
+    double2 t1 = P.tp1[s];
+    unsigned long long lb = (unsigned long long)__double_as_longlong(t1.x);
+    ps.beta = mk3((double)t0.x, (double)t0.y, (double)t0.z);
+    ps.L = mk3((double)t0.w, (double)__uint_as_float((unsigned)lb), (double)__uint_as_float((unsigned)(lb >> 32)));
+    ps.index = __double_as_longlong(t1.y);
+  } else {
+    double2 c = P.ray2[s];
+    ps.d = mk3(b.y, c.x, c.y);
+    double2 t0 = P.tp0[s], t1 = P.tp1[s], t2 = P.tp2[s];
+    ps.beta = mk3(t0.x, t0.y, t1.x);
+    ps.L = mk3(t1.y, t2.x, t2.y);
+    double2 m = P.misc[s];
+    ps.pdf_prev = m.x;
+    ps.index = __double_as_longlong(m.y);
+    ps.doct = 0;
+  }
   int f = P.flags[s];
   ps.bounce = f & F_BOUNCE;
   ps.spec_prev = (f & F_SPEC) ? 1 : 0;
   ps.nprev = nprev ? P.nprev[s] : 0;
 }
 
-__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps, bool nprev) {
+// compact: every stored value is already FP32-representable / an oct code (quantised where produced)
+__device__ __forceinline__ void store_state(const Pool& P, int s, const PathState& ps, bool nprev, bool compact) {
   P.ray0[s] = make_double2(ps.o.x, ps.o.y);
-  P.ray1[s] = make_double2(ps.o.z, ps.d.x);
-  P.ray2[s] = make_double2(ps.d.y, ps.d.z);
-  P.tp0[s] = make_double2(ps.beta.x, ps.beta.y);
-  P.tp1[s] = make_double2(ps.beta.z, ps.L.x);
-  P.tp2[s] = make_double2(ps.L.y, ps.L.z);
-  P.misc[s] = make_double2(ps.pdf_prev, __longlong_as_double(ps.index));
+  if (compact) {
+    P.ray1[s] = make_double2(ps.o.z, __longlong_as_double((long long)(((unsigned long long)ps.doct << 32) |
+                                                                          __float_as_uint((float)ps.pdf_prev))));
+    reinterpret_cast<float4*>(P.tp0)[s] =
+        make_float4((float)ps.beta.x, (float)ps.beta.y, (float)ps.beta.z, (float)ps.L.x);
+    P.tp1[s] = make_double2(__longlong_as_double((long long)pack2f(ps.L.y, ps.L.z)), __longlong_as_double(ps.index));
+  } else {
+    P.ray1[s] = make_double2(ps.o.z, ps.d.x);
+    P.ray2[s] = make_double2(ps.d.y, ps.d.z);
+    P.tp0[s] = make_double2(ps.beta.x, ps.beta.y);
+    P.tp1[s] = make_double2(ps.beta.z, ps.L.x);
+    P.tp2[s] = make_double2(ps.L.y, ps.L.z);
+    P.misc[s] = make_double2(ps.pdf_prev, __longlong_as_double(ps.index));
+  }
   P.flags[s] = ps.bounce | (ps.spec_prev ? F_SPEC : 0);
   if (nprev) P.nprev[s] = ps.nprev;
 }
 
-__device__ __forceinline__ v3 load_L(const Pool& P, int s) {
+__device__ __forceinline__ v3 load_L(const Pool& P, int s, bool compact) {
+  if (compact) {
+    float lx = reinterpret_cast<const float4*>(P.tp0)[s].w;
+    unsigned long long lb = (unsigned long long)__double_as_longlong(P.tp1[s].x);
+    return mk3((double)lx, (double)__uint_as_float((unsigned)lb), (double)__uint_as_float((unsigned)(lb >> 32)));
+  }
   double2 t1 = P.tp1[s], t2 = P.tp2[s];
   return mk3(t1.y, t2.x, t2.y);
 }
@@ -565,7 +611,7 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
 // `granted` free slots of the range, so a lane's queue offset is trace_prefix + min(want_prefix,
 // granted_left).  (Block-granular with a barrier per 256 slots, this scan cost ~170 us per wave on
 // C2 even when nothing was left to do; the per-warp form is bound by the stage-byte reads.)
-template <bool LPE>
+template <bool LPE, bool CMP>
 __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
                                                   Counters* __restrict__ cnt, LwLpe lpe) {
   if (cnt->tail) return;  // tail queue: no compaction, nothing to regenerate
@@ -614,7 +660,7 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
     int stage = P.stage[s];
     bool flushed = false;
     if (regen && stage == LW_STAGE_TERMINATED) {
-      bad += lw_accumulate(fb, P.pix[s], load_L(P, s));
+      bad += lw_accumulate(fb, P.pix[s], load_L(P, s, CMP));
       paths++;
       stage = LW_STAGE_GENERATE;
       flushed = true;
@@ -631,8 +677,8 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
         int pix;
         long long index = work_index(S, w, item, pix);
         PathState ps;
-        lw_path_init(S, index, ps);
-        store_state(P, s, ps, needs_nprev(S));
+        lw_path_init<CMP>(S, index, ps);
+        store_state(P, s, ps, needs_nprev(S), CMP);
         if (LPE) P.lpe_state[s] = lw_lpe_step(&lpe, lpe.start, LW_EV_C);
         P.pix[s] = pix;
         P.stage[s] = LW_STAGE_TRACE;
@@ -650,7 +696,7 @@ __global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange 
   warp_add(&cnt->paths, paths);
 }
 
-template <bool COUNT, int NODES>
+template <bool COUNT, int NODES, bool CMP>
 __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   RenderBVH bvh = stage_bvh(S.bvh, nrnodes, smem, use_smem != 0);
@@ -663,7 +709,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
       int s = P.q_ext[k];
       if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       double o[3], d[3];
-      load_ray(P, s, o, d);
+      load_ray(P, s, o, d, CMP);
       LwHit h;
       lw_trace_closest<COUNT, NODES, (LW_SPEC_SMEM & 1) != 0>(bvh, o, d, INFINITY, h, &tc);
       P.hit0[s] = make_double2(h.t, h.bu);
@@ -686,7 +732,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext(DevScene S, Po
 // of idling until the slowest lane of its warp is done, so the warp's SIMT efficiency does not
 // collapse on incoherent rays.  The traversal is the same as lw_trace_closest (same visit order,
 // same hits); the loop yields after every leaf so that refills can happen.
-template <bool COUNT, int NODES>
+template <bool COUNT, int NODES, bool CMP>
 __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, Pool P, Counters* __restrict__ cnt,
                                                                     int nrnodes) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -715,7 +761,7 @@ __global__ void __launch_bounds__(128, LW_TRACE_MINB) k_trace_ext_p(DevScene S, 
         if (k < n && (!tail || P.stage[P.q_ext[k]] == LW_STAGE_TRACE)) {
           s = P.q_ext[k];
           double o[3], d[3];
-          load_ray(P, s, o, d);
+          load_ray(P, s, o, d, CMP);
           lw_rayf_setup(r, bvh, o, d);
           ht = INFINITY;
           hu = hv = 0.0;
@@ -871,7 +917,7 @@ __device__ __forceinline__ void load_hit(const Pool& P, int s, LwHit& h) {
 
 // NEE half of the material stage (runs before k_shade so it sees the incoming throughput):
 // light / environment sample, BSDF evaluation, shadow-ray setup
-template <bool LPE, bool LT>
+template <bool LPE, bool LT, bool CMP>
 __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt,
                                                                 LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -892,11 +938,18 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
       int bounce = f & F_BOUNCE;
       if (h.tri >= 0 && bounce != S.max_depth - 1 && (!tail || P.stage[s] == LW_STAGE_TRACE)) {
         PathState ps;
-        double2 a = P.ray1[s], c = P.ray2[s];
-        ps.d = mk3(a.y, c.x, c.y);
-        double2 t0 = P.tp0[s], t1 = P.tp1[s];
-        ps.beta = mk3(t0.x, t0.y, t1.x);
-        ps.index = __double_as_longlong(P.misc[s].y);
+        if (CMP) {
+          ps.d = lw_oct_dir((unsigned)((unsigned long long)__double_as_longlong(P.ray1[s].y) >> 32));
+          float4 t0 = reinterpret_cast<const float4*>(P.tp0)[s];
+          ps.beta = mk3((double)t0.x, (double)t0.y, (double)t0.z);
+          ps.index = __double_as_longlong(P.tp1[s].y);
+        } else {
+          double2 a = P.ray1[s], c = P.ray2[s];
+          ps.d = mk3(a.y, c.x, c.y);
+          double2 t0 = P.tp0[s], t1 = P.tp1[s];
+          ps.beta = mk3(t0.x, t0.y, t1.x);
+          ps.index = __double_as_longlong(P.misc[s].y);
+        }
         ps.bounce = bounce;
         if (LPE) ps.lpe = P.lpe_state[s];
         ShadeGeom g;
@@ -927,7 +980,7 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
 }
 
 // material half: miss/emission (MIS), BSDF sampling, Russian roulette, next ray, stage tag
-template <bool LPE, bool LT>
+template <bool LPE, bool LT, bool CMP>
 __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
   LwLightTree lt;
@@ -941,18 +994,18 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
       int s = P.q_ext[k];
       if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       PathState ps;
-      load_state(P, s, ps, needs_nprev(S));
+      load_state(P, s, ps, needs_nprev(S), CMP);
       LwHit h;
       load_hit(P, s, h);
       ShadeGeom g;
       double w;
       bool alive = false;
       if (LPE) ps.lpe = P.lpe_state[s];
-      if (lw_shade_emission(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0, LT ? &lt : nullptr)) {
+      if (lw_shade_emission<CMP>(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0, LT ? &lt : nullptr)) {
         lw_shade_frame(S, ps.d, h, w, g);
-        alive = lw_shade_material(S, ps, g, LPE ? &lpe : nullptr);
+        alive = lw_shade_material<CMP>(S, ps, g, LPE ? &lpe : nullptr);
       }
-      store_state(P, s, ps, needs_nprev(S));
+      store_state(P, s, ps, needs_nprev(S), CMP);
       if (LPE) P.lpe_state[s] = ps.lpe;
       P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
       alive_count += alive ? 1 : 0;
@@ -962,14 +1015,28 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
 }
 
 // an unoccluded shadow ray adds its NEE contribution (and routes its LPE split)
-template <bool LPE>
+template <bool LPE, bool compact>
 __device__ __forceinline__ void shadow_unoccluded(const Pool& P, int s, double cx, const LwLpe& lpe) {
-  double2 f = P.sh4[s], t1 = P.tp1[s], t2 = P.tp2[s];
-  t1.y = t1.y + cx;
-  t2.x = t2.x + f.x;
-  t2.y = t2.y + f.y;
-  P.tp1[s] = t1;
-  P.tp2[s] = t2;
+  double2 f = P.sh4[s];
+  if (compact) {  // L = q32(L + contribution), as lw_q32v in the megakernel and the oracle
+    float4* t0p = reinterpret_cast<float4*>(P.tp0) + s;
+    float4 t0 = *t0p;
+    double2 t1 = P.tp1[s];
+    unsigned long long lb = (unsigned long long)__double_as_longlong(t1.x);
+    t0.w = __double2float_rn((double)t0.w + cx);
+    double ly = lw_q32((double)__uint_as_float((unsigned)lb) + f.x);
+    double lz = lw_q32((double)__uint_as_float((unsigned)(lb >> 32)) + f.y);
+    *t0p = t0;
+    t1.x = __longlong_as_double((long long)pack2f(ly, lz));
+    P.tp1[s] = t1;
+  } else {
+    double2 t1 = P.tp1[s], t2 = P.tp2[s];
+    t1.y = t1.y + cx;
+    t2.x = t2.x + f.x;
+    t2.y = t2.y + f.y;
+    P.tp1[s] = t1;
+    P.tp2[s] = t2;
+  }
   if (LPE) {
     double2 a5 = P.sh5[s], a6 = P.sh6[s], a7 = P.sh7[s];
     int sl = P.sh_lpe[s], st0 = sl & 0xffff, term = sl >> 16;
@@ -980,7 +1047,7 @@ __device__ __forceinline__ void shadow_unoccluded(const Pool& P, int s, double c
 }
 
 // persistent any-hit trace over a global-memory BVH with lane refill (see k_trace_ext_p)
-template <bool COUNT, bool LPE, int NODES>
+template <bool COUNT, bool LPE, int NODES, bool CMP>
 __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene S, Pool P, Counters* __restrict__ cnt,
                                                                         int nrnodes, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1063,7 +1130,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
     }
     if (occluded || ref == LW_REF_NONE) {
       if (!occluded) {
-        shadow_unoccluded<LPE>(P, s, cx, lpe);
+        shadow_unoccluded<LPE, CMP>(P, s, cx, lpe);
         if (COUNT) tc.lit++;
       }
       s = -1;
@@ -1099,7 +1166,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
     ref = sp > 0 && !occluded ? stk[--sp] : LW_REF_NONE;
     if (ref == LW_REF_NONE) {
       if (!occluded) {
-        shadow_unoccluded<LPE>(P, s, cx, lpe);
+        shadow_unoccluded<LPE, CMP>(P, s, cx, lpe);
         if (COUNT) tc.lit++;
       }
       s = -1;
@@ -1114,7 +1181,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow_p(DevScene
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->rays_shadow += (unsigned long long)n;
 }
 
-template <bool COUNT, bool LPE, int NODES>
+template <bool COUNT, bool LPE, int NODES, bool CMP>
 __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S, Pool P, Counters* __restrict__ cnt, int nrnodes, int use_smem,
                                                                       LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1128,7 +1195,7 @@ __global__ void __launch_bounds__(128, LW_SHADOW_MINB) k_trace_shadow(DevScene S
       double2 a = P.sh0[s], b = P.sh1[s], c = P.sh2[s], e = P.sh3[s];
       double o[3] = {a.x, a.y, b.x}, d[3] = {b.y, c.x, c.y};
       if (!lw_trace_any<COUNT, NODES, (LW_SPEC_SMEM & 2) != 0>(bvh, o, d, e.x, &tc)) {
-        shadow_unoccluded<LPE>(P, s, e.y, lpe);
+        shadow_unoccluded<LPE, CMP>(P, s, e.y, lpe);
         if (COUNT) tc.lit++;
       }
     }
@@ -1148,7 +1215,7 @@ __global__ void k_wave_end(Counters* cnt) {
 }
 
 // megakernel tail: run every in-flight path to completion, in pool order
-template <bool LPE>
+template <bool LPE, bool CMP>
 __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned long long* __restrict__ fb,
                                                    Counters* __restrict__ cnt, int nrnodes, int use_smem, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1158,9 +1225,9 @@ __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned 
     int s = base + threadIdx.x;
     if (s < P.size && P.stage[s] == LW_STAGE_TRACE) {
       PathState ps;
-      load_state(P, s, ps, needs_nprev(S));
+      load_state(P, s, ps, needs_nprev(S), CMP);
       if (LPE) ps.lpe = P.lpe_state[s];
-      run_to_completion(S, bvh, ps, next, nsh, LPE ? &lpe : nullptr, P.pix[s]);
+      run_to_completion<CMP>(S, bvh, ps, next, nsh, LPE ? &lpe : nullptr, P.pix[s]);
       bad += lw_accumulate(fb, P.pix[s], ps.L);
       paths++;
       P.stage[s] = LW_STAGE_GENERATE;
@@ -1428,28 +1495,29 @@ int alloc_pool(lw_ctx* c, int size) {
   return LW_OK;
 }
 
-template <int NODES>
+template <int NODES, bool CMP>
 void launch_shadow(lw_ctx* c, int grid, size_t smem, int nr, bool lpe_on, bool count) {
   cudaStream_t st = c->stream;
   if (NODES == LW_NODES_GLOBAL ? c->persist_sh : (c->persist_mask & 8) != 0) {
     if (lpe_on)
-      k_trace_shadow_p<false, true, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
+      k_trace_shadow_p<false, true, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
     else if (count)
-      k_trace_shadow_p<true, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
+      k_trace_shadow_p<true, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
     else
-      k_trace_shadow_p<false, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
+      k_trace_shadow_p<false, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
     return;
   }
   int use_smem = NODES == LW_NODES_SMEM ? 1 : 0;
   if (lpe_on)
-    k_trace_shadow<false, true, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+    k_trace_shadow<false, true, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
   else if (count)
-    k_trace_shadow<true, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+    k_trace_shadow<true, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
   else
-    k_trace_shadow<false, false, NODES><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
+    k_trace_shadow<false, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
 }
 
-int run_pass(lw_ctx* c, const WorkRange& w) {
+template <bool CMP>
+int run_pass_t(lw_ctx* c, const WorkRange& w) {
   LW_CHECK_ARG(c->has_scene, "render: no scene uploaded");
   LW_CHECK_ARG(c->configured, "render: lw_render_configure not called");
   cudaStream_t st = c->stream;
@@ -1471,9 +1539,9 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     long long need = (total + 127) / 128;
     if (need < grid) grid = (int)std::max<long long>(1, need);
     if (c->lpe.nlayers > 0)
-      k_megakernel<true><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+      k_megakernel<true, CMP><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
     else
-      k_megakernel<false><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+      k_megakernel<false, CMP><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
     LW_CUDA_TRY(cudaGetLastError());
     launches = 1;
   } else {
@@ -1514,53 +1582,53 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
         k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0, total, c->tail_div);
         mark(LW_PROF_GENERATE);
         if (lpe_on)
-          k_generate<true><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
+          k_generate<true, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
         else
-          k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
+          k_generate<false, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
         mark(LW_PROF_TRACE_EXT);
         if (use_smem && (c->persist_mask & 4)) {
           if (count)
-            k_trace_ext_p<true, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
+            k_trace_ext_p<true, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
           else
-            k_trace_ext_p<false, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
+            k_trace_ext_p<false, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
         } else if (use_smem) {
           if (count)
-            k_trace_ext<true, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+            k_trace_ext<true, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
           else
-            k_trace_ext<false, LW_NODES_SMEM><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+            k_trace_ext<false, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         } else {
           if (c->persist && count)
-            k_trace_ext_p<true, LW_NODES_GLOBAL><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
+            k_trace_ext_p<true, LW_NODES_GLOBAL, CMP><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
           else if (c->persist)
-            k_trace_ext_p<false, LW_NODES_GLOBAL><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
+            k_trace_ext_p<false, LW_NODES_GLOBAL, CMP><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
           else if (count)
-            k_trace_ext<true, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+            k_trace_ext<true, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
           else
-            k_trace_ext<false, LW_NODES_GLOBAL><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
+            k_trace_ext<false, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
         }
         mark(LW_PROF_SHADE_NEE);
         if (lpe_on && ltm)
-          k_shade_nee<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade_nee<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         else if (lpe_on)
-          k_shade_nee<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade_nee<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         else if (ltm)
-          k_shade_nee<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade_nee<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         else
-          k_shade_nee<false, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade_nee<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         mark(LW_PROF_SHADE);
         if (lpe_on && ltm)
-          k_shade<true, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         else if (lpe_on)
-          k_shade<true, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         else if (ltm)
-          k_shade<false, true><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         else
-          k_shade<false, false><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+          k_shade<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
         mark(LW_PROF_TRACE_SHADOW);
         if (use_smem)
-          launch_shadow<LW_NODES_SMEM>(c, gT, smem, nr, lpe_on, count);
+          launch_shadow<LW_NODES_SMEM, CMP>(c, gT, smem, nr, lpe_on, count);
         else
-          launch_shadow<LW_NODES_GLOBAL>(c, gT, smem, nr, lpe_on, count);
+          launch_shadow<LW_NODES_GLOBAL, CMP>(c, gT, smem, nr, lpe_on, count);
         mark(LW_PROF_OTHER);
         k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 7;
@@ -1574,9 +1642,9 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
       if (!work_left && h.n_alive == 0) break;
       if (!work_left && p.megakernel_tail > 0 && h.n_alive < p.megakernel_tail) {
         if (lpe_on)
-          k_mega_tail<true><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+          k_mega_tail<true, CMP><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
         else
-          k_mega_tail<false><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+          k_mega_tail<false, CMP><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
         k_tail_done<<<1, 1, 0, st>>>(c->d_cnt);
         launches += 2;
         break;
@@ -1590,7 +1658,7 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
     mark(LW_PROF_OTHER);
     k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1, total, 0);
     mark(LW_PROF_GENERATE);
-    k_generate<false><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
+    k_generate<false, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
     mark(LW_PROF_END);
     launches += 2;
   }
@@ -1638,6 +1706,9 @@ int run_pass(lw_ctx* c, const WorkRange& w) {
   c->stats.regenerations += (int64_t)h.regens;
   return LW_OK;
 }
+
+// compressed path state selects the stage-kernel instantiations (no runtime branch in the FP64 ones)
+int run_pass(lw_ctx* c, const WorkRange& w) { return c->S.compact ? run_pass_t<true>(c, w) : run_pass_t<false>(c, w); }
 
 }  // namespace
 
@@ -2177,6 +2248,7 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   c->S.max_depth = p->max_depth;
   c->S.rr_start = p->rr_start;
   c->S.estimator = p->estimator;
+  c->S.compact = p->compact_state != 0;
   int64_t px = (int64_t)p->width * p->height;
   if (px != c->fb_pixels) {
     free_lpe(c);  // layer framebuffers have the old size

@@ -26,7 +26,7 @@ class RenderParams:
     """Resolution, depth, QMC dimension table and engine knobs (LwRenderParams + owned arrays)."""
 
     def __init__(self, width, height, max_depth=8, rr_start=4, engine="wavefront", pool_log2=24,
-                 regen_fraction=0.5, megakernel_tail=0, estimator="mis"):
+                 regen_fraction=0.5, megakernel_tail=0, estimator="mis", compact_state=False):
         if engine not in ENGINES:
             raise ValueError(f"unknown engine '{engine}'")
         if estimator not in ESTIMATORS:
@@ -48,6 +48,8 @@ class RenderParams:
         s.regen_fraction = float(regen_fraction)
         s.megakernel_tail = int(megakernel_tail)
         s.estimator = ESTIMATORS[estimator]
+        s.compact_state = int(bool(compact_state))
+        self.compact_state = bool(compact_state)
         self.struct = s
         self.engine = engine
 
@@ -60,11 +62,12 @@ class Renderer:
     """Progressive renderer on one GPU."""
 
     def __init__(self, scene, width, height, max_depth=8, device=0, engine="wavefront", p_env=0.5, rr_start=4,
-                 pool_log2=24, regen_fraction=0.5, megakernel_tail=0, packed=None, estimator="mis"):
+                 pool_log2=24, regen_fraction=0.5, megakernel_tail=0, packed=None, estimator="mis",
+                 compact_state=False):
         self.lib = _abi.lib()
         self.packed = packed if packed is not None else pack_scene(scene, p_env=p_env)
         self.params = RenderParams(width, height, max_depth, rr_start, engine, pool_log2, regen_fraction,
-                                   megakernel_tail, estimator)
+                                   megakernel_tail, estimator, compact_state)
         self.device = int(device)
         h = C.c_void_p()
         check(self.lib.lw_ctx_create(self.device, C.byref(h)))
@@ -150,7 +153,7 @@ class Renderer:
             h.update(f"{name}={list(v) if isinstance(v, C.Array) else v!r};".encode())
         p = self.params
         s = p.struct
-        h.update(f"{s.width}x{s.height}d{s.max_depth}rr{s.rr_start}e{s.estimator}".encode())
+        h.update(f"{s.width}x{s.height}d{s.max_depth}rr{s.rr_start}e{s.estimator}c{s.compact_state}".encode())
         for a in (p.bases, p.perm_flat, p.perm_offset):
             h.update(a.tobytes())
         return h.hexdigest()

@@ -350,3 +350,41 @@ def test_cli_checkpoint_resume(gpu, tmp_path):
     assert cli.main(base + ["--iterations", "4", "--out", b, "--checkpoint", ck]) == 0
     assert cli.main(base + ["--iterations", "8", "--out", b, "--resume", ck]) == 0
     assert (read_pfm(a + "_000008.pfm") == read_pfm(b + "_000008.pfm")).all()
+
+
+# ---- compressed path state ---------------------------------
+
+@pytest.mark.parametrize("cfg", ["C1", "C3", "C4", "C5"])
+def test_compact_state_bit_exact_vs_oracle_both_engines(gpu, oracle, cfg):
+    """Oct-16 directions and FP32 throughput / radiance / pdf, quantised where produced: the
+    wavefront (64-byte pool state), the megakernel (registers) and the oracle agree bit for bit."""
+    from paper_1705_01263_b200.render import RenderParams
+
+    c = scenes.CONFIGS[cfg]
+    sc = {"C1": scenes.cornell, "C3": lambda: scenes.soup(1 << 16, n_materials=16),
+          "C4": lambda: scenes.envmap_scene(512, 256, sphere_subdiv=3), "C5": lambda: scenes.many_lights(2000)}[cfg]()
+    packed = pack_scene(sc)
+    W, H = (64, 64) if cfg == "C1" else (192, 108)
+    fbs = []
+    for engine in ("wavefront", "megakernel"):
+        with _renderer(packed, W, H, c.max_depth, engine=engine, compact_state=True, pool_log2=14) as r:
+            r.render_pass(0, 3)
+            fbs.append(r.framebuffer())
+    fb2, _ = oracle.OracleScene(packed).render(RenderParams(W, H, c.max_depth, compact_state=True), 0, 3)
+    assert np.array_equal(fbs[0], fb2) and np.array_equal(fbs[1], fb2)
+    # the compressed state changes bits, not the image: same mean radiance as the FP64 state
+    fb64, _ = oracle.OracleScene(packed).render(RenderParams(W, H, c.max_depth), 0, 3)
+    m_c, m_64 = fb2.astype(np.float64).mean(), fb64.astype(np.float64).mean()
+    assert not np.array_equal(fb2, fb64) and abs(m_c - m_64) <= 0.02 * m_64
+
+
+def test_compact_state_pool_and_tail_invariance(cornell_packed):
+    """Compact state under different pool sizes / regeneration / megakernel tail: identical."""
+    outs = []
+    for cfg in [dict(engine="megakernel"), dict(pool_log2=10), dict(pool_log2=16, regen_fraction=0.0),
+                dict(pool_log2=12, megakernel_tail=3000)]:
+        with _renderer(cornell_packed, 128, 96, 8, compact_state=True, **cfg) as r:
+            r.render_pass(0, 8)
+            outs.append(r.framebuffer())
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
