@@ -11,7 +11,9 @@
  * /root/reference by oracle/Makefile (oracle/_ref/) and against golden
  * vectors generated from the reference (tests/golden/, tests/gen_golden.py).
  * The render path (lwo_render) restates SPEC.md (the reference has no
- * renderer): it is "parity unpinned" beyond the SPEC known answers.
+ * renderer); it and the GPU are pinned to SPEC's known answers by
+ * tests/test_known_answers.py (BSDF / MIS / light and environment pdfs,
+ * estimator equivalence, an independent brute-force integrator).
  */
 #pragma once
 #include <stdint.h>

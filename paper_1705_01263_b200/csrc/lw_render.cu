@@ -12,6 +12,7 @@
 // independent of execution strategy, pool size, switch threshold and GPU count.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <string.h>
 
 #include <algorithm>
@@ -1707,8 +1708,17 @@ int run_pass_t(lw_ctx* c, const WorkRange& w) {
   return LW_OK;
 }
 
+// NVTX range for profilers (nsys / ncu --nvtx): header-only NVTX v3, free when no tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // compressed path state selects the stage-kernel instantiations (no runtime branch in the FP64 ones)
-int run_pass(lw_ctx* c, const WorkRange& w) { return c->S.compact ? run_pass_t<true>(c, w) : run_pass_t<false>(c, w); }
+int run_pass(lw_ctx* c, const WorkRange& w) {
+  NvtxRange r(c->S.compact ? "lw_render_pass (compact state)" : "lw_render_pass");
+  return c->S.compact ? run_pass_t<true>(c, w) : run_pass_t<false>(c, w);
+}
 
 }  // namespace
 
@@ -1864,6 +1874,7 @@ int lw_framebuffer_reduce(lw_ctx* c) {
     return LW_ERR_STATE;
   }
   cudaSetDevice(c->device);
+  NvtxRange nv("lw_framebuffer_reduce");
   NcclApi* api = nccl_api();
   LW_NCCL_TRY(api->all_reduce(c->d_fb, c->d_fb, (size_t)(3 * c->fb_pixels), ncclUint64, ncclSum, c->comm, c->stream));
   if (c->lpe.nlayers > 0)
@@ -1960,6 +1971,7 @@ int lw_ctx_destroy(lw_ctx* c) {
 
 int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   LW_CHECK_ARG(c && d, "null argument");
+  NvtxRange nv("lw_scene_upload");
   LW_CHECK_ARG(d->ntris >= 0 && (d->ntris == 0 || (d->verts && d->normals && d->material)), "bad geometry");
   LW_CHECK_ARG(d->nmaterials > 0 && d->materials, "scene needs at least one material");
   LW_CHECK_ARG(d->nemit >= 0 && (d->nemit == 0 || (d->emit_tri && d->emit_radiance && d->emit_twosided && d->emit_weight)),
