@@ -643,9 +643,11 @@ struct lwo_scene {
   int env_kind;
   int env_w, env_h;
   float* env_img;
-  double* env_prob;
-  int32_t* env_alias;
-  double* env_pdf;
+  double* env_prob;   /* per texel: alias table of its row (conditional over the columns) */
+  int32_t* env_alias; /* per texel: alias column within the row */
+  double* env_pdf;    /* per texel: p(row) * p(column | row) */
+  double* env_rprob;  /* per row: alias table over the row sums (marginal) */
+  int32_t* env_ralias;
   double p_env, p_tri;
   /* environment pyramid (light_sampler & LW_LIGHTS_ENV_PYRAMID) */
   int ep_on, ep_nl, ep_ntop;
@@ -1006,6 +1008,36 @@ static void lt_build(lwo_scene* s, const lw_scene_desc* d) {
 
 static void ep_build(lwo_scene* s, const lw_scene_desc* d);
 
+/* Two-level environment alias table (device: k_env_rows / k_env_marginal / k_env_pdf in
+ * lw_render.cu, built on the GPU at upload): per row, the Vose table of lwo_alias_build over the
+ * row's texel weights (rows of zero weight: prob 1, self alias, pdf 0); over the rows, the Vose
+ * table of the row sums (each summed in column order); texel pdf = p(row) * p(column | row).
+ * Sampling draws the row with the NEE uniform and the column with the rescaled remainder. */
+static int env_alias2_build(const double* w, int W, int H, double* prob, int32_t* alias, double* pdf, double* rprob,
+                            int32_t* ralias) {
+  double* rsum = (double*)malloc(sizeof(double) * H);
+  double* rpdf = (double*)malloc(sizeof(double) * H);
+  for (int r = 0; r < H; r++) {
+    const double* wr = w + (int64_t)r * W;
+    double t = 0.0;
+    for (int c = 0; c < W; c++) t += wr[c];
+    rsum[r] = t;
+    if (lwo_alias_build(wr, W, prob + (int64_t)r * W, alias + (int64_t)r * W, pdf + (int64_t)r * W))
+      for (int c = 0; c < W; c++) {
+        prob[(int64_t)r * W + c] = 1.0;
+        alias[(int64_t)r * W + c] = c;
+        pdf[(int64_t)r * W + c] = 0.0;
+      }
+  }
+  int bad = lwo_alias_build(rsum, H, rprob, ralias, rpdf);
+  if (!bad)
+    for (int r = 0; r < H; r++)
+      for (int c = 0; c < W; c++) pdf[(int64_t)r * W + c] = rpdf[r] * pdf[(int64_t)r * W + c];
+  free(rsum);
+  free(rpdf);
+  return bad;
+}
+
 lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
   lwo_scene* s = (lwo_scene*)calloc(1, sizeof(lwo_scene));
   s->d = *d;
@@ -1061,7 +1093,11 @@ lwo_scene* lwo_scene_create(const lw_scene_desc* d) {
     s->env_prob = (double*)malloc(sizeof(double) * nt);
     s->env_alias = (int32_t*)malloc(sizeof(int32_t) * nt);
     s->env_pdf = (double*)malloc(sizeof(double) * nt);
-    if (lwo_alias_build(d->env_weight, nt, s->env_prob, s->env_alias, s->env_pdf)) s->env_kind = LW_ENV_NONE;
+    s->env_rprob = (double*)malloc(sizeof(double) * s->env_h);
+    s->env_ralias = (int32_t*)malloc(sizeof(int32_t) * s->env_h);
+    if (env_alias2_build(d->env_weight, s->env_w, s->env_h, s->env_prob, s->env_alias, s->env_pdf, s->env_rprob,
+                         s->env_ralias))
+      s->env_kind = LW_ENV_NONE;
   }
   if (s->env_kind == LW_ENV_IMAGE && (d->light_sampler & LW_LIGHTS_ENV_PYRAMID)) ep_build(s, d);
   int has_env = s->env_kind != LW_ENV_NONE;
@@ -1095,6 +1131,8 @@ void lwo_scene_destroy(lwo_scene* s) {
   free(s->env_prob);
   free(s->env_alias);
   free(s->env_pdf);
+  free(s->env_rprob);
+  free(s->env_ralias);
   free(s->ep_lvl);
   free(s->ep_top);
   free(s->lt);
@@ -2037,9 +2075,10 @@ static int nee_light_sample(const lwo_scene* s, v3 p, v3 ngf, double ul, double 
         ep_sample(s, ep_bin(lwo_oct_encode(ngf.x, ngf.y, ngf.z)), ue, vl, &row, &col, &pt, &ur, &vr);
         j = row * s->env_w + col;
       } else {
-        j = alias_sample(s->env_prob, s->env_alias, (int64_t)s->env_w * s->env_h, ue, &ur);
-        row = j / s->env_w;
-        col = j % s->env_w;
+        double u1;
+        row = alias_sample(s->env_rprob, s->env_ralias, s->env_h, ue, &u1);
+        col = alias_sample(s->env_prob + row * s->env_w, s->env_alias + row * s->env_w, s->env_w, u1, &ur);
+        j = row * s->env_w + col;
         vr = vl;
         pt = s->env_pdf[j];
       }

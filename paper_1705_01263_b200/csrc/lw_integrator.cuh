@@ -39,9 +39,11 @@ struct DevScene {
   int env_kind;
   int env_w, env_h;
   const float* env_img;
-  const double* env_prob;
-  const double* env_pdf;
-  const int* env_alias;
+  const double* env_prob;   // per texel: Vose table of its row (column | row)
+  const double* env_pdf;    // per texel: p(row) * p(column | row)
+  const int* env_alias;     // per texel: alias column
+  const double* env_rprob;  // per row: Vose table over the row sums
+  const int* env_ralias;
   double env_const[3];
   double env_scale;
   double p_env, p_tri;
@@ -528,9 +530,12 @@ __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 
         lw_ep_sample(S.env_pyr, lw_ep_bin(lw_oct_encode(ngf.x, ngf.y, ngf.z)), ue, vl, row, col, pt, ur, vr);
         j = row * S.env_w + col;
       } else {
-        j = lw_alias_sample(S.env_prob, S.env_alias, nt, ue, ur);
-        row = j / S.env_w;
-        col = j % S.env_w;
+        // two-level alias table (built on the GPU at upload): row from the marginal table, column
+        // from the row's table with the rescaled remainder of the same uniform
+        double u1;
+        row = lw_alias_sample(S.env_rprob, S.env_ralias, S.env_h, ue, u1);
+        col = lw_alias_sample(S.env_prob + row * S.env_w, S.env_alias + row * S.env_w, S.env_w, u1, ur);
+        j = row * S.env_w + col;
         vr = vl;
         pt = __ldg(S.env_pdf + j);
       }
