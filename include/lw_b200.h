@@ -261,7 +261,13 @@ int lw_scene_upload(lw_ctx* ctx, const lw_scene_desc* scene);
 int lw_render_configure(lw_ctx* ctx, const lw_render_params* params);
 /* clears the fixed-point framebuffer */
 int lw_framebuffer_clear(lw_ctx* ctx);
-/* renders every pixel for iterations [it_begin, it_end) into the framebuffer (asynchronous) */
+/* renders every pixel for iterations [it_begin, it_end) into the framebuffer.  Asynchronous: the
+ * wavefront runs as one CUDA-graph launch whose conditional WHILE node repeats the wave until no
+ * work is left and no path is alive (device-side termination), so the call returns once the pass
+ * is queued on the context's stream; passes, reduces and accumulations queue behind each other.
+ * Statistics / profiles are completed on demand (lw_get_stats, lw_ctx_kernel_profile,
+ * lw_ctx_synchronize), which is also where device faults of the pass are reported.  The
+ * megakernel tail switch (megakernel_tail > 0) and LW_GRAPH=0 use a host-driven loop instead. */
 int lw_render_pass(lw_ctx* ctx, int64_t it_begin, int64_t it_end);
 /* renders pixels [pix_begin, pix_end) only (parity subsets) */
 int lw_render_pass_pixels(lw_ctx* ctx, int64_t it_begin, int64_t it_end, int64_t pix_begin, int64_t pix_end);

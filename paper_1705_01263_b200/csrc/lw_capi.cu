@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "lw_common.cuh"
@@ -471,9 +472,27 @@ __global__ void k_intersect_brute(const double* __restrict__ verts, long long nt
 
 #define S_ cudaStreamPerThread
 
+// stateless entry points allocate from the device's stream-ordered pool; keep freed blocks reserved
+// (release threshold) so repeated batches neither re-map memory nor synchronise in cudaFree
+static void keep_pool() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
 template <class T>
 static int upload(DevBuf& b, const T* host, int64_t count) {
-  LW_CUDA_TRY(b.alloc(sizeof(T) * (count > 0 ? count : 1)));
+  keep_pool();
+  LW_CUDA_TRY(b.alloc(sizeof(T) * (count > 0 ? count : 1), S_));  // stream-ordered pool: no sync, no remap
   if (count > 0) LW_CUDA_TRY(cudaMemcpyAsync(b.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, S_));
   return LW_OK;
 }
@@ -519,9 +538,10 @@ int lw_halton_batch(const int64_t* bases, int64_t ndims, const int64_t* perm_fla
   LW_CHECK_ARG(n >= 0 && (n == 0 || (indices && out)), "bad batch");
   DevBuf b_idx, b_out;
   LW_STATUS_TRY(upload(b_idx, indices, n));
-  LW_CUDA_TRY(b_out.alloc(sizeof(double) * (n > 0 ? n : 1)));
+  LW_CUDA_TRY(b_out.alloc(sizeof(double) * (n > 0 ? n : 1), S_));
   LW_STATUS_TRY(halton_impl(bases, ndims, perm_flat, perm_len, perm_offset, dim, b_idx.as<long long>(), n, b_out.as<double>()));
-  if (n > 0) LW_CUDA_TRY(cudaMemcpy(out, b_out.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (n > 0) LW_CUDA_TRY(cudaMemcpyAsync(out, b_out.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S_));
+  LW_CUDA_TRY(cudaStreamSynchronize(S_));
   return LW_OK;
 }
 
@@ -536,7 +556,7 @@ int lw_pixel_offset_batch(const double* u, int64_t n, double* out) {
   if (n == 0) return LW_OK;
   DevBuf b_u, b_o;
   LW_STATUS_TRY(upload(b_u, u, 2 * n));
-  LW_CUDA_TRY(b_o.alloc(sizeof(double) * 2 * n));
+  LW_CUDA_TRY(b_o.alloc(sizeof(double) * 2 * n, S_));
   k_pixel_offset<<<grid_for(2 * n, 256), 256, 0, S_>>>(b_u.as<double>(), 2 * n, b_o.as<double>());
   LW_CUDA_TRY(cudaGetLastError());
   LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, S_));
@@ -562,7 +582,7 @@ int lw_oct_encode_batch(const double* vecs, int64_t n, int64_t* out) {
   if (n == 0) return LW_OK;
   DevBuf b_v, b_o;
   LW_STATUS_TRY(upload(b_v, vecs, 3 * n));
-  LW_CUDA_TRY(b_o.alloc(sizeof(long long) * n));
+  LW_CUDA_TRY(b_o.alloc(sizeof(long long) * n, S_));
   k_oct_encode<<<grid_for(n, 256), 256, 0, S_>>>(b_v.as<double>(), n, b_o.as<long long>());
   LW_CUDA_TRY(cudaGetLastError());
   LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(long long) * n, cudaMemcpyDeviceToHost, S_));
@@ -575,7 +595,7 @@ int lw_oct_decode_batch(const int64_t* packed, int64_t n, double* out) {
   if (n == 0) return LW_OK;
   DevBuf b_p, b_o;
   LW_STATUS_TRY(upload(b_p, packed, n));
-  LW_CUDA_TRY(b_o.alloc(sizeof(double) * 3 * n));
+  LW_CUDA_TRY(b_o.alloc(sizeof(double) * 3 * n, S_));
   k_oct_decode<<<grid_for(n, 256), 256, 0, S_>>>(b_p.as<long long>(), n, b_o.as<double>());
   LW_CUDA_TRY(cudaGetLastError());
   LW_CUDA_TRY(cudaMemcpyAsync(out, b_o.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, S_));
@@ -615,9 +635,9 @@ int lw_intersect_batch(int mode, const double* bounds, const int64_t* children, 
   LW_STATUS_TRY(upload(b_o, origins, 3 * n));
   LW_STATUS_TRY(upload(b_d, dirs, 3 * n));
   LW_STATUS_TRY(upload(b_tm, tmaxs, n));
-  LW_CUDA_TRY(b_t.alloc(sizeof(double) * n));
-  LW_CUDA_TRY(b_tri.alloc(sizeof(int64_t) * n));
-  LW_CUDA_TRY(b_bary.alloc(sizeof(double) * 2 * n));
+  LW_CUDA_TRY(b_t.alloc(sizeof(double) * n, S_));
+  LW_CUDA_TRY(b_tri.alloc(sizeof(int64_t) * n, S_));
+  LW_CUDA_TRY(b_bary.alloc(sizeof(double) * 2 * n, S_));
   LW_STATUS_TRY(intersect_launch(mode, b_bounds.as<double>(), b_children.as<int64_t>(), b_order.as<int64_t>(),
                                  b_verts.as<double>(), ntris, b_o.as<double>(), b_d.as<double>(), b_tm.as<double>(), n,
                                  b_t.as<double>(), b_tri.as<int64_t>(), b_bary.as<double>()));

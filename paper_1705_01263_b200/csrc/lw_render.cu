@@ -54,7 +54,14 @@ using namespace lw;
 
 namespace {
 
+struct WorkRange {
+  long long it_begin, nits, pix_begin, npix;
+};
+
 struct Counters {
+  WorkRange wr;  // the pass's work (read by k_generate / the wave condition: graph launches stay valid)
+  int gwaves, overflow;  // waves run by the CUDA-graph loop; set if it hit the wave limit
+  int stamp_n;           // LW_INSTR_TIME: stage timestamps written this pass
   unsigned long long work_next;  // next work item (iteration-major over the pixel range)
   int n_ext, n_shadow, n_alive;
   int regen_now;  // decision of the current wave's regeneration step
@@ -88,6 +95,25 @@ struct Pool {
   int *q_ext, *q_shadow;
   void* block = nullptr;
 };
+
+// everything a wave's launches depend on (the CUDA graph is rebuilt when it changes)
+struct WaveCfg {
+  int pool = 0, cmp = 0, lpe_on = 0, ltm = 0, use_smem = 0, count = 0, timed = 0, persist_mask = 0, tail_div = 0;
+  size_t smem = 0, ltsm = 0;
+  void* pool_block = nullptr;
+  long long epoch = -1;
+  bool operator==(const WaveCfg& o) const {
+    return pool == o.pool && cmp == o.cmp && lpe_on == o.lpe_on && ltm == o.ltm && use_smem == o.use_smem &&
+           count == o.count && timed == o.timed && persist_mask == o.persist_mask && tail_div == o.tail_div &&
+           smem == o.smem && ltsm == o.ltsm && pool_block == o.pool_block && epoch == o.epoch;
+  }
+};
+
+constexpr int kStampCap = 1 << 16;  // stage timestamps per pass (7 per wave)
+// per-context device / pinned block: Counters, running statistics, stage timestamps
+constexpr size_t kAccOff = (sizeof(Counters) + 63) / 64 * 64;
+constexpr size_t kStampOff = kAccOff + 64;
+constexpr size_t kCtrBytes = kStampOff + sizeof(unsigned long long) * kStampCap;
 
 }  // namespace
 
@@ -135,6 +161,16 @@ struct lw_ctx {
   lw_kernel_profile prof;
   ncclComm_t comm = nullptr;  // sample-space partition: per-pass framebuffer sum over the ranks
   int comm_rank = 0, comm_world = 1;
+  // CUDA-graph wave loop (device-side termination) and asynchronous pass bookkeeping
+  bool use_graph = getenv("LW_GRAPH") ? atoi(getenv("LW_GRAPH")) != 0 : true;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t wave_exec = nullptr;
+  WaveCfg wave_key;
+  long long epoch = 0;  // bumped by scene upload / configure / LPE changes (parameters baked into the graph)
+  bool pass_pending = false, pass_graph = false, pass_timed = false;
+  int64_t pass_host_launches = 0;
+  unsigned long long *d_acc = nullptr, *h_acc = nullptr;        // running statistics [6]
+  unsigned long long *d_stamps = nullptr, *h_stamps = nullptr;  // stage timestamps of the pass
 };
 
 void free_lpe(lw_ctx* c) {
@@ -535,10 +571,6 @@ __global__ void k_env_pdf(double* __restrict__ pdf, const double* __restrict__ r
 
 // ---- megakernel ----------------------------------------------------------------------------
 
-struct WorkRange {
-  long long it_begin, nits, pix_begin, npix;
-};
-
 __device__ __forceinline__ long long work_index(const DevScene& S, const WorkRange& w, long long item, int& pix) {
   long long it = w.it_begin + item / w.npix;
   long long p = w.pix_begin + item % w.npix;
@@ -710,7 +742,8 @@ __device__ __forceinline__ v3 load_L(const Pool& P, int s, bool compact) {
 // fewer than pool / tail_div paths are alive, the next compaction is the last; later waves reuse
 // that queue (n_ext unchanged), k_generate returns at once and the stage kernels skip entries whose
 // path has finished.  `force` (the final flush) leaves tail mode.
-__global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int force, long long total, int tail_div) {
+__global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int force, int tail_div) {
+  const long long total = cnt->wr.nits * cnt->wr.npix;
   if (force) cnt->tail = cnt->tail_armed = 0;
   if (cnt->tail_armed) cnt->tail = 1;
   int alive = cnt->n_alive;
@@ -741,9 +774,10 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
 // granted_left).  (Block-granular with a barrier per 256 slots, this scan cost ~170 us per wave on
 // C2 even when nothing was left to do; the per-warp form is bound by the stage-byte reads.)
 template <bool LPE, bool CMP>
-__global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, WorkRange w, unsigned long long* __restrict__ fb,
+__global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, unsigned long long* __restrict__ fb,
                                                   Counters* __restrict__ cnt, LwLpe lpe) {
   if (cnt->tail) return;  // tail queue: no compaction, nothing to regenerate
+  const WorkRange w = cnt->wr;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const bool regen = cnt->regen_now != 0;
@@ -1370,6 +1404,40 @@ __global__ void __launch_bounds__(128) k_mega_tail(DevScene S, Pool P, unsigned 
 
 __global__ void k_tail_done(Counters* cnt) { cnt->n_alive = 0; }
 
+// LW_INSTR_TIME: %globaltimer (ns) and the stage starting now, appended to the pass's stamp list;
+// consecutive stamps bracket one stage (works inside CUDA graphs, unlike event records)
+__global__ void k_stamp(unsigned long long* stamps, Counters* cnt, int stage, int cap) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  int i = cnt->stamp_n;
+  if (i < cap) {
+    stamps[i] = (t << 4) | (unsigned long long)stage;
+    cnt->stamp_n = i + 1;
+  }
+}
+
+// end of a wave inside the CUDA-graph loop: run another while work is left or paths are alive
+__global__ void k_wave_cond(Counters* cnt, cudaGraphConditionalHandle h, int max_waves) {
+  const long long total = cnt->wr.nits * cnt->wr.npix;
+  int gw = ++cnt->gwaves;
+  bool more = (long long)cnt->work_next < total || cnt->n_alive > 0;
+  if (more && gw >= max_waves) {
+    cnt->overflow = 1;
+    more = false;
+  }
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// pass totals into the context's running statistics (device-side, so passes can queue up)
+__global__ void k_stats_accum(const Counters* cnt, unsigned long long* acc) {
+  acc[0] += cnt->paths;
+  acc[1] += cnt->rays_ext;
+  acc[2] += cnt->rays_shadow;
+  acc[3] += cnt->nonfinite;
+  acc[4] += cnt->waves;
+  acc[5] += cnt->regens;
+}
+
 // ---- debug / parity kernels -------------------------------------------------------------
 
 __global__ void k_trace_closest_dbg(DevScene S, const double* o, const double* d, const double* tm, long long n,
@@ -1625,8 +1693,7 @@ int alloc_pool(lw_ctx* c, int size) {
 }
 
 template <int NODES, bool CMP>
-void launch_shadow(lw_ctx* c, int grid, size_t smem, int nr, bool lpe_on, bool count) {
-  cudaStream_t st = c->stream;
+void launch_shadow(lw_ctx* c, cudaStream_t st, int grid, size_t smem, int nr, bool lpe_on, bool count) {
   if (NODES == LW_NODES_GLOBAL ? c->persist_sh : (c->persist_mask & 8) != 0) {
     if (lpe_on)
       k_trace_shadow_p<false, true, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, c->lpe);
@@ -1645,173 +1712,148 @@ void launch_shadow(lw_ctx* c, int grid, size_t smem, int nr, bool lpe_on, bool c
     k_trace_shadow<false, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
 }
 
+
+constexpr int kMaxWaves = 100000;   // a pass that needs more waves is reported as an error
+
+void stamp(lw_ctx* c, cudaStream_t st, const WaveCfg& wc, int stage) {
+  if (wc.timed) k_stamp<<<1, 1, 0, st>>>(c->d_stamps, c->d_cnt, stage, kStampCap);
+}
+
+// the launches of one wave (wave decision, regeneration / compaction, the four stage kernels,
+// wave end), identical on the host-loop path and inside the CUDA-graph loop
 template <bool CMP>
-int run_pass_t(lw_ctx* c, const WorkRange& w) {
-  LW_CHECK_ARG(c->has_scene, "render: no scene uploaded");
-  LW_CHECK_ARG(c->configured, "render: lw_render_configure not called");
-  cudaStream_t st = c->stream;
+void enqueue_wave(lw_ctx* c, cudaStream_t st, const WaveCfg& wc) {
   const lw_render_params& p = c->params;
-  int nr = c->nrnodes;
-  int use_smem = c->smem_bytes > 0 ? 1 : 0;
-  size_t smem = c->smem_bytes;
+  const int nr = c->nrnodes;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  Counters zero;
-  memset(&zero, 0, sizeof(zero));
-  LW_CUDA_TRY(cudaMemcpyAsync(c->d_cnt, &zero, sizeof(Counters), cudaMemcpyHostToDevice, st));
-  LW_CUDA_TRY(cudaEventRecord(c->ev0, st));
-  int64_t launches = 0;
-  long long total = w.nits * w.npix;
-  std::vector<std::pair<size_t, int>> marks;
-  if (p.engine == LW_ENGINE_MEGAKERNEL) {
-    int grid = nsm * 8;
-    long long need = (total + 127) / 128;
-    if (need < grid) grid = (int)std::max<long long>(1, need);
-    if (c->lpe.nlayers > 0)
-      k_megakernel<true, CMP><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+  const int gT = nsm * 8, gS = nsm * 8, gR = nsm * 4;
+  const bool lpe_on = wc.lpe_on, ltm = wc.ltm, count = wc.count, use_smem = wc.use_smem;
+  const size_t smem = wc.smem, ltsm = wc.ltsm;
+  stamp(c, st, wc, LW_PROF_OTHER);
+  k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, wc.pool, p.regen_fraction, 0, wc.tail_div);
+  stamp(c, st, wc, LW_PROF_GENERATE);
+  if (lpe_on)
+    k_generate<true, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, c->lpe);
+  else
+    k_generate<false, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, c->lpe);
+  stamp(c, st, wc, LW_PROF_TRACE_EXT);
+  if (use_smem && (wc.persist_mask & 4)) {
+    if (count)
+      k_trace_ext_p<true, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
     else
-      k_megakernel<false, CMP><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
-    LW_CUDA_TRY(cudaGetLastError());
-    launches = 1;
+      k_trace_ext_p<false, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
+  } else if (use_smem) {
+    if (count)
+      k_trace_ext<true, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, 1);
+    else
+      k_trace_ext<false, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, 1);
   } else {
-    const bool lpe_on = c->lpe.nlayers > 0;
-    const size_t ltsm = lt_smem_bytes(c);  // light-hierarchy top staged by the shading kernels
-    const bool ltm = ltsm > 0;
-    int pool = 1 << p.pool_log2;
-    if ((long long)pool > total) {
-      long long r = 1;
-      while (r < total) r <<= 1;
-      pool = (int)std::max<long long>(r, 1024);
-    }
-    LW_STATUS_TRY(alloc_pool(c, pool));
-    // every slot starts free
-    LW_CUDA_TRY(cudaMemsetAsync(c->pool.stage, LW_STAGE_GENERATE, pool, st));
-    const int gT = nsm * 8, gS = nsm * 8, gR = nsm * 4;
-    long long waves = 0;
-    const int check_every = 8;
-    const bool count = (c->instr & LW_INSTR_COUNT) != 0, timed = (c->instr & LW_INSTR_TIME) != 0;
-    size_t ev = 0;
-    auto event = [&](void) -> cudaEvent_t {
-      if (ev >= c->evpool.size()) {
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        c->evpool.push_back(e);
-      }
-      return c->evpool[ev++];
-    };
-    marks.clear();  // (event index, stage starting there: LW_PROF_*)
-    auto mark = [&](int stage) {
-      if (!timed) return;
-      marks.push_back({ev, stage});
-      cudaEventRecord(event(), st);
-    };
-    for (;;) {
-      for (int k = 0; k < check_every; k++) {
-        mark(LW_PROF_OTHER);
-        k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 0, total, c->tail_div);
-        mark(LW_PROF_GENERATE);
-        if (lpe_on)
-          k_generate<true, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
-        else
-          k_generate<false, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
-        mark(LW_PROF_TRACE_EXT);
-        if (use_smem && (c->persist_mask & 4)) {
-          if (count)
-            k_trace_ext_p<true, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
-          else
-            k_trace_ext_p<false, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr);
-        } else if (use_smem) {
-          if (count)
-            k_trace_ext<true, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
-          else
-            k_trace_ext<false, LW_NODES_SMEM, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
-        } else {
-          if (c->persist && count)
-            k_trace_ext_p<true, LW_NODES_GLOBAL, CMP><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
-          else if (c->persist)
-            k_trace_ext_p<false, LW_NODES_GLOBAL, CMP><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
-          else if (count)
-            k_trace_ext<true, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
-          else
-            k_trace_ext<false, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem);
-        }
-        mark(LW_PROF_SHADE_NEE);
-        if (lpe_on && ltm)
-          k_shade_nee<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        else if (lpe_on)
-          k_shade_nee<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        else if (ltm)
-          k_shade_nee<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        else
-          k_shade_nee<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        mark(LW_PROF_SHADE);
-        if (lpe_on && ltm)
-          k_shade<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        else if (lpe_on)
-          k_shade<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        else if (ltm)
-          k_shade<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        else
-          k_shade<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-        mark(LW_PROF_TRACE_SHADOW);
-        if (use_smem)
-          launch_shadow<LW_NODES_SMEM, CMP>(c, gT, smem, nr, lpe_on, count);
-        else
-          launch_shadow<LW_NODES_GLOBAL, CMP>(c, gT, smem, nr, lpe_on, count);
-        mark(LW_PROF_OTHER);
-        k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
-        launches += 7;
-        waves++;
-      }
-      LW_CUDA_TRY(cudaGetLastError());
-      LW_CUDA_TRY(cudaMemcpyAsync(c->h_cnt, c->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-      LW_CUDA_TRY(cudaStreamSynchronize(st));
-      const Counters& h = *c->h_cnt;
-      bool work_left = h.work_next < (unsigned long long)total;
-      if (!work_left && h.n_alive == 0) break;
-      if (!work_left && p.megakernel_tail > 0 && h.n_alive < p.megakernel_tail) {
-        if (lpe_on)
-          k_mega_tail<true, CMP><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
-        else
-          k_mega_tail<false, CMP><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
-        k_tail_done<<<1, 1, 0, st>>>(c->d_cnt);
-        launches += 2;
-        break;
-      }
-      if (waves > 100000) {
-        set_error("wavefront did not terminate");
-        return LW_ERR_STATE;
-      }
-    }
-    // flush the remaining finished paths
-    mark(LW_PROF_OTHER);
-    k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1, total, 0);
-    mark(LW_PROF_GENERATE);
-    k_generate<false, CMP><<<gR, 256, 0, st>>>(c->S, c->pool, w, c->d_fb, c->d_cnt, c->lpe);
-    mark(LW_PROF_END);
-    launches += 2;
+    if (c->persist && count)
+      k_trace_ext_p<true, LW_NODES_GLOBAL, CMP><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
+    else if (c->persist)
+      k_trace_ext_p<false, LW_NODES_GLOBAL, CMP><<<gT, 128, 0, st>>>(c->S, c->pool, c->d_cnt, nr);
+    else if (count)
+      k_trace_ext<true, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, 0);
+    else
+      k_trace_ext<false, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, 0);
   }
-  LW_CUDA_TRY(cudaGetLastError());
-  LW_CUDA_TRY(cudaEventRecord(c->ev1, st));
-  LW_CUDA_TRY(cudaMemcpyAsync(c->h_cnt, c->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  LW_CUDA_TRY(cudaStreamSynchronize(st));
+  stamp(c, st, wc, LW_PROF_SHADE_NEE);
+  if (lpe_on && ltm)
+    k_shade_nee<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (lpe_on)
+    k_shade_nee<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (ltm)
+    k_shade_nee<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else
+    k_shade_nee<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  stamp(c, st, wc, LW_PROF_SHADE);
+  if (lpe_on && ltm)
+    k_shade<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (lpe_on)
+    k_shade<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (ltm)
+    k_shade<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else
+    k_shade<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  stamp(c, st, wc, LW_PROF_TRACE_SHADOW);
+  if (use_smem)
+    launch_shadow<LW_NODES_SMEM, CMP>(c, st, gT, smem, nr, lpe_on, count);
+  else
+    launch_shadow<LW_NODES_GLOBAL, CMP>(c, st, gT, smem, nr, lpe_on, count);
+  stamp(c, st, wc, LW_PROF_OTHER);
+  k_wave_end<<<1, 1, 0, st>>>(c->d_cnt);
+}
+
+// Device-side termination (PAPER.md:599-699 state machine without host round trips): one CUDA
+// graph per wave configuration holding a conditional WHILE node whose body is one wave followed by
+// k_wave_cond, which keeps the loop running while work is left or paths are alive.  A pass is then
+// a handful of stream operations and returns without synchronising.
+template <bool CMP>
+int build_wave_graph(lw_ctx* c, const WaveCfg& wc) {
+  if (c->wave_exec) {
+    cudaGraphExecDestroy(c->wave_exec);
+    c->wave_exec = nullptr;
+  }
+  if (!c->cap_stream) LW_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  LW_CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  cudaGraphNodeParams np = {cudaGraphNodeTypeConditional};
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
+  if (e == cudaSuccess)
+    e = cudaStreamBeginCaptureToGraph(c->cap_stream, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    enqueue_wave<CMP>(c, c->cap_stream, wc);
+    k_wave_cond<<<1, 1, 0, c->cap_stream>>>(c->d_cnt, h, kMaxWaves);
+    cudaGraph_t body;
+    e = cudaStreamEndCapture(c->cap_stream, &body);
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&c->wave_exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c->wave_exec = nullptr;
+    set_error("CUDA graph of the wave loop: %s", cudaGetErrorString(e));
+    return LW_ERR_CUDA;
+  }
+  c->wave_key = wc;
+  return LW_OK;
+}
+
+// Completes the bookkeeping of the last queued pass: waits for the context stream, then fills the
+// per-pass profile (stage times from the timestamps of k_stamp, launches, traversal counters) and
+// the running statistics (accumulated on the device by k_stats_accum) from the pinned mirrors.
+int pass_fold(lw_ctx* c) {
+  if (!c->pass_pending) return LW_OK;
+  c->pass_pending = false;
+  LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const Counters& h = *c->h_cnt;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, c->ev0, c->ev1);
   c->last_total_ms = ms;
-  c->last_launches = launches;
-  const Counters& h = *c->h_cnt;
   memset(&c->prof, 0, sizeof(c->prof));
+  int64_t launches = c->pass_host_launches + 1;  // + k_stats_accum
+  if (c->pass_graph) launches += (int64_t)h.gwaves * 8;  // 7 wave kernels + the loop condition
+  if (c->pass_timed) {
+    int n = std::min(h.stamp_n, kStampCap);
+    launches += n;
+    for (int k = 0; k + 1 < n; k++) {
+      int sg = (int)(c->h_stamps[k] & 15u);
+      if (sg == LW_PROF_END) continue;
+      c->prof.stage_ms[sg] += (double)((c->h_stamps[k + 1] >> 4) - (c->h_stamps[k] >> 4)) * 1e-6;
+      if (sg != LW_PROF_OTHER) c->prof.stage_launches[sg]++;
+    }
+  }
   c->prof.total_ms = ms;
   c->prof.kernel_launches = launches;
-  // consecutive marks bracket one stage each; a stage's launch count is the number of its marks
-  for (size_t k = 0; k + 1 < marks.size(); k++) {
-    int sg = marks[k].second;
-    if (sg == LW_PROF_END) continue;
-    float e = 0.f;
-    cudaEventElapsedTime(&e, c->evpool[marks[k].first], c->evpool[marks[k + 1].first]);
-    c->prof.stage_ms[sg] += e;
-    if (sg != LW_PROF_OTHER) c->prof.stage_launches[sg]++;
-  }
+  c->last_launches = launches;
   c->prof.trace_ext_ms = c->prof.stage_ms[LW_PROF_TRACE_EXT];
   c->prof.trace_shadow_ms = c->prof.stage_ms[LW_PROF_TRACE_SHADOW];
   c->prof.trace_ext_launches = c->prof.stage_launches[LW_PROF_TRACE_EXT];
@@ -1827,12 +1869,129 @@ int run_pass_t(lw_ctx* c, const WorkRange& w) {
   c->prof.shadow_nodes = (int64_t)h.sh_nodes;
   c->prof.shadow_tris = (int64_t)h.sh_tris;
   c->prof.shadow_unoccluded = (int64_t)h.sh_unocc;
-  c->stats.paths += (int64_t)h.paths;
-  c->stats.rays_extension += (int64_t)h.rays_ext;
-  c->stats.rays_shadow += (int64_t)h.rays_shadow;
-  c->stats.nonfinite += (int64_t)h.nonfinite;
-  c->stats.waves += (int64_t)h.waves;
-  c->stats.regenerations += (int64_t)h.regens;
+  c->stats.paths = (int64_t)c->h_acc[0];
+  c->stats.rays_extension = (int64_t)c->h_acc[1];
+  c->stats.rays_shadow = (int64_t)c->h_acc[2];
+  c->stats.nonfinite = (int64_t)c->h_acc[3];
+  c->stats.waves = (int64_t)c->h_acc[4];
+  c->stats.regenerations = (int64_t)c->h_acc[5];
+  if (h.overflow) {
+    set_error("wavefront did not terminate");
+    return LW_ERR_STATE;
+  }
+  return LW_OK;
+}
+
+template <bool CMP>
+int run_pass_t(lw_ctx* c, const WorkRange& w) {
+  LW_CHECK_ARG(c->has_scene, "render: no scene uploaded");
+  LW_CHECK_ARG(c->configured, "render: lw_render_configure not called");
+  // no wait for a previous pass: passes queue on the stream; the profile describes the last one and
+  // the running statistics accumulate on the device
+  cudaStream_t st = c->stream;
+  const lw_render_params& p = c->params;
+  int nr = c->nrnodes;
+  int use_smem = c->smem_bytes > 0 ? 1 : 0;
+  size_t smem = c->smem_bytes;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  Counters zero;
+  memset(&zero, 0, sizeof(zero));
+  zero.wr = w;
+  LW_CUDA_TRY(cudaMemcpyAsync(c->d_cnt, &zero, sizeof(Counters), cudaMemcpyHostToDevice, st));
+  LW_CUDA_TRY(cudaEventRecord(c->ev0, st));
+  long long total = w.nits * w.npix;
+  c->pass_graph = false;
+  c->pass_timed = false;
+  c->pass_host_launches = 0;
+  if (p.engine == LW_ENGINE_MEGAKERNEL) {
+    int grid = nsm * 8;
+    long long need = (total + 127) / 128;
+    if (need < grid) grid = (int)std::max<long long>(1, need);
+    if (c->lpe.nlayers > 0)
+      k_megakernel<true, CMP><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+    else
+      k_megakernel<false, CMP><<<grid, 128, smem, st>>>(c->S, w, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+    LW_CUDA_TRY(cudaGetLastError());
+    c->pass_host_launches = 1;
+  } else {
+    WaveCfg wc;
+    wc.lpe_on = c->lpe.nlayers > 0;
+    wc.ltsm = lt_smem_bytes(c);  // light-hierarchy top staged by the shading kernels
+    wc.ltm = wc.ltsm > 0;
+    int pool = 1 << p.pool_log2;
+    if ((long long)pool > total) {
+      long long r = 1;
+      while (r < total) r <<= 1;
+      pool = (int)std::max<long long>(r, 1024);
+    }
+    LW_STATUS_TRY(alloc_pool(c, pool));
+    wc.pool = pool;
+    wc.cmp = CMP;
+    wc.use_smem = use_smem;
+    wc.smem = smem;
+    wc.count = (c->instr & LW_INSTR_COUNT) != 0;
+    wc.timed = (c->instr & LW_INSTR_TIME) != 0;
+    wc.persist_mask = c->persist_mask;
+    wc.tail_div = c->tail_div;
+    wc.pool_block = c->pool.block;
+    wc.epoch = c->epoch;
+    // every slot starts free
+    LW_CUDA_TRY(cudaMemsetAsync(c->pool.stage, LW_STAGE_GENERATE, pool, st));
+    const bool graph = c->use_graph && p.megakernel_tail == 0;
+    if (graph) {
+      if (!c->wave_exec || !(c->wave_key == wc)) LW_STATUS_TRY(build_wave_graph<CMP>(c, wc));
+      LW_CUDA_TRY(cudaGraphLaunch(c->wave_exec, st));
+      c->pass_graph = true;
+    } else {  // host loop: checks the counters every 8 waves (megakernel tail switch, LW_GRAPH=0)
+      const int check_every = 8;
+      long long waves = 0;
+      for (;;) {
+        for (int k = 0; k < check_every; k++) {
+          enqueue_wave<CMP>(c, st, wc);
+          c->pass_host_launches += 7;
+          waves++;
+        }
+        LW_CUDA_TRY(cudaGetLastError());
+        LW_CUDA_TRY(cudaMemcpyAsync(c->h_cnt, c->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        LW_CUDA_TRY(cudaStreamSynchronize(st));
+        const Counters& h = *c->h_cnt;
+        bool work_left = h.work_next < (unsigned long long)total;
+        if (!work_left && h.n_alive == 0) break;
+        if (!work_left && p.megakernel_tail > 0 && h.n_alive < p.megakernel_tail) {
+          if (wc.lpe_on)
+            k_mega_tail<true, CMP><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+          else
+            k_mega_tail<false, CMP><<<nsm * 4, 128, smem, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, nr, use_smem, c->lpe);
+          k_tail_done<<<1, 1, 0, st>>>(c->d_cnt);
+          c->pass_host_launches += 2;
+          break;
+        }
+        if (waves > kMaxWaves) {
+          set_error("wavefront did not terminate");
+          return LW_ERR_STATE;
+        }
+      }
+    }
+    // flush the remaining finished paths
+    stamp(c, st, wc, LW_PROF_OTHER);
+    k_wave_begin<<<1, 1, 0, st>>>(c->d_cnt, pool, p.regen_fraction, 1, 0);
+    stamp(c, st, wc, LW_PROF_GENERATE);
+    k_generate<false, CMP><<<nsm * 4, 256, 0, st>>>(c->S, c->pool, c->d_fb, c->d_cnt, c->lpe);
+    stamp(c, st, wc, LW_PROF_END);
+    c->pass_host_launches += 2;
+    c->pass_timed = wc.timed;
+  }
+  LW_CUDA_TRY(cudaGetLastError());
+  LW_CUDA_TRY(cudaEventRecord(c->ev1, st));
+  k_stats_accum<<<1, 1, 0, st>>>(c->d_cnt, c->d_acc);
+  LW_CUDA_TRY(cudaMemcpyAsync(c->h_cnt, c->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaMemcpyAsync(c->h_acc, c->d_acc, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
+  if (c->pass_timed && p.engine != LW_ENGINE_MEGAKERNEL)
+    LW_CUDA_TRY(cudaMemcpyAsync(c->h_stamps, c->d_stamps, sizeof(unsigned long long) * kStampCap,
+                                cudaMemcpyDeviceToHost, st));
+  LW_CUDA_TRY(cudaGetLastError());
+  c->pass_pending = true;
   return LW_OK;
 }
 
@@ -1880,8 +2039,8 @@ cudaError_t take_res(int device, CtxRes& r) {
   r.d_cnt = r.h_cnt = nullptr;
   r.ev0 = r.ev1 = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&r.d_cnt, sizeof(Counters));
-  if (e == cudaSuccess) e = cudaMallocHost(&r.h_cnt, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaMalloc(&r.d_cnt, kCtrBytes);
+  if (e == cudaSuccess) e = cudaMallocHost(&r.h_cnt, kCtrBytes);
   if (e == cudaSuccess) e = cudaEventCreate(&r.ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&r.ev1);
   return e;
@@ -2052,6 +2211,17 @@ int lw_ctx_create(int device, lw_ctx** out) {
   c->own_stream = c->stream = r.stream;
   c->d_cnt = r.d_cnt;
   c->h_cnt = r.h_cnt;
+  c->d_acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(r.d_cnt) + kAccOff);
+  c->h_acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(r.h_cnt) + kAccOff);
+  c->d_stamps = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(r.d_cnt) + kStampOff);
+  c->h_stamps = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(r.h_cnt) + kStampOff);
+  memset(c->h_acc, 0, 64);
+  if (cudaMemsetAsync(c->d_acc, 0, 64, c->stream) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    set_error("context creation failed");
+    give_res(r);
+    delete c;
+    return LW_ERR_CUDA;
+  }
   c->ev0 = r.ev0;
   c->ev1 = r.ev1;
   *out = c;
@@ -2060,6 +2230,7 @@ int lw_ctx_create(int device, lw_ctx** out) {
 
 int lw_ctx_set_stream(lw_ctx* c, void* stream) {
   LW_CHECK_ARG(c, "null ctx");
+  LW_STATUS_TRY(pass_fold(c));
   LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
   c->stream = stream ? (cudaStream_t)stream : c->own_stream;
   return LW_OK;
@@ -2073,6 +2244,7 @@ int lw_ctx_set_instrumentation(lw_ctx* c, int flags) {
 
 int lw_ctx_kernel_profile(lw_ctx* c, lw_kernel_profile* out) {
   LW_CHECK_ARG(c && out, "null argument");
+  LW_STATUS_TRY(pass_fold(c));
   *out = c->prof;
   return LW_OK;
 }
@@ -2080,6 +2252,7 @@ int lw_ctx_kernel_profile(lw_ctx* c, lw_kernel_profile* out) {
 int lw_ctx_destroy(lw_ctx* c) {
   if (!c) return LW_OK;
   cudaSetDevice(c->device);
+  pass_fold(c);
   cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   free_scene(c);
@@ -2091,6 +2264,8 @@ int lw_ctx_destroy(lw_ctx* c) {
   if (c->d_qperm) cudaFreeAsync(c->d_qperm, c->stream);
   cudaStreamSynchronize(c->stream);
   if (c->comm) nccl_api()->destroy(c->comm);
+  if (c->wave_exec) cudaGraphExecDestroy(c->wave_exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   CtxRes r{c->device, c->own_stream, c->d_cnt, c->h_cnt, c->ev0, c->ev1};
   give_res(r);
   delete c;
@@ -2105,7 +2280,9 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   LW_CHECK_ARG(d->nemit >= 0 && (d->nemit == 0 || (d->emit_tri && d->emit_radiance && d->emit_twosided && d->emit_weight)),
                "bad emitter arrays");
   cudaSetDevice(c->device);
+  LW_STATUS_TRY(pass_fold(c));
   free_scene(c);
+  c->epoch++;  // scene pointers are baked into the wave graph
   cudaStream_t st = c->stream;
   DevScene& S = c->S;
   int64_t n = d->ntris;
@@ -2398,6 +2575,7 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
   LW_CUDA_TRY(cudaMemcpyAsync(c->d_qdims, dims.data(), sizeof(QmcDim) * dims.size(), cudaMemcpyHostToDevice, c->stream));
   LW_CUDA_TRY(cudaMemcpyAsync(c->d_qperm, perm.data(), sizeof(uint16_t) * perm.size(), cudaMemcpyHostToDevice, c->stream));
   LW_CUDA_TRY(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  c->epoch++;
   c->params = *p;
   c->params.bases = nullptr;
   c->params.perm_flat = nullptr;
@@ -2425,6 +2603,9 @@ int lw_render_configure(lw_ctx* c, const lw_render_params* p) {
 
 int lw_framebuffer_clear(lw_ctx* c) {
   LW_CHECK_ARG(c && c->configured, "not configured");
+  LW_STATUS_TRY(pass_fold(c));
+  LW_CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 64, c->stream));
+  memset(c->h_acc, 0, 64);
   LW_CUDA_TRY(cudaMemsetAsync(c->d_fb, 0, sizeof(unsigned long long) * 3 * c->fb_pixels, c->stream));
   if (c->lpe.nlayers > 0)
     LW_CUDA_TRY(cudaMemsetAsync(c->lpe.fb, 0, sizeof(unsigned long long) * 3 * c->lpe.npix * c->lpe.nlayers, c->stream));
@@ -2455,6 +2636,7 @@ int lw_render_pass_pixels(lw_ctx* c, int64_t it_begin, int64_t it_end, int64_t p
 
 int lw_ctx_synchronize(lw_ctx* c) {
   LW_CHECK_ARG(c, "null ctx");
+  LW_STATUS_TRY(pass_fold(c));
   LW_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return LW_OK;
 }
@@ -2503,12 +2685,14 @@ int lw_framebuffer_load_device(lw_ctx* c, const void* src) {
 
 int lw_get_stats(lw_ctx* c, lw_render_stats* s) {
   LW_CHECK_ARG(c && s, "null argument");
+  LW_STATUS_TRY(pass_fold(c));
   *s = c->stats;
   return LW_OK;
 }
 
 int lw_ctx_last_pass_timing(lw_ctx* c, double* trace_ms, double* total_ms, int64_t* launches) {
   LW_CHECK_ARG(c, "null ctx");
+  LW_STATUS_TRY(pass_fold(c));
   if (trace_ms) *trace_ms = c->last_trace_ms;
   if (total_ms) *total_ms = c->last_total_ms;
   if (launches) *launches = c->last_launches;
@@ -2742,6 +2926,8 @@ int lw_ctx_set_lpe(lw_ctx* c, int32_t nlayers, int32_t nstates, const int16_t* t
                    int32_t start) {
   LW_CHECK_ARG(c && c->configured, "lw_render_configure must precede lw_ctx_set_lpe");
   cudaSetDevice(c->device);
+  LW_STATUS_TRY(pass_fold(c));
+  c->epoch++;  // the layer tables are baked into the wave graph
   free_lpe(c);
   if (nlayers == 0) return LW_OK;
   LW_CHECK_ARG(nlayers > 0 && nlayers <= 8 && nstates > 0 && trans && accept && start >= 0 && start < nstates,

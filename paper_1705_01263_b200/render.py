@@ -101,7 +101,9 @@ class Renderer:
         self.iterations = 0
 
     def render_pass(self, it_begin, it_end, pix_begin=0, pix_end=None):
-        """Accumulate iterations [it_begin, it_end) (optionally a pixel range) into the framebuffer."""
+        """Accumulate iterations [it_begin, it_end) (optionally a pixel range) into the framebuffer.
+        Asynchronous: returns once the pass is queued (one CUDA-graph launch with device-side
+        termination); framebuffer(), image(), stats() and synchronize() wait for it."""
         if pix_end is None:
             pix_end = self.params.pixels
         check(self.lib.lw_render_pass_pixels(self.ctx, int(it_begin), int(it_end), int(pix_begin), int(pix_end)))

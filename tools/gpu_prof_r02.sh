@@ -18,4 +18,12 @@ timeout 900 $N -k 'regex:k_shadeILb0ELb0ELb0E' -s 9 -c 1 -o gpurun_out/r02_C4_sh
 bash tools/gpu_kernel_traffic.sh
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/launches_C3.csv $B --config C3 > /dev/null 2>&1
-ls -la gpurun_out/*.ncu-rep
+# summaries on the box (gpurun brings back at most 64 MiB: the reports themselves stay there)
+for r in gpurun_out/r02_*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  python tools/ncu_summary.py $r --json gpurun_out/${b}_summary.json > /dev/null 2>&1
+  k=$(echo $b | sed -e 's/r02_C[0-9]_//')
+  python tools/ncu_lines.py $r "k_${k}" 40 > gpurun_out/${b}_lines.txt 2>&1
+done
+rm -f gpurun_out/*.ncu-rep
+ls -la gpurun_out/
