@@ -388,3 +388,92 @@ def test_compact_state_pool_and_tail_invariance(cornell_packed):
             outs.append(r.framebuffer())
     for o in outs[1:]:
         assert np.array_equal(outs[0], o)
+
+
+# ---- asynchronous passes: the CUDA-graph wave loop ------------------------------
+
+def test_queued_passes_equal_one_pass_and_host_loop(cornell_packed, monkeypatch):
+    """Passes queued back to back without a host sync (graph path) == one pass == the host-driven
+    loop (LW_GRAPH=0), bit for bit; the running statistics count every path."""
+    W, H = 96, 64
+    with _renderer(cornell_packed, W, H, 8, pool_log2=12) as r:
+        for a in range(0, 12, 3):
+            r.render_pass(a, a + 3)  # returns once queued
+        fb_q = r.framebuffer()
+        st = r.stats()
+    assert st["paths"] == W * H * 12
+    with _renderer(cornell_packed, W, H, 8, pool_log2=12) as r:
+        r.render_pass(0, 12)
+        fb_1 = r.framebuffer()
+    monkeypatch.setenv("LW_GRAPH", "0")
+    with _renderer(cornell_packed, W, H, 8, pool_log2=12) as r:
+        r.render_pass(0, 12)
+        fb_h = r.framebuffer()
+    assert np.array_equal(fb_q, fb_1) and np.array_equal(fb_1, fb_h)
+
+
+def test_stage_timing_inside_the_graph(cornell_packed):
+    """LW_INSTR_TIME stamps every stage inside the graph: every stage has time and launches, and
+    the stage times add up to at most the pass time."""
+    with _renderer(cornell_packed, 256, 256, 8) as r:
+        r.set_instrumentation(time_kernels=True)
+        r.render_pass(0, 16)
+        kp = r.kernel_profile()
+    for st in ("generate", "trace_ext", "shade_nee", "shade", "trace_shadow"):
+        assert kp["stage_ms"][st] > 0 and kp["stage_launches"][st] >= 1, st
+    assert sum(kp["stage_ms"].values()) <= kp["total_ms"] * 1.05
+    assert kp["ext_rays"] > 0 and kp["paths"] == 256 * 256 * 16
+
+
+def test_checkpoint_refuses_other_camera_material_or_environment(cornell_packed, tmp_path):
+    """The checkpoint fingerprint covers camera, materials, environment and sampler choices, not
+    only the geometry: a checkpoint is refused by a render that would produce a different image."""
+    from paper_1705_01263_b200.scene import make_camera
+
+    ck = str(tmp_path / "ck.npz")
+    with _renderer(cornell_packed, 32, 32, 4) as r:
+        r.render_pass(0, 2)
+        r.save_checkpoint(ck)
+    base = scenes.cornell()
+    moved = scenes.cornell()
+    moved.camera = make_camera((0.5, 0.55, 2.5), (0.5, 0.5, 0.0), fov_y=45.0)
+    tinted = scenes.cornell()
+    tinted.materials[2].nodes[0].value = (0.7, 0.75, 0.75)
+    env = scenes.cornell()
+    env.environment = Environment(constant=(0.1, 0.1, 0.1))
+    for variant in (pack_scene(moved), pack_scene(tinted), pack_scene(env), pack_scene(base, lights="tree")):
+        with _renderer(variant, 32, 32, 4) as r:
+            with pytest.raises(ValueError):
+                r.load_checkpoint(ck)
+    with _renderer(pack_scene(base), 32, 32, 4, compact_state=True) as r:  # different state layout
+        with pytest.raises(ValueError):
+            r.load_checkpoint(ck)
+    with _renderer(pack_scene(base), 32, 32, 4, engine="megakernel") as r:  # same image: accepted
+        r.load_checkpoint(ck)
+
+
+def test_checkpoint_resume_with_lpe_layers(cornell_packed, tmp_path):
+    """Checkpoints carry the LPE layer framebuffers: a resumed render's layers equal an
+    uninterrupted one's; a renderer with different layers refuses the checkpoint."""
+    ck = str(tmp_path / "ck.npz")
+    layers = {"direct": "C.?L", "all": "C.*[LE]"}
+    with _renderer(cornell_packed, 32, 32, 5) as r:
+        r.set_lpe_layers(layers)
+        r.render_pass(0, 4)
+        r.save_checkpoint(ck)
+    with _renderer(cornell_packed, 32, 32, 5) as r:  # layers restored from the checkpoint
+        r.load_checkpoint(ck)
+        r.render_pass(4, 8)
+        resumed = r.layer_framebuffers()
+        fb_resumed = r.framebuffer()
+    with _renderer(cornell_packed, 32, 32, 5) as r:
+        r.set_lpe_layers(layers)
+        r.render_pass(0, 8)
+        ref = r.layer_framebuffers()
+        assert np.array_equal(r.framebuffer(), fb_resumed)
+    for k in layers:
+        assert np.array_equal(resumed[k], ref[k]) and ref[k].sum() > 0
+    with _renderer(cornell_packed, 32, 32, 5) as r:
+        r.set_lpe_layers({"other": "C.*E"})
+        with pytest.raises(ValueError):
+            r.load_checkpoint(ck)
