@@ -28,8 +28,17 @@ namespace lw {
 
 namespace {
 
-constexpr int kBins = 16;
-constexpr int kMaxLeaf = 7;
+#ifndef LW_SAH_BINS
+#define LW_SAH_BINS 16
+#endif
+#ifndef LW_SAH_MAXLEAF
+#define LW_SAH_MAXLEAF 7
+#endif
+#ifndef LW_SAH_CTRAV
+#define LW_SAH_CTRAV 1.0
+#endif
+constexpr int kBins = LW_SAH_BINS;      // centroid bins per axis
+constexpr int kMaxLeaf = LW_SAH_MAXLEAF; // segments above this size are always split (leaf count field: <= 7)
 constexpr int kSmall = 32;   // segments up to this size are binned by one thread
 constexpr int kChunk = 1024; // positions per block in the large-segment binning pass
 
@@ -334,7 +343,7 @@ __global__ void k_sah_decide(const SSeg* __restrict__ seg, int nseg, const int* 
   }
   if (r.axis >= 0) {
     double aB = area6(g.B);
-    r.split = (g.n > kMaxLeaf || (aB + best) < (double)g.n * aB) ? 1 : 0;
+    r.split = (g.n > kMaxLeaf || (LW_SAH_CTRAV * aB + best) < (double)g.n * aB) ? 1 : 0;
   } else if (g.n > kMaxLeaf) {
     r.split = 1;  // coincident centroids: halve in the current order
     r.axis = -1;
@@ -495,7 +504,7 @@ __global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int
       r.CR[k] = CR[k];
     }
     double aB = area6(g.B);
-    r.split = (g.n > kMaxLeaf || (aB + wc) < (double)g.n * aB) ? 1 : 0;
+    r.split = (g.n > kMaxLeaf || (LW_SAH_CTRAV * aB + wc) < (double)g.n * aB) ? 1 : 0;
   } else {
     if (lane != 0) return;
     if (g.n > kMaxLeaf) {
