@@ -14,7 +14,7 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "n
         "msecond": 1e3, "ms": 1e3}
 # timed instantiations only (the <true>/<1> COUNT variants run in bench.py's untimed pass)
 PATTERNS = {
-    "k_generate": r"k_generate<(0|false)>",
+    "k_generate": r"k_generate<(0|false)[,>]",
     "k_trace_ext_p": r"k_trace_ext(_p)?<(0|false), ",
     "k_shade_nee": r"k_shade_nee<",
     "k_shade": r"k_shade<",
