@@ -166,6 +166,7 @@ struct lw_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t wave_exec = nullptr;
   WaveCfg wave_key;
+  WaveCfg last_key;  // configuration of the previous wavefront pass
   long long epoch = 0;  // bumped by scene upload / configure / LPE changes (parameters baked into the graph)
   bool pass_pending = false, pass_graph = false, pass_timed = false;
   int64_t pass_host_launches = 0;
@@ -1938,7 +1939,11 @@ int run_pass_t(lw_ctx* c, const WorkRange& w) {
     wc.epoch = c->epoch;
     // every slot starts free
     LW_CUDA_TRY(cudaMemsetAsync(c->pool.stage, LW_STAGE_GENERATE, pool, st));
-    const bool graph = c->use_graph && p.megakernel_tail == 0;
+    // the graph is captured when a configuration is used a second time: a context that renders a
+    // single pass (one job per context) does not pay the capture / instantiation
+    const bool ready = c->wave_exec && c->wave_key == wc;
+    const bool graph = c->use_graph && p.megakernel_tail == 0 && (ready || c->last_key == wc);
+    c->last_key = wc;
     if (graph) {
       if (!c->wave_exec || !(c->wave_key == wc)) LW_STATUS_TRY(build_wave_graph<CMP>(c, wc));
       LW_CUDA_TRY(cudaGraphLaunch(c->wave_exec, st));
