@@ -9,6 +9,7 @@ multi-GPU rendering partitions QMC sample space (distributed.py).
 from __future__ import annotations
 
 import ctypes as C
+import functools
 
 import numpy as np
 
@@ -22,6 +23,18 @@ ESTIMATORS = {"mis": _abi.LW_EST_MIS, "nee": _abi.LW_EST_NEE, "bsdf": _abi.LW_ES
 FB_SCALE = float(1 << _abi.LW_FB_FRAC_BITS)
 
 
+@functools.lru_cache(maxsize=None)
+def _dimension_table(depth: int):
+    """DimensionTable(depth) and its int64 arrays, built once per depth (qmc.py:274-305 is a pure
+    function of the depth; building it costs milliseconds of Python per Renderer otherwise).  The
+    arrays are shared read-only."""
+    t = DimensionTable(depth)
+    arrs = [np.ascontiguousarray(a, dtype=np.int64) for a in (t.bases, t.perm_flat, t.perm_offset)]
+    for a in arrs:
+        a.setflags(write=False)
+    return (t, *arrs)
+
+
 class RenderParams:
     """Resolution, depth, QMC dimension table and engine knobs (LwRenderParams + owned arrays)."""
 
@@ -32,10 +45,7 @@ class RenderParams:
         if estimator not in ESTIMATORS:
             raise ValueError(f"unknown estimator '{estimator}' (mis, nee, bsdf)")
         self.width, self.height, self.max_depth = int(width), int(height), int(max_depth)
-        self.table = DimensionTable(max(self.max_depth, 1))
-        self.bases = np.ascontiguousarray(self.table.bases, dtype=np.int64)
-        self.perm_flat = np.ascontiguousarray(self.table.perm_flat, dtype=np.int64)
-        self.perm_offset = np.ascontiguousarray(self.table.perm_offset, dtype=np.int64)
+        self.table, self.bases, self.perm_flat, self.perm_offset = _dimension_table(max(self.max_depth, 1))
         s = LwRenderParams()
         s.width, s.height, s.max_depth, s.rr_start = self.width, self.height, self.max_depth, int(rr_start)
         s.ndims = len(self.bases)
