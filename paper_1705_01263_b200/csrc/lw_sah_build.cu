@@ -378,11 +378,24 @@ __global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int
                                const BinAcc* __restrict__ bins, const int* __restrict__ ids,
                                const double* __restrict__ tb, const double* __restrict__ cen,
                                SSplit* __restrict__ out, int* __restrict__ split_flag) {
+  // small segments (<= 32 triangles): lane k holds triangle k, and the bins of an axis are built
+  // with ordered-u64 min / max atomics in this warp's shared-memory slice (exact, order-free: the
+  // same boxes and counts as the sequential loop, which had every lane re-read every triangle)
+  __shared__ unsigned long long sbin[4][kBins][13];
   const int s = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31, bin = lane & 15;
+  const int lane = threadIdx.x & 31, bin = lane & 15, wib = (threadIdx.x >> 5) & 3;
   if (s >= nseg) return;  // uniform per warp
   const SSeg g = seg[s];
   const int lr = large_rank[s];
+  const bool mine = lr < 0 && lane < g.n;
+  double mtb[6], mcn[3];
+  if (mine) {
+    int t = ids[g.start + lane];
+#pragma unroll
+    for (int k = 0; k < 6; k++) mtb[k] = tb[6 * (size_t)t + k];
+#pragma unroll
+    for (int k = 0; k < 3; k++) mcn[k] = cen[3 * (size_t)t + k];
+  }
   double best = INFINITY;
   int bkey = 1 << 30, bnl = 0;
   double L[6], R[6], CL[6], CR[6];
@@ -404,14 +417,37 @@ __global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int
           cb[k] = unordd(src.v[7 + k]);
         }
       } else {
-        for (int k = 0; k < g.n; k++) {
-          int t = ids[g.start + k];
-          const double* ct = cen + 3 * (size_t)t;
-          if (bin_of(ct[a], g.C[a], scale) != bin) continue;
-          cnt++;
-          box_grow(bb, tb + 6 * (size_t)t, tb + 6 * (size_t)t + 3);
-          box_grow(cb, ct, ct);
+        unsigned long long* mine_bin = sbin[wib][bin];
+        if (lane < kBins) {  // empty bin: the init values of k_sah_bins_init (decode to NaN bounds)
+          mine_bin[0] = 0ULL;
+#pragma unroll
+          for (int k = 0; k < 3; k++) {
+            mine_bin[1 + k] = ~0ULL;
+            mine_bin[4 + k] = 0ULL;
+            mine_bin[7 + k] = ~0ULL;
+            mine_bin[10 + k] = 0ULL;
+          }
         }
+        __syncwarp();
+        if (mine) {
+          unsigned long long* d = sbin[wib][bin_of(mcn[a], g.C[a], scale)];
+          atomicAdd(d, 1ULL);
+#pragma unroll
+          for (int k = 0; k < 3; k++) {
+            atomicMin(d + 1 + k, ordd(mtb[k]));
+            atomicMax(d + 4 + k, ordd(mtb[3 + k]));
+            atomicMin(d + 7 + k, ordd(mcn[k]));
+            atomicMax(d + 10 + k, ordd(mcn[k]));
+          }
+        }
+        __syncwarp();
+        cnt = (int)mine_bin[0];
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          bb[k] = unordd(mine_bin[1 + k]);
+          cb[k] = unordd(mine_bin[7 + k]);
+        }
+        __syncwarp();
       }
       // inclusive prefix (bins 0..bin) and suffix (bins bin..15)
       // scans start from the empty box grown by the bin's box, as the sequential sweep does: an
