@@ -374,13 +374,98 @@ __global__ void k_sah_decide(const SSeg* __restrict__ seg, int nseg, const int* 
 __device__ __forceinline__ double shfl_up_d(double v, int off) { return __shfl_up_sync(0xffffffffu, v, off, 16); }
 __device__ __forceinline__ double shfl_down_d(double v, int off) { return __shfl_down_sync(0xffffffffu, v, off, 16); }
 
-__global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int* __restrict__ large_rank,
+#ifndef LW_SAH_DEC_MINB
+#define LW_SAH_DEC_MINB 4
+#endif
+// bin `bin` of axis a of segment g: count, triangle-bounds box, centroid box.  Large segments read
+// the pre-binned accumulators; small ones (lane k holds triangle k) bin with ordered-u64 min / max
+// atomics in this warp's shared-memory slice (exact and order-free: the same boxes and counts as a
+// sequential loop).  An empty bin decodes to NaN bounds, which box_grow ignores.
+__device__ __forceinline__ void sah_bin_data(const SSeg& g, int lr, int a, double scale, int bin, int lane, bool mine,
+                                             const double mtb[6], const double mcn[3], const BinAcc* __restrict__ bins,
+                                             unsigned long long (*sb)[13], int& cnt, double bb[6], double cb[6]) {
+  if (lr >= 0) {
+    const BinAcc& src = bins[(size_t)lr * 3 * kBins + a * kBins + bin];
+    cnt = (int)src.v[0];
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      bb[k] = unordd(src.v[1 + k]);
+      cb[k] = unordd(src.v[7 + k]);
+    }
+    return;
+  }
+  if (lane < kBins) {
+    unsigned long long* e = sb[bin];
+    e[0] = 0ULL;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      e[1 + k] = ~0ULL;
+      e[4 + k] = 0ULL;
+      e[7 + k] = ~0ULL;
+      e[10 + k] = 0ULL;
+    }
+  }
+  __syncwarp();
+  if (mine) {
+    unsigned long long* d = sb[bin_of(mcn[a], g.C[a], scale)];
+    atomicAdd(d, 1ULL);
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      atomicMin(d + 1 + k, ordd(mtb[k]));
+      atomicMax(d + 4 + k, ordd(mtb[3 + k]));
+      atomicMin(d + 7 + k, ordd(mcn[k]));
+      atomicMax(d + 10 + k, ordd(mcn[k]));
+    }
+  }
+  __syncwarp();
+  const unsigned long long* e = sb[bin];
+  cnt = (int)e[0];
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    bb[k] = unordd(e[1 + k]);
+    cb[k] = unordd(e[7 + k]);
+  }
+  __syncwarp();
+}
+
+// inclusive prefix (bins 0..bin) and suffix (bins bin..15) of one box quantity over the half-warp,
+// started from the empty box grown by the bin's box as the sequential sweep does
+__device__ __forceinline__ void sah_scan_boxes(const double bx[6], int bin, double pb[6], double sb[6]) {
+  box_reset(pb);
+  box_grow(pb, bx, bx + 3);
+#pragma unroll
+  for (int k = 0; k < 6; k++) sb[k] = pb[k];
+#pragma unroll
+  for (int off = 1; off < kBins; off <<= 1) {
+    double ub[6], db[6];
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      ub[k] = shfl_up_d(pb[k], off);
+      db[k] = shfl_down_d(sb[k], off);
+    }
+    if (bin >= off) box_grow(pb, ub, ub + 3);
+    if (bin + off < kBins) box_grow(sb, db, db + 3);
+  }
+}
+
+__device__ __forceinline__ void sah_scan_counts(int cnt, int bin, int& pn, int& sn) {
+  pn = sn = cnt;
+#pragma unroll
+  for (int off = 1; off < kBins; off <<= 1) {
+    int un = __shfl_up_sync(0xffffffffu, pn, off, 16), dn = __shfl_down_sync(0xffffffffu, sn, off, 16);
+    if (bin >= off) pn += un;
+    if (bin + off < kBins) sn += dn;
+  }
+}
+
+// Two passes keep the live state small (206 -> ~100 registers): pass 1 scans counts and bounds of
+// every axis and keeps only (cost, key, nl) of each lane's best plane; after the warp argmin, pass 2
+// recomputes the winning axis' bins and scans to produce the four boxes of the split.  Every value
+// is the same expression of the same inputs as in the single pass, so the split is unchanged.
+__global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int* __restrict__ large_rank,
                                const BinAcc* __restrict__ bins, const int* __restrict__ ids,
                                const double* __restrict__ tb, const double* __restrict__ cen,
                                SSplit* __restrict__ out, int* __restrict__ split_flag) {
-  // small segments (<= 32 triangles): lane k holds triangle k, and the bins of an axis are built
-  // with ordered-u64 min / max atomics in this warp's shared-memory slice (exact, order-free: the
-  // same boxes and counts as the sequential loop, which had every lane re-read every triangle)
   __shared__ unsigned long long sbin[4][kBins][13];
   const int s = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, bin = lane & 15, wib = (threadIdx.x >> 5) & 3;
@@ -398,114 +483,27 @@ __global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int
   }
   double best = INFINITY;
   int bkey = 1 << 30, bnl = 0;
-  double L[6], R[6], CL[6], CR[6];
   if (g.n > 1) {
     for (int a = 0; a < 3; a++) {
       double ext = g.C[3 + a] - g.C[a];
       if (!(ext > 0.0)) continue;
       double scale = (double)kBins / ext;
-      int cnt = 0;
-      double bb[6], cb[6];
-      box_reset(bb);
-      box_reset(cb);
-      if (lr >= 0) {
-        const BinAcc& src = bins[(size_t)lr * 3 * kBins + a * kBins + bin];
-        cnt = (int)src.v[0];
-#pragma unroll
-        for (int k = 0; k < 6; k++) {
-          bb[k] = unordd(src.v[1 + k]);
-          cb[k] = unordd(src.v[7 + k]);
-        }
-      } else {
-        unsigned long long* mine_bin = sbin[wib][bin];
-        if (lane < kBins) {  // empty bin: the init values of k_sah_bins_init (decode to NaN bounds)
-          mine_bin[0] = 0ULL;
-#pragma unroll
-          for (int k = 0; k < 3; k++) {
-            mine_bin[1 + k] = ~0ULL;
-            mine_bin[4 + k] = 0ULL;
-            mine_bin[7 + k] = ~0ULL;
-            mine_bin[10 + k] = 0ULL;
-          }
-        }
-        __syncwarp();
-        if (mine) {
-          unsigned long long* d = sbin[wib][bin_of(mcn[a], g.C[a], scale)];
-          atomicAdd(d, 1ULL);
-#pragma unroll
-          for (int k = 0; k < 3; k++) {
-            atomicMin(d + 1 + k, ordd(mtb[k]));
-            atomicMax(d + 4 + k, ordd(mtb[3 + k]));
-            atomicMin(d + 7 + k, ordd(mcn[k]));
-            atomicMax(d + 10 + k, ordd(mcn[k]));
-          }
-        }
-        __syncwarp();
-        cnt = (int)mine_bin[0];
-#pragma unroll
-        for (int k = 0; k < 6; k++) {
-          bb[k] = unordd(mine_bin[1 + k]);
-          cb[k] = unordd(mine_bin[7 + k]);
-        }
-        __syncwarp();
-      }
-      // inclusive prefix (bins 0..bin) and suffix (bins bin..15)
-      // scans start from the empty box grown by the bin's box, as the sequential sweep does: an
-      // empty large-segment bin decodes to NaN bounds, which box_grow ignores
-      int pn = cnt, sn = cnt;
-      double pb[6], pc[6], sb[6], sc[6];
-      box_reset(pb);
-      box_reset(pc);
-      box_grow(pb, bb, bb + 3);
-      box_grow(pc, cb, cb + 3);
-#pragma unroll
-      for (int k = 0; k < 6; k++) {
-        sb[k] = pb[k];
-        sc[k] = pc[k];
-      }
-#pragma unroll
-      for (int off = 1; off < kBins; off <<= 1) {
-        int un = __shfl_up_sync(0xffffffffu, pn, off, 16), dn = __shfl_down_sync(0xffffffffu, sn, off, 16);
-        double ub[6], uc[6], db[6], dc[6];
-#pragma unroll
-        for (int k = 0; k < 6; k++) {
-          ub[k] = shfl_up_d(pb[k], off);
-          uc[k] = shfl_up_d(pc[k], off);
-          db[k] = shfl_down_d(sb[k], off);
-          dc[k] = shfl_down_d(sc[k], off);
-        }
-        if (bin >= off) {
-          pn += un;
-          box_grow(pb, ub, ub + 3);
-          box_grow(pc, uc, uc + 3);
-        }
-        if (bin + off < kBins) {
-          sn += dn;
-          box_grow(sb, db, db + 3);
-          box_grow(sc, dc, dc + 3);
-        }
-      }
+      int cnt, pn, sn;
+      double bb[6], cb[6], pb[6], sb[6];
+      sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbin[wib], cnt, bb, cb);
+      sah_scan_counts(cnt, bin, pn, sn);
+      sah_scan_boxes(bb, bin, pb, sb);
       // right side of plane p = bin: the suffix of bin + 1
       int rn = __shfl_down_sync(0xffffffffu, sn, 1, 16);
-      double rb[6], rc[6];
+      double rb[6];
 #pragma unroll
-      for (int k = 0; k < 6; k++) {
-        rb[k] = shfl_down_d(sb[k], 1);
-        rc[k] = shfl_down_d(sc[k], 1);
-      }
+      for (int k = 0; k < 6; k++) rb[k] = shfl_down_d(sb[k], 1);
       if (bin < kBins - 1 && pn != 0 && rn != 0) {
         double cost = area6(pb) * (double)pn + area6(rb) * (double)rn;
         if (cost < best) {
           best = cost;
           bkey = a * (kBins - 1) + bin;
           bnl = pn;
-#pragma unroll
-          for (int k = 0; k < 6; k++) {
-            L[k] = pb[k];
-            CL[k] = pc[k];
-            R[k] = rb[k];
-            CR[k] = rc[k];
-          }
         }
       }
     }
@@ -528,16 +526,30 @@ __global__ void k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int
   r.plane = -1;
   r.nl = 0;
   if (wk < (1 << 30)) {
-    if (lane != (wk % (kBins - 1))) return;  // the owning lane of group 0 writes the split
-    r.axis = wk / (kBins - 1);
-    r.plane = wk % (kBins - 1);
+    // pass 2: the winning axis again, now with the centroid boxes (whole warp, uniform)
+    const int a = wk / (kBins - 1), plane = wk % (kBins - 1);
+    double scale = (double)kBins / (g.C[3 + a] - g.C[a]);
+    int cnt;
+    double bb[6], cb[6], pb[6], sb[6], pc[6], sc[6];
+    sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbin[wib], cnt, bb, cb);
+    sah_scan_boxes(bb, bin, pb, sb);
+    sah_scan_boxes(cb, bin, pc, sc);
+    double rb[6], rc[6];
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      rb[k] = shfl_down_d(sb[k], 1);
+      rc[k] = shfl_down_d(sc[k], 1);
+    }
+    if (lane != plane) return;  // the owning lane of group 0 writes the split
+    r.axis = a;
+    r.plane = plane;
     r.nl = bnl;
 #pragma unroll
     for (int k = 0; k < 6; k++) {
-      r.L[k] = L[k];
-      r.CL[k] = CL[k];
-      r.R[k] = R[k];
-      r.CR[k] = CR[k];
+      r.L[k] = pb[k];
+      r.CL[k] = pc[k];
+      r.R[k] = rb[k];
+      r.CR[k] = rc[k];
     }
     double aB = area6(g.B);
     r.split = (g.n > kMaxLeaf || (LW_SAH_CTRAV * aB + wc) < (double)g.n * aB) ? 1 : 0;
