@@ -56,6 +56,7 @@ namespace {
 
 struct WorkRange {
   long long it_begin, nits, pix_begin, npix;
+  long long tiles_x;  // > 0: whole frame enumerated in 8x4-pixel tiles (tiles_x tiles per row)
 };
 
 struct Counters {
@@ -572,9 +573,20 @@ __global__ void k_env_pdf(double* __restrict__ pdf, const double* __restrict__ r
 
 // ---- megakernel ----------------------------------------------------------------------------
 
+// work item -> (iteration, pixel) -> QMC sample index.  A whole frame is enumerated in 8x4-pixel
+// tiles, so the 32 paths a warp generates (and, through the slot-ordered queues, traces and
+// shades) cover a compact patch instead of a 32x1 strip; the sample index of a (pixel, iteration)
+// is unchanged, so is every result.
 __device__ __forceinline__ long long work_index(const DevScene& S, const WorkRange& w, long long item, int& pix) {
   long long it = w.it_begin + item / w.npix;
-  long long p = w.pix_begin + item % w.npix;
+  long long q = item % w.npix;
+  long long p;
+  if (w.tiles_x > 0) {
+    long long t = q >> 5, r = q & 31;
+    p = ((t / w.tiles_x) * 4 + (r >> 3)) * (long long)S.W + (t % w.tiles_x) * 8 + (r & 7);
+  } else {
+    p = w.pix_begin + q;
+  }
   pix = (int)p;
   return it * ((long long)S.W * S.H) + p;
 }
@@ -2635,7 +2647,11 @@ int lw_render_pass_pixels(lw_ctx* c, int64_t it_begin, int64_t it_end, int64_t p
     return LW_ERR_OVERFLOW;
   }
   cudaSetDevice(c->device);
-  WorkRange w{it_begin, it_end - it_begin, pix_begin, pix_end - pix_begin};
+  WorkRange w{it_begin, it_end - it_begin, pix_begin, pix_end - pix_begin, 0};
+  // whole frames are enumerated in 8x4 tiles (LW_TILES=0: row order; results are identical)
+  static const bool tiles = getenv("LW_TILES") ? atoi(getenv("LW_TILES")) != 0 : true;
+  if (tiles && pix_begin == 0 && pix_end == c->fb_pixels && c->params.width % 8 == 0 && c->params.height % 4 == 0)
+    w.tiles_x = c->params.width / 8;
   return run_pass(c, w);
 }
 
