@@ -56,7 +56,8 @@ namespace {
 
 struct WorkRange {
   long long it_begin, nits, pix_begin, npix;
-  long long tiles_x;  // > 0: whole frame enumerated in 8x4-pixel tiles (tiles_x tiles per row)
+  long long tiles_x;  // > 0: whole frame enumerated in tiles of tw x th pixels x ti iterations (32 items)
+  int tw, th, ti;
 };
 
 struct Counters {
@@ -578,14 +579,17 @@ __global__ void k_env_pdf(double* __restrict__ pdf, const double* __restrict__ r
 // shades) cover a compact patch instead of a 32x1 strip; the sample index of a (pixel, iteration)
 // is unchanged, so is every result.
 __device__ __forceinline__ long long work_index(const DevScene& S, const WorkRange& w, long long item, int& pix) {
-  long long it = w.it_begin + item / w.npix;
-  long long q = item % w.npix;
-  long long p;
+  long long it, p;
   if (w.tiles_x > 0) {
-    long long t = q >> 5, r = q & 31;
-    p = ((t / w.tiles_x) * 4 + (r >> 3)) * (long long)S.W + (t % w.tiles_x) * 8 + (r & 7);
+    // iteration block, then tile, then the 32 items of the tile (pixel-minor)
+    const long long blk = item / (w.npix * w.ti), q = item % (w.npix * w.ti);
+    const long long t = q >> 5;
+    const int r = (int)(q & 31), tp = w.tw * w.th, ri = r / tp, rp = r % tp;
+    it = w.it_begin + blk * w.ti + ri;
+    p = ((t / w.tiles_x) * w.th + rp / w.tw) * (long long)S.W + (t % w.tiles_x) * w.tw + rp % w.tw;
   } else {
-    p = w.pix_begin + q;
+    it = w.it_begin + item / w.npix;
+    p = w.pix_begin + item % w.npix;
   }
   pix = (int)p;
   return it * ((long long)S.W * S.H) + p;
@@ -2647,11 +2651,23 @@ int lw_render_pass_pixels(lw_ctx* c, int64_t it_begin, int64_t it_end, int64_t p
     return LW_ERR_OVERFLOW;
   }
   cudaSetDevice(c->device);
-  WorkRange w{it_begin, it_end - it_begin, pix_begin, pix_end - pix_begin, 0};
-  // whole frames are enumerated in 8x4 tiles (LW_TILES=0: row order; results are identical)
+  WorkRange w{it_begin, it_end - it_begin, pix_begin, pix_end - pix_begin, 0, 1, 1, 1};
+  // whole frames are enumerated in tiles of 32 items: 8x4 pixels, or with LW_TILE_ITS = 2 / 4 / 8
+  // iterations of 4x4 / 4x2 / 2x2 pixels (LW_TILES=0: row order); the sample index of a
+  // (pixel, iteration) -- hence the image -- does not depend on the order
   static const bool tiles = getenv("LW_TILES") ? atoi(getenv("LW_TILES")) != 0 : true;
-  if (tiles && pix_begin == 0 && pix_end == c->fb_pixels && c->params.width % 8 == 0 && c->params.height % 4 == 0)
-    w.tiles_x = c->params.width / 8;
+  static const int tis = getenv("LW_TILE_ITS") ? atoi(getenv("LW_TILE_ITS")) : 8;
+  int ti = (tis == 1 || tis == 2 || tis == 4 || tis == 8 || tis == 16 || tis == 32) ? tis : 8;
+  while (ti > 1 && (it_end - it_begin) % ti != 0) ti >>= 1;  // the pass's iterations split into blocks
+  static const int tws[6] = {8, 4, 4, 2, 2, 1};  // tile width for ti = 1, 2, 4, 8, 16, 32
+  const int tw = tws[__builtin_ctz(ti)], th = 32 / (ti * tw);
+  if (tiles && pix_begin == 0 && pix_end == c->fb_pixels && c->params.width % tw == 0 &&
+      c->params.height % th == 0 && (it_end - it_begin) % ti == 0) {
+    w.tiles_x = c->params.width / tw;
+    w.tw = tw;
+    w.th = th;
+    w.ti = ti;
+  }
   return run_pass(c, w);
 }
 
