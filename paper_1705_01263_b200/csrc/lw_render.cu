@@ -31,7 +31,7 @@ using namespace lw;
 // persistent trace kernels: refill when >= LW_REFILL lanes of a warp are idle; speculative
 // traversal in the persistent kernels (LW_SPEC) and in the one-ray-per-thread kernels (LW_SPEC_SMEM)
 #ifndef LW_REFILL
-#define LW_REFILL 16
+#define LW_REFILL 24
 #endif
 #ifndef LW_SPEC
 #define LW_SPEC 3  // bit 0: extension rays, bit 1: shadow rays
