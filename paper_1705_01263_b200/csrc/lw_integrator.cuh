@@ -57,6 +57,29 @@ struct DevScene {
   const uint16_t* qperm;
 };
 
+// Scene classes: the shading kernels are compiled per class of the uploaded scene (the
+// JIT-compiled material code of PAPER.md:416-418; the layered BSDF itself stays generic, one code
+// path for every thread).  Each bit folds a scene-wide property to a constant:
+//   LW_MC_DIFFUSE  every material is one uncoated diffuse layer (layer count / kind / coat);
+//   LW_MC_NOENV    no environment (env_kind == LW_ENV_NONE);
+//   LW_MC_ALIAS    emitters chosen by the alias table (light_mode != LW_LIGHTS_TREE).
+// The arithmetic executed is the same, so results are identical; the dead code and its registers
+// disappear.  0 (LW_MC_ANY) evaluates anything.  (A class for "diffuse + glossy layers only"
+// spilled more than LW_MC_ANY and was dropped.)
+#define LW_MC_ANY 0
+#define LW_MC_DIFFUSE 1
+#define LW_MC_NOENV 2
+#define LW_MC_ALIAS 4
+template <int MC>
+__device__ __forceinline__ int lw_mat_nlayers(const lw_material& m) { return (MC & LW_MC_DIFFUSE) ? 1 : m.nlayers; }
+template <int MC>
+__device__ __forceinline__ int lw_layer_kind(const lw_layer& L) { return (MC & LW_MC_DIFFUSE) ? LW_BSDF_DIFFUSE : L.kind; }
+template <int MC>
+__device__ __forceinline__ int lw_env_kind(const DevScene& S) { return (MC & LW_MC_NOENV) ? LW_ENV_NONE : S.env_kind; }
+template <int MC>
+__device__ __forceinline__ int lw_light_mode(const DevScene& S) { return (MC & LW_MC_ALIAS) ? LW_LIGHTS_ALIAS : S.light_mode; }
+
+
 struct PathState {
   v3 o, d;
   v3 beta, L;
@@ -162,12 +185,14 @@ __device__ __forceinline__ v3 lw_offset_origin(v3 p, v3 n, v3 dir) {
 }
 
 // nprev: packed facing normal of the vertex the ray left (selects the pyramid's top levels)
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ v3 lw_env_eval(const DevScene& S, v3 d, int nprev, double& pdf) {
-  if (S.env_kind == LW_ENV_CONSTANT) {
+  const int env_kind = lw_env_kind<MC>(S);
+  if (env_kind == LW_ENV_CONSTANT) {
     pdf = S.p_env * LW_INV_FOUR_PI;
     return mk3(S.env_const[0] * S.env_scale, S.env_const[1] * S.env_scale, S.env_const[2] * S.env_scale);
   }
-  if (S.env_kind == LW_ENV_IMAGE) {
+  if (env_kind == LW_ENV_IMAGE) {
     double phi = lw_atan2(d.z, d.x);
     if (phi < 0.0) phi = phi + LW_TWO_PI;
     double sin_t = sqrt(d.x * d.x + d.z * d.z);
@@ -235,6 +260,11 @@ __device__ __forceinline__ double lw_schlick(double cosv, double ior) {
   return f0 + (1.0 - f0) * (m2 * m2 * m);
 }
 
+// (the scene class MC and its accessors are defined with DevScene above)
+template <int MC>
+__device__ __forceinline__ int lw_layer_coat(const lw_layer& L) { return (MC & LW_MC_DIFFUSE) ? 0 : L.coat; }
+
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ void lw_layer_weights(const lw_material& m, double cos_o, LayerW& lw) {
   double r = 1.0;
   lw.sum_a = 0.0;
@@ -242,13 +272,14 @@ __device__ __forceinline__ void lw_layer_weights(const lw_material& m, double co
 #pragma unroll
   for (int l = 0; l < LW_MAX_LAYERS; l++) {
     lw.a[l] = 0.0;
-    if (l >= m.nlayers) continue;
+    if (l >= lw_mat_nlayers<MC>(m)) continue;
     const lw_layer& L = m.layers[l];
-    double a = L.coat ? r * (L.weight * lw_schlick(cos_o, m.ior)) : r * L.weight;
+    const int kind = lw_layer_kind<MC>(L);
+    double a = lw_layer_coat<MC>(L) ? r * (L.weight * lw_schlick(cos_o, m.ior)) : r * L.weight;
     lw.a[l] = a;
     r = r - a;
     lw.sum_a = lw.sum_a + a;
-    if (a > 0.0 && (L.kind == LW_BSDF_DIFFUSE || L.kind == LW_BSDF_GLOSSY)) lw.nonspec = 1;
+    if (a > 0.0 && (kind == LW_BSDF_DIFFUSE || kind == LW_BSDF_GLOSSY)) lw.nonspec = 1;
   }
   lw.inv_sum = lw.sum_a > 0.0 ? 1.0 / lw.sum_a : 0.0;
 }
@@ -269,22 +300,24 @@ __device__ __forceinline__ double lw_alpha_of(const lw_layer& L) {
   return a;
 }
 
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& lw, v3 wo, v3 wi, double& pdf) {
   v3 f = mk3(0.0, 0.0, 0.0);
   pdf = 0.0;
   if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return f;
 #pragma unroll
   for (int l = 0; l < LW_MAX_LAYERS; l++) {
-    if (l >= m.nlayers) break;
+    if (l >= lw_mat_nlayers<MC>(m)) break;
     const lw_layer& L = m.layers[l];
+    const int kind = lw_layer_kind<MC>(L);
     double a = lw.a[l];
     if (!(a > 0.0)) continue;
     double sel = a * lw.inv_sum;
-    if (L.kind == LW_BSDF_DIFFUSE) {
+    if (kind == LW_BSDF_DIFFUSE) {
       double k = a * LW_INV_PI;
       f = f + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
       pdf = pdf + sel * (wi.z * LW_INV_PI);
-    } else if (L.kind == LW_BSDF_GLOSSY) {
+    } else if (kind == LW_BSDF_GLOSSY) {
       double al = lw_alpha_of(L);
       v3 h = normalize3(wo + wi);
       double D = lw_ggx_d(al, h.z);
@@ -299,6 +332,7 @@ __device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& l
 }
 
 // the diffuse and glossy parts of lw_bsdf_eval's f (LPE routing of NEE contributions)
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ void lw_bsdf_eval_split(const lw_material& m, const LayerW& lw, v3 wo, v3 wi, v3& fd,
                                                    v3& fg) {
   fd = mk3(0.0, 0.0, 0.0);
@@ -306,14 +340,15 @@ __device__ __forceinline__ void lw_bsdf_eval_split(const lw_material& m, const L
   if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return;
 #pragma unroll
   for (int l = 0; l < LW_MAX_LAYERS; l++) {
-    if (l >= m.nlayers) break;
+    if (l >= lw_mat_nlayers<MC>(m)) break;
     const lw_layer& L = m.layers[l];
+    const int kind = lw_layer_kind<MC>(L);
     double a = lw.a[l];
     if (!(a > 0.0)) continue;
-    if (L.kind == LW_BSDF_DIFFUSE) {
+    if (kind == LW_BSDF_DIFFUSE) {
       double k = a * LW_INV_PI;
       fd = fd + mk3(L.tint[0] * k, L.tint[1] * k, L.tint[2] * k);
-    } else if (L.kind == LW_BSDF_GLOSSY) {
+    } else if (kind == LW_BSDF_GLOSSY) {
       double al = lw_alpha_of(L);
       v3 h = normalize3(wo + wi);
       double D = lw_ggx_d(al, h.z);
@@ -340,6 +375,7 @@ struct BSample {
   int event;  // LPE event of the sampled lobe (LW_EV_RD / RG / RS / TS)
 };
 
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const LayerW& lw, v3 wo, bool front, double u,
                                                double v, BSample& bs) {
   if (!(lw.sum_a > 0.0) || wo.z <= 0.0) return false;
@@ -349,7 +385,7 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
   bool done = false;
 #pragma unroll
   for (int l = 0; l < LW_MAX_LAYERS; l++) {
-    if (done || l >= m.nlayers || !(lw.a[l] > 0.0)) continue;
+    if (done || l >= lw_mat_nlayers<MC>(m) || !(lw.a[l] > 0.0)) continue;
     prev = cum;
     cum = cum + lw.a[l];
     pick = l;
@@ -361,15 +397,16 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
   if (ur < 0.0) ur = 0.0;
   if (ur >= 1.0) ur = 0.9999999999999999;
   const lw_layer& L = m.layers[pick];
+  const int kind = lw_layer_kind<MC>(L);
   bs.delta = 0;
   bs.transmit = 0;
-  bs.event = L.kind == LW_BSDF_DIFFUSE ? LW_EV_RD : (L.kind == LW_BSDF_GLOSSY ? LW_EV_RG : LW_EV_RS);
-  if (L.kind == LW_BSDF_DIFFUSE) {
+  bs.event = kind == LW_BSDF_DIFFUSE ? LW_EV_RD : (kind == LW_BSDF_GLOSSY ? LW_EV_RG : LW_EV_RS);
+  if (kind == LW_BSDF_DIFFUSE) {
     double r = sqrt(ur), sp, cp;
     lw_sincos2pi(v, &sp, &cp);
     double z = 1.0 - ur;
     bs.wi = mk3(r * cp, r * sp, sqrt(z > 0.0 ? z : 0.0));
-  } else if (L.kind == LW_BSDF_GLOSSY) {
+  } else if (kind == LW_BSDF_GLOSSY) {
     double al = lw_alpha_of(L);
     double tan2 = al * al * ur / (1.0 - ur);
     double ch = 1.0 / sqrt(1.0 + tan2);
@@ -380,7 +417,7 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
     v3 h = mk3(sh * cp, sh * sp, ch);
     double oh = dot3(wo, h);
     bs.wi = h * (2.0 * oh) - wo;
-  } else if (L.kind == LW_BSDF_SPECULAR_REFLECT) {
+  } else if (kind == LW_BSDF_SPECULAR_REFLECT) {
     bs.wi = mk3(-wo.x, -wo.y, wo.z);
     bs.delta = 1;
     bs.weight = mk3(lw.sum_a * L.tint[0], lw.sum_a * L.tint[1], lw.sum_a * L.tint[2]);
@@ -407,7 +444,7 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
   }
   if (bs.wi.z <= 0.0) return false;
   double pdf;
-  v3 f = lw_bsdf_eval(m, lw, wo, bs.wi, pdf);
+  v3 f = lw_bsdf_eval<MC>(m, lw, wo, bs.wi, pdf);
   if (!(pdf > 0.0)) return false;
   double k = bs.wi.z / pdf;
   bs.weight = mk3(f.x * k, f.y * k, f.z * k);
@@ -482,6 +519,7 @@ __device__ __forceinline__ void lw_shade_hit(const DevScene& S, v3 d, const LwHi
 }
 
 // shading frame, material and layer weights (vertices with a scattering event)
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const LwHit& h, double w, ShadeGeom& g) {
   const double* nn = S.normals + 9 * h.tri;
   v3 ns = bary3(lw_ld3(nn), lw_ld3(nn + 3), lw_ld3(nn + 6), w, h.bu, h.bv);
@@ -494,7 +532,7 @@ __device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const Lw
   g.fr = lw_make_frame(ns);
   g.wol = lw_to_local(g.fr, wo);
   g.m = &S.materials[S.material[h.tri]];  // read in place (no local-memory copy)
-  lw_layer_weights(*g.m, g.wol.z, g.lw);
+  lw_layer_weights<MC>(*g.m, g.wol.z, g.lw);
 }
 
 // light half of next-event estimation (SPEC.md:204-230 sample_light / sample_env): from the point p
@@ -502,6 +540,7 @@ __device__ __forceinline__ void lw_shade_frame(const DevScene& S, v3 d, const Lw
 // an emitter and a direction wi towards it; Le its radiance, pl the solid-angle pdf of wi (selection
 // probabilities included), tmax the shadow-ray length (INFINITY for the environment), e the emitter
 // (-1: environment).  Returns false when the sample carries no light (back side, sin(theta) = 0).
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 ngf, double ul, double vl,
                                                     const LwLightTree* lt, v3& wi, v3& Le, double& pl,
                                                     double& tmax_sh, long long& e_out) {
@@ -511,9 +550,10 @@ __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 
   tmax_sh = INFINITY;
   e_out = -1;
   bool ok = false;
-  if (S.env_kind != LW_ENV_NONE && ul < S.p_env) {
+  const int env_kind = lw_env_kind<MC>(S);
+  if (env_kind != LW_ENV_NONE && ul < S.p_env) {
     double ue = S.nemit > 0 ? ul / S.p_env : ul;
-    if (S.env_kind == LW_ENV_CONSTANT) {
+    if (env_kind == LW_ENV_CONSTANT) {
       double z = 1.0 - 2.0 * ue;
       double r2 = 1.0 - z * z;
       double r = sqrt(r2 > 0.0 ? r2 : 0.0), sp, cp;
@@ -554,10 +594,10 @@ __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 
       }
     }
   } else if (S.nemit > 0) {
-    double ut = S.env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
+    double ut = env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
     double ur, psel;
     long long le;
-    if (S.light_mode == LW_LIGHTS_TREE) {
+    if (lw_light_mode<MC>(S) == LW_LIGHTS_TREE) {
       v3 xr = lw_offset_origin(p, ngf, ngf);
       v3 nr = lw_lt_ref_normal((int)lw_oct_encode(ngf.x, ngf.y, ngf.z));
       le = lw_lt_sample(lt ? *lt : S.lt, xr, nr, ut, psel, ur);
@@ -593,10 +633,11 @@ __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 
 // solid-angle light-sampling pdf of emitter e reached by a ray from `o` (leaving a vertex whose
 // packed facing normal is nprev) that hits it at distance t with geometric normal ng along d: the
 // MIS counterpart of lw_nee_light_sample for BSDF-sampled emitter hits (SPEC.md:213-221 light_pdf)
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ double lw_emitter_hit_pdf(const DevScene& S, long long e, v3 o, int nprev, v3 ng, v3 d,
                                                      double t, const LwLightTree* lt) {
   double cos_l = fabs(dot3(ng, d));
-  double psel = S.light_mode == LW_LIGHTS_TREE ? lw_lt_pdf(lt ? *lt : S.lt, e, o, lw_lt_ref_normal(nprev))
+  double psel = lw_light_mode<MC>(S) == LW_LIGHTS_TREE ? lw_lt_pdf(lt ? *lt : S.lt, e, o, lw_lt_ref_normal(nprev))
                                                : S.emit_pdf[e];
   double pdf_area = S.p_tri * psel / S.emit_area[e];
   return pdf_area * (t * t) / cos_l;
@@ -604,23 +645,24 @@ __device__ __forceinline__ double lw_emitter_hit_pdf(const DevScene& S, long lon
 
 // next-event estimation: fills sh (valid = 0 if no contribution)
 // lt: the light hierarchy with its top staged in shared memory (nullptr: S.lt, global memory)
+template <int MC = LW_MC_ANY>
 __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState& ps, const ShadeGeom& g, ShadowRay& sh,
                                              const LwLpe* lpe = nullptr, const LwLightTree* lt = nullptr) {
   sh.valid = 0;
   const lw_material& m = *g.m;
   const LayerW& lw = g.lw;
-  if (!(lw.nonspec && (S.nemit > 0 || S.env_kind != LW_ENV_NONE)) || S.estimator == LW_EST_BSDF) return;
+  if (!(lw.nonspec && (S.nemit > 0 || lw_env_kind<MC>(S) != LW_ENV_NONE)) || S.estimator == LW_EST_BSDF) return;
   const int bd = 4 + 8 * ps.bounce;
   double ul, vl;
   lw_halton2(S.qdims, S.qperm, bd + 2, bd + 3, ps.index, ul, vl);
   v3 wi, Le;
   double pl, tmax_sh;
   long long le;
-  bool ok = lw_nee_light_sample(S, g.p, g.ngf, ul, vl, lt, wi, Le, pl, tmax_sh, le);
+  bool ok = lw_nee_light_sample<MC>(S, g.p, g.ngf, ul, vl, lt, wi, Le, pl, tmax_sh, le);
   if (ok && pl > 0.0 && dot3(g.ngf, wi) > 0.0) {
     v3 wil = lw_to_local(g.fr, wi);
     double pb;
-    v3 f = lw_bsdf_eval(m, lw, g.wol, wil, pb);
+    v3 f = lw_bsdf_eval<MC>(m, lw, g.wol, wil, pb);
     if (f.x > 0.0 || f.y > 0.0 || f.z > 0.0) {
       double wm = S.estimator == LW_EST_NEE ? 1.0 : lw_mis_balance(pl, pb);
       double k = (wil.z * wm) / pl;
@@ -631,7 +673,7 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
       sh.valid = 1;
       if (lpe) {  // the diffuse and glossy parts, routed after the shadow test
         v3 fd, fg;
-        lw_bsdf_eval_split(m, lw, g.wol, wil, fd, fg);
+        lw_bsdf_eval_split<MC>(m, lw, g.wol, wil, fd, fg);
         sh.c_diffuse = mk3(ps.beta.x * fd.x * Le.x * k, ps.beta.y * fd.y * Le.y * k, ps.beta.z * fd.z * Le.z * k);
         sh.c_glossy = mk3(ps.beta.x * fg.x * Le.x * k, ps.beta.y * fg.y * Le.y * k, ps.beta.z * fg.z * Le.z * k);
         sh.term = tmax_sh == INFINITY ? LW_EV_E : LW_EV_L;
@@ -643,15 +685,15 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
 
 // miss / emission part: returns false if the path ends before any scattering
 // lpe (megakernel with LPE layers): routes the emission to the layers accepting ... L / ... E
-template <bool CMP = false>
+template <bool CMP = false, int MC = LW_MC_ANY>
 __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& ps, const LwHit& h, ShadeGeom& g,
                                                   double& w, const LwLpe* lpe = nullptr, long long pix = 0,
                                                   const LwLightTree* lt = nullptr) {
   v3 d = ps.d;
   if (h.tri < 0) {
-    if (S.env_kind != LW_ENV_NONE) {
+    if (lw_env_kind<MC>(S) != LW_ENV_NONE) {
       double pe;
-      v3 Le = lw_env_eval(S, d, ps.nprev, pe);
+      v3 Le = lw_env_eval<MC>(S, d, ps.nprev, pe);
       double wm = ps.spec_prev ? 1.0 : lw_bsdf_hit_weight(S, ps.pdf_prev, pe);
       v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
       ps.L = CMP ? lw_q32v(ps.L + c) : ps.L + c;
@@ -664,7 +706,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
   if (e >= 0 && S.nemit > 0 && (g.front || S.emit_two[e])) {
     v3 Le = lw_ld3(S.emit_rad + 3 * e);
     double wm = 1.0;
-    if (!ps.spec_prev) wm = lw_bsdf_hit_weight(S, ps.pdf_prev, lw_emitter_hit_pdf(S, e, ps.o, ps.nprev, g.ng, d, h.t, lt));
+    if (!ps.spec_prev) wm = lw_bsdf_hit_weight(S, ps.pdf_prev, lw_emitter_hit_pdf<MC>(S, e, ps.o, ps.nprev, g.ng, d, h.t, lt));
     v3 c = mk3(ps.beta.x * Le.x * wm, ps.beta.y * Le.y * wm, ps.beta.z * Le.z * wm);
     ps.L = CMP ? lw_q32v(ps.L + c) : ps.L + c;
     if (lpe) lw_lpe_route(lpe, lw_lpe_step(lpe, ps.lpe, LW_EV_L), pix, c);
@@ -673,7 +715,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
 }
 
 // BSDF sampling, Russian roulette and the next ray; returns true if the path continues
-template <bool CMP = false>
+template <bool CMP = false, int MC = LW_MC_ANY>
 __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& ps, const ShadeGeom& g,
                                                   const LwLpe* lpe = nullptr) {
   const int b = ps.bounce;
@@ -681,7 +723,7 @@ __device__ __forceinline__ bool lw_shade_material(const DevScene& S, PathState& 
   BSample bs;
   double ub, vb;
   lw_halton2(S.qdims, S.qperm, bd + 0, bd + 1, ps.index, ub, vb);
-  if (!lw_bsdf_sample(*g.m, g.lw, g.wol, g.front, ub, vb, bs)) return false;
+  if (!lw_bsdf_sample<MC>(*g.m, g.lw, g.wol, g.front, ub, vb, bs)) return false;
   if (lpe) ps.lpe = lw_lpe_step(lpe, ps.lpe, bs.event);
   v3 wi = lw_to_world(g.fr, bs.wi);
   unsigned code = 0;

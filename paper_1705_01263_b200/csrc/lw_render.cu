@@ -51,6 +51,13 @@ using namespace lw;
 #ifndef LW_NEE_MINB
 #define LW_NEE_MINB 4
 #endif
+// the same for the diffuse material class (LW_MC_DIFFUSE instantiations, fewer live registers)
+#ifndef LW_SHADE_MINB_D
+#define LW_SHADE_MINB_D 4
+#endif
+#ifndef LW_NEE_MINB_D
+#define LW_NEE_MINB_D 4
+#endif
 
 namespace {
 
@@ -100,13 +107,13 @@ struct Pool {
 
 // everything a wave's launches depend on (the CUDA graph is rebuilt when it changes)
 struct WaveCfg {
-  int pool = 0, cmp = 0, lpe_on = 0, ltm = 0, use_smem = 0, count = 0, timed = 0, persist_mask = 0, tail_div = 0;
+  int pool = 0, cmp = 0, lpe_on = 0, ltm = 0, use_smem = 0, count = 0, timed = 0, persist_mask = 0, tail_div = 0, mc = 0;
   size_t smem = 0, ltsm = 0;
   void* pool_block = nullptr;
   long long epoch = -1;
   bool operator==(const WaveCfg& o) const {
     return pool == o.pool && cmp == o.cmp && lpe_on == o.lpe_on && ltm == o.ltm && use_smem == o.use_smem &&
-           count == o.count && timed == o.timed && persist_mask == o.persist_mask && tail_div == o.tail_div &&
+           count == o.count && timed == o.timed && persist_mask == o.persist_mask && tail_div == o.tail_div && mc == o.mc &&
            smem == o.smem && ltsm == o.ltsm && pool_block == o.pool_block && epoch == o.epoch;
   }
 };
@@ -156,6 +163,11 @@ struct lw_ctx {
   // tail queue: keep the compacted queue once fewer than pool / tail_div paths are
   // alive and nothing is left to regenerate (0 = compact every wave); LW_TAIL_QUEUE overrides
   int tail_div = getenv("LW_TAIL_QUEUE") ? atoi(getenv("LW_TAIL_QUEUE")) : 16;
+  // scene class (LW_MC_* in lw_integrator.cuh) the shading kernels are instantiated for:
+  // mat_diffuse = every material one uncoated diffuse layer (set by lw_scene_upload); the
+  // environment / light-selection bits come from DevScene.  LW_MATCLASS=0 forces LW_MC_ANY (A/B).
+  bool mat_diffuse = false;
+  bool mat_class_on = getenv("LW_MATCLASS") ? atoi(getenv("LW_MATCLASS")) != 0 : true;
   int nrnodes = 0;        // internal nodes of the render BVH
   cudaStream_t own_stream = nullptr;
   int instr = 0;
@@ -687,7 +699,10 @@ __device__ __forceinline__ void load_ray(const Pool& P, int s, double o[3], doub
 }
 
 // nprev (previous vertex normal) is only consumed by the light hierarchy / environment pyramid MIS
-__device__ __forceinline__ bool needs_nprev(const DevScene& S) { return S.light_mode != 0 || S.env_mode != 0; }
+template <int MC = LW_MC_ANY>
+__device__ __forceinline__ bool needs_nprev(const DevScene& S) {
+  return lw_light_mode<MC>(S) != 0 || ((MC & LW_MC_NOENV) ? 0 : S.env_mode) != 0;
+}
 
 __device__ __forceinline__ void load_state(const Pool& P, int s, PathState& ps, bool nprev, bool compact) {
   double2 a = P.ray0[s], b = P.ray1[s];
@@ -1097,8 +1112,8 @@ __device__ __forceinline__ void load_hit(const Pool& P, int s, LwHit& h) {
 
 // NEE half of the material stage (runs before k_shade so it sees the incoming throughput):
 // light / environment sample, BSDF evaluation, shadow-ray setup
-template <bool LPE, bool LT, bool CMP>
-__global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt,
+template <bool LPE, bool LT, bool CMP, int MC>
+__global__ void __launch_bounds__(128, (MC & LW_MC_DIFFUSE) ? LW_NEE_MINB_D : LW_NEE_MINB) k_shade_nee(DevScene S, Pool P, Counters* __restrict__ cnt,
                                                                 LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
   LwLightTree lt;
@@ -1135,9 +1150,9 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
         ShadeGeom g;
         double w;
         lw_shade_hit(S, ps.d, h, g, w);
-        lw_shade_frame(S, ps.d, h, w, g);
+        lw_shade_frame<MC>(S, ps.d, h, w, g);
         ShadowRay sh;
-        lw_shade_nee(S, ps, g, sh, LPE ? &lpe : nullptr, LT ? &lt : nullptr);
+        lw_shade_nee<MC>(S, ps, g, sh, LPE ? &lpe : nullptr, LT ? &lt : nullptr);
         shadow = sh.valid != 0;
         if (LPE && shadow) {
           P.sh5[s] = make_double2(sh.c_diffuse.x, sh.c_diffuse.y);
@@ -1160,8 +1175,8 @@ __global__ void __launch_bounds__(128, LW_NEE_MINB) k_shade_nee(DevScene S, Pool
 }
 
 // material half: miss/emission (MIS), BSDF sampling, Russian roulette, next ray, stage tag
-template <bool LPE, bool LT, bool CMP>
-__global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt, LwLpe lpe) {
+template <bool LPE, bool LT, bool CMP, int MC>
+__global__ void __launch_bounds__(128, (MC & LW_MC_DIFFUSE) ? LW_SHADE_MINB_D : LW_SHADE_MINB) k_shade(DevScene S, Pool P, Counters* __restrict__ cnt, LwLpe lpe) {
   extern __shared__ __align__(16) unsigned char smem[];
   LwLightTree lt;
   if (LT) lt = lw_lt_stage(S.lt, S.lt_nheap, smem);
@@ -1174,18 +1189,18 @@ __global__ void __launch_bounds__(128, LW_SHADE_MINB) k_shade(DevScene S, Pool P
       int s = P.q_ext[k];
       if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       PathState ps;
-      load_state(P, s, ps, needs_nprev(S), CMP);
+      load_state(P, s, ps, needs_nprev<MC>(S), CMP);
       LwHit h;
       load_hit(P, s, h);
       ShadeGeom g;
       double w;
       bool alive = false;
       if (LPE) ps.lpe = P.lpe_state[s];
-      if (lw_shade_emission<CMP>(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0, LT ? &lt : nullptr)) {
-        lw_shade_frame(S, ps.d, h, w, g);
-        alive = lw_shade_material<CMP>(S, ps, g, LPE ? &lpe : nullptr);
+      if (lw_shade_emission<CMP, MC>(S, ps, h, g, w, LPE ? &lpe : nullptr, LPE ? P.pix[s] : 0, LT ? &lt : nullptr)) {
+        lw_shade_frame<MC>(S, ps.d, h, w, g);
+        alive = lw_shade_material<CMP, MC>(S, ps, g, LPE ? &lpe : nullptr);
       }
-      store_state(P, s, ps, needs_nprev(S), CMP);
+      store_state(P, s, ps, needs_nprev<MC>(S), CMP);
       if (LPE) P.lpe_state[s] = ps.lpe;
       P.stage[s] = alive ? LW_STAGE_TRACE : LW_STAGE_TERMINATED;
       alive_count += alive ? 1 : 0;
@@ -1729,6 +1744,41 @@ void launch_shadow(lw_ctx* c, cudaStream_t st, int grid, size_t smem, int nr, bo
     k_trace_shadow<false, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
 }
 
+// scene class of the wave (LW_MC_*): the largest instantiated class the scene belongs to --
+// diffuse + no environment + alias lights (Cornell box), diffuse + no environment (light
+// hierarchy), diffuse, or any
+int scene_class(const lw_ctx* c) {
+  if (!c->mat_diffuse) return LW_MC_ANY;
+  if (c->S.env_kind != LW_ENV_NONE) return LW_MC_DIFFUSE;
+  if (c->S.light_mode != LW_LIGHTS_TREE) return LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS;
+  return LW_MC_DIFFUSE | LW_MC_NOENV;
+}
+
+// the two shading kernels for the wave's LPE / light-hierarchy / scene-class configuration (the
+// scene classes are instantiated without LPE layers only: wc.mc is LW_MC_ANY when layers are set)
+template <bool CMP, int MC>
+void launch_shade_nee(lw_ctx* c, cudaStream_t st, int gS, bool lpe_on, bool ltm, size_t ltsm) {
+  if (MC == LW_MC_ANY && lpe_on && ltm)
+    k_shade_nee<true, true, CMP, LW_MC_ANY><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (MC == LW_MC_ANY && lpe_on)
+    k_shade_nee<true, false, CMP, LW_MC_ANY><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (ltm)
+    k_shade_nee<false, true, CMP, MC><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else
+    k_shade_nee<false, false, CMP, MC><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+}
+
+template <bool CMP, int MC>
+void launch_shade(lw_ctx* c, cudaStream_t st, int gS, bool lpe_on, bool ltm, size_t ltsm) {
+  if (MC == LW_MC_ANY && lpe_on && ltm)
+    k_shade<true, true, CMP, LW_MC_ANY><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (MC == LW_MC_ANY && lpe_on)
+    k_shade<true, false, CMP, LW_MC_ANY><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else if (ltm)
+    k_shade<false, true, CMP, MC><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  else
+    k_shade<false, false, CMP, MC><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+}
 
 constexpr int kMaxWaves = 100000;   // a pass that needs more waves is reported as an error
 
@@ -1776,23 +1826,19 @@ void enqueue_wave(lw_ctx* c, cudaStream_t st, const WaveCfg& wc) {
       k_trace_ext<false, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, 0);
   }
   stamp(c, st, wc, LW_PROF_SHADE_NEE);
-  if (lpe_on && ltm)
-    k_shade_nee<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-  else if (lpe_on)
-    k_shade_nee<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-  else if (ltm)
-    k_shade_nee<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-  else
-    k_shade_nee<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  switch (wc.mc) {
+    case LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS: launch_shade_nee<CMP, LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS>(c, st, gS, lpe_on, ltm, ltsm); break;
+    case LW_MC_DIFFUSE | LW_MC_NOENV: launch_shade_nee<CMP, LW_MC_DIFFUSE | LW_MC_NOENV>(c, st, gS, lpe_on, ltm, ltsm); break;
+    case LW_MC_DIFFUSE: launch_shade_nee<CMP, LW_MC_DIFFUSE>(c, st, gS, lpe_on, ltm, ltsm); break;
+    default: launch_shade_nee<CMP, LW_MC_ANY>(c, st, gS, lpe_on, ltm, ltsm);
+  }
   stamp(c, st, wc, LW_PROF_SHADE);
-  if (lpe_on && ltm)
-    k_shade<true, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-  else if (lpe_on)
-    k_shade<true, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-  else if (ltm)
-    k_shade<false, true, CMP><<<gS, 128, ltsm, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
-  else
-    k_shade<false, false, CMP><<<gS, 128, 0, st>>>(c->S, c->pool, c->d_cnt, c->lpe);
+  switch (wc.mc) {
+    case LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS: launch_shade<CMP, LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS>(c, st, gS, lpe_on, ltm, ltsm); break;
+    case LW_MC_DIFFUSE | LW_MC_NOENV: launch_shade<CMP, LW_MC_DIFFUSE | LW_MC_NOENV>(c, st, gS, lpe_on, ltm, ltsm); break;
+    case LW_MC_DIFFUSE: launch_shade<CMP, LW_MC_DIFFUSE>(c, st, gS, lpe_on, ltm, ltsm); break;
+    default: launch_shade<CMP, LW_MC_ANY>(c, st, gS, lpe_on, ltm, ltsm);
+  }
   stamp(c, st, wc, LW_PROF_TRACE_SHADOW);
   if (use_smem)
     launch_shadow<LW_NODES_SMEM, CMP>(c, st, gT, smem, nr, lpe_on, count);
@@ -1951,6 +1997,7 @@ int run_pass_t(lw_ctx* c, const WorkRange& w) {
     wc.timed = (c->instr & LW_INSTR_TIME) != 0;
     wc.persist_mask = c->persist_mask;
     wc.tail_div = c->tail_div;
+    wc.mc = (c->mat_class_on && !wc.lpe_on) ? scene_class(c) : LW_MC_ANY;
     wc.pool_block = c->pool.block;
     wc.epoch = c->epoch;
     // every slot starts free
@@ -2319,6 +2366,11 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   LW_STATUS_TRY(dev_upload(c, dm, (const int*)d->material, n));
   lw_material* dmat;
   LW_STATUS_TRY(dev_upload(c, dmat, d->materials, d->nmaterials));
+  c->mat_diffuse = true;
+  for (int k = 0; k < d->nmaterials; k++) {
+    const lw_material& m = d->materials[k];
+    if (!(m.nlayers == 1 && m.layers[0].kind == LW_BSDF_DIFFUSE && m.layers[0].coat == 0)) c->mat_diffuse = false;
+  }
   S.verts = dv;
   S.normals = dn;
   S.material = dm;

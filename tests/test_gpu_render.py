@@ -131,6 +131,21 @@ def test_execution_strategy_invariance(cornell_packed):
         assert np.array_equal(outs[0], o)
 
 
+def test_material_class_instantiations_identical(cornell_packed, oracle, monkeypatch):
+    """All-diffuse scenes run the LW_MC_DIFFUSE shading kernels (layer count / kind / coat folded to
+    constants): identical to the general instantiations (LW_MATCLASS=0) and to the oracle."""
+    from paper_1705_01263_b200.render import RenderParams
+
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("LW_MATCLASS", v)
+        with _renderer(cornell_packed, 128, 96, 8, pool_log2=12) as r:
+            r.render_pass(0, 6)
+            outs.append(r.framebuffer())
+    fb2, _ = oracle.OracleScene(cornell_packed).render(RenderParams(128, 96, 8), 0, 6)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], fb2)
+
+
 @pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
 def test_other_configs_subset_bit_exact(gpu, oracle, cfg):
     from paper_1705_01263_b200.render import RenderParams
