@@ -62,7 +62,9 @@ struct DevScene {
 // path for every thread).  Each bit folds a scene-wide property to a constant:
 //   LW_MC_DIFFUSE  every material is one uncoated diffuse layer (layer count / kind / coat);
 //   LW_MC_NOENV    no environment (env_kind == LW_ENV_NONE);
-//   LW_MC_ALIAS    emitters chosen by the alias table (light_mode != LW_LIGHTS_TREE).
+//   LW_MC_ALIAS    emitters chosen by the alias table (light_mode != LW_LIGHTS_TREE);
+//   LW_MC_NOTRI    no emissive triangles (nemit == 0);
+//   LW_MC_ENVCONST no image environment (env_kind is constant or none).
 // The arithmetic executed is the same, so results are identical; the dead code and its registers
 // disappear.  0 (LW_MC_ANY) evaluates anything.  (A class for "diffuse + glossy layers only"
 // spilled more than LW_MC_ANY and was dropped.)
@@ -70,12 +72,20 @@ struct DevScene {
 #define LW_MC_DIFFUSE 1
 #define LW_MC_NOENV 2
 #define LW_MC_ALIAS 4
+#define LW_MC_NOTRI 8
+#define LW_MC_ENVCONST 16
 template <int MC>
 __device__ __forceinline__ int lw_mat_nlayers(const lw_material& m) { return (MC & LW_MC_DIFFUSE) ? 1 : m.nlayers; }
 template <int MC>
 __device__ __forceinline__ int lw_layer_kind(const lw_layer& L) { return (MC & LW_MC_DIFFUSE) ? LW_BSDF_DIFFUSE : L.kind; }
 template <int MC>
-__device__ __forceinline__ int lw_env_kind(const DevScene& S) { return (MC & LW_MC_NOENV) ? LW_ENV_NONE : S.env_kind; }
+__device__ __forceinline__ int lw_env_kind(const DevScene& S) {
+  if (MC & LW_MC_NOENV) return LW_ENV_NONE;
+  if (MC & LW_MC_ENVCONST) return S.env_kind == LW_ENV_CONSTANT ? LW_ENV_CONSTANT : LW_ENV_NONE;
+  return S.env_kind;
+}
+template <int MC>
+__device__ __forceinline__ long long lw_nemit(const DevScene& S) { return (MC & LW_MC_NOTRI) ? 0 : S.nemit; }
 template <int MC>
 __device__ __forceinline__ int lw_light_mode(const DevScene& S) { return (MC & LW_MC_ALIAS) ? LW_LIGHTS_ALIAS : S.light_mode; }
 
@@ -552,7 +562,7 @@ __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 
   bool ok = false;
   const int env_kind = lw_env_kind<MC>(S);
   if (env_kind != LW_ENV_NONE && ul < S.p_env) {
-    double ue = S.nemit > 0 ? ul / S.p_env : ul;
+    double ue = lw_nemit<MC>(S) > 0 ? ul / S.p_env : ul;
     if (env_kind == LW_ENV_CONSTANT) {
       double z = 1.0 - 2.0 * ue;
       double r2 = 1.0 - z * z;
@@ -593,7 +603,7 @@ __device__ __forceinline__ bool lw_nee_light_sample(const DevScene& S, v3 p, v3 
         ok = true;
       }
     }
-  } else if (S.nemit > 0) {
+  } else if (lw_nemit<MC>(S) > 0) {
     double ut = env_kind != LW_ENV_NONE ? (ul - S.p_env) / (1.0 - S.p_env) : ul;
     double ur, psel;
     long long le;
@@ -651,7 +661,7 @@ __device__ __forceinline__ void lw_shade_nee(const DevScene& S, const PathState&
   sh.valid = 0;
   const lw_material& m = *g.m;
   const LayerW& lw = g.lw;
-  if (!(lw.nonspec && (S.nemit > 0 || lw_env_kind<MC>(S) != LW_ENV_NONE)) || S.estimator == LW_EST_BSDF) return;
+  if (!(lw.nonspec && (lw_nemit<MC>(S) > 0 || lw_env_kind<MC>(S) != LW_ENV_NONE)) || S.estimator == LW_EST_BSDF) return;
   const int bd = 4 + 8 * ps.bounce;
   double ul, vl;
   lw_halton2(S.qdims, S.qperm, bd + 2, bd + 3, ps.index, ul, vl);
@@ -703,7 +713,7 @@ __device__ __forceinline__ bool lw_shade_emission(const DevScene& S, PathState& 
   }
   lw_shade_hit(S, d, h, g, w);
   int e = S.emit_of_tri[h.tri];
-  if (e >= 0 && S.nemit > 0 && (g.front || S.emit_two[e])) {
+  if (e >= 0 && lw_nemit<MC>(S) > 0 && (g.front || S.emit_two[e])) {
     v3 Le = lw_ld3(S.emit_rad + 3 * e);
     double wm = 1.0;
     if (!ps.spec_prev) wm = lw_bsdf_hit_weight(S, ps.pdf_prev, lw_emitter_hit_pdf<MC>(S, e, ps.o, ps.nprev, g.ng, d, h.t, lt));

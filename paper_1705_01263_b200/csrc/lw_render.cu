@@ -1744,14 +1744,30 @@ void launch_shadow(lw_ctx* c, cudaStream_t st, int grid, size_t smem, int nr, bo
     k_trace_shadow<false, false, NODES, CMP><<<grid, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, use_smem, c->lpe);
 }
 
-// scene class of the wave (LW_MC_*): the largest instantiated class the scene belongs to --
-// diffuse + no environment + alias lights (Cornell box), diffuse + no environment (light
-// hierarchy), diffuse, or any
+// the instantiated scene classes, most specific first: diffuse + no environment + alias lights
+// (Cornell box), diffuse + no environment (light hierarchy), diffuse, alias lights + constant
+// environment (layered / glossy materials under a sky colour), alias + no emitters (image
+// environment only), any.  k_shade_nee keeps the general kernel for the last two (with the layered
+// BSDF its register allocation came out 2-6 registers larger and C4's NEE 4.6 % slower).
+#define LW_SCENE_CLASSES_NEE(X) \
+  X(LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS) X(LW_MC_DIFFUSE | LW_MC_NOENV) X(LW_MC_DIFFUSE)
+#define LW_SCENE_CLASSES(X) \
+  LW_SCENE_CLASSES_NEE(X) X(LW_MC_ALIAS | LW_MC_ENVCONST) X(LW_MC_ALIAS | LW_MC_NOTRI)
+
+// scene class of the wave: the first instantiated class whose properties the scene has
 int scene_class(const lw_ctx* c) {
-  if (!c->mat_diffuse) return LW_MC_ANY;
-  if (c->S.env_kind != LW_ENV_NONE) return LW_MC_DIFFUSE;
-  if (c->S.light_mode != LW_LIGHTS_TREE) return LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS;
-  return LW_MC_DIFFUSE | LW_MC_NOENV;
+  const DevScene& S = c->S;
+  int m = 0;
+  if (c->mat_diffuse) m |= LW_MC_DIFFUSE;
+  if (S.env_kind == LW_ENV_NONE) m |= LW_MC_NOENV;
+  if (S.light_mode != LW_LIGHTS_TREE) m |= LW_MC_ALIAS;
+  if (S.nemit == 0) m |= LW_MC_NOTRI;
+  if (S.env_kind == LW_ENV_NONE || S.env_kind == LW_ENV_CONSTANT) m |= LW_MC_ENVCONST;
+#define LW_SC_PICK(k) \
+  if ((m & (k)) == (k)) return (k);
+  LW_SCENE_CLASSES(LW_SC_PICK)
+#undef LW_SC_PICK
+  return LW_MC_ANY;
 }
 
 // the two shading kernels for the wave's LPE / light-hierarchy / scene-class configuration (the
@@ -1826,19 +1842,21 @@ void enqueue_wave(lw_ctx* c, cudaStream_t st, const WaveCfg& wc) {
       k_trace_ext<false, LW_NODES_GLOBAL, CMP><<<gT, 128, smem, st>>>(c->S, c->pool, c->d_cnt, nr, 0);
   }
   stamp(c, st, wc, LW_PROF_SHADE_NEE);
+#define LW_SC_NEE(k) \
+  case (k): launch_shade_nee<CMP, (k)>(c, st, gS, lpe_on, ltm, ltsm); break;
   switch (wc.mc) {
-    case LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS: launch_shade_nee<CMP, LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS>(c, st, gS, lpe_on, ltm, ltsm); break;
-    case LW_MC_DIFFUSE | LW_MC_NOENV: launch_shade_nee<CMP, LW_MC_DIFFUSE | LW_MC_NOENV>(c, st, gS, lpe_on, ltm, ltsm); break;
-    case LW_MC_DIFFUSE: launch_shade_nee<CMP, LW_MC_DIFFUSE>(c, st, gS, lpe_on, ltm, ltsm); break;
+    LW_SCENE_CLASSES_NEE(LW_SC_NEE)
     default: launch_shade_nee<CMP, LW_MC_ANY>(c, st, gS, lpe_on, ltm, ltsm);
   }
+#undef LW_SC_NEE
   stamp(c, st, wc, LW_PROF_SHADE);
+#define LW_SC_SHADE(k) \
+  case (k): launch_shade<CMP, (k)>(c, st, gS, lpe_on, ltm, ltsm); break;
   switch (wc.mc) {
-    case LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS: launch_shade<CMP, LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS>(c, st, gS, lpe_on, ltm, ltsm); break;
-    case LW_MC_DIFFUSE | LW_MC_NOENV: launch_shade<CMP, LW_MC_DIFFUSE | LW_MC_NOENV>(c, st, gS, lpe_on, ltm, ltsm); break;
-    case LW_MC_DIFFUSE: launch_shade<CMP, LW_MC_DIFFUSE>(c, st, gS, lpe_on, ltm, ltsm); break;
+    LW_SCENE_CLASSES(LW_SC_SHADE)
     default: launch_shade<CMP, LW_MC_ANY>(c, st, gS, lpe_on, ltm, ltsm);
   }
+#undef LW_SC_SHADE
   stamp(c, st, wc, LW_PROF_TRACE_SHADOW);
   if (use_smem)
     launch_shadow<LW_NODES_SMEM, CMP>(c, st, gT, smem, nr, lpe_on, count);
