@@ -51,6 +51,11 @@ using namespace lw;
 #ifndef LW_NEE_MINB
 #define LW_NEE_MINB 4
 #endif
+// k_generate: 4 blocks of 256 -> 64 registers (5 -> 48 with spills: 1-3 % slower generate; no
+// bound -> 90 registers: C2 generate 0.22 -> 0.31 ms)
+#ifndef LW_GEN_MINB
+#define LW_GEN_MINB 4
+#endif
 // the same for the diffuse material class (LW_MC_DIFFUSE instantiations, fewer live registers)
 #ifndef LW_SHADE_MINB_D
 #define LW_SHADE_MINB_D 4
@@ -806,7 +811,7 @@ __global__ void k_wave_begin(Counters* cnt, int pool, double regen_fraction, int
 // granted_left).  (Block-granular with a barrier per 256 slots, this scan cost ~170 us per wave on
 // C2 even when nothing was left to do; the per-warp form is bound by the stage-byte reads.)
 template <bool LPE, bool CMP>
-__global__ void __launch_bounds__(256) k_generate(DevScene S, Pool P, unsigned long long* __restrict__ fb,
+__global__ void __launch_bounds__(256, LW_GEN_MINB) k_generate(DevScene S, Pool P, unsigned long long* __restrict__ fb,
                                                   Counters* __restrict__ cnt, LwLpe lpe) {
   if (cnt->tail) return;  // tail queue: no compaction, nothing to regenerate
   const WorkRange w = cnt->wr;
