@@ -16,6 +16,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
 #include <vector>
 
@@ -1667,10 +1668,12 @@ int collapse_wide(lw_ctx* c, const SahNode* bn, int nr, int root_ref, int levels
   if (nr <= 0 || root_ref < 0) return LW_OK;
   cudaStream_t st = c->stream;
   DevBuf f0, f1, need, cnt;
-  LW_CUDA_TRY(f0.alloc(sizeof(int) * nr));
-  LW_CUDA_TRY(f1.alloc(sizeof(int) * nr));
-  LW_CUDA_TRY(need.alloc(sizeof(int) * nr));
-  LW_CUDA_TRY(cnt.alloc(sizeof(int) * (levels + 2)));
+  // stream-ordered scratch like the rest of the upload (a synchronous cudaMalloc here stalled on
+  // the reserved pool memory: 2 -> 386 ms over five C3 uploads)
+  LW_CUDA_TRY(f0.alloc(sizeof(int) * nr, st));
+  LW_CUDA_TRY(f1.alloc(sizeof(int) * nr, st));
+  LW_CUDA_TRY(need.alloc(sizeof(int) * nr, st));
+  LW_CUDA_TRY(cnt.alloc(sizeof(int) * (levels + 2), st));
   LW_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (levels + 2), st));
   LW_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(WNode) * nr, st));
   int one = 1, zero = 0;
@@ -2378,6 +2381,24 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   DevScene& S = c->S;
   int64_t n = d->ntris;
   c->ntris = n;
+  // LW_DEBUG_UPLOAD=1: host wall-clock phases of the upload (stream synchronised) on stderr
+  static const bool dbg_up = getenv("LW_DEBUG_UPLOAD") != nullptr;
+  auto now_ms = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  auto phase = [&](const char* what, double& t) {
+    if (!dbg_up) return;
+    cudaStreamSynchronize(st);
+    double t1 = now_ms();
+    cudaMemPool_t mp;
+    uint64_t res = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&mp, c->device) == cudaSuccess) {
+      cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReservedMemCurrent, &res);
+      cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    fprintf(stderr, "lw_scene_upload %s %.3f ms (pool reserved %.0f MB, used %.0f MB)\n", what, t1 - t, res / 1e6,
+            used / 1e6);
+    t = t1;
+  };
+  double tph = dbg_up ? now_ms() : 0.0;
   for (int64_t k = 0; k < n; k++)
     LW_CHECK_ARG(d->material[k] >= 0 && d->material[k] < d->nmaterials, "material index out of range");
   for (int64_t e = 0; e < d->nemit; e++) LW_CHECK_ARG(d->emit_tri[e] >= 0 && d->emit_tri[e] < n, "emitter triangle out of range");
@@ -2398,6 +2419,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   S.normals = dn;
   S.material = dm;
   S.materials = dmat;
+  phase("validate+copy", tph);
   // the reference-layout median tree (geometry.py:100-148 arrays) is built here only when it is
   // the render tree; otherwise on demand by lw_ctx_bvh_info / lw_ctx_bvh_download
   c->ref_built = false;
@@ -2466,6 +2488,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   }
   LW_STATUS_TRY(dev_alloc(c, wn, nr > 0 ? nr : 1));
   int max_need = 0;
+  phase("binary-tree", tph);
   int rc_w = collapse_wide(c, bn, nr, root_ref, levels, wn, max_need);
   if (bn) cudaFreeAsync(bn, st);
   LW_STATUS_TRY(rc_w);
@@ -2478,6 +2501,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   set_error("render BVH too deep: a path needs %d traversal stack entries (limit %d)", max_need, LW_STACK);
   return LW_ERR_INVALID;
   }
+  phase("collapse", tph);
   c->nrnodes = nr;
   S.bvh.nodes = wn;
   S.bvh.tris = lt;
@@ -2645,6 +2669,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   }
   S.tan_half = d->tan_half_fov;
   LW_CUDA_TRY(cudaStreamSynchronize(st));
+  phase("lights+env", tph);
   c->has_scene = true;
   return LW_OK;
 }

@@ -13,9 +13,9 @@ from paper_1705_01263_b200.scene import pack_scene  # noqa: E402
 
 lib = _abi.lib()
 reps = 5
-for cfg in sys.argv[1:] or ["C2"]:
+for cfg in [a for a in sys.argv[1:] if not a.startswith("--")] or ["C2"]:
     c = scenes.CONFIGS[cfg]
-    packed = pack_scene(c.builder())
+    packed = pack_scene(c.builder()).pinned()  # as bench.py's e2e: scene arrays in pinned memory
     its = max(1, (1 << 24) // (c.width * c.height))
     params = RenderParams(c.width, c.height, c.max_depth, 4, "wavefront", 22, 0.5, 0)
     for rep in range(reps):
@@ -32,6 +32,13 @@ for cfg in sys.argv[1:] or ["C2"]:
         r.lib, r.ctx, r.params, r.packed, r.iterations, r.device = lib, h, params, packed, 0, 0
         r.render_pass(rep * its, (rep + 1) * its)
         torch.cuda.synchronize(); t.append(time.perf_counter())
+        dev1 = r.last_pass_timing()["total_ms"]
+        if "--second-pass" in sys.argv:  # a second pass on the same context (wall, device)
+            t2 = time.perf_counter()
+            r.render_pass(rep * its, (rep + 1) * its)
+            torch.cuda.synchronize()
+            print(cfg, rep, f"second pass wall {1e3 * (time.perf_counter() - t2):.2f} device {r.last_pass_timing()['total_ms']:.2f}"
+                  f" (first pass device {dev1:.2f})", flush=True)
         r.image(its)
         torch.cuda.synchronize(); t.append(time.perf_counter())
         r.close()
