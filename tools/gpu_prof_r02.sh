@@ -2,6 +2,9 @@
 # + CPU baselines), ncu --set full captures of the stage kernels (timed instantiations, a
 # full-size wave), the per-stage-kernel DRAM traffic (tools/gpu_kernel_traffic.sh) and the C2/C3
 # launch lists.  Copy the gpurun_out/ products into profiles/ afterwards (tools/prof_r02_collect.sh).
+# DRAM traffic first, so the bench line's roofline.kernels carries this code's ncu bytes
+bash tools/gpu_kernel_traffic.sh > /dev/null 2>&1
+cp gpurun_out/r02_kernel_traffic.json profiles/r02_kernel_traffic.json
 python bench.py > gpurun_out/r02_bench_final.json 2> gpurun_out/r02_bench_final.err
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-per-config"
 N="ncu --set full --clock-control none --import-source on --kernel-name-base mangled"
@@ -15,7 +18,6 @@ for c in C3 C5; do
   timeout 900 $N -k 'regex:k_trace_ext_pILb0E' -s 1 -c 1 -o gpurun_out/r02_${c}_trace_ext -f $B --config $c > /dev/null 2>&1
 done
 timeout 900 $N -k 'regex:k_shadeILb0ELb0ELb0E' -s 9 -c 1 -o gpurun_out/r02_C4_shade -f $B --config C4 > /dev/null 2>&1
-bash tools/gpu_kernel_traffic.sh
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/launches_C3.csv $B --config C3 > /dev/null 2>&1
 # summaries on the box (gpurun brings back at most 64 MiB: the reports themselves stay there)
