@@ -462,14 +462,13 @@ __device__ __forceinline__ void sah_scan_counts(int cnt, int bin, int& pn, int& 
 // every axis and keeps only (cost, key, nl) of each lane's best plane; after the warp argmin, pass 2
 // recomputes the winning axis' bins and scans to produce the four boxes of the split.  Every value
 // is the same expression of the same inputs as in the single pass, so the split is unchanged.
-__global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int* __restrict__ large_rank,
-                               const BinAcc* __restrict__ bins, const int* __restrict__ ids,
-                               const double* __restrict__ tb, const double* __restrict__ cen,
-                               SSplit* __restrict__ out, int* __restrict__ split_flag) {
-  __shared__ unsigned long long sbin[4][kBins][13];
-  const int s = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31, bin = lane & 15, wib = (threadIdx.x >> 5) & 3;
-  if (s >= nseg) return;  // uniform per warp
+// the decision for segment s by one whole warp (sbw: the warp's shared-memory bin slice)
+__device__ __forceinline__ void sah_decide_seg(int s, const SSeg* __restrict__ seg, const int* __restrict__ large_rank,
+                                               const BinAcc* __restrict__ bins, const int* __restrict__ ids,
+                                               const double* __restrict__ tb, const double* __restrict__ cen,
+                                               SSplit* __restrict__ out, int* __restrict__ split_flag,
+                                               unsigned long long (*sbw)[13], int lane) {
+  const int bin = lane & 15;
   const SSeg g = seg[s];
   const int lr = large_rank[s];
   const bool mine = lr < 0 && lane < g.n;
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSe
       double scale = (double)kBins / ext;
       int cnt, pn, sn;
       double bb[6], cb[6], pb[6], sb[6];
-      sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbin[wib], cnt, bb, cb);
+      sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbw, cnt, bb, cb);
       sah_scan_counts(cnt, bin, pn, sn);
       sah_scan_boxes(bb, bin, pb, sb);
       // right side of plane p = bin: the suffix of bin + 1
@@ -531,7 +530,7 @@ __global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSe
     double scale = (double)kBins / (g.C[3 + a] - g.C[a]);
     int cnt;
     double bb[6], cb[6], pb[6], sb[6], pc[6], sc[6];
-    sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbin[wib], cnt, bb, cb);
+    sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbw, cnt, bb, cb);
     sah_scan_boxes(bb, bin, pb, sb);
     sah_scan_boxes(cb, bin, pc, sc);
     double rb[6], rc[6];
@@ -576,16 +575,26 @@ __global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSe
   split_flag[s] = r.split;
 }
 
+__global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSeg* __restrict__ seg, int nseg, const int* __restrict__ large_rank,
+                               const BinAcc* __restrict__ bins, const int* __restrict__ ids,
+                               const double* __restrict__ tb, const double* __restrict__ cen,
+                               SSplit* __restrict__ out, int* __restrict__ split_flag) {
+  __shared__ unsigned long long sbin[4][kBins][13];
+  const int s = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31, wib = (threadIdx.x >> 5) & 3;
+  if (s >= nseg) return;  // uniform per warp
+  sah_decide_seg(s, seg, large_rank, bins, ids, tb, cen, out, split_flag, sbin[wib], lane);
+}
+
 __device__ __forceinline__ int leaf_ref32(long long start, long long count) {
   return (int)(-(1 + ((start << 3) | count)));
 }
 
 // node ids, parent refs, node boxes and the next level's segment table
-__global__ void k_sah_emit(const SSeg* __restrict__ seg, int nseg, const SSplit* __restrict__ sp,
-                           const int* __restrict__ split_rank, int node_base, SahNode* __restrict__ nodes,
-                           int* __restrict__ root_ref, SSeg* __restrict__ next) {
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
+__device__ __forceinline__ void sah_emit_seg(int s, const SSeg* __restrict__ seg, const SSplit* __restrict__ sp,
+                                             const int* __restrict__ split_rank, int node_base,
+                                             SahNode* __restrict__ nodes, int* __restrict__ root_ref,
+                                             SSeg* __restrict__ next) {
   const SSeg g = seg[s];
   const SSplit& r = sp[s];
   int ref;
@@ -624,11 +633,16 @@ __global__ void k_sah_emit(const SSeg* __restrict__ seg, int nseg, const SSplit*
     nodes[g.parent].ref[g.side] = ref;
 }
 
-__global__ void k_sah_flags(const int* __restrict__ pos_seg, const int* __restrict__ ids, int n,
-                            const SSeg* __restrict__ seg, const SSplit* __restrict__ sp, const double* __restrict__ cen,
-                            int* __restrict__ left) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__global__ void k_sah_emit(const SSeg* __restrict__ seg, int nseg, const SSplit* __restrict__ sp,
+                           const int* __restrict__ split_rank, int node_base, SahNode* __restrict__ nodes,
+                           int* __restrict__ root_ref, SSeg* __restrict__ next) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) sah_emit_seg(s, seg, sp, split_rank, node_base, nodes, root_ref, next);
+}
+
+__device__ __forceinline__ int sah_left_of(int i, const int* __restrict__ pos_seg, const int* __restrict__ ids,
+                                           const SSeg* __restrict__ seg, const SSplit* __restrict__ sp,
+                                           const double* __restrict__ cen) {
   int s = pos_seg[i];
   int f = 0;
   if (s >= 0 && sp[s].split) {
@@ -642,15 +656,21 @@ __global__ void k_sah_flags(const int* __restrict__ pos_seg, const int* __restri
       f = b <= r.plane;
     }
   }
-  left[i] = f;
+  return f;
 }
 
-__global__ void k_sah_scatter(const int* __restrict__ pos_seg, const int* __restrict__ ids, int n,
-                              const SSeg* __restrict__ seg, const SSplit* __restrict__ sp,
-                              const int* __restrict__ split_rank, const int* __restrict__ left,
-                              const int* __restrict__ scan, int* __restrict__ ids_out, int* __restrict__ pos_out) {
+__global__ void k_sah_flags(const int* __restrict__ pos_seg, const int* __restrict__ ids, int n,
+                            const SSeg* __restrict__ seg, const SSplit* __restrict__ sp, const double* __restrict__ cen,
+                            int* __restrict__ left) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i < n) left[i] = sah_left_of(i, pos_seg, ids, seg, sp, cen);
+}
+
+__device__ __forceinline__ void sah_scatter_pos(int i, const int* __restrict__ pos_seg, const int* __restrict__ ids,
+                                                const SSeg* __restrict__ seg, const SSplit* __restrict__ sp,
+                                                const int* __restrict__ split_rank, const int* __restrict__ left,
+                                                const int* __restrict__ scan, int* __restrict__ ids_out,
+                                                int* __restrict__ pos_out) {
   int s = pos_seg[i];
   if (s < 0 || !sp[s].split) {
     ids_out[i] = ids[i];
@@ -667,6 +687,14 @@ __global__ void k_sah_scatter(const int* __restrict__ pos_seg, const int* __rest
   pos_out[np] = 2 * split_rank[s] + (l ? 0 : 1);
 }
 
+__global__ void k_sah_scatter(const int* __restrict__ pos_seg, const int* __restrict__ ids, int n,
+                              const SSeg* __restrict__ seg, const SSplit* __restrict__ sp,
+                              const int* __restrict__ split_rank, const int* __restrict__ left,
+                              const int* __restrict__ scan, int* __restrict__ ids_out, int* __restrict__ pos_out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) sah_scatter_pos(i, pos_seg, ids, seg, sp, split_rank, left, scan, ids_out, pos_out);
+}
+
 __global__ void k_large_flags(const SSeg* __restrict__ seg, int nseg, int* __restrict__ flag) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < nseg) flag[s] = seg[s].n > kSmall ? 1 : 0;
@@ -675,6 +703,122 @@ __global__ void k_large_flags(const SSeg* __restrict__ seg, int nseg, int* __res
 __global__ void k_large_rank(const int* __restrict__ flag, const int* __restrict__ scan, int nseg, int* __restrict__ rank) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < nseg) rank[s] = flag[s] ? scan[s] : -1;
+}
+
+// ---- small scenes: the whole level loop in one thread block ------------------------------------
+// The level-synchronous build above reads two counts back per level (segments to bin, nodes
+// emitted), ~100 us of launches and round trips per level: 0.8 ms for the 36-triangle Cornell box,
+// whose whole render pass is 16 ms.  Up to kSmallBuildMax triangles one block runs the same
+// per-level steps -- large-segment binning with the same exact atomics, the warp decision
+// (sah_decide_seg), node emission, stable partition -- with block-wide scans in place of the
+// device-wide ones: the same tree, one launch, one read-back.
+constexpr int kSmallBuildThreads = 256;
+constexpr int kSmallBuildMax = 4096;
+
+struct SmallBuildResult {
+  int nnodes, levels, root_ref, pad;
+};
+
+// exclusive scan of in[0, m) into out[0, m], out[m] = total (returned); the whole block calls it
+__device__ int block_exscan(const int* __restrict__ in, int* __restrict__ out, int m) {
+  using BlockScan = cub::BlockScan<int, kSmallBuildThreads>;
+  __shared__ typename BlockScan::TempStorage ts;
+  __shared__ int carry;
+  __syncthreads();  // in[] complete
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < m; base += kSmallBuildThreads) {
+    int i = base + threadIdx.x;
+    int v = i < m ? in[i] : 0, x, agg;
+    BlockScan(ts).ExclusiveSum(v, x, agg);
+    int c = carry;
+    if (i < m) out[i] = c + x;
+    __syncthreads();  // carry read and temp storage reuse
+    if (threadIdx.x == 0) carry = c + agg;
+    __syncthreads();
+  }
+  int total = carry;
+  if (threadIdx.x == 0) out[m] = total;
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(kSmallBuildThreads) k_sah_small(
+    int n, const double* __restrict__ tb, const double* __restrict__ cen, int* __restrict__ ids, int* __restrict__ ids2,
+    int* pos_a, int* pos_b, SSeg* seg_a, SSeg* seg_b, SSplit* __restrict__ split, int* __restrict__ sflag,
+    int* __restrict__ srank, int* __restrict__ lflag, int* __restrict__ lscan, int* __restrict__ lrank,
+    int* __restrict__ left, int* __restrict__ scan, BinAcc* __restrict__ bins, SahNode* __restrict__ nodes,
+    int* __restrict__ root_ref, SmallBuildResult* __restrict__ res) {
+  __shared__ unsigned long long sbin[kSmallBuildThreads / 32][kBins][13];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kSmallBuildThreads / 32;
+  SSeg* seg = seg_a;
+  SSeg* nxt = seg_b;
+  int* pos = pos_a;
+  int* pos2 = pos_b;
+  int nseg = 1, node_base = 0, levels = 0;
+  while (nseg > 0) {
+    // large segments: ranks, then their bins over all positions (exact order-free atomics)
+    for (int q = tid; q < nseg; q += kSmallBuildThreads) lflag[q] = seg[q].n > kSmall ? 1 : 0;
+    const int nlarge = block_exscan(lflag, lscan, nseg);
+    for (int q = tid; q < nseg; q += kSmallBuildThreads) lrank[q] = lflag[q] ? lscan[q] : -1;
+    for (int q = tid; q < nlarge * 3 * kBins; q += kSmallBuildThreads) {
+      unsigned long long* b = bins[q].v;
+      b[0] = 0;
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        b[1 + k] = ~0ULL;
+        b[4 + k] = 0ULL;
+        b[7 + k] = ~0ULL;
+        b[10 + k] = 0ULL;
+      }
+    }
+    __syncthreads();
+    if (nlarge > 0) {
+      for (int i = tid; i < n; i += kSmallBuildThreads) {
+        int sg = pos[i];
+        if (sg < 0) continue;
+        int lr = lrank[sg];
+        if (lr < 0) continue;
+        int t = ids[i];
+        const double* tbt = tb + 6 * (size_t)t;
+        const double* ct = cen + 3 * (size_t)t;
+        const SSeg& g = seg[sg];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          double ext = g.C[3 + a] - g.C[a];
+          if (!(ext > 0.0)) continue;
+          int b = bin_of(ct[a], g.C[a], (double)kBins / ext);
+          bin_add(bins[(size_t)lr * 3 * kBins + a * kBins + b].v, tbt, ct, false);
+        }
+      }
+    }
+    __syncthreads();
+    // split decisions, one warp per segment
+    for (int q = warp; q < nseg; q += nw) sah_decide_seg(q, seg, lrank, bins, ids, tb, cen, split, sflag, sbin[warp], lane);
+    const int nsplit = block_exscan(sflag, srank, nseg);
+    for (int q = tid; q < nseg; q += kSmallBuildThreads) sah_emit_seg(q, seg, split, srank, node_base, nodes, root_ref, nxt);
+    // stable partition of the positions
+    for (int i = tid; i < n; i += kSmallBuildThreads) left[i] = sah_left_of(i, pos, ids, seg, split, cen);
+    block_exscan(left, scan, n);
+    for (int i = tid; i < n; i += kSmallBuildThreads) sah_scatter_pos(i, pos, ids, seg, split, srank, left, scan, ids2, pos2);
+    __syncthreads();
+    for (int i = tid; i < n; i += kSmallBuildThreads) ids[i] = ids2[i];
+    __syncthreads();
+    int* tp = pos;
+    pos = pos2;
+    pos2 = tp;
+    SSeg* ts = seg;
+    seg = nxt;
+    nxt = ts;
+    node_base += nsplit;
+    nseg = 2 * nsplit;
+    levels++;
+  }
+  if (tid == 0) {
+    res->nnodes = node_base;
+    res->levels = levels;
+    res->root_ref = *root_ref;
+  }
 }
 
 }  // namespace
@@ -728,6 +872,32 @@ int sah_build_device(const double* d_verts, int64_t n64, cudaStream_t st, Device
   size_t tb1 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb1, b_left.as<int>(), b_scan.as<int>(), n + 1, st);
   TRY(b_tmp.alloc(tb1, st));
+  if (n <= kSmallBuildMax && !getenv("LW_SAH_LEVELS") && !getenv("LW_SAH_SERIAL") && !getenv("LW_SAH_CHECK")) {
+    DevBuf b_res;
+    TRY(b_res.alloc(sizeof(SmallBuildResult), st));
+    k_sah_small<<<1, kSmallBuildThreads, 0, st>>>(
+        n, b_tb.as<double>(), b_cen.as<double>(), ids, ids2, pos, pos2, b_seg[0].as<SSeg>(), b_seg[1].as<SSeg>(),
+        b_split.as<SSplit>(), b_sflag.as<int>(), b_srank.as<int>(), b_lflag.as<int>(), b_lscan.as<int>(),
+        b_lrank.as<int>(), b_left.as<int>(), b_scan.as<int>(), b_bins.as<BinAcc>(), out.nodes, b_root.as<int>(),
+        b_res.as<SmallBuildResult>());
+    TRY(cudaGetLastError());
+    SmallBuildResult hr;
+    unsigned long long acc[12];
+    TRY(cudaMemcpyAsync(&hr, b_res.p, sizeof(hr), cudaMemcpyDeviceToHost, st));
+    TRY(cudaMemcpyAsync(acc, b_acc.p, sizeof(acc), cudaMemcpyDeviceToHost, st));
+    TRY(cudaStreamSynchronize(st));
+    out.nnodes = hr.nnodes;
+    out.levels = hr.levels;
+    out.root_ref = hr.root_ref;
+    for (int k = 0; k < 6; k++) {
+      unsigned long long u = acc[k];
+      unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
+      double d;
+      memcpy(&d, &b, sizeof(d));
+      out.root_box[k] = d;
+    }
+    return LW_OK;
+  }
   int nseg = 1, cur = 0, node_base = 0;
   int h_counts[2];
   while (nseg > 0) {

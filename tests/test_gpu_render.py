@@ -312,6 +312,40 @@ def test_warp_sah_decide_builds_the_serial_tree(gpu, name, monkeypatch):
     assert prof[0]["ext_nodes"] > 0
 
 
+@pytest.mark.parametrize("name", ["cornell", "soup1000", "soup4096", "coincident"])
+def test_single_block_sah_build_matches_level_build(gpu, name, monkeypatch):
+    """Scenes up to 4096 triangles build their SAH tree in one thread block (k_sah_small); the tree
+    is the level-synchronous build's (LW_SAH_LEVELS=1): same hits and same traversal work."""
+    if name == "coincident":
+        sc = scenes.soup(3000, n_materials=1, seed=7)
+        m = sc.meshes[0]
+        m.positions[: len(m.positions) // 3] = m.positions[0]
+    else:
+        sc = {"cornell": lambda: scenes.cornell(), "soup1000": lambda: scenes.soup(1000, n_materials=1, seed=3),
+              "soup4096": lambda: scenes.soup(4096, n_materials=1, seed=4)}[name]()
+    packed = pack_scene(sc, bvh="sah")
+    lo, hi = (np.array([0.0, 0.0, -0.5]), np.array([1.0, 1.0, 3.0])) if name == "cornell" else (np.zeros(3), np.full(3, 20.0))
+    o, d = _random_rays(20000, lo, hi, 9)
+    monkeypatch.setenv("LW_TRACE_PERSIST", "0")
+    outs = []
+    for levels in (False, True):
+        if levels:
+            monkeypatch.setenv("LW_SAH_LEVELS", "1")
+        else:
+            monkeypatch.delenv("LW_SAH_LEVELS", raising=False)
+        with _renderer(packed, 96, 64, 5) as r:
+            hits = r.trace_closest(o, d)
+            r.set_instrumentation(count_work=True)
+            r.render_pass(0, 2)
+            p = r.kernel_profile()
+            outs.append((hits, {k: p[k] for k in ("ext_nodes", "ext_tris")}, r.framebuffer()))
+    (h0, c0, f0), (h1, c1, f1) = outs
+    assert all(np.array_equal(_bits(a) if a.dtype == np.float64 else a, _bits(b) if b.dtype == np.float64 else b)
+               for a, b in zip(h0, h1))
+    assert c0 == c1 and c0["ext_nodes"] > 0
+    assert np.array_equal(f0, f1)
+
+
 def test_degenerate_deep_sah_tree_falls_back_to_median(gpu, oracle):
     """A SAH tree deeper than the traversal stack (exponentially spaced triangles) is replaced by the
     median tree at upload; hits do not depend on the tree, so the image still matches the oracle."""
