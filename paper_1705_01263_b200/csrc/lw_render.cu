@@ -585,6 +585,126 @@ __global__ void k_env_marginal(const double* __restrict__ rsum, int H, double* _
   }
 }
 
+// The same construction with one thread block per table, staged in shared memory (the per-thread
+// form above walks W texels of its own row through L2 with dependent loads: 8.8 ms for 4096x2048,
+// 64 warps on the whole GPU).  Thread 0 keeps every order-dependent step sequential -- the row sum
+// in texel order and the Vose pairing -- while the block loads the weights, divides by the sum and
+// sorts texels into the small / large worklists with a block scan (both in texel order, as the
+// sequential pushes leave them), so every value is the sequential one.  Shared memory: W scaled
+// weights (8 B) + one W-entry worklist array holding the small stack from the bottom and the large
+// stack from the top (their sizes add up to at most W).
+constexpr int kAliasThreads = 256;
+__device__ void alias_build_block(const double* __restrict__ w, int n, double* __restrict__ prob, int* __restrict__ alias,
+                                  double* __restrict__ pdf, double* total_out, int* bad_out, bool uniform_if_bad,
+                                  double* sp, int* stk) {
+  using BlockScan = cub::BlockScan<int, kAliasThreads>;
+  __shared__ typename BlockScan::TempStorage ts;
+  __shared__ double s_total;
+  __shared__ int s_ok, s_carry;
+  for (int c = threadIdx.x; c < n; c += kAliasThreads) sp[c] = w[c];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    int ok = 1;
+    for (int c = 0; c < n; c++) {
+      double x = sp[c];
+      if (!(x >= 0.0) || x == INFINITY) ok = 0;
+      total += x;
+    }
+    s_total = total;
+    s_ok = ok && total > 0.0;
+    s_carry = 0;
+    if (total_out) *total_out = total;
+    if (bad_out) *bad_out = s_ok ? 0 : 1;
+  }
+  __syncthreads();
+  const double total = s_total;
+  if (!s_ok) {
+    if (uniform_if_bad)  // a row without weight is never drawn
+      for (int c = threadIdx.x; c < n; c += kAliasThreads) {
+        prob[c] = 1.0;
+        alias[c] = c;
+        pdf[c] = 0.0;
+      }
+    return;
+  }
+  // scaled weights and the worklists in index order (small: sc < 1 from the bottom, large from the top)
+  const double dn = (double)n;
+  for (int base = 0; base < n; base += kAliasThreads) {
+    int c = base + threadIdx.x;
+    int small = 0;
+    if (c < n) {
+      double pc = sp[c] / total;
+      pdf[c] = pc;
+      double sc = pc * dn;
+      sp[c] = sc;
+      small = sc < 1.0 ? 1 : 0;
+    }
+    int pos, cnt;
+    BlockScan(ts).ExclusiveSum(small, pos, cnt);
+    int carry = s_carry;
+    if (c < n) {
+      if (small)
+        stk[carry + pos] = c;
+      else
+        stk[n - 1 - (c - carry - pos)] = c;  // large entry k = c - (smalls before c) at n-1-k
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + cnt;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int ns = s_carry, nl = n - ns;
+    while (ns > 0 && nl > 0) {
+      int sm = stk[--ns];
+      int l = stk[n - nl];
+      --nl;
+      alias[sm] = l;  // prob[sm] keeps its scaled weight
+      double nv = (sp[l] + sp[sm]) - 1.0;
+      sp[l] = nv;
+      if (nv < 1.0)
+        stk[ns++] = l;
+      else
+        stk[n - 1 - nl++] = l;
+    }
+    while (nl > 0) {
+      int l = stk[n - nl];
+      --nl;
+      sp[l] = 1.0;
+      alias[l] = l;
+    }
+    while (ns > 0) {
+      int sm = stk[--ns];
+      sp[sm] = 1.0;
+      alias[sm] = sm;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += kAliasThreads) prob[c] = sp[c];
+}
+
+__global__ void __launch_bounds__(kAliasThreads) k_env_rows_blk(const double* __restrict__ w, int W, int H,
+                                                                double* __restrict__ prob, int* __restrict__ alias,
+                                                                double* __restrict__ pdf, double* __restrict__ rsum) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sp = reinterpret_cast<double*>(smem);
+  int* stk = reinterpret_cast<int*>(sp + W);
+  for (int r = blockIdx.x; r < H; r += gridDim.x) {
+    const size_t o = (size_t)r * W;
+    alias_build_block(w + o, W, prob + o, alias + o, pdf + o, rsum + r, nullptr, true, sp, stk);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kAliasThreads) k_env_marginal_blk(const double* __restrict__ rsum, int H,
+                                                                    double* __restrict__ rprob, int* __restrict__ ralias,
+                                                                    double* __restrict__ rpdf, int* __restrict__ bad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sp = reinterpret_cast<double*>(smem);
+  int* stk = reinterpret_cast<int*>(sp + H);
+  alias_build_block(rsum, H, rprob, ralias, rpdf, nullptr, bad, false, sp, stk);
+}
+
 __global__ void k_env_pdf(double* __restrict__ pdf, const double* __restrict__ rpdf, int W, long long n) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
     pdf[j] = rpdf[j / W] * pdf[j];
@@ -2623,9 +2743,23 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     LW_CUDA_TRY(bbad.alloc(sizeof(int), st));
     dw = bw.as<double>();
     LW_CUDA_TRY(cudaMemcpyAsync(dw, d->env_weight, sizeof(double) * nt, cudaMemcpyHostToDevice, st));
-    k_env_rows<<<(H + 63) / 64, 64, 0, st>>>(dw, W, H, pp, pa, pd, brs.as<double>(), bs.as<int>(), bl.as<int>());
-    k_env_marginal<<<1, 1, 0, st>>>(brs.as<double>(), H, rp, ra, brp.as<double>(), bs.as<int>(), bl.as<int>(),
-                                    bbad.as<int>());
+    // per-table thread blocks in shared memory when a row / the marginal fits (W, H <= 16384);
+    // LW_ENV_SERIAL=1 (or larger images) keeps the one-thread-per-row form -- identical tables
+    static const bool env_serial = getenv("LW_ENV_SERIAL") != nullptr;
+    const size_t row_smem = (size_t)W * 12, col_smem = (size_t)H * 12;
+    if (!env_serial && row_smem <= 192 * 1024 && col_smem <= 192 * 1024) {
+      const int mx = (int)std::max(row_smem, col_smem);
+      LW_CUDA_TRY(cudaFuncSetAttribute(k_env_rows_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      LW_CUDA_TRY(cudaFuncSetAttribute(k_env_marginal_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+      k_env_rows_blk<<<std::min(H, nsm * 8), kAliasThreads, row_smem, st>>>(dw, W, H, pp, pa, pd, brs.as<double>());
+      k_env_marginal_blk<<<1, kAliasThreads, col_smem, st>>>(brs.as<double>(), H, rp, ra, brp.as<double>(), bbad.as<int>());
+    } else {
+      k_env_rows<<<(H + 63) / 64, 64, 0, st>>>(dw, W, H, pp, pa, pd, brs.as<double>(), bs.as<int>(), bl.as<int>());
+      k_env_marginal<<<1, 1, 0, st>>>(brs.as<double>(), H, rp, ra, brp.as<double>(), bs.as<int>(), bl.as<int>(),
+                                      bbad.as<int>());
+    }
     k_env_pdf<<<grid_for(nt, 256, 148 * 16), 256, 0, st>>>(pd, brp.as<double>(), W, nt);
     LW_CUDA_TRY(cudaGetLastError());
     int bad = 1;
