@@ -37,6 +37,9 @@ namespace {
 #ifndef LW_SAH_CTRAV
 #define LW_SAH_CTRAV 1.0
 #endif
+#ifndef LW_SAH_PRIV
+#define LW_SAH_PRIV 1  // large-segment bins privatised in shared memory per 1024-position chunk
+#endif
 constexpr int kBins = LW_SAH_BINS;      // centroid bins per axis
 constexpr int kMaxLeaf = LW_SAH_MAXLEAF; // segments above this size are always split (leaf count field: <= 7)
 constexpr int kSmall = 32;   // segments up to this size are binned by one thread
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(256) k_sah_bin_large(const int* __restrict__ p
   if (c0 >= n) return;
   int c1 = min(c0 + kChunk, n);
   int s_first = pos_seg[c0], s_last = pos_seg[c1 - 1];
-  bool priv = s_first >= 0 && s_first == s_last && large_rank[s_first] >= 0;
+  bool priv = LW_SAH_PRIV && s_first >= 0 && s_first == s_last && large_rank[s_first] >= 0;
   if (priv) {
     for (int k = threadIdx.x; k < 3 * kBins; k += blockDim.x) {
       unsigned long long* b = sb + 13 * k;
@@ -378,12 +381,16 @@ __device__ __forceinline__ double shfl_down_d(double v, int off) { return __shfl
 #define LW_SAH_DEC_MINB 4
 #endif
 // bin `bin` of axis a of segment g: count, triangle-bounds box, centroid box.  Large segments read
-// the pre-binned accumulators; small ones (lane k holds triangle k) bin with ordered-u64 min / max
-// atomics in this warp's shared-memory slice (exact and order-free: the same boxes and counts as a
-// sequential loop).  An empty bin decodes to NaN bounds, which box_grow ignores.
-__device__ __forceinline__ void sah_bin_data(const SSeg& g, int lr, int a, double scale, int bin, int lane, bool mine,
-                                             const double mtb[6], const double mcn[3], const BinAcc* __restrict__ bins,
-                                             unsigned long long (*sb)[13], int& cnt, double bb[6], double cb[6]) {
+// the pre-binned accumulators; for small ones the warp's triangles sit in its shared-memory slice
+// (tri[k] = triangle k's bounds and centroid, written once per segment); lane k computes triangle
+// k's bin and a ballot per bin gives each lane the triangles of its own bin to fold in: min / max
+// and counts are exact and order-free, so these are the boxes and counts of a sequential loop.  (Binning with ordered-u64 min / max
+// atomics compiled to shared-memory CAS loops, ATOMS.CAST.SPIN.64, that serialised on the lanes
+// sharing a bin.)  An empty large-segment bin decodes to NaN bounds, an empty small-segment bin to
+// the reset box; box_grow ignores both.
+__device__ __forceinline__ void sah_bin_data(const SSeg& g, int lr, int a, double scale, int bin,
+                                             const BinAcc* __restrict__ bins, const double (*tri)[9], int& cnt,
+                                             double bb[6], double cb[6]) {
   if (lr >= 0) {
     const BinAcc& src = bins[(size_t)lr * 3 * kBins + a * kBins + bin];
     cnt = (int)src.v[0];
@@ -394,38 +401,24 @@ __device__ __forceinline__ void sah_bin_data(const SSeg& g, int lr, int a, doubl
     }
     return;
   }
-  if (lane < kBins) {
-    unsigned long long* e = sb[bin];
-    e[0] = 0ULL;
+  // lane k bins triangle k once; one ballot per bin hands every lane the members of its bin
+  const int lane = threadIdx.x & 31;
+  const int mb = lane < g.n ? bin_of(tri[lane][6 + a], g.C[a], scale) : -1;
+  unsigned members = 0;
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-      e[1 + k] = ~0ULL;
-      e[4 + k] = 0ULL;
-      e[7 + k] = ~0ULL;
-      e[10 + k] = 0ULL;
-    }
+  for (int j = 0; j < kBins; j++) {
+    unsigned m = __ballot_sync(0xffffffffu, mb == j);
+    if (j == bin) members = m;
   }
-  __syncwarp();
-  if (mine) {
-    unsigned long long* d = sb[bin_of(mcn[a], g.C[a], scale)];
-    atomicAdd(d, 1ULL);
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      atomicMin(d + 1 + k, ordd(mtb[k]));
-      atomicMax(d + 4 + k, ordd(mtb[3 + k]));
-      atomicMin(d + 7 + k, ordd(mcn[k]));
-      atomicMax(d + 10 + k, ordd(mcn[k]));
-    }
+  cnt = __popc(members);
+  box_reset(bb);
+  box_reset(cb);
+  while (members) {
+    const double* t = tri[__ffs(members) - 1];
+    members &= members - 1;
+    box_grow(bb, t, t + 3);
+    box_grow(cb, t + 6, t + 6);
   }
-  __syncwarp();
-  const unsigned long long* e = sb[bin];
-  cnt = (int)e[0];
-#pragma unroll
-  for (int k = 0; k < 6; k++) {
-    bb[k] = unordd(e[1 + k]);
-    cb[k] = unordd(e[7 + k]);
-  }
-  __syncwarp();
 }
 
 // inclusive prefix (bins 0..bin) and suffix (bins bin..15) of one box quantity over the half-warp,
@@ -467,19 +460,19 @@ __device__ __forceinline__ void sah_decide_seg(int s, const SSeg* __restrict__ s
                                                const BinAcc* __restrict__ bins, const int* __restrict__ ids,
                                                const double* __restrict__ tb, const double* __restrict__ cen,
                                                SSplit* __restrict__ out, int* __restrict__ split_flag,
-                                               unsigned long long (*sbw)[13], int lane) {
+                                               double (*tri)[9], int lane) {
   const int bin = lane & 15;
   const SSeg g = seg[s];
   const int lr = large_rank[s];
-  const bool mine = lr < 0 && lane < g.n;
-  double mtb[6], mcn[3];
-  if (mine) {
+  __syncwarp();  // the previous segment's reads of tri are done
+  if (lr < 0 && lane < g.n) {
     int t = ids[g.start + lane];
 #pragma unroll
-    for (int k = 0; k < 6; k++) mtb[k] = tb[6 * (size_t)t + k];
+    for (int k = 0; k < 6; k++) tri[lane][k] = tb[6 * (size_t)t + k];
 #pragma unroll
-    for (int k = 0; k < 3; k++) mcn[k] = cen[3 * (size_t)t + k];
+    for (int k = 0; k < 3; k++) tri[lane][6 + k] = cen[3 * (size_t)t + k];
   }
+  __syncwarp();
   double best = INFINITY;
   int bkey = 1 << 30, bnl = 0;
   if (g.n > 1) {
@@ -489,7 +482,7 @@ __device__ __forceinline__ void sah_decide_seg(int s, const SSeg* __restrict__ s
       double scale = (double)kBins / ext;
       int cnt, pn, sn;
       double bb[6], cb[6], pb[6], sb[6];
-      sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbw, cnt, bb, cb);
+      sah_bin_data(g, lr, a, scale, bin, bins, tri, cnt, bb, cb);
       sah_scan_counts(cnt, bin, pn, sn);
       sah_scan_boxes(bb, bin, pb, sb);
       // right side of plane p = bin: the suffix of bin + 1
@@ -530,7 +523,7 @@ __device__ __forceinline__ void sah_decide_seg(int s, const SSeg* __restrict__ s
     double scale = (double)kBins / (g.C[3 + a] - g.C[a]);
     int cnt;
     double bb[6], cb[6], pb[6], sb[6], pc[6], sc[6];
-    sah_bin_data(g, lr, a, scale, bin, lane, mine, mtb, mcn, bins, sbw, cnt, bb, cb);
+    sah_bin_data(g, lr, a, scale, bin, bins, tri, cnt, bb, cb);
     sah_scan_boxes(bb, bin, pb, sb);
     sah_scan_boxes(cb, bin, pc, sc);
     double rb[6], rc[6];
@@ -579,11 +572,11 @@ __global__ void __launch_bounds__(128, LW_SAH_DEC_MINB) k_sah_decide_w(const SSe
                                const BinAcc* __restrict__ bins, const int* __restrict__ ids,
                                const double* __restrict__ tb, const double* __restrict__ cen,
                                SSplit* __restrict__ out, int* __restrict__ split_flag) {
-  __shared__ unsigned long long sbin[4][kBins][13];
+  __shared__ double tri[4][32][9];
   const int s = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, wib = (threadIdx.x >> 5) & 3;
   if (s >= nseg) return;  // uniform per warp
-  sah_decide_seg(s, seg, large_rank, bins, ids, tb, cen, out, split_flag, sbin[wib], lane);
+  sah_decide_seg(s, seg, large_rank, bins, ids, tb, cen, out, split_flag, tri[wib], lane);
 }
 
 __device__ __forceinline__ int leaf_ref32(long long start, long long count) {
@@ -749,7 +742,7 @@ __global__ void __launch_bounds__(kSmallBuildThreads) k_sah_small(
     int* __restrict__ srank, int* __restrict__ lflag, int* __restrict__ lscan, int* __restrict__ lrank,
     int* __restrict__ left, int* __restrict__ scan, BinAcc* __restrict__ bins, SahNode* __restrict__ nodes,
     int* __restrict__ root_ref, SmallBuildResult* __restrict__ res) {
-  __shared__ unsigned long long sbin[kSmallBuildThreads / 32][kBins][13];
+  __shared__ double tri[kSmallBuildThreads / 32][32][9];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kSmallBuildThreads / 32;
   SSeg* seg = seg_a;
   SSeg* nxt = seg_b;
@@ -794,7 +787,7 @@ __global__ void __launch_bounds__(kSmallBuildThreads) k_sah_small(
     }
     __syncthreads();
     // split decisions, one warp per segment
-    for (int q = warp; q < nseg; q += nw) sah_decide_seg(q, seg, lrank, bins, ids, tb, cen, split, sflag, sbin[warp], lane);
+    for (int q = warp; q < nseg; q += nw) sah_decide_seg(q, seg, lrank, bins, ids, tb, cen, split, sflag, tri[warp], lane);
     const int nsplit = block_exscan(sflag, srank, nseg);
     for (int q = tid; q < nseg; q += kSmallBuildThreads) sah_emit_seg(q, seg, split, srank, node_base, nodes, root_ref, nxt);
     // stable partition of the positions
