@@ -198,61 +198,109 @@ __device__ __forceinline__ void bin_add(unsigned long long* b, const double* tb,
   (void)shared_mem;
 }
 
+// value k of a triangle's bin record (BinAcc v[1 + k]): k < 3 box min, < 6 box max, < 9 centroid
+// min, < 12 centroid max, as ordered u64
+__device__ __forceinline__ unsigned long long bin_val(int k, const double* tbt, const double* ct) {
+  return k < 6 ? ordd(tbt[k]) : ordd(ct[(k - 6) % 3]);
+}
+
+// Large-segment bins.  A 1024-position chunk inside one segment accumulates privately in shared
+// memory and flushes once with global atomics (native 64-bit min / max, REDG.E.MIN.64).  Shared
+// 64-bit min / max would compile to CAS loops (ATOMS.CAST.SPIN.64) that serialise the threads of a
+// bin, so the private minima / maxima are exact 64-bit results of two native 32-bit passes: the
+// high words first, then the low words of the values whose high word won.
 __global__ void __launch_bounds__(256) k_sah_bin_large(const int* __restrict__ pos_seg, const int* __restrict__ ids,
                                                        int n, const SSeg* __restrict__ seg,
                                                        const int* __restrict__ large_rank, const double* __restrict__ tb,
                                                        const double* __restrict__ cen, BinAcc* __restrict__ bins) {
-  __shared__ unsigned long long sb[3 * kBins * 13];
+  __shared__ unsigned s_cnt[3 * kBins], s_hi[3 * kBins][12], s_lo[3 * kBins][12];
   int c0 = blockIdx.x * kChunk;
   if (c0 >= n) return;
   int c1 = min(c0 + kChunk, n);
   int s_first = pos_seg[c0], s_last = pos_seg[c1 - 1];
   bool priv = LW_SAH_PRIV && s_first >= 0 && s_first == s_last && large_rank[s_first] >= 0;
-  if (priv) {
-    for (int k = threadIdx.x; k < 3 * kBins; k += blockDim.x) {
-      unsigned long long* b = sb + 13 * k;
-      b[0] = 0;
-      for (int a = 0; a < 3; a++) {
-        b[1 + a] = ~0ULL;
-        b[4 + a] = 0ULL;
-        b[7 + a] = ~0ULL;
-        b[10 + a] = 0ULL;
-      }
-    }
-    __syncthreads();
-  }
-  for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-    int s = pos_seg[i];
-    if (s < 0) continue;
-    int lr = large_rank[s];
-    if (lr < 0) continue;
-    int t = ids[i];
-    const double* tbt = tb + 6 * (size_t)t;
-    const double* ct = cen + 3 * (size_t)t;
-    const SSeg& g = seg[s];
+  if (!priv) {
+    for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      int s = pos_seg[i];
+      if (s < 0) continue;
+      int lr = large_rank[s];
+      if (lr < 0) continue;
+      int t = ids[i];
+      const double* tbt = tb + 6 * (size_t)t;
+      const double* ct = cen + 3 * (size_t)t;
+      const SSeg& g = seg[s];
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-      double ext = g.C[3 + a] - g.C[a];
-      if (!(ext > 0.0)) continue;
-      int b = bin_of(ct[a], g.C[a], (double)kBins / ext);
-      unsigned long long* dst = priv ? sb + 13 * (a * kBins + b) : bins[(size_t)lr * 3 * kBins + a * kBins + b].v;
-      bin_add(dst, tbt, ct, priv);
+      for (int a = 0; a < 3; a++) {
+        double ext = g.C[3 + a] - g.C[a];
+        if (!(ext > 0.0)) continue;
+        int b = bin_of(ct[a], g.C[a], (double)kBins / ext);
+        bin_add(bins[(size_t)lr * 3 * kBins + a * kBins + b].v, tbt, ct, false);
+      }
+    }
+    return;
+  }
+  for (int q = threadIdx.x; q < 3 * kBins; q += blockDim.x) {
+    s_cnt[q] = 0;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      bool mx = (k % 6) >= 3;
+      s_hi[q][k] = mx ? 0u : ~0u;
+      s_lo[q][k] = mx ? 0u : ~0u;
     }
   }
-  if (priv) {
-    __syncthreads();
-    int lr = large_rank[s_first];
-    for (int k = threadIdx.x; k < 3 * kBins; k += blockDim.x) {
-      unsigned long long* b = sb + 13 * k;
-      if (b[0] == 0) continue;
-      unsigned long long* d = bins[(size_t)lr * 3 * kBins + k].v;
-      atomicAdd(d, b[0]);
+  __syncthreads();
+  const SSeg& g = seg[s_first];
+  double scale[3];
+  bool live[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    double ext = g.C[3 + a] - g.C[a];
+    live[a] = ext > 0.0;
+    scale[a] = (double)kBins / ext;
+  }
+  for (int pass = 0; pass < 2; pass++) {
+    for (int i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      int t = ids[i];
+      const double* tbt = tb + 6 * (size_t)t;
+      const double* ct = cen + 3 * (size_t)t;
+#pragma unroll
       for (int a = 0; a < 3; a++) {
-        atomicMin(d + 1 + a, b[1 + a]);
-        atomicMax(d + 4 + a, b[4 + a]);
-        atomicMin(d + 7 + a, b[7 + a]);
-        atomicMax(d + 10 + a, b[10 + a]);
+        if (!live[a]) continue;
+        int q = a * kBins + bin_of(ct[a], g.C[a], scale[a]);
+        if (pass == 0) atomicAdd(&s_cnt[q], 1u);
+#pragma unroll
+        for (int k = 0; k < 12; k++) {
+          unsigned long long v = bin_val(k, tbt, ct);
+          unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+          bool mx = (k % 6) >= 3;
+          if (pass == 0) {
+            if (mx)
+              atomicMax(&s_hi[q][k], hi);
+            else
+              atomicMin(&s_hi[q][k], hi);
+          } else if (hi == s_hi[q][k]) {
+            if (mx)
+              atomicMax(&s_lo[q][k], lo);
+            else
+              atomicMin(&s_lo[q][k], lo);
+          }
+        }
       }
+    }
+    __syncthreads();
+  }
+  const int lr = large_rank[s_first];
+  for (int q = threadIdx.x; q < 3 * kBins; q += blockDim.x) {
+    if (s_cnt[q] == 0) continue;
+    unsigned long long* d = bins[(size_t)lr * 3 * kBins + q].v;
+    atomicAdd(d, (unsigned long long)s_cnt[q]);
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      unsigned long long v = ((unsigned long long)s_hi[q][k] << 32) | s_lo[q][k];
+      if ((k % 6) >= 3)
+        atomicMax(d + 1 + k, v);
+      else
+        atomicMin(d + 1 + k, v);
     }
   }
 }
