@@ -184,6 +184,8 @@ struct lw_ctx {
   // CUDA-graph wave loop (device-side termination) and asynchronous pass bookkeeping
   bool use_graph = getenv("LW_GRAPH") ? atoi(getenv("LW_GRAPH")) != 0 : true;
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t side_stream = nullptr;  // scene-upload copies overlapping the BVH build
+  cudaEvent_t ev_side0 = nullptr, ev_side1 = nullptr;
   cudaGraphExec_t wave_exec = nullptr;
   WaveCfg wave_key;
   WaveCfg last_key;  // configuration of the previous wavefront pass
@@ -2232,6 +2234,8 @@ struct CtxRes {
   cudaStream_t stream;
   Counters *d_cnt, *h_cnt;
   cudaEvent_t ev0, ev1;
+  cudaStream_t side;          // scene upload: copies that overlap the BVH build
+  cudaEvent_t ev_side0, ev_side1;
 };
 std::mutex g_res_mu;
 std::vector<CtxRes> g_res_free;
@@ -2252,11 +2256,16 @@ cudaError_t take_res(int device, CtxRes& r) {
   r.stream = nullptr;
   r.d_cnt = r.h_cnt = nullptr;
   r.ev0 = r.ev1 = nullptr;
+  r.side = nullptr;
+  r.ev_side0 = r.ev_side1 = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&r.d_cnt, kCtrBytes);
   if (e == cudaSuccess) e = cudaMallocHost(&r.h_cnt, kCtrBytes);
   if (e == cudaSuccess) e = cudaEventCreate(&r.ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&r.ev1);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.ev_side0, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.ev_side1, cudaEventDisableTiming);
   return e;
 }
 
@@ -2272,6 +2281,9 @@ void give_res(const CtxRes& r) {
   if (r.h_cnt) cudaFreeHost(r.h_cnt);
   if (r.ev0) cudaEventDestroy(r.ev0);
   if (r.ev1) cudaEventDestroy(r.ev1);
+  if (r.ev_side0) cudaEventDestroy(r.ev_side0);
+  if (r.ev_side1) cudaEventDestroy(r.ev_side1);
+  if (r.side) cudaStreamDestroy(r.side);
   if (r.stream) cudaStreamDestroy(r.stream);
 }
 // NCCL, resolved at first use with dlopen("libnccl.so.2"): in a PyTorch process this is the
@@ -2423,6 +2435,9 @@ int lw_ctx_create(int device, lw_ctx** out) {
     return LW_ERR_CUDA;
   }
   c->own_stream = c->stream = r.stream;
+  c->side_stream = r.side;
+  c->ev_side0 = r.ev_side0;
+  c->ev_side1 = r.ev_side1;
   c->d_cnt = r.d_cnt;
   c->h_cnt = r.h_cnt;
   c->d_acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(r.d_cnt) + kAccOff);
@@ -2480,7 +2495,7 @@ int lw_ctx_destroy(lw_ctx* c) {
   if (c->comm) nccl_api()->destroy(c->comm);
   if (c->wave_exec) cudaGraphExecDestroy(c->wave_exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  CtxRes r{c->device, c->own_stream, c->d_cnt, c->h_cnt, c->ev0, c->ev1};
+  CtxRes r{c->device, c->own_stream, c->d_cnt, c->h_cnt, c->ev0, c->ev1, c->side_stream, c->ev_side0, c->ev_side1};
   give_res(r);
   delete c;
   return LW_OK;
@@ -2524,8 +2539,32 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   for (int64_t e = 0; e < d->nemit; e++) LW_CHECK_ARG(d->emit_tri[e] >= 0 && d->emit_tri[e] < n, "emitter triangle out of range");
   double* dv;
   LW_STATUS_TRY(dev_upload(c, dv, d->verts, 9 * n));
+  // Copies the BVH build does not need (shading normals, environment image and texel weights) run
+  // on the context's side stream and overlap the build; the main stream waits for them before the
+  // environment tables (and, through `side_done`, before any exit path frees a buffer).
+  const bool env_img = d->env_kind == LW_ENV_IMAGE && d->env_width > 0 && d->env_height > 0 && d->env_image &&
+                       d->env_weight;
+  const int64_t env_nt = env_img ? (int64_t)d->env_width * d->env_height : 0;
   double* dn;
-  LW_STATUS_TRY(dev_upload(c, dn, d->normals, 9 * n));
+  LW_STATUS_TRY(dev_alloc(c, dn, 9 * n));
+  float* env_dimg = nullptr;
+  DevBuf env_wbuf;  // texel weights: scratch, freed once the tables are built
+  if (env_img) {
+    LW_STATUS_TRY(dev_alloc(c, env_dimg, 3 * env_nt));
+    LW_CUDA_TRY(env_wbuf.alloc(sizeof(double) * env_nt, st));
+  }
+  LW_CUDA_TRY(cudaEventRecord(c->ev_side0, st));  // allocations ordered before the side copies
+  LW_CUDA_TRY(cudaStreamWaitEvent(c->side_stream, c->ev_side0, 0));
+  if (n > 0) LW_CUDA_TRY(cudaMemcpyAsync(dn, d->normals, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, c->side_stream));
+  if (env_img) {
+    LW_CUDA_TRY(cudaMemcpyAsync(env_dimg, d->env_image, sizeof(float) * 3 * env_nt, cudaMemcpyHostToDevice, c->side_stream));
+    LW_CUDA_TRY(cudaMemcpyAsync(env_wbuf.p, d->env_weight, sizeof(double) * env_nt, cudaMemcpyHostToDevice, c->side_stream));
+  }
+  LW_CUDA_TRY(cudaEventRecord(c->ev_side1, c->side_stream));
+  struct SideDone {  // main stream waits for the side copies on every exit (before env_wbuf's free)
+    lw_ctx* c;
+    ~SideDone() { cudaStreamWaitEvent(c->stream, c->ev_side1, 0); }
+  } side_done{c};
   int* dm;
   LW_STATUS_TRY(dev_upload(c, dm, (const int*)d->material, n));
   lw_material* dmat;
@@ -2724,25 +2763,23 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     LW_CHECK_ARG(d->env_width > 0 && d->env_height > 0 && d->env_image && d->env_weight, "bad environment image");
     int64_t nt = (int64_t)d->env_width * d->env_height;
     const int W = d->env_width, H = d->env_height;
-    float* img;
+    float* img = env_dimg;  // copied on the side stream at the start of the upload
     double *dw, *pp, *pd, *rp;
     int *pa, *ra;
-    LW_STATUS_TRY(dev_upload(c, img, d->env_image, 3 * nt));
     LW_STATUS_TRY(dev_alloc(c, pp, nt));
     LW_STATUS_TRY(dev_alloc(c, pd, nt));
     LW_STATUS_TRY(dev_alloc(c, pa, nt));
     LW_STATUS_TRY(dev_alloc(c, rp, H));
     LW_STATUS_TRY(dev_alloc(c, ra, H));
-    // weights and worklists are scratch: freed (stream-ordered) once the tables are built
-    DevBuf bw, bs, bl, brs, brp, bbad;
-    LW_CUDA_TRY(bw.alloc(sizeof(double) * nt, st));
+    // worklists are scratch: freed (stream-ordered) once the tables are built
+    DevBuf bs, bl, brs, brp, bbad;
     LW_CUDA_TRY(bs.alloc(sizeof(int) * nt, st));
     LW_CUDA_TRY(bl.alloc(sizeof(int) * nt, st));
     LW_CUDA_TRY(brs.alloc(sizeof(double) * H, st));
     LW_CUDA_TRY(brp.alloc(sizeof(double) * H, st));
     LW_CUDA_TRY(bbad.alloc(sizeof(int), st));
-    dw = bw.as<double>();
-    LW_CUDA_TRY(cudaMemcpyAsync(dw, d->env_weight, sizeof(double) * nt, cudaMemcpyHostToDevice, st));
+    dw = env_wbuf.as<double>();
+    LW_CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side1, 0));  // image and weights are on the device
     // per-table thread blocks in shared memory when a row / the marginal fits (W, H <= 16384);
     // LW_ENV_SERIAL=1 (or larger images) keeps the one-thread-per-row form -- identical tables
     static const bool env_serial = getenv("LW_ENV_SERIAL") != nullptr;
@@ -2802,6 +2839,7 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
     S.cam_up[k] = d->cam_up[k];
   }
   S.tan_half = d->tan_half_fov;
+  LW_CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side1, 0));  // shading normals (and the environment) landed
   LW_CUDA_TRY(cudaStreamSynchronize(st));
   phase("lights+env", tph);
   c->has_scene = true;
