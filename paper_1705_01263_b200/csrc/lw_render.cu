@@ -54,6 +54,9 @@ using namespace lw;
 #endif
 // k_generate: 4 blocks of 256 -> 64 registers (5 -> 48 with spills: 1-3 % slower generate; no
 // bound -> 90 registers: C2 generate 0.22 -> 0.31 ms)
+#ifndef LW_GEN_PREFETCH
+#define LW_GEN_PREFETCH 2  // 0 none, 1 stage bytes two rounds ahead, 2 + flush data one round ahead
+#endif
 #ifndef LW_GEN_MINB
 #define LW_GEN_MINB 4
 #endif
@@ -978,12 +981,43 @@ __global__ void __launch_bounds__(256, LW_GEN_MINB) k_generate(DevScene S, Pool 
   int enext = __shfl_sync(0xffffffffu, eb, 0);       // next queue position of this warp
   unsigned long long bad = 0, paths = 0;
   if (c_trace == 0 && (!regen || c_want == 0)) return;  // nothing to flush, generate or queue here
+#if LW_GEN_PREFETCH
+  // Loads run ahead of the round that uses them (other slots: no ordering with this round's
+  // stores), so the round loop is not a chain of dependent load latencies: stage bytes two rounds
+  // ahead, a finished path's pixel and radiance one round ahead (issued once its stage byte, loaded
+  // the round before, is known).
+  int stage_n1 = P.stage[r0 + lane];
+  int stage_n2 = r0 + 32 < r1 ? P.stage[r0 + 32 + lane] : 0;
+  int pix_n1 = 0;
+  v3 L_n1 = mk3(0.0, 0.0, 0.0);
+  if (LW_GEN_PREFETCH > 1 && regen && stage_n1 == LW_STAGE_TERMINATED) {
+    pix_n1 = P.pix[r0 + lane];
+    L_n1 = load_L(P, r0 + lane, CMP);
+  }
+#endif
   for (int base = r0; base < r1; base += 32) {
     int s = base + lane;
+#if LW_GEN_PREFETCH
+    const int stage0 = stage_n1;
+    const int fpix = pix_n1;
+    const v3 fL = L_n1;
+    stage_n1 = stage_n2;
+    if (base + 64 < r1) stage_n2 = P.stage[s + 64];
+    if (LW_GEN_PREFETCH > 1 && regen && base + 32 < r1 && stage_n1 == LW_STAGE_TERMINATED) {
+      pix_n1 = P.pix[s + 32];
+      L_n1 = load_L(P, s + 32, CMP);
+    }
+    int stage = stage0;
+#else
     int stage = P.stage[s];
+#endif
     bool flushed = false;
     if (regen && stage == LW_STAGE_TERMINATED) {
+#if LW_GEN_PREFETCH > 1
+      bad += lw_accumulate(fb, fpix, fL);
+#else
       bad += lw_accumulate(fb, P.pix[s], load_L(P, s, CMP));
+#endif
       paths++;
       stage = LW_STAGE_GENERATE;
       flushed = true;
