@@ -54,6 +54,9 @@ using namespace lw;
 #endif
 // k_generate: 4 blocks of 256 -> 64 registers (5 -> 48 with spills: 1-3 % slower generate; no
 // bound -> 90 registers: C2 generate 0.22 -> 0.31 ms)
+#ifndef LW_SHADE_PREFETCH
+#define LW_SHADE_PREFETCH 1  // shading kernels: queue entries read one grid stride ahead
+#endif
 #ifndef LW_GEN_PREFETCH
 #define LW_GEN_PREFETCH 2  // 0 none, 1 stage bytes two rounds ahead, 2 + flush data one round ahead
 #endif
@@ -1282,13 +1285,25 @@ __global__ void __launch_bounds__(128, (MC & LW_MC_DIFFUSE) ? LW_NEE_MINB_D : LW
   if (LT) lt = lw_lt_stage(S.lt, S.lt_nheap, smem);
   int n = cnt->n_ext;
   const bool tail = cnt->tail != 0;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+  const int stride = gridDim.x * blockDim.x;
+#if LW_SHADE_PREFETCH
+  int s_next = blockIdx.x * blockDim.x + threadIdx.x < n ? P.q_ext[blockIdx.x * blockDim.x + threadIdx.x] : 0;
+#endif
+  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
     int k = base + threadIdx.x;
     bool valid = k < n;
     int s = 0;
     bool shadow = false;
+#if LW_SHADE_PREFETCH
+    const int s_cur = s_next;  // queue entries read one grid stride ahead
+    if (k + stride < n) s_next = P.q_ext[k + stride];
+#endif
     if (valid) {
+#if LW_SHADE_PREFETCH
+      s = s_cur;
+#else
       s = P.q_ext[k];
+#endif
       LwHit h;
       load_hit(P, s, h);
       int f = P.flags[s];
@@ -1345,10 +1360,18 @@ __global__ void __launch_bounds__(128, (MC & LW_MC_DIFFUSE) ? LW_SHADE_MINB_D : 
   int n = cnt->n_ext;
   const bool tail = cnt->tail != 0;
   unsigned long long alive_count = 0;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+  const int stride = gridDim.x * blockDim.x;
+  // queue entries read one grid stride ahead (the general-material kernel spills more with the
+  // extra live value: C4 k_shade +4 %, so it keeps the plain load)
+  constexpr bool PF = LW_SHADE_PREFETCH && (MC & LW_MC_DIFFUSE);
+  int s_next = 0;
+  if (PF && blockIdx.x * blockDim.x + threadIdx.x < n) s_next = P.q_ext[blockIdx.x * blockDim.x + threadIdx.x];
+  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
     int k = base + threadIdx.x;
+    const int s_cur = s_next;
+    if (PF && k + stride < n) s_next = P.q_ext[k + stride];
     if (k < n) {
-      int s = P.q_ext[k];
+      int s = PF ? s_cur : P.q_ext[k];
       if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       PathState ps;
       load_state(P, s, ps, needs_nprev<MC>(S), CMP);
