@@ -55,7 +55,10 @@ using namespace lw;
 // k_generate: 4 blocks of 256 -> 64 registers (5 -> 48 with spills: 1-3 % slower generate; no
 // bound -> 90 registers: C2 generate 0.22 -> 0.31 ms)
 #ifndef LW_SHADE_PREFETCH
-#define LW_SHADE_PREFETCH 1  // shading kernels: queue entries read one grid stride ahead
+#define LW_SHADE_PREFETCH 2  // shading kernels: 1 queue entries read a grid stride ahead, 2 + NEE hit / flags
+#endif
+#ifndef LW_SHADE_K2
+#define LW_SHADE_K2 1  // k_shade (diffuse classes): also the next entry's hit record a stride ahead
 #endif
 #ifndef LW_GEN_PREFETCH
 #define LW_GEN_PREFETCH 2  // 0 none, 1 stage bytes two rounds ahead, 2 + flush data one round ahead
@@ -1286,27 +1289,51 @@ __global__ void __launch_bounds__(128, (MC & LW_MC_DIFFUSE) ? LW_NEE_MINB_D : LW
   int n = cnt->n_ext;
   const bool tail = cnt->tail != 0;
   const int stride = gridDim.x * blockDim.x;
-#if LW_SHADE_PREFETCH
-  int s_next = blockIdx.x * blockDim.x + threadIdx.x < n ? P.q_ext[blockIdx.x * blockDim.x + threadIdx.x] : 0;
-#endif
+  // LW_SHADE_PREFETCH 1: queue entries read one grid stride ahead; 2: two strides ahead, and the
+  // next entry's hit record and flags one stride ahead
+  const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int s_next = LW_SHADE_PREFETCH && k0 < n ? P.q_ext[k0] : 0;
+  int s_next2 = LW_SHADE_PREFETCH > 1 && k0 + stride < n ? P.q_ext[k0 + stride] : 0;
+  double2 h0n = make_double2(0.0, 0.0), h1n = make_double2(0.0, 0.0);
+  int fn = 0;
+  if (LW_SHADE_PREFETCH > 1 && k0 < n) {
+    h0n = P.hit0[s_next];
+    h1n = P.hit1[s_next];
+    fn = P.flags[s_next];
+  }
   for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
     int k = base + threadIdx.x;
     bool valid = k < n;
     int s = 0;
     bool shadow = false;
-#if LW_SHADE_PREFETCH
-    const int s_cur = s_next;  // queue entries read one grid stride ahead
-    if (k + stride < n) s_next = P.q_ext[k + stride];
-#endif
+    const int s_cur = s_next;
+    const double2 h0c = h0n, h1c = h1n;
+    const int fc = fn;
+    if (LW_SHADE_PREFETCH > 1) {
+      s_next = s_next2;
+      if (k + 2 * stride < n) s_next2 = P.q_ext[k + 2 * stride];
+      if (k + stride < n) {
+        h0n = P.hit0[s_next];
+        h1n = P.hit1[s_next];
+        fn = P.flags[s_next];
+      }
+    } else if (LW_SHADE_PREFETCH && k + stride < n) {
+      s_next = P.q_ext[k + stride];
+    }
     if (valid) {
-#if LW_SHADE_PREFETCH
-      s = s_cur;
-#else
-      s = P.q_ext[k];
-#endif
+      s = LW_SHADE_PREFETCH ? s_cur : P.q_ext[k];
       LwHit h;
-      load_hit(P, s, h);
-      int f = P.flags[s];
+      int f;
+      if (LW_SHADE_PREFETCH > 1) {
+        h.t = h0c.x;
+        h.bu = h0c.y;
+        h.bv = h1c.x;
+        h.tri = __double_as_longlong(h1c.y);
+        f = fc;
+      } else {
+        load_hit(P, s, h);
+        f = P.flags[s];
+      }
       int bounce = f & F_BOUNCE;
       if (h.tri >= 0 && bounce != S.max_depth - 1 && (!tail || P.stage[s] == LW_STAGE_TRACE)) {
         PathState ps;
@@ -1364,19 +1391,43 @@ __global__ void __launch_bounds__(128, (MC & LW_MC_DIFFUSE) ? LW_SHADE_MINB_D : 
   // queue entries read one grid stride ahead (the general-material kernel spills more with the
   // extra live value: C4 k_shade +4 %, so it keeps the plain load)
   constexpr bool PF = LW_SHADE_PREFETCH && (MC & LW_MC_DIFFUSE);
-  int s_next = 0;
-  if (PF && blockIdx.x * blockDim.x + threadIdx.x < n) s_next = P.q_ext[blockIdx.x * blockDim.x + threadIdx.x];
+  constexpr bool PF2 = PF && LW_SHADE_K2;  // two-deep: the next entry's hit record one stride ahead
+  const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int s_next = PF && k0 < n ? P.q_ext[k0] : 0;
+  int s_next2 = PF2 && k0 + stride < n ? P.q_ext[k0 + stride] : 0;
+  double2 h0n = make_double2(0.0, 0.0), h1n = make_double2(0.0, 0.0);
+  if (PF2 && k0 < n) {
+    h0n = P.hit0[s_next];
+    h1n = P.hit1[s_next];
+  }
   for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
     int k = base + threadIdx.x;
     const int s_cur = s_next;
-    if (PF && k + stride < n) s_next = P.q_ext[k + stride];
+    const double2 h0c = h0n, h1c = h1n;
+    if (PF2) {
+      s_next = s_next2;
+      if (k + 2 * stride < n) s_next2 = P.q_ext[k + 2 * stride];
+      if (k + stride < n) {
+        h0n = P.hit0[s_next];
+        h1n = P.hit1[s_next];
+      }
+    } else if (PF && k + stride < n) {
+      s_next = P.q_ext[k + stride];
+    }
     if (k < n) {
       int s = PF ? s_cur : P.q_ext[k];
       if (tail && P.stage[s] != LW_STAGE_TRACE) continue;  // finished entry of the tail queue
       PathState ps;
       load_state(P, s, ps, needs_nprev<MC>(S), CMP);
       LwHit h;
-      load_hit(P, s, h);
+      if (PF2) {
+        h.t = h0c.x;
+        h.bu = h0c.y;
+        h.bv = h1c.x;
+        h.tri = __double_as_longlong(h1c.y);
+      } else {
+        load_hit(P, s, h);
+      }
       ShadeGeom g;
       double w;
       bool alive = false;
