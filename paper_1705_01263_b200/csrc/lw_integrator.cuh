@@ -64,7 +64,8 @@ struct DevScene {
 //   LW_MC_NOENV    no environment (env_kind == LW_ENV_NONE);
 //   LW_MC_ALIAS    emitters chosen by the alias table (light_mode != LW_LIGHTS_TREE);
 //   LW_MC_NOTRI    no emissive triangles (nemit == 0);
-//   LW_MC_ENVCONST no image environment (env_kind is constant or none).
+//   LW_MC_ENVCONST no image environment (env_kind is constant or none);
+//   LW_MC_L2       no material has more than two layers (the layer loops stop at 2).
 // The arithmetic executed is the same, so results are identical; the dead code and its registers
 // disappear.  0 (LW_MC_ANY) evaluates anything.  (A class for "diffuse + glossy layers only"
 // spilled more than LW_MC_ANY and was dropped.)
@@ -74,6 +75,12 @@ struct DevScene {
 #define LW_MC_ALIAS 4
 #define LW_MC_NOTRI 8
 #define LW_MC_ENVCONST 16
+#define LW_MC_L2 32
+// compile-time bound of the layer loops of class MC
+template <int MC>
+struct LwLayers {
+  static constexpr int max = (MC & LW_MC_DIFFUSE) ? 1 : (MC & LW_MC_L2) ? 2 : LW_MAX_LAYERS;
+};
 template <int MC>
 __device__ __forceinline__ int lw_mat_nlayers(const lw_material& m) { return (MC & LW_MC_DIFFUSE) ? 1 : m.nlayers; }
 template <int MC>
@@ -280,7 +287,7 @@ __device__ __forceinline__ void lw_layer_weights(const lw_material& m, double co
   lw.sum_a = 0.0;
   lw.nonspec = 0;
 #pragma unroll
-  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+  for (int l = 0; l < LwLayers<MC>::max; l++) {
     lw.a[l] = 0.0;
     if (l >= lw_mat_nlayers<MC>(m)) continue;
     const lw_layer& L = m.layers[l];
@@ -316,7 +323,7 @@ __device__ __forceinline__ v3 lw_bsdf_eval(const lw_material& m, const LayerW& l
   pdf = 0.0;
   if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return f;
 #pragma unroll
-  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+  for (int l = 0; l < LwLayers<MC>::max; l++) {
     if (l >= lw_mat_nlayers<MC>(m)) break;
     const lw_layer& L = m.layers[l];
     const int kind = lw_layer_kind<MC>(L);
@@ -349,7 +356,7 @@ __device__ __forceinline__ void lw_bsdf_eval_split(const lw_material& m, const L
   fg = mk3(0.0, 0.0, 0.0);
   if (wi.z <= 0.0 || wo.z <= 0.0 || !(lw.sum_a > 0.0)) return;
 #pragma unroll
-  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+  for (int l = 0; l < LwLayers<MC>::max; l++) {
     if (l >= lw_mat_nlayers<MC>(m)) break;
     const lw_layer& L = m.layers[l];
     const int kind = lw_layer_kind<MC>(L);
@@ -394,7 +401,7 @@ __device__ __forceinline__ bool lw_bsdf_sample(const lw_material& m, const Layer
   double cum = 0.0, prev = 0.0, a_pick = 0.0;
   bool done = false;
 #pragma unroll
-  for (int l = 0; l < LW_MAX_LAYERS; l++) {
+  for (int l = 0; l < LwLayers<MC>::max; l++) {
     if (done || l >= lw_mat_nlayers<MC>(m) || !(lw.a[l] > 0.0)) continue;
     prev = cum;
     cum = cum + lw.a[l];

@@ -60,6 +60,9 @@ using namespace lw;
 #ifndef LW_SHADE_K2
 #define LW_SHADE_K2 1  // k_shade (diffuse classes): also the next entry's hit record a stride ahead
 #endif
+#ifndef LW_NEE_L2
+#define LW_NEE_L2 1  // k_shade_nee also instantiated for the two-layer classes
+#endif
 #ifndef LW_GEN_PREFETCH
 #define LW_GEN_PREFETCH 2  // 0 none, 1 stage bytes two rounds ahead, 2 + flush data one round ahead
 #endif
@@ -182,6 +185,7 @@ struct lw_ctx {
   // mat_diffuse = every material one uncoated diffuse layer (set by lw_scene_upload); the
   // environment / light-selection bits come from DevScene.  LW_MATCLASS=0 forces LW_MC_ANY (A/B).
   bool mat_diffuse = false;
+  int mat_max_layers = LW_MAX_LAYERS;  // largest layer count of the scene's materials
   bool mat_class_on = getenv("LW_MATCLASS") ? atoi(getenv("LW_MATCLASS")) != 0 : true;
   int nrnodes = 0;        // internal nodes of the render BVH
   cudaStream_t own_stream = nullptr;
@@ -1989,8 +1993,13 @@ void launch_shadow(lw_ctx* c, cudaStream_t st, int grid, size_t smem, int nr, bo
 // BSDF its register allocation came out 2-6 registers larger and C4's NEE 4.6 % slower).
 #define LW_SCENE_CLASSES_NEE(X) \
   X(LW_MC_DIFFUSE | LW_MC_NOENV | LW_MC_ALIAS) X(LW_MC_DIFFUSE | LW_MC_NOENV) X(LW_MC_DIFFUSE)
+#if LW_NEE_L2
+#define LW_SCENE_CLASSES_NEE_L2(X) X(LW_MC_ALIAS | LW_MC_ENVCONST | LW_MC_L2) X(LW_MC_ALIAS | LW_MC_NOTRI | LW_MC_L2)
+#else
+#define LW_SCENE_CLASSES_NEE_L2(X)
+#endif
 #define LW_SCENE_CLASSES(X) \
-  LW_SCENE_CLASSES_NEE(X) X(LW_MC_ALIAS | LW_MC_ENVCONST) X(LW_MC_ALIAS | LW_MC_NOTRI)
+  LW_SCENE_CLASSES_NEE(X) X(LW_MC_ALIAS | LW_MC_ENVCONST | LW_MC_L2) X(LW_MC_ALIAS | LW_MC_NOTRI | LW_MC_L2)
 
 // scene class of the wave: the first instantiated class whose properties the scene has
 int scene_class(const lw_ctx* c) {
@@ -2001,6 +2010,7 @@ int scene_class(const lw_ctx* c) {
   if (S.light_mode != LW_LIGHTS_TREE) m |= LW_MC_ALIAS;
   if (S.nemit == 0) m |= LW_MC_NOTRI;
   if (S.env_kind == LW_ENV_NONE || S.env_kind == LW_ENV_CONSTANT) m |= LW_MC_ENVCONST;
+  if (c->mat_max_layers <= 2) m |= LW_MC_L2;
 #define LW_SC_PICK(k) \
   if ((m & (k)) == (k)) return (k);
   LW_SCENE_CLASSES(LW_SC_PICK)
@@ -2084,6 +2094,7 @@ void enqueue_wave(lw_ctx* c, cudaStream_t st, const WaveCfg& wc) {
   case (k): launch_shade_nee<CMP, (k)>(c, st, gS, lpe_on, ltm, ltsm); break;
   switch (wc.mc) {
     LW_SCENE_CLASSES_NEE(LW_SC_NEE)
+    LW_SCENE_CLASSES_NEE_L2(LW_SC_NEE)
     default: launch_shade_nee<CMP, LW_MC_ANY>(c, st, gS, lpe_on, ltm, ltsm);
   }
 #undef LW_SC_NEE
@@ -2678,9 +2689,11 @@ int lw_scene_upload(lw_ctx* c, const lw_scene_desc* d) {
   lw_material* dmat;
   LW_STATUS_TRY(dev_upload(c, dmat, d->materials, d->nmaterials));
   c->mat_diffuse = true;
+  c->mat_max_layers = 0;
   for (int k = 0; k < d->nmaterials; k++) {
     const lw_material& m = d->materials[k];
     if (!(m.nlayers == 1 && m.layers[0].kind == LW_BSDF_DIFFUSE && m.layers[0].coat == 0)) c->mat_diffuse = false;
+    c->mat_max_layers = std::max(c->mat_max_layers, (int)m.nlayers);
   }
   S.verts = dv;
   S.normals = dn;
