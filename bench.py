@@ -403,6 +403,36 @@ def load_kernel_traffic():
         return None
 
 
+def load_ncu_stage():
+    """ncu --set full summaries of the stage kernels (profiles/r02_ncu_stage_kernels.json, keys
+    <config>_<stage>: C2 every stage, C3 / C5 trace_ext, C4 shade)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_stage_kernels.json")))["kernels"]
+    except (OSError, KeyError, ValueError):
+        return {}
+
+
+def limiter_of(n, smem_bvh_stage):
+    """What bounds a stage kernel, read from its ncu summary: issue rate, dependent-load latency or
+    fixed-latency arithmetic chains (profiles/README.md)."""
+    if not n:
+        return None
+    stalls = n.get("top_stalls_per_issue") or {}
+    top = max((k for k in stalls if k not in ("selected", "not_selected")), key=lambda k: stalls[k], default=None)
+    issue = n.get("issue_active_pct", 0.0)
+    if issue >= 65.0:
+        kind = "instruction issue"
+    elif top == "long_scoreboard":
+        kind = "latency of dependent L1TEX/L2 loads"
+    else:
+        kind = "latency of FP64 dependency chains"
+    text = (f"{kind}: {issue:.0f} % issue-active, {n.get('threads_per_warp_inst', 0):.1f} of 32 lanes per "
+            f"instruction, {n.get('occupancy_pct', 0):.0f} % occupancy ({n.get('regs', 0):.0f} registers), top stall {top}")
+    if smem_bvh_stage:
+        text += "; BVH in shared memory, so the HBM bytes are the ray state only"
+    return text
+
+
 STAGE_KERNELS = {"generate": "k_generate", "trace_ext": "k_trace_ext_p", "shade_nee": "k_shade_nee",
                  "shade": "k_shade", "trace_shadow": "k_trace_shadow_p"}
 
@@ -450,6 +480,7 @@ def roofline_block(a, config, prof, work, smem_bvh, nprev_bytes, peaks, traffic)
     b, smem = stage_bytes(prof, work, smem_bvh, nprev_bytes)
     total_ms = prof["total_ms"]
     tcfg = ((traffic or {}).get("configs") or {}).get(config, {})
+    ncu = load_ncu_stage()
     kernels = []
     for st, kname in STAGE_KERNELS.items():
         ms, n = prof["stage_ms"][st], max(prof["stage_launches"][st], 1)
@@ -462,11 +493,12 @@ def roofline_block(a, config, prof, work, smem_bvh, nprev_bytes, peaks, traffic)
              "ncu_dram_bytes_per_launch": t.get("dram_bytes_per_launch"),
              "ncu_duration_us_per_launch": t.get("duration_us_per_launch"),
              "ncu_dram_frac": (t["dram_bytes_per_launch"] / (t["duration_us_per_launch"] * 1e3) / peak)
-             if t.get("duration_us_per_launch") else None}
+             if t.get("duration_us_per_launch") else None,
+             "limiter": limiter_of(ncu.get(f"{config}_{st}"), smem_bvh and st.startswith("trace"))}
         kernels.append(e)
     dom = max(kernels, key=lambda e: e["share_of_step"] or 0.0)
     return {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": dom["frac"],
-            "traffic": dom["ncu_dram_bytes_per_launch"], "kernel": dom["kernel"],
+            "traffic": dom["ncu_dram_bytes_per_launch"], "kernel": dom["kernel"], "limiter": dom["limiter"],
             "avg_launch_ms": dom["avg_launch_ms"], "share_of_step": dom["share_of_step"],
             "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
             "definition": "achieved = algorithmic bytes per launch (SoA state the stage must move, + BVH "
