@@ -131,19 +131,37 @@ def test_execution_strategy_invariance(cornell_packed):
         assert np.array_equal(outs[0], o)
 
 
-def test_material_class_instantiations_identical(cornell_packed, oracle, monkeypatch):
-    """All-diffuse scenes run the LW_MC_DIFFUSE shading kernels (layer count / kind / coat folded to
-    constants): identical to the general instantiations (LW_MATCLASS=0) and to the oracle."""
+def _class_scene(name):
+    if name == "cornell":  # diffuse + no environment + alias lights
+        return pack_scene(scenes.cornell())
+    if name == "tree":  # diffuse + no environment (light hierarchy)
+        return pack_scene(scenes.many_lights(300), lights="tree")
+    if name == "furnace":  # diffuse under a constant environment
+        sc = scenes.cornell()
+        sc.environment = Environment(constant=(0.3, 0.3, 0.3))
+        return pack_scene(sc)
+    if name == "soup":  # one-layer diffuse / glossy, constant sky, alias lights, two layers at most
+        return pack_scene(scenes.soup(1 << 14, n_materials=8))
+    return pack_scene(scenes.envmap_scene(256, 128, sphere_subdiv=2))  # layered, image env, no emitters
+
+
+@pytest.mark.parametrize("name", ["cornell", "tree", "furnace", "soup", "envmap"])
+def test_material_class_instantiations_identical(gpu, oracle, monkeypatch, name):
+    """Each scene class runs its specialised shading kernels (constants folded for the
+    scene's materials, environment and light selection): identical to the general instantiations
+    (LW_MATCLASS=0) and to the oracle."""
     from paper_1705_01263_b200.render import RenderParams
 
+    packed = _class_scene(name)
+    W, H, D = 96, 64, 8
     outs = []
     for v in ("1", "0"):
         monkeypatch.setenv("LW_MATCLASS", v)
-        with _renderer(cornell_packed, 128, 96, 8, pool_log2=12) as r:
-            r.render_pass(0, 6)
+        with _renderer(packed, W, H, D, pool_log2=12) as r:
+            r.render_pass(0, 4)
             outs.append(r.framebuffer())
-    fb2, _ = oracle.OracleScene(cornell_packed).render(RenderParams(128, 96, 8), 0, 6)
-    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], fb2)
+    fb2, _ = oracle.OracleScene(packed).render(RenderParams(W, H, D), 0, 4)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], fb2) and outs[0].sum() > 0
 
 
 @pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
