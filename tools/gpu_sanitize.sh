@@ -11,7 +11,7 @@ for engine in ("wavefront", "megakernel"):
     # (persistent lane-refill kernels on both placements); with and without LPE layers, FP64 and
     # compact path state, the three estimators
     for packed in (pack_scene(scenes.cornell()), pack_scene(scenes.many_lights(300), lights="tree"),
-                   pack_scene(scenes.soup(4096))):
+                   pack_scene(scenes.soup(4096)), pack_scene(scenes.envmap_scene(128, 64, sphere_subdiv=1))):
         for lpe, compact, est in ((True, False, "mis"), (False, False, "mis"), (False, True, "mis"),
                                   (False, False, "nee"), (False, True, "bsdf")):
             with Renderer(None, 24, 16, 5, packed=packed, engine=engine, pool_log2=10, compact_state=compact,
